@@ -1,0 +1,405 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+Every test here runs without a GPU (-m "not gpu").  Each checks the oracle
+against something other than itself: torch fp64 library routines
+(ref_torch.py), closed forms implied by Eq.(2), brute force, the paper's
+printed example (tests/golden/nine_pixels.json), or SPEC worked
+examples (tests/golden/spec_examples.json).  PIN numbers follow SURVEY §8(c).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle
+import workloads as W
+from workloads import Net, init_weights, CONV, RELU, SILU, MAXPOOL, ADD, SE, OUTPUT
+from ref_torch import dense_forward64, close, max_err
+from netgen import random_net, random_frames
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _single(kind_fn, in_c, h, w, seed=0):
+    n = Net(in_c, h, w)
+    x = kind_fn(n)
+    n.output(x)
+    init_weights(n, seed)
+    return n
+
+
+# ------------------------------------------------------------------ dense
+@pytest.mark.parametrize("seed", range(40))
+def test_dense_matches_torch_fp64(oracle_lib, seed):
+    """Oracle dense forward (Eq.1 etc.) == torch fp64 routines within R29."""
+    net = random_net(seed)
+    x = np.random.default_rng(seed).random((net.in_h, net.in_w, net.in_c)).astype(np.float32)
+    ours = oracle.dense_forward(net, x)
+    ref = dense_forward64(net, x)
+    for i, (a, b) in enumerate(zip(ours, ref)):
+        assert a.shape == b.shape, (i, a.shape, b.shape)
+        assert close(a, b), (seed, i, W.KIND_NAMES[net.layers[i]["kind"]], max_err(a, b))
+
+
+def test_dense_models_match_torch(oracle_lib):
+    """cfg1 and a reduced-resolution CRNN / ResNet-18 / EfficientNet-B0."""
+    for net in (W.models.toy_encoder(16, 16), W.models.crnn_vgg7(32, 64),
+                W.models.resnet18(64, 64), W.models.efficientnet_b0(64, 64)):
+        init_weights(net, 5)
+        x = np.random.default_rng(1).random((net.in_h, net.in_w, net.in_c)).astype(np.float32)
+        ours = oracle.dense_forward(net, x)
+        ref = dense_forward64(net, x)
+        for i, (a, b) in enumerate(zip(ours, ref)):
+            assert close(a, b, rel=3e-4, abs_=3e-5), (net.name, i, max_err(a, b))
+
+
+def test_dense_spec_scalars(oracle_lib):
+    g = _gold("spec_examples.json")
+    e = g["dense_scalar_conv"]
+    n = Net(1, 1, 1)
+    c = n.conv(-1, 1, 1, 1, 0)
+    n.output(c)
+    n.layers[c]["w"] = np.array([[[[e["w"]]]]], np.float32)
+    n.layers[c]["b"] = np.array([e["b"]], np.float32)
+    y = oracle.dense_forward(n, np.array([[[e["x"]]]], np.float32))
+    assert y[-1][0, 0, 0] == e["expect"]
+    n = Net(1, 3, 3)
+    c = n.conv(-1, 1, 3, 1, 0)
+    n.output(c)
+    n.layers[c]["w"] = np.ones((1, 1, 3, 3), np.float32)
+    n.layers[c]["b"] = np.zeros(1, np.float32)
+    y = oracle.dense_forward(n, np.ones((3, 3, 1), np.float32))
+    assert y[-1].shape == (1, 1, 1) and y[-1][0, 0, 0] == g["dense_window_sum"]["expect"]
+
+
+# ------------------------------------------------------- PIN1 theta = 0
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("order", [0, 1])
+def test_pin1_zero_threshold_equals_dense(oracle_lib, seed, order):
+    """theta = 0 everywhere => per-frame diff output == dense output
+    (Eq.2 linearity + Eq.3 correction), against torch fp64."""
+    net = random_net(100 + seed)
+    L = 8
+    fr = random_frames(seed, L, net.in_h, net.in_w, net.in_c)
+    r = oracle.run_chunk(net, fr, 0.0, layer_outer=bool(order))
+    tap = [i for i, l in enumerate(net.layers) if l["kind"] == OUTPUT][0]
+    for t in range(L):
+        ref = dense_forward64(net, fr[t])[tap]
+        assert close(r["taps"][tap][t], ref, rel=2e-4, abs_=2e-5), (seed, t, max_err(r["taps"][tap][t], ref))
+
+
+def test_pin1_models_zero_threshold(oracle_lib):
+    for net in (W.models.toy_encoder(24, 24), W.models.crnn_vgg7(32, 48), W.models.resnet18(48, 48),
+                W.models.efficientnet_b0(64, 64)):
+        init_weights(net, 3)
+        fr = random_frames(7, 4, net.in_h, net.in_w, net.in_c, p_change=0.2, scale=0.2)
+        r = oracle.run_chunk(net, fr, 0.0, want_masks=False)
+        for tap, O in r["taps"].items():
+            for t in range(4):
+                ref = dense_forward64(net, fr[t])[tap]
+                assert close(O[t], ref, rel=5e-4, abs_=5e-5), (net.name, tap, t, max_err(O[t], ref))
+
+
+# ---------------------------------------------- PIN2 input-only threshold
+@pytest.mark.parametrize("seed", range(10))
+def test_pin2_input_threshold_only(oracle_lib, seed):
+    """theta_0 > 0, all other theta = 0  =>  output_t = dense(S_t), S_t the
+    propagated Subtraction buffer (closed form of Eq.2 + Eq.3 at theta=0)."""
+    net = random_net(300 + seed)
+    L, th0 = 8, 0.15
+    fr = random_frames(seed + 50, L, net.in_h, net.in_w, net.in_c, p_change=0.5, scale=0.2)
+    ns = oracle.num_sites(net)
+    th = np.zeros(ns, np.float32)
+    th[0] = th0
+    r = oracle.run_chunk(net, fr, th)
+    # S_t by the buffer rule (R3), written out independently here
+    S = fr[0].copy()
+    tap = [i for i, l in enumerate(net.layers) if l["kind"] == OUTPUT][0]
+    for t in range(1, L):
+        raw = fr[t] - S
+        act = np.abs(raw).max(axis=2) > np.float32(th0)
+        S = np.where(act[..., None], S + raw, S).astype(np.float32)
+        ref = dense_forward64(net, S)[tap]
+        assert close(r["taps"][tap][t], ref, rel=2e-4, abs_=2e-5), (seed, t)
+
+
+# ---------------------------------------------------- PIN3 identical frames
+def test_pin3_identical_frames(oracle_lib):
+    net = random_net(7)
+    fr = np.repeat(random_frames(1, 1, net.in_h, net.in_w, net.in_c), 6, axis=0)
+    r = oracle.run_chunk(net, fr, 0.0)
+    assert all(m.sum() == 0 for m in r["masks"].values())
+    assert r["counts"].sum() == 0
+    for O in r["taps"].values():
+        for t in range(1, 6):
+            assert np.array_equal(O[t], O[0])
+
+
+# ------------------------------------------------ PIN4 nine pixels
+def test_pin4_nine_pixels(oracle_lib):
+    g = _gold("nine_pixels.json")
+    H, Wd = g["map_hw"]
+    for case in g["cases"]:
+        n = Net(1, H, Wd)
+        c = n.conv(-1, 2, tuple(g["kernel"]), tuple(g["stride"]), tuple(g["pad"]))
+        n.output(c)
+        init_weights(n, 0)
+        fr = np.zeros((2, H, Wd, 1), np.float32)
+        fr[1, case["pixel"][0], case["pixel"][1], 0] = 1.0
+        r = oracle.run_chunk(n, fr, 0.0)
+        m = r["masks"][c][0]
+        assert m.sum() == case["active_out"]
+        r0, r1 = case["block_rows"]
+        c0, c1 = case["block_cols"]
+        assert m[r0:r1 + 1, c0:c1 + 1].all()
+
+
+def test_pin4_conv_bias_absent(oracle_lib):
+    e = _gold("spec_examples.json")["conv_bias_absent"]
+    H, Wd = e["map_hw"]
+    n = Net(1, H, Wd)
+    c = n.conv(-1, 1, 3, 1, 1)
+    n.output(c)
+    n.layers[c]["w"] = np.full((1, 1, 3, 3), e["kernel_value"], np.float32)
+    n.layers[c]["b"] = np.array([e["bias"]], np.float32)
+    fr = np.zeros((2, H, Wd, 1), np.float32)
+    fr[1, e["pixel"][0], e["pixel"][1], 0] = e["delta"]
+    r = oracle.run_chunk(n, fr, 0.0, want_deltas=True)
+    m, d = r["masks"][c][0], r["deltas"][c][0]
+    assert m.sum() == e["expect_active"]
+    assert np.all(d[m.astype(bool)] == e["expect_value"])
+    assert np.all(d[~m.astype(bool)] == 0)
+
+
+# ------------------------------------------- PIN5 accumulation identity
+@pytest.mark.parametrize("seed", range(8))
+def test_pin5_accumulation(oracle_lib, seed):
+    """O_t = O_0 + sum_{t'<=t} delta_tap(t'), checked in fp64, and
+    pixels outside the tap mask are bit-identical to frame t-1."""
+    net = random_net(500 + seed)
+    L = 7
+    fr = random_frames(seed, L, net.in_h, net.in_w, net.in_c)
+    r = oracle.run_chunk(net, fr, 0.05, want_deltas=True)
+    tap = [i for i, l in enumerate(net.layers) if l["kind"] == OUTPUT][0]
+    O = r["taps"][tap].astype(np.float64)
+    D = r["deltas"][tap].astype(np.float64)
+    M = r["masks"][tap]
+    for t in range(1, L):
+        np.testing.assert_allclose(O[t], O[0] + D[:t].sum(0), rtol=1e-5, atol=1e-5)
+        off = ~M[t - 1].astype(bool)
+        assert np.array_equal(r["taps"][tap][t][off], r["taps"][tap][t - 1][off])
+
+
+# -------------------------------------- PIN6 truncation rule / conservation
+@pytest.mark.parametrize("seed", range(20))
+def test_pin6_input_truncation(oracle_lib, seed):
+    """Site 0: emitted = raw at masked pixels, residual = raw elsewhere,
+    emitted + residual == raw bit-exact, max|raw| > theta iff masked (P:143,
+    R1/R2)."""
+    rng = np.random.default_rng(seed)
+    net = _single(lambda n: n.relu(-1), 2, 6, 7, seed)
+    L = 9
+    fr = random_frames(seed, L, 6, 7, 2, p_change=0.6, scale=0.1)
+    th = float(rng.uniform(0.01, 0.2))
+    r = oracle.run_chunk(net, fr, [th, 0.0], want_deltas=True)
+    D = r["deltas"][0]   # relu layer delta is not the input delta -> recompute input deltas
+    S = fr[0].copy()
+    for t in range(1, L):
+        raw = (fr[t] - S).astype(np.float32)
+        mx = np.abs(raw).max(axis=2)
+        act = mx > np.float32(th)
+        emitted = np.where(act[..., None], raw, 0).astype(np.float32)
+        residual = np.where(act[..., None], 0, raw).astype(np.float32)
+        assert np.array_equal(emitted + residual, raw)
+        assert not np.any(act & (mx <= th))
+        assert int(act.sum()) == r["counts"][0][t - 1]
+        S = (S + emitted).astype(np.float32)
+    assert D.shape[0] == L - 1
+
+
+@pytest.mark.parametrize("case", ["subtract_one_pixel", "truncate_all_below", "truncate_pixel_granular"])
+def test_pin6_spec_truncation_examples(oracle_lib, case):
+    e = _gold("spec_examples.json")[case]
+    net = _single(lambda n: n.relu(-1), 2, 1, 1)
+    ref = np.array(e.get("ref", [0.0, 0.0]), np.float32)
+    new = np.array(e.get("new", e.get("delta")), np.float32) + ref
+    fr = np.stack([ref, new]).reshape(2, 1, 1, 2)
+    r = oracle.run_chunk(net, fr, [e["theta"], 0.0])
+    assert bool(r["counts"][0][0]) == e["expect_emitted"]
+
+
+# ------------------------------------------------ PIN7 bounded residual
+@pytest.mark.parametrize("seed", range(10))
+def test_pin7_bounded_residual(oracle_lib, seed):
+    """max_c |f(x_acc) - y_acc| <= theta at every pixel after truncation
+    (SPEC S:250): x_acc = x0 + sum input deltas, y_acc = y0 + sum
+    emitted, rebuilt here from the oracle's outputs with fp32 adds."""
+    net = Net(2, 9, 9)
+    c = net.conv(-1, 6, 3)
+    a = net.relu(c)
+    c2 = net.conv(a, 4, 3)
+    s2 = net.silu(c2)
+    net.output(s2)
+    init_weights(net, seed)
+    L, th = 8, 0.07
+    fr = random_frames(seed, L, 9, 9, 2, p_change=0.5, scale=0.3)
+    r = oracle.run_chunk(net, fr, th, want_deltas=True, want_dense0=True)
+    for src, site, f in ((c, a, lambda x: np.maximum(x, 0)),
+                         (c2, s2, lambda x: x / (1 + np.exp(-x.astype(np.float64))))):
+        xa = r["dense0"][src].copy()
+        ya = r["dense0"][site].copy()
+        for t in range(L - 1):
+            xa = (xa + r["deltas"][src][t]).astype(np.float32)
+            ya = (ya + r["deltas"][site][t]).astype(np.float32)
+            res = np.abs(f(xa) - ya).max(axis=2)
+            assert res.max() <= th + 1e-6, (seed, t, res.max())
+
+
+# ------------------------------------------------ PIN8 brute force deltas
+@pytest.mark.parametrize("seed", range(12))
+def test_pin8_conv_delta_bruteforce(oracle_lib, seed):
+    """Eq.(2): delta_out = conv(X_t) - conv(X_{t-1}) exactly in fp64 where the
+    input delta is exact (theta = 0), bias absent; off-mask exactly 0."""
+    rng = np.random.default_rng(seed)
+    k = int(rng.choice([1, 2, 3]))
+    s = int(rng.choice([1, 2]))
+    p = int(rng.integers(0, k // 2 + 1))
+    cin, cout = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+    n = Net(cin, 8, 9)
+    c = n.conv(-1, cout, k, s, p)
+    n.output(c)
+    init_weights(n, seed)
+    fr = random_frames(seed, 4, 8, 9, cin, p_change=0.25)
+    r = oracle.run_chunk(n, fr, 0.0, want_deltas=True)
+    for t in range(1, 4):
+        a = dense_forward64(n, fr[t])[c]
+        b = dense_forward64(n, fr[t - 1])[c]
+        assert close(r["deltas"][c][t - 1], a - b, rel=1e-4, abs_=1e-5)
+        m = r["masks"][c][t - 1].astype(bool)
+        assert np.all(r["deltas"][c][t - 1][~m] == 0)
+
+
+@pytest.mark.parametrize("case", ["relu_dead_zone", "relu_cross_zero"])
+def test_pin8_relu_spec(oracle_lib, case):
+    e = _gold("spec_examples.json")[case]
+    net = _single(lambda n: n.relu(-1), 1, 1, 1)
+    fr = np.array([e["x_ref"], e["x_new"]], np.float32).reshape(2, 1, 1, 1)
+    r = oracle.run_chunk(net, fr, [0.0, e["theta"]], want_deltas=True)
+    assert bool(r["masks"][0][0, 0, 0]) == e["expect_emitted"]
+    assert r["deltas"][0][0, 0, 0, 0] == e["expect_value"]
+
+
+def test_pin8_maxpool_spec(oracle_lib):
+    e = _gold("spec_examples.json")["maxpool_window"]
+    net = _single(lambda n: n.maxpool(-1, 2, 2), 1, 2, 2)
+    fr = np.array([e["window_ref"], e["window_new"]], np.float32).reshape(2, 2, 2, 1)
+    r = oracle.run_chunk(net, fr, [0.0, e["theta"]], want_deltas=True)
+    assert r["deltas"][0][0, 0, 0, 0] == e["expect_value"]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_pin8_nonlinear_bruteforce(oracle_lib, seed):
+    """At theta = 0 every non-linear delta equals f(x_t) - f(x_{t-1}) (fp64)."""
+    for mk in (lambda n: n.relu(-1), lambda n: n.silu(-1), lambda n: n.maxpool(-1, 3, 2, 1),
+               lambda n: n.se(-1, 2)):
+        net = _single(mk, 3, 7, 6, seed)
+        fr = random_frames(seed, 5, 7, 6, 3, p_change=0.3)
+        r = oracle.run_chunk(net, fr, 0.0, want_deltas=True)
+        for t in range(1, 5):
+            a = dense_forward64(net, fr[t])[0]
+            b = dense_forward64(net, fr[t - 1])[0]
+            assert close(r["deltas"][0][t - 1], a - b, rel=1e-4, abs_=2e-6), (seed, t)
+
+
+# --------------------------------------------------------- PIN9 drift
+def test_pin9_drift(oracle_lib):
+    e = _gold("spec_examples.json")["drift"]
+    net = _single(lambda n: n.relu(-1), 1, 1, 1)
+    fr = (np.arange(e["frames"], dtype=np.float32) * np.float32(e["per_frame"])).reshape(-1, 1, 1, 1)
+    r = oracle.run_chunk(net, fr, [e["theta"], 0.0], want_deltas=True)
+    emit_frames = [t + 1 for t in range(e["frames"] - 1) if r["counts"][0][t]]
+    assert emit_frames == e["expect_emit_frames"]
+    # input delta at frame 3 flows through relu of a positive ramp unchanged
+    assert abs(r["deltas"][0][2, 0, 0, 0] - e["expect_value_frame3"]) <= e["value_tol"]
+
+
+# ----------------------------------------------------- PIN10 dilation
+def test_pin10_dilation_vs_indicator_conv(oracle_lib):
+    """Dilation == (indicator map conv ones-kernel) > 0 on 200 random
+    geometries, and monotone."""
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        H, Wd = int(rng.integers(1, 20)), int(rng.integers(1, 20))
+        kh, kw = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+        sh, sw = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        ph, pw = int(rng.integers(0, kh // 2 + 1)), int(rng.integers(0, kw // 2 + 1))
+        Ho, Wo = (H + 2 * ph - kh) // sh + 1, (Wd + 2 * pw - kw) // sw + 1
+        if Ho < 1 or Wo < 1:
+            continue
+        m = (rng.random((H, Wd)) < rng.uniform(0, 0.3)).astype(np.uint8)
+        got = oracle.dilate(m, (kh, kw), (sh, sw), (ph, pw), (Ho, Wo))
+        ind = F.conv2d(torch.from_numpy(m.astype(np.float64))[None, None], torch.ones(1, 1, kh, kw, dtype=torch.float64),
+                       stride=(sh, sw), padding=(ph, pw))[0, 0].numpy() > 0
+        assert np.array_equal(got.astype(bool), ind)
+        m2 = m | (rng.random((H, Wd)) < 0.1).astype(np.uint8)
+        got2 = oracle.dilate(m2, (kh, kw), (sh, sw), (ph, pw), (Ho, Wo))
+        assert np.all(got2 >= got)
+
+
+# -------------------------------------------- PIN12 schedule equivalence
+@pytest.mark.parametrize("seed", range(12))
+def test_pin12_frame_outer_equals_layer_outer(oracle_lib, seed):
+    """SparseBatch ('N' order) == vanilla frame order, bit-exact."""
+    net = random_net(700 + seed)
+    fr = random_frames(seed, 7, net.in_h, net.in_w, net.in_c)
+    a = oracle.run_chunk(net, fr, 0.06, layer_outer=False, want_deltas=True)
+    b = oracle.run_chunk(net, fr, 0.06, layer_outer=True, want_deltas=True)
+    for i in a["masks"]:
+        assert np.array_equal(a["masks"][i], b["masks"][i])
+        assert np.array_equal(a["deltas"][i], b["deltas"][i])
+    for i in a["taps"]:
+        assert np.array_equal(a["taps"][i], b["taps"][i])
+    assert np.array_equal(a["counts"], b["counts"])
+
+
+# ------------------------------------------------ PIN13 memory accountant
+def test_pin13_memory_separation(oracle_lib):
+    """SparseBatch persistent is independent of the number of non-linear
+    layers; vanilla grows with it (P:139 vs P:152)."""
+    rows = []
+    for nl in (1, 4, 16, 32):
+        n = Net(64, 56, 56)
+        x = -1
+        for _ in range(nl):
+            x = n.relu(n.conv(x, 64, 3))
+        n.output(x)
+        sb = oracle.account_memory(n, "sparsebatch")
+        va = oracle.account_memory(n, "vanilla", L=4)
+        rows.append((nl, sb["persistent_values"], va["persistent_values"]))
+        assert sb["persistent_values"] == 2 * 64 * 56 * 56
+        assert sb["pass_count"] == 1 and va["pass_count"] == 4
+    assert len({r[1] for r in rows}) == 1
+    inc = [rows[i + 1][2] - rows[i][2] for i in range(3)]
+    per = [(rows[i + 1][0] - rows[i][0]) for i in range(3)]
+    assert all(d % p == 0 and d // p == inc[0] // per[0] for d, p in zip(inc, per))  # affine in N
+    n16 = [r for r in rows if r[0] == 16][0]
+    assert n16[2] >= 10 * n16[1]
+
+
+# -------------------------------------------------------- PIN16 SE exact
+def test_pin16_se_zero_threshold(oracle_lib):
+    net = _single(lambda n: n.se(-1, 3), 6, 5, 5, 2)
+    fr = random_frames(4, 6, 5, 5, 6, p_change=0.4)
+    r = oracle.run_chunk(net, fr, 0.0)
+    for t in range(6):
+        assert close(r["taps"][1][t], dense_forward64(net, fr[t])[0], rel=1e-5, abs_=1e-6)

@@ -1,0 +1,71 @@
+"""The five BASELINE.json configurations (SURVEY §8(d) input recipe).
+
+Each config names the topology, the frame geometry, chunk length L, chunks per
+step B, the synthetic-video recipe and the threshold policy.  cfg ids are
+1-based like SURVEY (cfg1 = BASELINE.json configs[0]).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import models
+
+SEED_BASE = 2410207900
+
+
+@dataclass
+class Config:
+    cid: int
+    name: str
+    model: str
+    h: int
+    w: int
+    c: int
+    L: int
+    chunks_per_step: int
+    steps: int
+    video: dict = field(default_factory=dict)
+    policy: str = "fixed"          # fixed | bst | ibst
+    theta_fixed: float = 0.05
+    T: float = 0.9
+    eps: float = 0.05
+    cycle: int = 8
+    note: str = ""
+
+    def build_net(self, weight_seed=None):
+        net = {"toy": models.toy_encoder, "crnn": models.crnn_vgg7,
+               "resnet18": models.resnet18, "effb0": models.efficientnet_b0}[self.model](self.h, self.w)
+        models.init_weights(net, SEED_BASE + 1000 * self.cid + 999 if weight_seed is None else weight_seed)
+        return net
+
+    def video_seed(self, chunk):
+        return SEED_BASE + 1000 * self.cid + chunk
+
+
+CONFIGS = {
+    1: Config(1, "toy", "toy", 64, 64, 3, L=8, chunks_per_step=1, steps=1,
+              video=dict(n_objects=3, size=(8, 16), speed=(1, 1), frames_per_px=2,
+                         noise_q=0.05, noise_amp=1),
+              policy="fixed", theta_fixed=0.05,
+              note="toy encoder, one 8-frame chunk of 64x64x3 slow-motion video, threshold 0.05"),
+    2: Config(2, "crnn", "crnn", 32, 128, 1, L=32, chunks_per_step=64, steps=4,
+              video=dict(text=True, n_objects=0, frames_per_px=2, noise_q=0.05, noise_amp=1),
+              policy="fixed", theta_fixed=0.05,
+              note="CRNN VGG-7 conv encoder, 32-frame chunks of 32x128 grayscale synthetic text video"),
+    3: Config(3, "effb0_512", "effb0", 512, 512, 3, L=16, chunks_per_step=8, steps=16,
+              video=dict(n_objects=12, size=(16, 96), speed=(1, 3), noise_q=0.10, noise_amp=2),
+              policy="ibst", T=0.9, eps=0.05, cycle=8,
+              note="EfficientNet-B0 backbone @512x512, 16-frame chunks, online threshold adjustment"),
+    4: Config(4, "resnet18_720p", "resnet18", 720, 1280, 3, L=32, chunks_per_step=8, steps=1,
+              video=dict(n_objects=10, size=(96, 320), speed=(1, 4), noise_q=0.10, noise_amp=2),
+              policy="bst", T=0.9, eps=0.02,
+              note="ResNet-18 @720p, 32-frame chunks, sparsity sweep"),
+    5: Config(5, "effdet_d0_1080p", "effb0", 1080, 1920, 3, L=16, chunks_per_step=8, steps=8,
+              video=dict(n_objects=12, size=(32, 192), speed=(1, 3), noise_q=0.10, noise_amp=2),
+              policy="ibst", T=0.9, eps=0.05, cycle=8,
+              note="EfficientDet-D0 backbone @1080p, 64 chunks, chunk-sharded over GPUs"),
+}
+
+
+def get_config(cid: int) -> Config:
+    return CONFIGS[cid]

@@ -1,0 +1,232 @@
+"""Network topologies as layer-spec lists, plus seeded weights.
+
+A layer is a dict whose integer fields mirror ``st_layer_spec`` in
+``include/sparsetem.h``:
+
+    kind, src, src2, c_out, groups, k_h, k_w, s_h, s_w, p_h, p_w, se_hidden
+    w, b, w2, b2   (numpy float32 arrays; None when unused)
+
+``src`` is the producer layer index (-1 = network input).  Kinds:
+
+* CONV    -- Eq.(1) convolution, PAPER.md P:119-122 (zero padding, groups,
+             weights OIHW ``[c_out][c_in/groups][k_h][k_w]``, bias ``[c_out]``);
+             BatchNorm is folded into w/b.
+* RELU, SILU -- pointwise non-linearities.
+* MAXPOOL -- window max, -inf padding (reading R11).
+* ADD     -- residual join of ``src`` and ``src2`` (linear).
+* SE      -- squeeze-excitation x * sigmoid(W2 silu(W1 mean(x) + b1) + b2)
+             (EfficientNet block; reading R8).
+* OUTPUT  -- an output tap: the dense per-frame output is accumulated here
+             (Accumulation).
+
+Truncation sites: the network input (site 0) and then every
+RELU/SILU/MAXPOOL/SE layer in spec order.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+CONV, RELU, SILU, MAXPOOL, ADD, SE, OUTPUT = range(7)
+KIND_NAMES = {CONV: "conv", RELU: "relu", SILU: "silu", MAXPOOL: "maxpool",
+              ADD: "add", SE: "se", OUTPUT: "output"}
+NONLINEAR = (RELU, SILU, MAXPOOL, SE)
+
+
+def _out_dim(n, k, s, p):
+    # geometry of SPEC S:59: floor((h + 2p - k)/s) + 1
+    return (n + 2 * p - k) // s + 1
+
+
+class Net:
+    """Tiny topology builder.  Produces a list of layer dicts (no weights)."""
+
+    def __init__(self, in_c, in_h, in_w, name="net"):
+        self.in_c, self.in_h, self.in_w = in_c, in_h, in_w
+        self.name = name
+        self.layers: list[dict] = []
+
+    def _add(self, **kw):
+        base = dict(kind=None, src=-1, src2=-1, c_out=0, groups=1, k_h=1, k_w=1,
+                    s_h=1, s_w=1, p_h=0, p_w=0, se_hidden=0,
+                    w=None, b=None, w2=None, b2=None, act_gain=2.0)
+        base.update(kw)
+        self.layers.append(base)
+        return len(self.layers) - 1
+
+    def conv(self, src, c_out, k, s=1, p=None, groups=1, act_gain=2.0):
+        kh, kw = (k, k) if isinstance(k, int) else k
+        sh, sw = (s, s) if isinstance(s, int) else s
+        if p is None:
+            p = (kh // 2, kw // 2)
+        ph, pw = (p, p) if isinstance(p, int) else p
+        return self._add(kind=CONV, src=src, c_out=c_out, groups=groups, k_h=kh, k_w=kw,
+                         s_h=sh, s_w=sw, p_h=ph, p_w=pw, act_gain=act_gain)
+
+    def relu(self, src):
+        return self._add(kind=RELU, src=src)
+
+    def silu(self, src):
+        return self._add(kind=SILU, src=src)
+
+    def maxpool(self, src, k, s, p=0):
+        kh, kw = (k, k) if isinstance(k, int) else k
+        sh, sw = (s, s) if isinstance(s, int) else s
+        ph, pw = (p, p) if isinstance(p, int) else p
+        return self._add(kind=MAXPOOL, src=src, k_h=kh, k_w=kw, s_h=sh, s_w=sw, p_h=ph, p_w=pw)
+
+    def add(self, a, b):
+        return self._add(kind=ADD, src=a, src2=b)
+
+    def se(self, src, hidden):
+        return self._add(kind=SE, src=src, se_hidden=hidden)
+
+    def output(self, src):
+        return self._add(kind=OUTPUT, src=src)
+
+
+def infer_shapes(net: Net):
+    """(h, w, c) of every layer's output.  Plumbing for buffer allocation."""
+    shapes = []
+    for l in net.layers:
+        def sh(i):
+            return (net.in_h, net.in_w, net.in_c) if i < 0 else shapes[i]
+        h, w, c = sh(l["src"])
+        k = l["kind"]
+        if k == CONV:
+            shapes.append((_out_dim(h, l["k_h"], l["s_h"], l["p_h"]),
+                           _out_dim(w, l["k_w"], l["s_w"], l["p_w"]), l["c_out"]))
+        elif k == MAXPOOL:
+            shapes.append((_out_dim(h, l["k_h"], l["s_h"], l["p_h"]),
+                           _out_dim(w, l["k_w"], l["s_w"], l["p_w"]), c))
+        elif k == ADD:
+            assert sh(l["src2"]) == (h, w, c), "ADD operands differ in shape"
+            shapes.append((h, w, c))
+        else:
+            shapes.append((h, w, c))
+    return shapes
+
+
+def site_layers(net: Net):
+    """Layer index of every truncation site; entry 0 (-1) is the network input."""
+    return [-1] + [i for i, l in enumerate(net.layers) if l["kind"] in NONLINEAR]
+
+
+def init_weights(net: Net, seed: int):
+    """Seeded synthetic weights (trained weights are out of scope).
+
+    CONV: He-normal, std = sqrt(gain / fan_in), fan_in = (c_in/groups)*k_h*k_w,
+    so activations stay O(1) through ReLU/SiLU stacks (DESIGN.md input recipe);
+    bias ~ U(-0.1, 0.1) (BatchNorm folded).
+    SE: FC1 [hidden][C] std 1/sqrt(C), FC2 [C][hidden] std 1/sqrt(hidden),
+    biases small, so gates sit mid-range.
+    Returns the same Net with w/b filled (float32, C-contiguous).
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shapes = infer_shapes(net)
+    for i, l in enumerate(net.layers):
+        src_c = net.in_c if l["src"] < 0 else shapes[l["src"]][2]
+        if l["kind"] == CONV:
+            cin_g = src_c // l["groups"]
+            fan_in = cin_g * l["k_h"] * l["k_w"]
+            std = math.sqrt(l["act_gain"] / fan_in)
+            l["w"] = (rng.standard_normal((l["c_out"], cin_g, l["k_h"], l["k_w"])) * std).astype(np.float32)
+            l["b"] = rng.uniform(-0.1, 0.1, l["c_out"]).astype(np.float32)
+        elif l["kind"] == SE:
+            c, hd = src_c, l["se_hidden"]
+            l["w"] = (rng.standard_normal((hd, c)) / math.sqrt(c)).astype(np.float32)
+            l["b"] = rng.uniform(-0.1, 0.1, hd).astype(np.float32)
+            l["w2"] = (rng.standard_normal((c, hd)) / math.sqrt(hd)).astype(np.float32)
+            l["b2"] = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    return net
+
+
+# ----------------------------------------------------------------------------
+# The five BASELINE.json topologies
+# ----------------------------------------------------------------------------
+
+def toy_encoder(h=64, w=64):
+    """cfg1: 3x3 conv 3->16 + ReLU + 1x1 conv 16->8 (BASELINE.json configs[0])."""
+    n = Net(3, h, w, "toy")
+    c1 = n.conv(-1, 16, 3)
+    r1 = n.relu(c1)
+    c2 = n.conv(r1, 8, 1, act_gain=1.0)
+    n.output(c2)
+    return n
+
+
+def crnn_vgg7(h=32, w=128):
+    """cfg2: CRNN conv encoder, VGG-style, 7 convs (SURVEY reading R27).
+
+    Conv64-P2-Conv128-P2-Conv256-Conv256-P((2,2),(2,1),(0,1))-Conv512-Conv512-
+    P(same)-Conv512 2x2 valid; every conv followed by ReLU; output 512x1x33.
+    """
+    n = Net(1, h, w, "crnn_vgg7")
+    x = n.relu(n.conv(-1, 64, 3))
+    x = n.maxpool(x, 2, 2)
+    x = n.relu(n.conv(x, 128, 3))
+    x = n.maxpool(x, 2, 2)
+    x = n.relu(n.conv(x, 256, 3))
+    x = n.relu(n.conv(x, 256, 3))
+    x = n.maxpool(x, (2, 2), (2, 1), (0, 1))
+    x = n.relu(n.conv(x, 512, 3))
+    x = n.relu(n.conv(x, 512, 3))
+    x = n.maxpool(x, (2, 2), (2, 1), (0, 1))
+    x = n.relu(n.conv(x, 512, 2, 1, 0))
+    n.output(x)
+    return n
+
+
+def resnet18(h=720, w=1280):
+    """cfg4: torchvision ResNet-18 topology without avgpool/fc (reading R28)."""
+    n = Net(3, h, w, "resnet18")
+    x = n.relu(n.conv(-1, 64, 7, 2, 3))
+    x = n.maxpool(x, 3, 2, 1)
+    c = 64
+    for stage, (co, s) in enumerate([(64, 1), (128, 2), (256, 2), (512, 2)]):
+        for blk in range(2):
+            stride = s if blk == 0 else 1
+            y = n.relu(n.conv(x, co, 3, stride, 1))
+            y = n.conv(y, co, 3, 1, 1, act_gain=1.0)
+            if stride != 1 or c != co:
+                sc = n.conv(x, co, 1, stride, 0, act_gain=1.0)
+            else:
+                sc = x
+            x = n.relu(n.add(y, sc))
+            c = co
+    n.output(x)
+    return n
+
+
+def efficientnet_b0(h=512, w=512):
+    """cfg3/cfg5: EfficientNet-B0 backbone (EfficientDet-D0), taps P3/P4/P5.
+
+    MBConv: [1x1 expand -> SiLU] -> kxk depthwise -> SiLU -> SE -> 1x1 project
+    (+ residual when stride 1 and c_in == c_out).  Symmetric k//2 padding
+    (reading R11).  Taps = outputs of stages 3/5/7 (reading R13).
+    """
+    n = Net(3, h, w, "efficientnet_b0")
+    x = n.silu(n.conv(-1, 32, 3, 2, 1))
+    c = 32
+    stages = [  # expand, k, stride, c_out, repeats
+        (1, 3, 1, 16, 1), (6, 3, 2, 24, 2), (6, 5, 2, 40, 2), (6, 3, 2, 80, 3),
+        (6, 5, 1, 112, 3), (6, 5, 2, 192, 4), (6, 3, 1, 320, 1)]
+    for si, (e, k, s, co, rep) in enumerate(stages):
+        for r in range(rep):
+            stride = s if r == 0 else 1
+            inp = x
+            ce = c * e
+            y = x
+            if e != 1:
+                y = n.silu(n.conv(y, ce, 1, 1, 0))
+            y = n.silu(n.conv(y, ce, k, stride, k // 2, groups=ce))
+            y = n.se(y, max(1, c // 4))
+            y = n.conv(y, co, 1, 1, 0, act_gain=1.0)
+            if stride == 1 and c == co:
+                y = n.add(y, inp)
+            x = y
+            c = co
+        if si in (2, 4, 6):
+            n.output(x)
+    return n
