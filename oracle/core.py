@@ -44,7 +44,7 @@ def _load():
         lib.orc_num_sites.argtypes = [P, C.c_int]
         lib.orc_dense_forward.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P]
         lib.orc_run_chunk.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
-                                      C.c_int, P, P, P, P, P]
+                                      C.c_int, P, P, P, P, P, P, P]
         lib.orc_dilate.argtypes = [P] + [C.c_int] * 10 + [P]
         _lib = lib
     return _lib
@@ -118,6 +118,7 @@ def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_
       dense0[l] float32 [H_l][W_l][C_l]
       taps[l]   float32 [L][H_l][W_l][C_l] for OUTPUT layers
       counts    int64 [n_sites][L-1]
+      in_mask   uint8 [L-1][H][W]   input-site mask; in_delta float32 [L-1][H][W][C]
     """
     lib = _load()
     sp = _Spec(net)
@@ -144,11 +145,15 @@ def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_
             taps[i] = np.zeros((Lf,) + s, np.float32)
             tp[i] = taps[i].ctypes.data
     counts = np.zeros((ns, max(F, 1)), np.int64)
+    in_mask = np.zeros((max(F, 1), net.in_h, net.in_w), np.uint8)
+    in_delta = np.zeros((max(F, 1), net.in_h, net.in_w, net.in_c), np.float32) if want_deltas else None
     r = lib.orc_run_chunk(sp.ptr, n, net.in_h, net.in_w, net.in_c, Lf, fr.ctypes.data,
-                          th.ctypes.data, int(bool(layer_outer)), mp, dp, zp, tp, counts.ctypes.data)
+                          th.ctypes.data, int(bool(layer_outer)), mp, dp, zp, tp, counts.ctypes.data,
+                          in_mask.ctypes.data, None if in_delta is None else in_delta.ctypes.data)
     if r:
         raise ValueError(f"oracle run_chunk failed ({r})")
-    return dict(masks=masks, deltas=deltas, dense0=dense0, taps=taps, counts=counts[:, :F])
+    return dict(masks=masks, deltas=deltas, dense0=dense0, taps=taps, counts=counts[:, :F],
+                in_mask=in_mask[:F], in_delta=None if in_delta is None else in_delta[:F])
 
 
 def dilate(mask, k, s, p, out_hw):

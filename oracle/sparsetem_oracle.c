@@ -446,11 +446,14 @@ static void step_layer(ctx_t *c, int i, int t, const float *d_a, const uint8_t *
  *   dense0[l]  float [N_l][C_l]          frame-0 dense output of layer l
  *   taps[l]    float [L][N_l][C_l]       accumulated outputs of OUTPUT layers
  *   counts     int64 [n_sites][L-1]      emitted-pixel counts per site/frame
+ *   in_mask    uint8 [(L-1)][N_in]       input-site (Subtraction) mask
+ *   in_delta   float [(L-1)][N_in][C]    input-site emitted delta
  * thresholds: float [n_sites]; site 0 = input, then nonlinear layers in order.
  */
 int orc_run_chunk(const orc_layer *L, int n, int in_h, int in_w, int in_c, int Lf,
                   const float *frames, const float *thresholds, int layer_outer,
-                  uint8_t **masks, float **deltas, float **dense0, float **taps, int64_t *counts) {
+                  uint8_t **masks, float **deltas, float **dense0, float **taps, int64_t *counts,
+                  uint8_t *in_mask, float *in_delta) {
     if (Lf < 1 || in_c > 64) return -10;
     ctx_t c;
     memset(&c, 0, sizeof c);
@@ -510,6 +513,8 @@ int orc_run_chunk(const orc_layer *L, int n, int in_h, int in_w, int in_c, int L
             uint8_t *min = (uint8_t *)malloc((size_t)in_h * in_w);
             for (int t = 1; t < Lf; t++) {
                 step_input(&c, t, frames + (size_t)t * nin, din, min);
+                if (in_mask) memcpy(in_mask + (size_t)(t - 1) * in_h * in_w, min, (size_t)in_h * in_w);
+                if (in_delta) memcpy(in_delta + (size_t)(t - 1) * nin, din, nin * sizeof(float));
                 for (int i = 0; i < n; i++) {
                     const orc_layer *l = &L[i];
                     const float *da = l->src < 0 ? din : d[l->src];
@@ -537,6 +542,8 @@ int orc_run_chunk(const orc_layer *L, int n, int in_h, int in_w, int in_c, int L
             const size_t Nin = (size_t)in_h * in_w;
             for (int t = 1; t < Lf; t++)
                 step_input(&c, t, frames + (size_t)t * nin, Din + (size_t)(t - 1) * nin, Min + (size_t)(t - 1) * Nin);
+            if (in_mask) memcpy(in_mask, Min, (size_t)F * Nin);
+            if (in_delta) memcpy(in_delta, Din, (size_t)F * nin * sizeof(float));
             for (int i = 0; i < n; i++) {
                 const orc_layer *l = &L[i];
                 const size_t ne = numel(c.s[i]), No = (size_t)c.s[i].h * c.s[i].w;

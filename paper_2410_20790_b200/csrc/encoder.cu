@@ -1,0 +1,875 @@
+// encoder.cu -- host runtime of libsparsetem.so: validation, shape inference,
+// the SparseBatch cache-lifetime planner and arena, the
+// per-step executor (a1-a8) and the C ABI of include/sparsetem.h.
+//
+// SparseBatch: one pass per step.  Layers run in
+// topological order; for each layer the reference-frame dense op runs first,
+// then the layer's diff op over ALL diff frames of ALL chunks ("N" order).
+// A layer's dense reference output (x0 / y0) and its diff tensor live only
+// until their last consumer has run; the planner turns those lifetimes into
+// arena offsets (greedy first-fit by size over overlapping intervals), so
+// the per-layer caches of DeltaCNN never exist.  Only the staged
+// reference frames ("one buffer for Subtraction") and the output taps ("one
+// for Accumulation") persist across the step.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "sparsetem.h"
+
+using namespace st;
+
+namespace {
+
+constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
+              KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
+              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_N = 14;
+const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
+                              "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
+                              "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense"};
+
+struct Buf {
+    int64_t bytes = 0;
+    int first = 0, last = 0;   // live interval in step time (0 = input site, l+1 = layer l)
+    int64_t off = -1;
+};
+
+struct LayerRT {
+    st_layer_spec spec{};
+    int kind = 0, src = -1, src2 = -1;
+    int H = 0, W = 0, C = 0;   // output shape
+    int site = 0;
+    Geo geo{};
+    bool depthwise = false;
+    int n_consumers = 0, last_consumer = 0;
+    // device weights (separate allocation)
+    float *wk = nullptr, *bias = nullptr;
+    // buffer ids (-1 = none / alias)
+    int b_y0 = -1, b_act = -1, b_slot = -1, b_pbase = -1, b_rows = -1, b_ridx = -1, b_out = -1;
+    int alias_rows_of = -1;   // rows / slot / pbase borrowed from another tensor
+    int64_t rows_cap = 0;     // rows excluding the zero row
+};
+
+struct LaunchRec {
+    int cls, layer;
+    cudaEvent_t e0, e1;
+};
+
+}  // namespace
+
+struct st_encoder {
+    st_encoder_config cfg{};
+    std::vector<LayerRT> L;
+    int n_sites = 1;
+    int in_H = 0, in_W = 0, in_C = 0;
+    int B = 0, F = 0;   // max chunks, max diff frames
+    // input site tensor buffers
+    int in_act = -1, in_pbase = -1, in_rows = -1;
+    int64_t in_rows_cap = 0;
+    std::vector<Buf> bufs;
+    char *arena = nullptr;
+    int64_t arena_bytes = 0, persistent_bytes = 0, peak_transient = 0;
+    // small fixed device areas
+    char *smallmem = nullptr;
+    int32_t *totals = nullptr;   // [n_layers + 1] device row counts
+    long long *counts = nullptr; // [B][n_sites][32]
+    long long *stats = nullptr;  // [n_layers + 1][3] rows_in, rows_out, touched
+    long long *site_sum = nullptr; // [n_sites]
+    int32_t *scan_tmp = nullptr;
+    float *ref = nullptr;        // staged reference frames [B][N][C]
+    float *weights_mem = nullptr;
+    // state
+    int staged_chunks = 0;       // >0 after encode_reference
+    int last_chunks = 0, last_ndiff = -1;
+    cudaStream_t last_stream = nullptr;
+    std::string err;
+    // profiling
+    bool prof = false;
+    std::vector<LaunchRec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    int launches = 0;
+    double prof_ms[KC_N] = {0};
+    int64_t prof_n[KC_N] = {0};
+    double prof_bytes[KC_N] = {0}, prof_flops[KC_N] = {0};
+
+    char *ptr(int id) const { return id < 0 ? nullptr : arena + bufs[id].off; }
+    template <class T> T *p(int id) const { return reinterpret_cast<T *>(ptr(id)); }
+};
+
+static st_status fail(st_encoder *e, st_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (e) e->err = buf;
+    return s;
+}
+
+#define CUDA_OK(e, call)                                                                          \
+    do {                                                                                          \
+        cudaError_t _r = (call);                                                                  \
+        if (_r != cudaSuccess) return fail(e, ST_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(_r)); \
+    } while (0)
+
+static bool is_site(int k) { return k == ST_RELU || k == ST_SILU || k == ST_MAXPOOL || k == ST_SE; }
+static int out_dim(int n, int k, int s, int p) { return (n + 2 * p - k) / s + 1; }
+
+// ----------------------------------------------------------------- profiling
+static void prof_begin(st_encoder *e, int cls, int layer, cudaStream_t s) {
+    e->launches++;
+    if (!e->prof) return;
+    while (e->ev_used + 2 > e->ev_pool.size()) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        e->ev_pool.push_back(ev);
+    }
+    LaunchRec r{cls, layer, e->ev_pool[e->ev_used], e->ev_pool[e->ev_used + 1]};
+    e->ev_used += 2;
+    cudaEventRecord(r.e0, s);
+    e->recs.push_back(r);
+}
+static void prof_end(st_encoder *e, cudaStream_t s) {
+    if (!e->prof) return;
+    cudaEventRecord(e->recs.back().e1, s);
+}
+#define LAUNCH(e, cls, layer, s, stmt) \
+    do {                               \
+        prof_begin(e, cls, layer, s);  \
+        stmt;                          \
+        prof_end(e, s);                \
+    } while (0)
+
+// ------------------------------------------------------------------- create
+static st_status plan(st_encoder *e);
+
+extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_layer_spec *layers, int32_t n,
+                                       st_encoder **out) {
+    if (!cfg || !out || (n > 0 && !layers) || n < 1) return ST_ERR_ARG;
+    *out = nullptr;
+    std::unique_ptr<st_encoder> e(new st_encoder());
+    e->cfg = *cfg;
+    if (cfg->in_c < 1 || cfg->in_c > 4 || cfg->in_h < 1 || cfg->in_w < 1)
+        return ST_ERR_SHAPE;
+    if (cfg->max_chunks < 1 || cfg->max_frames < 1) return ST_ERR_SHAPE;
+    if (cfg->max_frames > 33) return ST_ERR_UNSUPPORTED;   // frame words hold L-1 <= 32 (R25)
+    if (cfg->precision != ST_FP32) return ST_ERR_UNSUPPORTED;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return ST_ERR_CUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) return ST_ERR_CUDA;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return ST_ERR_CUDA;
+    e->in_H = cfg->in_h;
+    e->in_W = cfg->in_w;
+    e->in_C = cfg->in_c;
+    e->B = cfg->max_chunks;
+    e->F = cfg->max_frames - 1;
+    e->L.resize(n);
+    // ---- validate + shapes
+    for (int i = 0; i < n; i++) {
+        LayerRT &l = e->L[i];
+        l.spec = layers[i];
+        l.kind = layers[i].kind;
+        l.src = layers[i].src;
+        l.src2 = layers[i].src2;
+        if (l.src < -1 || l.src >= i) return ST_ERR_ARG;
+        const int sh = l.src < 0 ? e->in_H : e->L[l.src].H, sw = l.src < 0 ? e->in_W : e->L[l.src].W,
+                  sc = l.src < 0 ? e->in_C : e->L[l.src].C;
+        switch (l.kind) {
+        case ST_CONV: {
+            const st_layer_spec &s = layers[i];
+            if (!s.w || !s.b || s.c_out < 1 || s.groups < 1 || s.k_h < 1 || s.k_w < 1 || s.s_h < 1 || s.s_w < 1 ||
+                s.p_h < 0 || s.p_w < 0)
+                return ST_ERR_ARG;
+            if (s.groups != 1 && !(s.groups == sc && s.c_out == sc)) return ST_ERR_UNSUPPORTED;
+            l.depthwise = s.groups != 1;
+            l.H = out_dim(sh, s.k_h, s.s_h, s.p_h);
+            l.W = out_dim(sw, s.k_w, s.s_w, s.p_w);
+            l.C = s.c_out;
+            if (s.k_h * s.k_w > 49) return ST_ERR_UNSUPPORTED;
+            break;
+        }
+        case ST_MAXPOOL: {
+            const st_layer_spec &s = layers[i];
+            if (s.k_h < 1 || s.k_w < 1 || s.s_h < 1 || s.s_w < 1 || s.p_h < 0 || s.p_w < 0) return ST_ERR_ARG;
+            if (s.k_h * s.k_w > 9) return ST_ERR_UNSUPPORTED;
+            l.H = out_dim(sh, s.k_h, s.s_h, s.p_h);
+            l.W = out_dim(sw, s.k_w, s.s_w, s.p_w);
+            l.C = sc;
+            break;
+        }
+        case ST_ADD: {
+            if (l.src2 < -1 || l.src2 >= i) return ST_ERR_ARG;
+            const int h2 = l.src2 < 0 ? e->in_H : e->L[l.src2].H, w2 = l.src2 < 0 ? e->in_W : e->L[l.src2].W,
+                      c2 = l.src2 < 0 ? e->in_C : e->L[l.src2].C;
+            if (h2 != sh || w2 != sw || c2 != sc) return ST_ERR_SHAPE;
+            l.H = sh; l.W = sw; l.C = sc;
+            break;
+        }
+        case ST_RELU: case ST_SILU: case ST_OUTPUT:
+            l.H = sh; l.W = sw; l.C = sc;
+            break;
+        case ST_SE:
+            return ST_ERR_UNSUPPORTED;
+        default:
+            return ST_ERR_ARG;
+        }
+        if (l.H < 1 || l.W < 1) return ST_ERR_SHAPE;
+        if (l.kind == ST_CONV || l.kind == ST_MAXPOOL) {
+            const st_layer_spec &s = layers[i];
+            l.geo = Geo{sh, sw, sc, l.H, l.W, l.C, s.k_h, s.k_w, s.s_h, s.s_w, s.p_h, s.p_w, s.groups};
+        }
+        if (is_site(l.kind)) l.site = e->n_sites++;
+        if (l.C > 1152) return ST_ERR_UNSUPPORTED;
+    }
+    // consumers
+    for (int i = 0; i < n; i++) {
+        LayerRT &l = e->L[i];
+        for (int s : {l.src, l.kind == ST_ADD ? l.src2 : -2}) {
+            if (s >= 0) {
+                e->L[s].n_consumers++;
+                e->L[s].last_consumer = std::max(e->L[s].last_consumer, i);
+            }
+        }
+    }
+    // ---- weights (K-major repack: wk[(dy*kw+dx)*cin_g + ci][co], reading R18)
+    int64_t wfloats = 0;
+    for (auto &l : e->L)
+        if (l.kind == ST_CONV) {
+            const int cin_g = l.geo.Cin / l.spec.groups;
+            wfloats += (int64_t)l.spec.k_h * l.spec.k_w * cin_g * l.C + l.C;
+        }
+    CUDA_OK(e.get(), cudaMalloc(&e->weights_mem, std::max<int64_t>(wfloats, 1) * sizeof(float)));
+    {
+        std::vector<float> host(std::max<int64_t>(wfloats, 1));
+        int64_t o = 0;
+        for (auto &l : e->L) {
+            if (l.kind != ST_CONV) continue;
+            const int kh = l.spec.k_h, kw = l.spec.k_w, cin_g = l.geo.Cin / l.spec.groups, co = l.C;
+            l.wk = e->weights_mem + o;
+            for (int dy = 0; dy < kh; dy++)
+                for (int dx = 0; dx < kw; dx++)
+                    for (int ci = 0; ci < cin_g; ci++)
+                        for (int c = 0; c < co; c++)
+                            host[o + ((int64_t)(dy * kw + dx) * cin_g + ci) * co + c] =
+                                l.spec.w[(((int64_t)c * cin_g + ci) * kh + dy) * kw + dx];
+            o += (int64_t)kh * kw * cin_g * co;
+            l.bias = e->weights_mem + o;
+            for (int c = 0; c < co; c++) host[o + c] = l.spec.b[c];
+            o += co;
+        }
+        CUDA_OK(e.get(), cudaMemcpy(e->weights_mem, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
+    st_status r = plan(e.get());
+    if (r != ST_OK) {
+        cudaFree(e->weights_mem);
+        return r;
+    }
+    *out = e.release();
+    return ST_OK;
+}
+
+// ------------------------------------------------------------------- planner
+static st_status plan(st_encoder *e) {
+    const int n = (int)e->L.size();
+    const int64_t B = e->B, F = e->F;
+    const int END = n + 1;   // step end
+    auto add = [&](int64_t bytes, int first, int last) {
+        Buf b;
+        b.bytes = (bytes + 255) / 256 * 256;
+        if (e->cfg.debug_retain) { first = 0; last = END; }
+        b.first = first;
+        b.last = last;
+        e->bufs.push_back(b);
+        return (int)e->bufs.size() - 1;
+    };
+    auto t_of = [](int layer) { return layer + 1; };   // step time of a layer
+    // input site: consumers of -1
+    int in_last = 0;
+    for (int i = 0; i < n; i++)
+        if (e->L[i].src == -1 || (e->L[i].kind == ST_ADD && e->L[i].src2 == -1)) in_last = std::max(in_last, t_of(i));
+    const int64_t Nin = (int64_t)e->in_H * e->in_W;
+    e->in_rows_cap = B * F * Nin;
+    e->in_act = add(B * Nin * 4, 0, in_last);
+    e->in_pbase = add(B * Nin * 4, 0, in_last);
+    e->in_rows = add((e->in_rows_cap + 1) * e->in_C * 4, 0, in_last);
+    // per-layer tensors
+    for (int i = 0; i < n; i++) {
+        LayerRT &l = e->L[i];
+        const int64_t N = (int64_t)l.H * l.W;
+        const int tdef = t_of(i);
+        const int tlast = std::max(tdef, l.n_consumers ? t_of(l.last_consumer) : tdef);
+        if (l.kind == ST_OUTPUT) {
+            // Accumulation buffer: persistent [B][L][N][C]
+            l.b_out = add(B * (F + 1) * N * l.C * 4, 0, END);
+            continue;
+        }
+        l.b_y0 = add(B * N * l.C * 4, tdef, tlast);
+        l.b_act = add(B * N * 4, tdef, tlast);
+        l.rows_cap = B * F * N;
+        switch (l.kind) {
+        case ST_CONV:
+            l.b_pbase = add(B * N * 4, tdef, tlast);
+            l.b_rows = add((l.rows_cap + 1) * l.C * 4, tdef, tlast);
+            l.b_ridx = add(std::max<int64_t>(l.rows_cap, 1) * 4, tdef, tdef);
+            break;
+        case ST_MAXPOOL: case ST_ADD:
+            l.b_slot = add(B * N * 4, tdef, tlast);
+            l.b_pbase = add(B * N * 4, tdef, tlast);
+            l.b_rows = add((l.rows_cap + 1) * l.C * 4, tdef, tlast);
+            break;
+        case ST_RELU: case ST_SILU: {
+            // emitted rows go into the input's slot layout; in place when
+            // this site is the input's only consumer (and not debugging)
+            const LayerRT *sl = l.src >= 0 ? &e->L[l.src] : nullptr;
+            const bool sole = sl ? sl->n_consumers == 1 : false;
+            if (sole && !e->cfg.debug_retain) {
+                l.alias_rows_of = l.src;
+            } else {
+                l.alias_rows_of = l.src;   // slot/pbase still borrowed
+                const int64_t cap = sl ? sl->rows_cap : e->in_rows_cap;
+                l.b_rows = add((cap + 1) * l.C * 4, tdef, tlast);
+            }
+            break;
+        }
+        default:
+            break;
+        }
+    }
+    // aliases extend the lifetime of the borrowed buffers
+    for (int i = 0; i < n; i++) {
+        LayerRT &l = e->L[i];
+        if (l.alias_rows_of < 0 && !(l.kind == ST_RELU || l.kind == ST_SILU)) continue;
+        const int tlast = std::max(t_of(i), l.n_consumers ? t_of(l.last_consumer) : t_of(i));
+        int s = l.src;
+        while (true) {   // walk to the tensor that owns slot/pbase (and maybe rows)
+            if (s < 0) {
+                for (int id : {e->in_act, e->in_pbase, e->in_rows}) e->bufs[id].last = std::max(e->bufs[id].last, tlast);
+                break;
+            }
+            LayerRT &o = e->L[s];
+            for (int id : {o.b_act, o.b_slot, o.b_pbase, o.b_rows})
+                if (id >= 0) e->bufs[id].last = std::max(e->bufs[id].last, tlast);
+            if (o.kind == ST_RELU || o.kind == ST_SILU) { s = o.src; continue; }
+            break;
+        }
+    }
+    // ---- first-fit arena assignment, largest first
+    std::vector<int> order(e->bufs.size());
+    for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return e->bufs[a].bytes > e->bufs[b].bytes; });
+    std::vector<int> placed;
+    int64_t total = 0;
+    for (int id : order) {
+        Buf &b = e->bufs[id];
+        std::vector<std::pair<int64_t, int64_t>> busy;
+        for (int pid : placed) {
+            const Buf &o = e->bufs[pid];
+            if (o.first <= b.last && b.first <= o.last) busy.push_back({o.off, o.off + o.bytes});
+        }
+        std::sort(busy.begin(), busy.end());
+        int64_t off = 0;
+        for (auto &iv : busy) {
+            if (off + b.bytes <= iv.first) break;
+            off = std::max(off, iv.second);
+        }
+        b.off = off;
+        total = std::max(total, off + b.bytes);
+        placed.push_back(id);
+    }
+    e->arena_bytes = total;
+    // memory report
+    int64_t persistent = 0;
+    for (auto &l : e->L)
+        if (l.b_out >= 0) persistent += e->bufs[l.b_out].bytes;
+    persistent += B * Nin * e->in_C * 4;   // staged reference (Subtraction buffer)
+    e->persistent_bytes = persistent;
+    int64_t peak = 0;
+    for (int t = 0; t <= END; t++) {
+        int64_t live = 0;
+        for (auto &b : e->bufs)
+            if (b.first <= t && t <= b.last && b.first != 0) live += b.bytes;
+        for (auto &b : e->bufs)
+            if (b.first == 0 && b.last != END && t <= b.last) live += b.bytes;
+        peak = std::max(peak, live);
+    }
+    e->peak_transient = peak;
+    // ---- allocations
+    if (cudaMalloc(&e->arena, std::max<int64_t>(total, 256)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(e, ST_ERR_OOM, "arena of %lld bytes failed", (long long)total);
+    }
+    int64_t max_words = B * Nin;
+    for (auto &l : e->L) max_words = std::max<int64_t>(max_words, B * l.H * l.W);
+    const int64_t small = (n + 1) * 4 + B * e->n_sites * 32 * 8 + (n + 1) * 3 * 8 + e->n_sites * 8 +
+                          scan_tmp_ints(max_words) * 4 + B * Nin * e->in_C * 4 + 1024;
+    CUDA_OK(e, cudaMalloc(&e->smallmem, small));
+    char *p = e->smallmem;
+    auto take = [&](int64_t bytes) { char *r = p; p += (bytes + 255) / 256 * 256; return r; };
+    e->totals = (int32_t *)take((n + 1) * 4);
+    e->counts = (long long *)take(B * e->n_sites * 32 * 8);
+    e->stats = (long long *)take((n + 1) * 3 * 8);
+    e->site_sum = (long long *)take(e->n_sites * 8);
+    e->scan_tmp = (int32_t *)take(scan_tmp_ints(max_words) * 4);
+    (void)take(0);
+    CUDA_OK(e, cudaMalloc(&e->ref, B * Nin * e->in_C * 4));
+    // zero rows (row 0 of every rows buffer) are written per step (arena reuse)
+    return ST_OK;
+}
+
+extern "C" void st_encoder_destroy(st_encoder *e) {
+    if (!e) return;
+    cudaFree(e->arena);
+    cudaFree(e->smallmem);
+    cudaFree(e->ref);
+    cudaFree(e->weights_mem);
+    for (auto ev : e->ev_pool) cudaEventDestroy(ev);
+    delete e;
+}
+
+extern "C" int32_t st_encoder_num_sites(const st_encoder *e) { return e ? e->n_sites : 0; }
+
+extern "C" st_status st_layer_shape(const st_encoder *e, int32_t layer, int32_t hwc[3]) {
+    if (!e || !hwc || layer < -1 || layer >= (int)e->L.size()) return ST_ERR_ARG;
+    if (layer < 0) { hwc[0] = e->in_H; hwc[1] = e->in_W; hwc[2] = e->in_C; }
+    else { hwc[0] = e->L[layer].H; hwc[1] = e->L[layer].W; hwc[2] = e->L[layer].C; }
+    return ST_OK;
+}
+
+// ------------------------------------------------------------ encode calls
+extern "C" st_status st_encode_reference(st_encoder *e, const float *ref_dev, int32_t n_chunks, int64_t chunk_stride,
+                                         void *stream) {
+    if (!e) return ST_ERR_ARG;
+    if (!ref_dev) return fail(e, ST_ERR_ARG, "ref_dev is null");
+    if (n_chunks < 1 || n_chunks > e->B) return fail(e, ST_ERR_SHAPE, "n_chunks %d outside [1, %d]", n_chunks, e->B);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t per = (int64_t)e->in_H * e->in_W * e->in_C;
+    const int64_t stride = chunk_stride ? chunk_stride : per;
+    if (stride < per) return fail(e, ST_ERR_ARG, "chunk_stride smaller than a frame");
+    CUDA_OK(e, cudaSetDevice(e->cfg.device));
+    CUDA_OK(e, cudaMemcpy2DAsync(e->ref, per * 4, ref_dev, stride * 4, per * 4, n_chunks, cudaMemcpyDeviceToDevice, s));
+    e->staged_chunks = n_chunks;
+    return ST_OK;
+}
+
+static DView view_of(const st_encoder *e, int t) {
+    DView v;
+    if (t < 0) {
+        v.act = e->p<uint32_t>(e->in_act);
+        v.slot = v.act;
+        v.pbase = e->p<int32_t>(e->in_pbase);
+        v.rows = e->p<float>(e->in_rows);
+        return v;
+    }
+    const LayerRT &l = e->L[t];
+    if (l.kind == ST_OUTPUT) return view_of(e, l.src);
+    v.act = e->p<uint32_t>(l.b_act);
+    if (l.kind == ST_RELU || l.kind == ST_SILU) {
+        DView s = view_of(e, l.src);
+        v.slot = s.slot;
+        v.pbase = s.pbase;
+        v.rows = l.b_rows >= 0 ? e->p<float>(l.b_rows) : s.rows;
+        return v;
+    }
+    v.slot = l.b_slot >= 0 ? e->p<uint32_t>(l.b_slot) : v.act;
+    v.pbase = e->p<int32_t>(l.b_pbase);
+    v.rows = e->p<float>(l.b_rows);
+    return v;
+}
+
+static const float *dense_of(const st_encoder *e, int t) {
+    if (t < 0) return e->ref;
+    const LayerRT &l = e->L[t];
+    if (l.kind == ST_OUTPUT) return dense_of(e, l.src);
+    return e->p<float>(l.b_y0);
+}
+
+static int64_t rows_cap_of(const st_encoder *e, int t) {
+    if (t < 0) return e->in_rows_cap;
+    const LayerRT &l = e->L[t];
+    if (l.kind == ST_RELU || l.kind == ST_SILU || l.kind == ST_OUTPUT) return rows_cap_of(e, l.src);
+    return l.rows_cap;
+}
+
+extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int32_t n_diff, int64_t chunk_stride,
+                                    const float *thresholds, void *stream) {
+    if (!e) return ST_ERR_ARG;
+    if (!thresholds) return fail(e, ST_ERR_ARG, "thresholds is null");
+    if (n_diff < 0 || n_diff > e->F) return fail(e, ST_ERR_SHAPE, "n_diff %d outside [0, %d]", n_diff, e->F);
+    if (n_diff > 0 && !frames_dev) return fail(e, ST_ERR_ARG, "frames_dev is null");
+    if (e->staged_chunks <= 0) return fail(e, ST_ERR_STATE, "st_encode_diff without st_encode_reference");
+    for (int i = 0; i < e->n_sites; i++)
+        if (!(thresholds[i] >= 0.0f)) return fail(e, ST_ERR_ARG, "threshold %d is negative or NaN", i);
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_OK(e, cudaSetDevice(e->cfg.device));
+    const int B = e->staged_chunks, F = n_diff, n = (int)e->L.size();
+    const int64_t Nin = (int64_t)e->in_H * e->in_W;
+    const int64_t per = Nin * e->in_C;
+    const int64_t fstride = chunk_stride ? chunk_stride : (int64_t)F * per;
+    e->launches = 0;
+    e->last_chunks = B;
+    e->last_ndiff = F;
+    e->last_stream = s;
+    if (e->prof) { e->recs.clear(); e->ev_used = 0; }
+    CUDA_OK(e, cudaMemsetAsync(e->counts, 0, (size_t)e->B * e->n_sites * 32 * 8, s));
+    CUDA_OK(e, cudaMemsetAsync(e->stats, 0, (size_t)(n + 1) * 3 * 8, s));
+    CUDA_OK(e, cudaMemsetAsync(e->site_sum, 0, (size_t)e->n_sites * 8, s));
+    const int64_t cstride = (int64_t)e->n_sites * 32;
+    auto zero_row = [&](int buf, int C) {
+        if (buf >= 0) cudaMemsetAsync(e->ptr(buf), 0, (size_t)C * 4, s);
+    };
+
+    // ---------------- input site: Subtraction + truncation + compaction (a2)
+    if (F > 0) {
+        uint32_t *act = e->p<uint32_t>(e->in_act);
+        int32_t *pb = e->p<int32_t>(e->in_pbase);
+        float *rows = e->p<float>(e->in_rows);
+        const float *fr = frames_dev;
+        LAUNCH(e, KC_SUBTRACT, -1, s,
+               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds[0], act, s));
+        LAUNCH(e, KC_SCAN, -1, s,
+               launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
+        zero_row(e->in_rows, e->in_C);
+        LAUNCH(e, KC_SUBTRACT, -1, s,
+               launch_subtract_rows(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, act, pb, rows, s));
+        LAUNCH(e, KC_COUNTS, -1, s,
+               launch_frame_counts(act, B, (int)Nin, e->counts, cstride, e->site_sum, nullptr, s));
+    }
+
+    // ---------------- layers in topological order, dense then diff ("N")
+    for (int i = 0; i < n; i++) {
+        LayerRT &l = e->L[i];
+        const int64_t N = (int64_t)l.H * l.W;
+        const int64_t Ns = l.src < 0 ? Nin : (int64_t)e->L[l.src].H * e->L[l.src].W;
+        const int Cs = l.src < 0 ? e->in_C : e->L[l.src].C;
+        const float *x_src = dense_of(e, l.src);
+        long long *st = e->stats + 3 * i;
+        DView in = F > 0 ? view_of(e, l.src) : DView{};
+        if (F > 0 && l.kind != ST_OUTPUT)   // rows_in / touched of this layer
+            LAUNCH(e, KC_COUNTS, i, s, launch_frame_counts(in.act, B, (int)Ns, nullptr, 0, st, st + 2, s));
+        switch (l.kind) {
+        case ST_CONV: {
+            ConvCall c{};
+            c.g = l.geo;
+            c.B = B;
+            c.dense = true;
+            c.a_dense = x_src;
+            c.wk = l.wk;
+            c.bias = l.bias;
+            c.out = e->p<float>(l.b_y0);
+            LAUNCH(e, l.depthwise ? KC_DW_DENSE : KC_CONV_DENSE, i, s,
+                   l.depthwise ? launch_dwconv_f32(c, s) : launch_conv_f32(c, s));
+            if (F == 0) break;
+            uint32_t *act = e->p<uint32_t>(l.b_act);
+            int32_t *pb = e->p<int32_t>(l.b_pbase);
+            LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, act, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(act, B * N, pb, e->totals + i, e->scan_tmp, st + 1, s));
+            LAUNCH(e, KC_ENUM, i, s, launch_enumerate(act, pb, B * N, e->p<int32_t>(l.b_ridx), s));
+            zero_row(l.b_rows, l.C);
+            c.dense = false;
+            c.a = in;
+            c.ridx = e->p<int32_t>(l.b_ridx);
+            c.m_dev = e->totals + i;
+            c.m_cap = (int64_t)B * F * N;
+            c.out = e->p<float>(l.b_rows);
+            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : KC_CONV_SPARSE, i, s,
+                   l.depthwise ? launch_dwconv_f32(c, s) : launch_conv_f32(c, s));
+            break;
+        }
+        case ST_RELU: case ST_SILU: {
+            const int act_kind = l.kind == ST_RELU ? ACT_RELU : ACT_SILU;
+            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, act_kind, s));
+            if (F == 0) break;
+            DView me = view_of(e, i);
+            LAUNCH(e, KC_SITE_PW, i, s,
+                   launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds[l.site],
+                                         e->p<uint32_t>(l.b_act), const_cast<float *>(me.rows), s));
+            LAUNCH(e, KC_COUNTS, i, s,
+                   launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
+                                       e->site_sum + l.site, nullptr, s));
+            break;
+        }
+        case ST_MAXPOOL: {
+            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_maxpool(x_src, e->p<float>(l.b_y0), B, l.geo, s));
+            if (F == 0) break;
+            uint32_t *slot = e->p<uint32_t>(l.b_slot);
+            int32_t *pb = e->p<int32_t>(l.b_pbase);
+            LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, slot, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            LAUNCH(e, KC_SITE_MP, i, s,
+                   launch_site_maxpool(in, x_src, B, l.geo, thresholds[l.site], slot, pb, e->p<uint32_t>(l.b_act),
+                                       e->p<float>(l.b_rows), s));
+            LAUNCH(e, KC_COUNTS, i, s,
+                   launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
+                                       e->site_sum + l.site, nullptr, s));
+            break;
+        }
+        case ST_ADD: {
+            const float *x2 = dense_of(e, l.src2);
+            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, s));
+            if (F == 0) break;
+            DView in2 = view_of(e, l.src2);
+            uint32_t *slot = e->p<uint32_t>(l.b_slot);
+            int32_t *pb = e->p<int32_t>(l.b_pbase);
+            LAUNCH(e, KC_ADD, i, s, launch_or_words(in.act, in2.act, B * N, slot, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            zero_row(l.b_rows, l.C);
+            LAUNCH(e, KC_ADD, i, s, launch_add_rows(in, in2, slot, pb, B, (int)N, l.C, e->p<float>(l.b_rows), s));
+            CUDA_OK(e, cudaMemcpyAsync(e->p<uint32_t>(l.b_act), slot, (size_t)B * N * 4, cudaMemcpyDeviceToDevice, s));
+            break;
+        }
+        case ST_OUTPUT: {
+            DView v = F > 0 ? in : DView{};
+            LAUNCH(e, KC_ACCUM, i, s,
+                   launch_accumulate(v, x_src, B, (int)N, l.C, F, e->p<float>(l.b_out), s));
+            break;
+        }
+        default:
+            return fail(e, ST_ERR_INTERNAL, "layer kind %d not executable", l.kind);
+        }
+        (void)Cs;
+    }
+    CUDA_OK(e, cudaGetLastError());
+    return ST_OK;
+}
+
+// ------------------------------------------------------------- statistics
+extern "C" st_status st_get_sparsity(st_encoder *e, int64_t *active, int64_t *site_active, int64_t *site_pixels) {
+    if (!e) return ST_ERR_ARG;
+    if (e->last_ndiff < 0) return fail(e, ST_ERR_STATE, "no encode_diff yet");
+    CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    const int B = e->last_chunks, F = e->last_ndiff, S = e->n_sites;
+    if (active) {
+        std::vector<long long> h((size_t)e->B * S * 32);
+        CUDA_OK(e, cudaMemcpy(h.data(), e->counts, h.size() * 8, cudaMemcpyDeviceToHost));
+        for (int b = 0; b < B; b++)
+            for (int si = 0; si < S; si++)
+                for (int t = 0; t < F; t++) active[((int64_t)b * S + si) * F + t] = h[((size_t)b * S + si) * 32 + t];
+    }
+    if (site_active) {
+        std::vector<long long> h(S);
+        CUDA_OK(e, cudaMemcpy(h.data(), e->site_sum, S * 8, cudaMemcpyDeviceToHost));
+        for (int si = 0; si < S; si++) site_active[si] = h[si];
+    }
+    if (site_pixels) {
+        site_pixels[0] = (int64_t)B * F * e->in_H * e->in_W;
+        for (auto &l : e->L)
+            if (l.site) site_pixels[l.site] = (int64_t)B * F * l.H * l.W;
+    }
+    return ST_OK;
+}
+
+extern "C" st_status st_copy_site_counts(st_encoder *e, int64_t *dst_dev, void *stream) {
+    if (!e || !dst_dev) return ST_ERR_ARG;
+    if (e->last_ndiff < 0) return fail(e, ST_ERR_STATE, "no encode_diff yet");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int S = e->n_sites;
+    CUDA_OK(e, cudaMemcpyAsync(dst_dev, e->site_sum, S * 8, cudaMemcpyDeviceToDevice, s));
+    std::vector<long long> pix(S);
+    pix[0] = (long long)e->last_chunks * e->last_ndiff * e->in_H * e->in_W;
+    for (auto &l : e->L)
+        if (l.site) pix[l.site] = (long long)e->last_chunks * e->last_ndiff * l.H * l.W;
+    // pixel counts are host-known constants: small H2D copy (pageable -> staged by the driver)
+    CUDA_OK(e, cudaMemcpyAsync(dst_dev + S, pix.data(), S * 8, cudaMemcpyHostToDevice, s));
+    CUDA_OK(e, cudaStreamSynchronize(s));
+    return ST_OK;
+}
+
+extern "C" st_status st_get_layer_counts(st_encoder *e, int64_t *rows_in, int64_t *rows_out, int64_t *touched) {
+    if (!e) return ST_ERR_ARG;
+    if (e->last_ndiff < 0) return fail(e, ST_ERR_STATE, "no encode_diff yet");
+    CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    const int n = (int)e->L.size();
+    std::vector<long long> h((size_t)(n + 1) * 3);
+    CUDA_OK(e, cudaMemcpy(h.data(), e->stats, h.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> tot(n + 1);
+    CUDA_OK(e, cudaMemcpy(tot.data(), e->totals, tot.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<long long> ss(e->n_sites);
+    CUDA_OK(e, cudaMemcpy(ss.data(), e->site_sum, ss.size() * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; i++) {
+        const LayerRT &l = e->L[i];
+        int64_t out = 0;
+        if (l.kind == ST_CONV) out = tot[i];
+        else if (is_site(l.kind)) out = ss[l.site];
+        else if (l.kind == ST_ADD) out = tot[i];
+        if (rows_in) rows_in[i] = h[3 * i];
+        if (rows_out) rows_out[i] = out;
+        if (touched) touched[i] = h[3 * i + 2];
+    }
+    return ST_OK;
+}
+
+extern "C" st_status st_get_output(st_encoder *e, int32_t tap, int32_t chunk, int32_t frame, const float **dev_ptr,
+                                   int32_t hwc[3]) {
+    if (!e || !dev_ptr) return ST_ERR_ARG;
+    if (tap < 0 || tap >= (int)e->L.size() || e->L[tap].kind != ST_OUTPUT)
+        return fail(e, ST_ERR_ARG, "layer %d is not an OUTPUT tap", tap);
+    if (e->last_ndiff < 0) return fail(e, ST_ERR_STATE, "no encode yet");
+    if (chunk < 0 || chunk >= e->last_chunks || frame < 0 || frame > e->last_ndiff)
+        return fail(e, ST_ERR_ARG, "chunk/frame out of range");
+    const LayerRT &l = e->L[tap];
+    const int64_t fs = (int64_t)l.H * l.W * l.C;
+    *dev_ptr = e->p<float>(l.b_out) + ((int64_t)chunk * (e->last_ndiff + 1) + frame) * fs;
+    if (hwc) { hwc[0] = l.H; hwc[1] = l.W; hwc[2] = l.C; }
+    return ST_OK;
+}
+
+// ------------------------------------------------------------------ debug
+static st_status debug_words(st_encoder *e, int layer, int chunk, int frame, std::vector<uint32_t> &act,
+                             std::vector<uint32_t> &slot, std::vector<int32_t> &pbase, int &H, int &W, int &C,
+                             DView &v) {
+    if (!e->cfg.debug_retain) return fail(e, ST_ERR_STATE, "debug getters need debug_retain");
+    if (e->last_ndiff < 1) return fail(e, ST_ERR_STATE, "no diff frames encoded");
+    if (layer < -1 || layer >= (int)e->L.size()) return fail(e, ST_ERR_ARG, "bad layer");
+    if (chunk < 0 || chunk >= e->last_chunks || frame < 1 || frame > e->last_ndiff)
+        return fail(e, ST_ERR_ARG, "chunk/frame out of range");
+    CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    if (layer < 0) { H = e->in_H; W = e->in_W; C = e->in_C; }
+    else { H = e->L[layer].H; W = e->L[layer].W; C = e->L[layer].C; }
+    v = view_of(e, layer);
+    const int64_t N = (int64_t)H * W;
+    act.resize(N); slot.resize(N); pbase.resize(N);
+    CUDA_OK(e, cudaMemcpy(act.data(), v.act + chunk * N, N * 4, cudaMemcpyDeviceToHost));
+    CUDA_OK(e, cudaMemcpy(slot.data(), v.slot + chunk * N, N * 4, cudaMemcpyDeviceToHost));
+    CUDA_OK(e, cudaMemcpy(pbase.data(), v.pbase + chunk * N, N * 4, cudaMemcpyDeviceToHost));
+    return ST_OK;
+}
+
+extern "C" st_status st_debug_get_mask(st_encoder *e, int32_t layer, int32_t chunk, int32_t frame, uint32_t *words) {
+    if (!e || !words) return ST_ERR_ARG;
+    std::vector<uint32_t> act, slot;
+    std::vector<int32_t> pb;
+    int H, W, C;
+    DView v;
+    st_status r = debug_words(e, layer, chunk, frame, act, slot, pb, H, W, C, v);
+    if (r) return r;
+    const int64_t N = (int64_t)H * W;
+    for (int64_t j = 0; j < (N + 31) / 32; j++) words[j] = 0;
+    for (int64_t p = 0; p < N; p++)
+        if ((act[p] >> (frame - 1)) & 1u) words[p / 32] |= 1u << (p % 32);
+    return ST_OK;
+}
+
+extern "C" st_status st_debug_get_rows(st_encoder *e, int32_t layer, int32_t chunk, int32_t frame, int32_t *idx,
+                                       float *rows, int64_t *n_out) {
+    if (!e) return ST_ERR_ARG;
+    std::vector<uint32_t> act, slot;
+    std::vector<int32_t> pb;
+    int H, W, C;
+    DView v;
+    st_status r = debug_words(e, layer, chunk, frame, act, slot, pb, H, W, C, v);
+    if (r) return r;
+    const int64_t N = (int64_t)H * W;
+    const int t1 = frame - 1;
+    int64_t k = 0;
+    for (int64_t p = 0; p < N; p++) {
+        if (!((act[p] >> t1) & 1u)) continue;
+        if (idx) idx[k] = (int32_t)p;
+        if (rows) {
+            const int64_t row = 1 + pb[p] + __builtin_popcount(slot[p] & ((1u << t1) - 1u));
+            CUDA_OK(e, cudaMemcpy(rows + k * C, v.rows + row * C, C * 4, cudaMemcpyDeviceToHost));
+        }
+        k++;
+    }
+    if (n_out) *n_out = k;
+    return ST_OK;
+}
+
+extern "C" st_status st_debug_get_dense0(st_encoder *e, int32_t layer, int32_t chunk, float *host) {
+    if (!e || !host) return ST_ERR_ARG;
+    if (!e->cfg.debug_retain) return fail(e, ST_ERR_STATE, "debug getters need debug_retain");
+    if (layer < 0 || layer >= (int)e->L.size() || chunk < 0 || chunk >= e->last_chunks)
+        return fail(e, ST_ERR_ARG, "bad layer/chunk");
+    CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    const LayerRT &l = e->L[layer];
+    const int64_t ne = (int64_t)l.H * l.W * l.C;
+    CUDA_OK(e, cudaMemcpy(host, dense_of(e, layer) + chunk * ne, ne * 4, cudaMemcpyDeviceToHost));
+    return ST_OK;
+}
+
+extern "C" st_status st_memory_report(const st_encoder *e, int64_t *persistent, int64_t *peak, int64_t *arena) {
+    if (!e) return ST_ERR_ARG;
+    if (persistent) *persistent = e->persistent_bytes;
+    if (peak) *peak = e->peak_transient;
+    if (arena) *arena = e->arena_bytes;
+    return ST_OK;
+}
+
+// ---------------------------------------------------------------- profiling
+extern "C" st_status st_set_profiling(st_encoder *e, int32_t on) {
+    if (!e) return ST_ERR_ARG;
+    e->prof = on != 0;
+    e->recs.clear();
+    e->ev_used = 0;
+    return ST_OK;
+}
+extern "C" int32_t st_num_kernel_classes(void) { return KC_N; }
+extern "C" const char *st_kernel_class_name(int32_t i) { return i >= 0 && i < KC_N ? KC_NAMES[i] : ""; }
+
+extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *launches, double *bytes, double *flops,
+                                         int32_t reset) {
+    if (!e) return ST_ERR_ARG;
+    if (e->last_stream || e->last_ndiff >= 0) CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    // fold pending records of the last encode call
+    if (!e->recs.empty()) {
+        std::vector<int64_t> rin(e->L.size()), rout(e->L.size()), tch(e->L.size());
+        if (e->last_ndiff > 0) st_get_layer_counts(e, rin.data(), rout.data(), tch.data());
+        for (auto &r : e->recs) {
+            float t = 0;
+            cudaEventElapsedTime(&t, r.e0, r.e1);
+            e->prof_ms[r.cls] += t;
+            e->prof_n[r.cls] += 1;
+            if (r.layer >= 0 && (r.cls == KC_CONV_SPARSE || r.cls == KC_CONV_DENSE || r.cls == KC_DW_SPARSE ||
+                                 r.cls == KC_DW_DENSE)) {
+                const LayerRT &l = e->L[r.layer];
+                const int64_t K = (int64_t)l.geo.kh * l.geo.kw * (l.geo.Cin / l.geo.groups);
+                const int64_t M = (r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE)
+                                      ? rout[r.layer]
+                                      : (int64_t)e->last_chunks * l.H * l.W;
+                const int64_t Min = (r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE)
+                                        ? rin[r.layer]
+                                        : (int64_t)e->last_chunks * l.geo.Hin * l.geo.Win;
+                e->prof_flops[r.cls] += 2.0 * K * l.C * M;
+                // algorithmic bytes: each active input row once, each output row once, weights once
+                e->prof_bytes[r.cls] += 4.0 * ((double)Min * l.geo.Cin + (double)M * l.C + (double)K * l.C) +
+                                        ((r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE) ? 4.0 * M : 0.0);
+            }
+        }
+        e->recs.clear();
+        e->ev_used = 0;
+    }
+    for (int i = 0; i < KC_N; i++) {
+        if (ms) ms[i] = e->prof_ms[i];
+        if (launches) launches[i] = e->prof_n[i];
+        if (bytes) bytes[i] = e->prof_bytes[i];
+        if (flops) flops[i] = e->prof_flops[i];
+    }
+    if (reset)
+        for (int i = 0; i < KC_N; i++) { e->prof_ms[i] = 0; e->prof_n[i] = 0; e->prof_bytes[i] = 0; e->prof_flops[i] = 0; }
+    return ST_OK;
+}
+
+extern "C" int32_t st_last_launch_count(const st_encoder *e) { return e ? e->launches : 0; }
+
+extern "C" const char *st_status_string(st_status s) {
+    switch (s) {
+    case ST_OK: return "ok";
+    case ST_ERR_ARG: return "invalid argument";
+    case ST_ERR_SHAPE: return "shape mismatch";
+    case ST_ERR_STATE: return "call out of order";
+    case ST_ERR_UNSUPPORTED: return "unsupported";
+    case ST_ERR_OOM: return "out of device memory";
+    case ST_ERR_CUDA: return "CUDA error";
+    case ST_ERR_INTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+
+extern "C" const char *st_last_error(const st_encoder *e) { return e ? e->err.c_str() : ""; }

@@ -1,0 +1,92 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (internal, not ABI).
+//
+// Data layout of a diff tensor (one layer boundary, all chunks of a step;
+// DESIGN.md "Data layout in HBM"):
+//   act  [B][N] uint32   bit (t-1) set <=> pixel active in diff frame t
+//                        (pixel-major "frame words", so L-1 <= 32, R25)
+//   slot [B][N] uint32   frame bits that own a row (superset of act)
+//   pbase[B][N] int32    exclusive prefix over (b,p) of popc(slot)
+//   rows [1+cap][C] f32  packed delta rows in (b, p, t) order; row 0 = zeros
+// Row of (b,p,t) = 1 + pbase[b,p] + popc(slot[b,p] & ((1<<(t-1))-1)) when the
+// act bit is set, else row 0.  Consumers never read rows of inactive bits.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace st {
+
+struct DView {
+    const uint32_t *act = nullptr;
+    const uint32_t *slot = nullptr;
+    const int32_t *pbase = nullptr;
+    const float *rows = nullptr;
+};
+
+struct Geo {   // conv / pool geometry
+    int Hin, Win, Cin, Hout, Wout, Cout, kh, kw, sh, sw, ph, pw, groups;
+};
+
+// ---- masks, compaction (kernels_mask.cu) ----
+// Subtraction pass 1 (site 0): act bits per pixel, sequential over frames.
+void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
+                          int B, int N, int C, int n_diff, float theta, uint32_t *act, cudaStream_t s);
+// Subtraction pass 2: write emitted rows at the slots of `act`.
+void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
+                          int B, int N, int C, const uint32_t *act, const int32_t *pbase, float *rows,
+                          cudaStream_t s);
+// out[b][q] = OR of in[b][p] over the receptive field (dense amplification)
+void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaStream_t s);
+// pbase = exclusive prefix of popc(words) over n words; *total = sum; also
+// adds the total into *stat (int64) if stat != nullptr.  tmp: scan scratch
+// (scan_tmp_ints(n) int32).
+int64_t scan_tmp_ints(int64_t n);
+void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp,
+                      long long *stat, cudaStream_t s);
+// ridx[pbase+j] = ((b*N+q) << 5) | t1 for every set bit of slot (conv M rows)
+void launch_enumerate(const uint32_t *slot, const int32_t *pbase, int64_t n, int32_t *ridx, cudaStream_t s);
+// per (b, t1) popcounts of act into counts[b*cstride + t1] (int64 atomics,
+// counts may be null); sum of popc into *stat, number of non-zero words into
+// *stat_nz (either may be null).
+void launch_frame_counts(const uint32_t *act, int B, int N, long long *counts, int64_t cstride,
+                         long long *stat, long long *stat_nz, cudaStream_t s);
+void launch_or_words(const uint32_t *a, const uint32_t *b, int64_t n, uint32_t *out, cudaStream_t s);
+
+// ---- convolution (kernels_conv.cu) ----
+struct ConvCall {
+    Geo g;
+    int B;
+    bool dense;             // reference-frame mode
+    // A operand
+    const float *a_dense;   // dense: [B][Nin][Cin]
+    DView a;                // sparse
+    const int32_t *ridx;    // sparse: M-row list
+    const int32_t *m_dev;   // sparse: device M
+    int64_t m_cap;          // sparse: upper bound of M (grid sizing)
+    // B operand / output
+    const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
+    const float *bias;      // dense only
+    float *out;             // dense: [B*Nout][Cout]; sparse: rows_out (row 1+r)
+};
+void launch_conv_f32(const ConvCall &c, cudaStream_t s);
+void launch_dwconv_f32(const ConvCall &c, cudaStream_t s);
+
+// ---- sites, joins, accumulation (kernels_site.cu) ----
+enum Act { ACT_RELU = 0, ACT_SILU = 1 };
+void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t s);
+void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s);
+void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s);
+// pointwise site: emitted rows written into out_rows at the input slots
+void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta,
+                           uint32_t *out_act, float *out_rows, cudaStream_t s);
+// maxpool site: touched layout (t_slot, t_pbase) = dilation of in.act
+void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta,
+                         const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act,
+                         float *out_rows, cudaStream_t s);
+// residual add: out slot layout = act_a | act_b (already scanned into pbase)
+void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C,
+                     float *out_rows, cudaStream_t s);
+// Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0)
+void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, float *out,
+                       cudaStream_t s);
+
+}  // namespace st

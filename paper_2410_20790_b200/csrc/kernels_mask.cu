@@ -1,0 +1,291 @@
+// kernels_mask.cu -- Subtraction, truncation, mask dilation and ordered
+// compaction on sm_100a.
+//
+// Subtraction + pixel-granular truncation
+// (readings R1-R3): per pixel, sequential over diff frames with the
+// Subtraction buffer S in registers, raw = X_t - S, active iff
+// max_c |raw| > theta_0, S += raw when active.  Masks are pixel-major frame
+// words (one uint32 per pixel, bit t-1 = frame t) so a warp reads 32
+// consecutive pixels' words with one coalesced 128-byte load and a pixel's
+// frames are one register.  Compaction is an ordered exclusive scan of
+// popc(word) -- deterministic, no atomics on the data path.
+#include "common.cuh"
+
+namespace st {
+
+// ------------------------------------------------------------ subtraction
+template <int C>
+__global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__ ref, int64_t ref_stride,
+                                                       const float *__restrict__ fr, int64_t fr_stride, int B,
+                                                       int N, int n_diff, float theta, uint32_t *__restrict__ act) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)B * N) return;
+    const int b = (int)(i / N), p = (int)(i % N);
+    const float *r = ref + b * ref_stride + (int64_t)p * C;
+    float S[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) S[c] = __ldg(r + c);
+    const float *f = fr + b * fr_stride + (int64_t)p * C;
+    const int64_t fs = (int64_t)N * C;
+    uint32_t w = 0;
+#pragma unroll 4
+    for (int t1 = 0; t1 < n_diff; ++t1) {
+        float raw[C];
+        float mx = 0.0f;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            raw[c] = __fsub_rn(__ldg(f + t1 * fs + c), S[c]);
+            mx = fmaxf(mx, fabsf(raw[c]));
+        }
+        if (mx > theta) {                       // R1: strict comparison
+#pragma unroll
+            for (int c = 0; c < C; c++) S[c] = __fadd_rn(S[c], raw[c]);   // R3
+            w |= 1u << t1;
+        }
+    }
+    act[i] = w;
+}
+
+template <int C>
+__global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__ ref, int64_t ref_stride,
+                                                       const float *__restrict__ fr, int64_t fr_stride, int B,
+                                                       int N, const uint32_t *__restrict__ act,
+                                                       const int32_t *__restrict__ pbase, float *__restrict__ rows) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)B * N) return;
+    uint32_t w = act[i];
+    if (!w) return;
+    const int b = (int)(i / N), p = (int)(i % N);
+    const float *r = ref + b * ref_stride + (int64_t)p * C;
+    float S[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) S[c] = __ldg(r + c);
+    const float *f = fr + b * fr_stride + (int64_t)p * C;
+    const int64_t fs = (int64_t)N * C;
+    float *o = rows + (int64_t)(1 + pbase[i]) * C;
+    while (w) {
+        const int t1 = __ffs(w) - 1;
+        w &= w - 1;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            const float raw = __fsub_rn(__ldg(f + t1 * fs + c), S[c]);
+            S[c] = __fadd_rn(S[c], raw);
+            o[c] = raw;
+        }
+        o += C;
+    }
+}
+
+#define SUB_DISPATCH(C_, KERNEL, ...)                                                    \
+    switch (C_) {                                                                        \
+    case 1: KERNEL<1><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
+    case 2: KERNEL<2><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
+    case 3: KERNEL<3><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
+    case 4: KERNEL<4><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
+    default: break;                                                                      \
+    }
+
+void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
+                          int N, int C, int n_diff, float theta, uint32_t *act, cudaStream_t s) {
+    const int grid = cdiv((int64_t)B * N, 256);
+    SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta, act);
+}
+
+void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
+                          int N, int C, const uint32_t *act, const int32_t *pbase, float *rows, cudaStream_t s) {
+    const int grid = cdiv((int64_t)B * N, 256);
+    SUB_DISPATCH(C, k_subtract_rows, ref, ref_stride, frames, fr_stride, B, N, act, pbase, rows);
+}
+
+// --------------------------------------------------------------- dilation
+__global__ void __launch_bounds__(256) k_dilate(const uint32_t *__restrict__ in, int B, Geo g,
+                                                uint32_t *__restrict__ out) {
+    const int No = g.Hout * g.Wout;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)B * No) return;
+    const int b = (int)(i / No), q = (int)(i % No);
+    const int oy = q / g.Wout, ox = q % g.Wout;
+    const uint32_t *src = in + (int64_t)b * g.Hin * g.Win;
+    uint32_t w = 0;
+    for (int dy = 0; dy < g.kh; dy++) {
+        const int iy = oy * g.sh - g.ph + dy;
+        if (iy < 0 || iy >= g.Hin) continue;
+        for (int dx = 0; dx < g.kw; dx++) {
+            const int ix = ox * g.sw - g.pw + dx;
+            if (ix < 0 || ix >= g.Win) continue;
+            w |= __ldg(src + iy * g.Win + ix);
+        }
+    }
+    out[i] = w;
+}
+
+void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaStream_t s) {
+    const int64_t n = (int64_t)B * g.Hout * g.Wout;
+    k_dilate<<<cdiv(n, 256), 256, 0, s>>>(in, B, g, out);
+}
+
+// ------------------------------------------------------------------- scan
+constexpr int SCAN_T = 256, SCAN_E = 8, SCAN_TILE = SCAN_T * SCAN_E;
+
+int64_t scan_tmp_ints(int64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 2; }
+
+__device__ __forceinline__ int block_excl_scan(int v, int *warp_sums, int &block_total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += y;
+        }
+        if (lane < (int)(blockDim.x >> 5)) warp_sums[lane] = ws;
+    }
+    __syncthreads();
+    block_total = warp_sums[(blockDim.x >> 5) - 1];
+    const int res = (wid ? warp_sums[wid - 1] : 0) + x - v;
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan1(const uint32_t *__restrict__ w, int64_t n, int32_t *tmp) {
+    __shared__ int ws[32];
+    const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_E;
+    int s = 0;
+#pragma unroll
+    for (int e = 0; e < SCAN_E; e++)
+        if (base + e < n) s += __popc(__ldg(w + base + e));
+    int tot;
+    block_excl_scan(s, ws, tot);
+    if (threadIdx.x == 0) tmp[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *total, long long *stat) {
+    __shared__ int ws[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + threadIdx.x;
+        const int v = i < nb ? tmp[i] : 0;
+        int tot;
+        const int ex = block_excl_scan(v, ws, tot);
+        if (i < nb) tmp[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *total = carry;
+        if (stat) atomicAdd((unsigned long long *)stat, (unsigned long long)carry);
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w, int64_t n,
+                                                  const int32_t *__restrict__ tmp, int32_t *__restrict__ pbase) {
+    __shared__ int ws[32];
+    const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_E;
+    int c[SCAN_E];
+    int s = 0;
+#pragma unroll
+    for (int e = 0; e < SCAN_E; e++) {
+        c[e] = base + e < n ? __popc(__ldg(w + base + e)) : 0;
+        s += c[e];
+    }
+    int tot;
+    int off = block_excl_scan(s, ws, tot) + tmp[blockIdx.x];
+#pragma unroll
+    for (int e = 0; e < SCAN_E; e++) {
+        if (base + e < n) pbase[base + e] = off;
+        off += c[e];
+    }
+}
+
+void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp,
+                      long long *stat, cudaStream_t s) {
+    const int nb = cdiv(n, SCAN_TILE);
+    if (nb == 0) {
+        cudaMemsetAsync(total, 0, sizeof(int32_t), s);
+        return;
+    }
+    k_scan1<<<nb, SCAN_T, 0, s>>>(words, n, tmp);
+    k_scan2<<<1, 1024, 0, s>>>(tmp, nb, total, stat);
+    k_scan3<<<nb, SCAN_T, 0, s>>>(words, n, tmp, pbase);
+}
+
+// -------------------------------------------------------------- enumerate
+__global__ void __launch_bounds__(256) k_enumerate(const uint32_t *__restrict__ slot, const int32_t *__restrict__ pbase,
+                                                   int64_t n, int32_t *__restrict__ ridx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t w = slot[i];
+    if (!w) return;
+    int32_t *o = ridx + pbase[i];
+    const int32_t code = (int32_t)(i << 5);
+    while (w) {
+        const int t1 = __ffs(w) - 1;
+        w &= w - 1;
+        *o++ = code | t1;
+    }
+}
+
+void launch_enumerate(const uint32_t *slot, const int32_t *pbase, int64_t n, int32_t *ridx, cudaStream_t s) {
+    k_enumerate<<<cdiv(n, 256), 256, 0, s>>>(slot, pbase, n, ridx);
+}
+
+// ----------------------------------------------------------------- counts
+constexpr int CNT_E = 8;
+__global__ void __launch_bounds__(256) k_frame_counts(const uint32_t *__restrict__ act, int N, long long *counts,
+                                                      int64_t cstride, long long *stat, long long *stat_nz) {
+    __shared__ int cnt[32];
+    __shared__ int nz;
+    if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) nz = 0;
+    __syncthreads();
+    const int b = blockIdx.y;
+    const int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * CNT_E;
+    const uint32_t *a = act + (int64_t)b * N;
+    for (int e = 0; e < CNT_E; e++) {
+        if (p0 + e >= N) break;
+        uint32_t w = __ldg(a + p0 + e);
+        if (w) atomicAdd(&nz, 1);
+        while (w) {
+            const int t1 = __ffs(w) - 1;
+            w &= w - 1;
+            atomicAdd(&cnt[t1], 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int v = cnt[threadIdx.x];
+        if (v) {
+            if (counts) atomicAdd((unsigned long long *)(counts + b * cstride + threadIdx.x), (unsigned long long)v);
+            if (stat) atomicAdd((unsigned long long *)stat, (unsigned long long)v);
+        }
+        if (threadIdx.x == 0 && stat_nz && nz) atomicAdd((unsigned long long *)stat_nz, (unsigned long long)nz);
+    }
+}
+
+void launch_frame_counts(const uint32_t *act, int B, int N, long long *counts, int64_t cstride, long long *stat,
+                         long long *stat_nz, cudaStream_t s) {
+    dim3 grid(cdiv(N, 256 * CNT_E), B);
+    k_frame_counts<<<grid, 256, 0, s>>>(act, N, counts, cstride, stat, stat_nz);
+}
+
+__global__ void k_or_words(const uint32_t *a, const uint32_t *b, int64_t n, uint32_t *o) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) o[i] = a[i] | b[i];
+}
+
+void launch_or_words(const uint32_t *a, const uint32_t *b, int64_t n, uint32_t *out, cudaStream_t s) {
+    k_or_words<<<cdiv(n, 256), 256, 0, s>>>(a, b, n, out);
+}
+
+}  // namespace st

@@ -1,0 +1,390 @@
+// kernels_site.cu -- non-linear correction + truncation sites, residual joins
+// and Accumulation on sm_100a.
+//
+// Non-linear correction (Eq.(3), reading R7): per
+// touched pixel, sequentially over diff frames with x_acc / y_acc held in
+// registers (the SparseBatch "N" order: the state is born from the
+// reference frame's x0 and dies with the kernel -- no per-layer cache is
+// kept in HBM):
+//     x_acc += Delta_t;  c = f(x_acc) - y_acc;
+//     emit iff max_c |c| > theta (pixel granularity, R1/R2);
+//     y_acc += c when emitted.
+// A pixel is owned by a group of G lanes (G = 32 for C >= 32, else the next
+// power of two >= C), each lane holding CPL channels; the channel max is a
+// group shuffle reduction.  Emitted rows are written in the input's slot
+// layout (in place), so no compaction pass is needed after a site.
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace st {
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+    if constexpr (G == 32) {
+        return 0xffffffffu;
+    } else {
+        const int lane = threadIdx.x & 31;
+        return ((1u << G) - 1u) << (lane & ~(G - 1));
+    }
+}
+
+template <int G>
+__device__ __forceinline__ float gmax(float v, unsigned mask) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+}
+
+template <int ACT>
+__device__ __forceinline__ float actf(float x) {
+    return ACT == ACT_RELU ? relu_f(x) : silu_f(x);
+}
+
+// ---------------------------------------------------------------- dense ops
+template <int ACT>
+__global__ void k_dense_act(const float *__restrict__ x, float *__restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = actf<ACT>(x[i]);
+}
+
+void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+    if (grid <= 0) return;
+    if (act == ACT_RELU) k_dense_act<ACT_RELU><<<grid, 256, 0, s>>>(x, y, n);
+    else k_dense_act<ACT_SILU><<<grid, 256, 0, s>>>(x, y, n);
+}
+
+__global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g) {
+    const int No = g.Hout * g.Wout;
+    const int64_t n = (int64_t)B * No * g.Cin;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % g.Cin);
+        const int64_t bq = i / g.Cin;
+        const int b = (int)(bq / No), q = (int)(bq % No);
+        const int oy = q / g.Wout, ox = q % g.Wout;
+        float m = -CUDART_INF_F;
+        for (int dy = 0; dy < g.kh; dy++) {
+            const int iy = oy * g.sh - g.ph + dy;
+            if (iy < 0 || iy >= g.Hin) continue;
+            for (int dx = 0; dx < g.kw; dx++) {
+                const int ix = ox * g.sw - g.pw + dx;
+                if (ix < 0 || ix >= g.Win) continue;
+                const float v = __ldg(x + (((int64_t)b * g.Hin + iy) * g.Win + ix) * g.Cin + c);
+                m = v > m ? v : m;
+            }
+        }
+        y[i] = m;
+    }
+}
+
+void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s) {
+    const int64_t n = (int64_t)B * g.Hout * g.Wout * g.Cin;
+    const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+    if (grid > 0) k_dense_maxpool<<<grid, 256, 0, s>>>(x, y, B, g);
+}
+
+__global__ void k_dense_add(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __fadd_rn(a[i], b[i]);
+}
+
+void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+    if (grid > 0) k_dense_add<<<grid, 256, 0, s>>>(a, b, y, n);
+}
+
+// ------------------------------------------------------- pointwise site
+template <int G, int CPL, int ACT>
+__global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
+                                                 float theta, uint32_t *__restrict__ out_act, float *out_rows) {
+    const int lane = threadIdx.x & (G - 1);
+    const unsigned mask = group_mask<G>();
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t bp = grp; bp < BN; bp += ngrp) {
+        uint32_t a = __ldg(in.act + bp);
+        if (!a) {
+            if (lane == 0) out_act[bp] = 0;
+            continue;
+        }
+        float xa[CPL], ya[CPL];
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = lane + G * i;
+            xa[i] = ch < C ? __ldg(x0 + bp * C + ch) : 0.0f;
+            ya[i] = actf<ACT>(xa[i]);
+        }
+        const int base = 1 + __ldg(in.pbase + bp);
+        const uint32_t sl = __ldg(in.slot + bp);
+        uint32_t emit = 0;
+        while (a) {
+            const int t1 = __ffs(a) - 1;
+            a &= a - 1;
+            const int64_t row = base + __popc(sl & lowmask(t1));
+            float cand[CPL];
+            float mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + G * i;
+                if (ch < C) {
+                    xa[i] = __fadd_rn(xa[i], in.rows[row * C + ch]);       // reconstruct x (Eq.3)
+                    cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);          // restore the delta
+                    mx = fmaxf(mx, fabsf(cand[i]));
+                } else {
+                    cand[i] = 0.0f;
+                }
+            }
+            mx = gmax<G>(mx, mask);
+            if (mx > theta) {                                              // truncation
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    const int ch = lane + G * i;
+                    if (ch < C) {
+                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                        out_rows[row * C + ch] = cand[i];
+                    }
+                }
+                emit |= 1u << t1;
+            }
+        }
+        if (lane == 0) out_act[bp] = emit;
+    }
+}
+
+#define CH_DISPATCH(C_, LAUNCH)                                    \
+    if ((C_) <= 1) { LAUNCH(1, 1); }                               \
+    else if ((C_) <= 2) { LAUNCH(2, 1); }                          \
+    else if ((C_) <= 4) { LAUNCH(4, 1); }                          \
+    else if ((C_) <= 8) { LAUNCH(8, 1); }                          \
+    else if ((C_) <= 16) { LAUNCH(16, 1); }                        \
+    else if ((C_) <= 32) { LAUNCH(32, 1); }                        \
+    else if ((C_) <= 64) { LAUNCH(32, 2); }                        \
+    else if ((C_) <= 96) { LAUNCH(32, 3); }                        \
+    else if ((C_) <= 128) { LAUNCH(32, 4); }                       \
+    else if ((C_) <= 160) { LAUNCH(32, 5); }                       \
+    else if ((C_) <= 256) { LAUNCH(32, 8); }                       \
+    else if ((C_) <= 480) { LAUNCH(32, 15); }                      \
+    else if ((C_) <= 512) { LAUNCH(32, 16); }                      \
+    else if ((C_) <= 672) { LAUNCH(32, 21); }                      \
+    else { LAUNCH(32, 36); }
+
+static int groups_grid(int64_t n_groups, int G) {
+    const int64_t threads = n_groups * G;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(threads, 256), 148 * 8));
+}
+
+void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta, uint32_t *out_act,
+                           float *out_rows, cudaStream_t s) {
+    const int64_t BN = (int64_t)B * N;
+#define L_PW(G_, CPL_)                                                                                   \
+    {                                                                                                    \
+        const int grid = groups_grid(BN, G_);                                                            \
+        if (act == ACT_RELU)                                                                             \
+            k_site_pw<G_, CPL_, ACT_RELU><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act, out_rows); \
+        else                                                                                             \
+            k_site_pw<G_, CPL_, ACT_SILU><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act, out_rows); \
+    }
+    CH_DISPATCH(C, L_PW)
+#undef L_PW
+}
+
+// --------------------------------------------------------- maxpool site
+// Touched set T = footprint dilation of the input mask (R7);
+// each touched window is re-evaluated from x_acc of its input pixels.
+template <int G, int CPL, int KMAX>
+__global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__restrict__ x0, int B, Geo g,
+                                                      float theta, const uint32_t *__restrict__ t_slot,
+                                                      const int32_t *__restrict__ t_pbase,
+                                                      uint32_t *__restrict__ out_act, float *__restrict__ out_rows) {
+    const int lane = threadIdx.x & (G - 1);
+    const unsigned mask = group_mask<G>();
+    const int C = g.Cin;
+    const int Nin = g.Hin * g.Win, No = g.Hout * g.Wout;
+    const int64_t BN = (int64_t)B * No;
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t bq = grp; bq < BN; bq += ngrp) {
+        const uint32_t T = __ldg(t_slot + bq);
+        if (!T) {
+            if (lane == 0) out_act[bq] = 0;
+            continue;
+        }
+        const int b = (int)(bq / No), q = (int)(bq % No);
+        const int oy = q / g.Wout, ox = q % g.Wout;
+        int64_t wp[KMAX];
+        float xa[KMAX][CPL];
+#pragma unroll
+        for (int w = 0; w < KMAX; w++) {
+            wp[w] = -1;
+            const int dy = w / g.kw, dx = w % g.kw;
+            const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+            if (w < g.kh * g.kw && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win)
+                wp[w] = (int64_t)b * Nin + iy * g.Win + ix;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + G * i;
+                xa[w][i] = (wp[w] >= 0 && ch < C) ? __ldg(x0 + wp[w] * C + ch) : -CUDART_INF_F;
+            }
+        }
+        float ya[CPL];
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            float m = -CUDART_INF_F;
+#pragma unroll
+            for (int w = 0; w < KMAX; w++)
+                if (wp[w] >= 0) m = xa[w][i] > m ? xa[w][i] : m;
+            ya[i] = m;
+        }
+        const int base = 1 + __ldg(t_pbase + bq);
+        uint32_t bits = T, emit = 0;
+        while (bits) {
+            const int t1 = __ffs(bits) - 1;
+            bits &= bits - 1;
+#pragma unroll
+            for (int w = 0; w < KMAX; w++) {
+                if (wp[w] < 0) continue;
+                const int row = row_of(in, wp[w], t1);
+                if (!row) continue;
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    const int ch = lane + G * i;
+                    if (ch < C) xa[w][i] = __fadd_rn(xa[w][i], in.rows[(int64_t)row * C + ch]);
+                }
+            }
+            float cand[CPL];
+            float mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                float m = -CUDART_INF_F;
+#pragma unroll
+                for (int w = 0; w < KMAX; w++)
+                    if (wp[w] >= 0) m = xa[w][i] > m ? xa[w][i] : m;
+                cand[i] = __fsub_rn(m, ya[i]);
+                const int ch = lane + G * i;
+                if (ch < C) mx = fmaxf(mx, fabsf(cand[i]));
+            }
+            mx = gmax<G>(mx, mask);
+            if (mx > theta) {
+                const int64_t orow = base + __popc(T & lowmask(t1));
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    const int ch = lane + G * i;
+                    if (ch < C) {
+                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                        out_rows[orow * C + ch] = cand[i];
+                    }
+                }
+                emit |= 1u << t1;
+            }
+        }
+        if (lane == 0) out_act[bq] = emit;
+    }
+}
+
+void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta, const uint32_t *t_slot,
+                         const int32_t *t_pbase, uint32_t *out_act, float *out_rows, cudaStream_t s) {
+    const int64_t BN = (int64_t)B * g.Hout * g.Wout;
+    const int kk = g.kh * g.kw;
+#define L_MP(G_, CPL_)                                                                                         \
+    {                                                                                                          \
+        const int grid = groups_grid(BN, G_);                                                                  \
+        if (kk <= 4)                                                                                           \
+            k_site_maxpool<G_, CPL_, 4><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase, out_act,    \
+                                                             out_rows);                                        \
+        else                                                                                                   \
+            k_site_maxpool<G_, CPL_, 9><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase, out_act,    \
+                                                             out_rows);                                        \
+    }
+    CH_DISPATCH(g.Cin, L_MP)
+#undef L_MP
+}
+
+// ---------------------------------------------------------- residual add
+template <int G, int CPL>
+__global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32_t *__restrict__ slot,
+                                                  const int32_t *__restrict__ pbase, int64_t BN, int C,
+                                                  float *__restrict__ out) {
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t bp = grp; bp < BN; bp += ngrp) {
+        uint32_t w = __ldg(slot + bp);
+        if (!w) continue;
+        int64_t row = 1 + __ldg(pbase + bp);
+        while (w) {
+            const int t1 = __ffs(w) - 1;
+            w &= w - 1;
+            const int ra = row_of(a, bp, t1), rb = row_of(b, bp, t1);
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + G * i;
+                if (ch < C) {
+                    const float va = ra ? a.rows[(int64_t)ra * C + ch] : 0.0f;
+                    const float vb = rb ? b.rows[(int64_t)rb * C + ch] : 0.0f;
+                    out[row * C + ch] = __fadd_rn(va, vb);
+                }
+            }
+            row++;
+        }
+    }
+}
+
+void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C,
+                     float *out_rows, cudaStream_t s) {
+    const int64_t BN = (int64_t)B * N;
+#define L_ADD(G_, CPL_) k_add_rows<G_, CPL_><<<groups_grid(BN, G_), 256, 0, s>>>(a, b, slot, pbase, BN, C, out_rows);
+    CH_DISPATCH(C, L_ADD)
+#undef L_ADD
+}
+
+// ---------------------------------------------------------- accumulation
+// O_t = O_{t-1} + Delta_t, dense per-frame outputs [B][L][N][C].
+template <int G, int CPL>
+__global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__restrict__ y0, int B, int N, int C,
+                                                    int n_diff, float *__restrict__ out) {
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t BN = (int64_t)B * N;
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int64_t fstride = (int64_t)N * C;
+    for (int64_t bq = grp; bq < BN; bq += ngrp) {
+        const int b = (int)(bq / N), q = (int)(bq % N);
+        const uint32_t a = n_diff ? __ldg(in.act + bq) : 0u;
+        const int base = a ? 1 + __ldg(in.pbase + bq) : 0;
+        const uint32_t sl = a ? __ldg(in.slot + bq) : 0u;
+        float O[CPL];
+        float *o = out + (int64_t)b * (n_diff + 1) * fstride + (int64_t)q * C;
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = lane + G * i;
+            O[i] = ch < C ? __ldg(y0 + bq * C + ch) : 0.0f;
+            if (ch < C) o[ch] = O[i];
+        }
+        for (int t1 = 0; t1 < n_diff; t1++) {
+            o += fstride;
+            if ((a >> t1) & 1u) {
+                const int64_t row = base + __popc(sl & lowmask(t1));
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    const int ch = lane + G * i;
+                    if (ch < C) O[i] = __fadd_rn(O[i], in.rows[row * C + ch]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + G * i;
+                if (ch < C) o[ch] = O[i];
+            }
+        }
+    }
+}
+
+void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, float *out, cudaStream_t s) {
+    const int64_t BN = (int64_t)B * N;
+#define L_ACC(G_, CPL_) k_accumulate<G_, CPL_><<<groups_grid(BN, G_), 256, 0, s>>>(in, y0, B, N, C, n_diff, out);
+    CH_DISPATCH(C, L_ACC)
+#undef L_ACC
+}
+
+}  // namespace st

@@ -1,0 +1,94 @@
+"""Helpers for -m gpu parity tests: run the CUDA path (through the C ABI via
+the binding) and the oracle on the same seeded inputs and compare.
+
+Parity bar: FP32 mode on ReLU/maxpool/add networks is
+bit-exact -- masks (= active-index lists) of every layer and frame, delta
+rows, tap outputs and per-site counts; SiLU layers are compared within the
+R29 tolerance (exp differs by at most rounding, reading R10).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import workloads as W
+
+REL, ABS = 1e-4, 1e-5   # north_star fp32 tolerance (reading R29)
+
+
+def gpu_run(net, frames_np, thresholds, debug=True, device=0, max_frames=None):
+    """frames_np float32 [B][L][H][W][C] -> (encoder, torch frames)."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    B, L = frames_np.shape[:2]
+    enc = Encoder(net, max_chunks=B, max_frames=max_frames or L, debug_retain=debug, device=device)
+    fr = torch.from_numpy(np.ascontiguousarray(frames_np)).to(f"cuda:{device}")
+    enc.encode_reference(fr[:, 0])
+    enc.encode_diff(fr[:, 1:] if L > 1 else None, thresholds)
+    torch.cuda.synchronize()
+    return enc, fr
+
+
+def within(a, b, rel=REL, abs_=ABS):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return bool(np.all(np.abs(a - b) <= abs_ + rel * np.abs(b)))
+
+
+def compare_chunk(enc, net, frames_chunk, thresholds, chunk, exact=True, check_rows=True):
+    """Compare one chunk of a debug_retain GPU run against the oracle."""
+    L = frames_chunk.shape[0]
+    r = oracle.run_chunk(net, frames_chunk, thresholds, want_deltas=check_rows)
+    F = L - 1
+    report = dict(layers=0, frames=F, mismatched_masks=0)
+    # input site
+    for t in range(1, L):
+        m = enc.debug_mask(-1, chunk, t)
+        assert np.array_equal(m, r["in_mask"][t - 1]), f"input mask chunk {chunk} frame {t}"
+        if check_rows:
+            idx, rows = enc.debug_rows(-1, chunk, t)
+            exp_idx = np.flatnonzero(r["in_mask"][t - 1].ravel())
+            assert np.array_equal(idx, exp_idx)
+            exp = r["in_delta"][t - 1].reshape(-1, net.in_c)[exp_idx]
+            assert np.array_equal(rows, exp), "input delta rows"
+    for i, l in enumerate(net.layers):
+        for t in range(1, L):
+            m = enc.debug_mask(i, chunk, t)
+            om = r["masks"][i][t - 1]
+            if not np.array_equal(m, om):
+                raise AssertionError(f"layer {i} ({W.KIND_NAMES[l['kind']]}) chunk {chunk} frame {t}: "
+                                     f"mask differs in {int((m != om).sum())} px (gpu {int(m.sum())}, "
+                                     f"oracle {int(om.sum())})")
+            if check_rows:
+                idx, rows = enc.debug_rows(i, chunk, t)
+                exp_idx = np.flatnonzero(om.ravel())
+                assert np.array_equal(idx, exp_idx), f"layer {i} index list"
+                C = rows.shape[1] if rows.ndim == 2 else 1
+                exp = r["deltas"][i][t - 1].reshape(-1, C)[exp_idx]
+                if exact:
+                    if not np.array_equal(rows, exp):
+                        d = np.abs(rows.astype(np.float64) - exp)
+                        raise AssertionError(f"layer {i} ({W.KIND_NAMES[l['kind']]}) frame {t}: rows differ, "
+                                             f"max abs {d.max():.3e} in {int((d > 0).sum())} values")
+                else:
+                    assert within(rows, exp), f"layer {i} rows beyond tolerance"
+        report["layers"] += 1
+    # taps
+    for tap, O in r["taps"].items():
+        got = enc.outputs(tap)[chunk].cpu().numpy()
+        if exact:
+            assert np.array_equal(got, O), f"tap {tap} outputs differ (max {np.abs(got - O).max():.3e})"
+        else:
+            assert within(got, O), f"tap {tap} outputs beyond tolerance"
+    # counts
+    act, _, _ = enc.get_sparsity()
+    assert np.array_equal(act[chunk], r["counts"]), "per-site per-frame counts"
+    return report
+
+
+def make_frames(cfg, n_chunks, L=None, h=None, w=None):
+    L = L or cfg.L
+    h = h or cfg.h
+    w = w or cfg.w
+    u8 = W.gen_video(n_chunks, L, h, w, cfg.c, cfg.video_seed(0), **cfg.video)
+    return W.to_float(u8)

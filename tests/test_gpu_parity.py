@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle (-m gpu).
+
+FP32 mode: masks / active-index lists of every layer and frame are
+bit-exact, delta rows, tap outputs and per-site counts are bit-exact
+(fixed fma order, reading R18).  Sizes span several tiles and a ragged tail;
+full BASELINE sizes are checked on sampled chunks (chunks are independent,
+P:113, so the oracle computes a sampled chunk exactly)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from workloads import Net, init_weights
+from gpu_harness import gpu_run, compare_chunk, make_frames, within
+from netgen import random_net, random_frames
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2410_20790_b200 import load_library
+    load_library()
+
+
+def test_cfg1_toy_exact():
+    cfg = W.get_config(1)
+    net = cfg.build_net()
+    fr = make_frames(cfg, 3)
+    enc, _ = gpu_run(net, fr, cfg.theta_fixed)
+    for b in range(3):
+        compare_chunk(enc, net, fr[b], cfg.theta_fixed, b)
+
+
+@pytest.mark.parametrize("theta", [0.0, 0.02, 0.1])
+def test_cfg1_thresholds(theta):
+    cfg = W.get_config(1)
+    net = cfg.build_net()
+    fr = make_frames(cfg, 2)
+    enc, _ = gpu_run(net, fr, theta)
+    for b in range(2):
+        compare_chunk(enc, net, fr[b], theta, b)
+
+
+def test_cfg2_crnn_exact():
+    cfg = W.get_config(2)
+    net = cfg.build_net()
+    fr = make_frames(cfg, 2, L=12)
+    enc, _ = gpu_run(net, fr, cfg.theta_fixed)
+    for b in range(2):
+        compare_chunk(enc, net, fr[b], cfg.theta_fixed, b)
+
+
+def test_resnet18_small_exact():
+    net = W.models.resnet18(64, 96)
+    init_weights(net, 11)
+    cfg = W.get_config(4)
+    u8 = W.gen_video(2, 6, 64, 96, 3, 77, n_objects=4, size=(8, 24), speed=(1, 3), noise_q=0.1, noise_amp=2)
+    fr = W.to_float(u8)
+    enc, _ = gpu_run(net, fr, 0.05)
+    for b in range(2):
+        compare_chunk(enc, net, fr[b], 0.05, b)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_nets(seed):
+    net = random_net(900 + seed, allow_se=False, allow_silu=(seed % 2 == 0))
+    fr = np.stack([random_frames(seed * 3 + b, 7, net.in_h, net.in_w, net.in_c) for b in range(2)])
+    th = 0.03 + 0.01 * (seed % 4)
+    enc, _ = gpu_run(net, fr, th)
+    exact = not any(l["kind"] == W.SILU for l in net.layers)
+    for b in range(2):
+        compare_chunk(enc, net, fr[b], th, b, exact=exact)
+
+
+def test_identical_frames_empty_masks():
+    cfg = W.get_config(1)
+    net = cfg.build_net()
+    fr = np.repeat(make_frames(cfg, 1, L=1), 5, axis=1)
+    enc, _ = gpu_run(net, fr, 0.05)
+    act, sa, _ = enc.get_sparsity()
+    assert act.sum() == 0 and sa.sum() == 0
+    out = enc.outputs(3)[0].cpu().numpy()
+    for t in range(1, 5):
+        assert np.array_equal(out[t], out[0])
+
+
+def test_dense_only_and_max_frames():
+    cfg = W.get_config(1)
+    net = cfg.build_net()
+    fr = make_frames(cfg, 1, L=33, h=24, w=40)
+    net = W.models.toy_encoder(24, 40)
+    init_weights(net, 3)
+    enc, _ = gpu_run(net, fr, 0.05)                  # 32 diff frames: full frame word
+    compare_chunk(enc, net, fr[0], 0.05, 0)
+    enc0, _ = gpu_run(net, fr[:, :1], 0.05)          # n_diff = 0: dense pass only
+    o = enc0.outputs(3)[0, 0].cpu().numpy()
+    assert np.array_equal(o, oracle.dense_forward(net, fr[0, 0])[2])
+
+
+def test_cfg2_full_size_sampled():
+    """BASELINE cfg2 at full size (B=64 chunks x L=32) in the bench's launch
+    configuration; sampled chunks checked exactly against the oracle."""
+    cfg = W.get_config(2)
+    net = cfg.build_net()
+    fr = make_frames(cfg, cfg.chunks_per_step)
+    enc, _ = gpu_run(net, fr, cfg.theta_fixed, debug=False)
+    act, _, _ = enc.get_sparsity()
+    tap = enc.taps[0]
+    out = enc.outputs(tap)
+    for b in (0, 37, 63):
+        r = oracle.run_chunk(net, fr[b], cfg.theta_fixed, want_masks=False)
+        assert np.array_equal(out[b].cpu().numpy(), r["taps"][tap]), f"chunk {b}"
+        assert np.array_equal(act[b], r["counts"])
+
+
+def test_errors_and_state():
+    from paper_2410_20790_b200 import Encoder, StError
+    import torch
+    net = W.get_config(1).build_net()
+    enc = Encoder(net, 2, 4)
+    fr = torch.zeros(2, 3, 64, 64, 3, device="cuda")
+    with pytest.raises(StError):            # diff before reference
+        enc.encode_diff(fr, 0.05)
+    enc.encode_reference(fr[:, 0])
+    with pytest.raises(StError):            # too many frames
+        enc.encode_diff(torch.zeros(2, 5, 64, 64, 3, device="cuda"), 0.05)
+    with pytest.raises(StError):            # negative threshold
+        enc.encode_diff(fr, -1.0)
+    enc.encode_diff(fr, 0.05)
