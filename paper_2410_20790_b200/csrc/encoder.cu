@@ -243,7 +243,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     for (auto &l : e->L)
         if (l.kind == ST_CONV) {
             const int cin_g = l.geo.Cin / l.spec.groups;
-            wfloats += (int64_t)l.spec.k_h * l.spec.k_w * cin_g * l.C + l.C;
+            wfloats += ((int64_t)l.spec.k_h * l.spec.k_w * cin_g * l.C + 63) / 64 * 64 + (l.C + 63) / 64 * 64;
         }
     CUDA_OK(e.get(), cudaMalloc(&e->weights_mem, std::max<int64_t>(wfloats, 1) * sizeof(float)));
     {
@@ -259,10 +259,10 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                         for (int c = 0; c < co; c++)
                             host[o + ((int64_t)(dy * kw + dx) * cin_g + ci) * co + c] =
                                 l.spec.w[(((int64_t)c * cin_g + ci) * kh + dy) * kw + dx];
-            o += (int64_t)kh * kw * cin_g * co;
+            o += ((int64_t)kh * kw * cin_g * co + 63) / 64 * 64;   // 256-byte aligned (float4 loads)
             l.bias = e->weights_mem + o;
             for (int c = 0; c < co; c++) host[o + c] = l.spec.b[c];
-            o += co;
+            o += (co + 63) / 64 * 64;
         }
         CUDA_OK(e.get(), cudaMemcpy(e->weights_mem, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice));
     }

@@ -15,5 +15,5 @@ from .models import (  # noqa: F401
     CONV, RELU, SILU, MAXPOOL, ADD, SE, OUTPUT, KIND_NAMES, NONLINEAR,
     Net, infer_shapes, init_weights, site_layers,
 )
-from .video import gen_video, to_float  # noqa: F401
+from .video import gen_video, gen_chunk, to_float  # noqa: F401
 from .configs import CONFIGS, get_config  # noqa: F401
