@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--policy", default=None, choices=[None, "fixed", "bst", "ibst"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"],
+                    help="fp32: exact CUDA-core path; bf16: tcgen05 tensor-core convs (R22-BF16)")
     ap.add_argument("--no-dense", action="store_true", help="skip the own-dense-path reference timing")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     return ap.parse_args()
@@ -198,7 +200,7 @@ def main():
     policy = args.policy or cfg.policy
     B, L = cfg.chunks_per_step, cfg.L
     net = cfg.build_net()
-    enc = Encoder(net, max_chunks=B, max_frames=L, device=local)
+    enc = Encoder(net, max_chunks=B, max_frames=L, device=local, precision=args.precision)
     ns = enc.n_sites
     ctl = ThresholdController(ns, policy=policy, T=cfg.T, eps=cfg.eps, theta_fixed=cfg.theta_fixed,
                               cycle=cfg.cycle)
@@ -302,7 +304,15 @@ def main():
     peaks, peak_src = measured_peaks()
     d = kt[dom]
     nl = max(d["launches"], 1)
-    if d["flops"] > 0 and dom.startswith("conv"):
+    if d["flops"] > 0 and dom.startswith("conv_tc"):
+        # tcgen05 bf16: measured cuBLAS bf16 peak, sustained figure (kernel timed inside a long step)
+        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+        ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": ncu_traffic(dom), "kernel": dom,
+                "peak_source": f"{peak_src} bf16_tflops_sustained",
+                "share_of_step": d["ms"] / args.steps / step_kernel_ms}
+    elif d["flops"] > 0 and dom.startswith("conv"):
         # FP32 CUDA-core FFMA: 148 SMs x 128 lanes x 2 flop x max SM clock
         peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
@@ -320,7 +330,7 @@ def main():
     # ---- own dense path: every frame as a reference frame, same kernels
     dense = None
     if not args.no_dense:
-        denc = Encoder(net, max_chunks=B * L, max_frames=1, device=local)
+        denc = Encoder(net, max_chunks=B * L, max_frames=1, device=local, precision=args.precision)
         xd = batches[0].reshape(B * L, cfg.h, cfg.w, cfg.c)
         for _ in range(2):
             denc.encode_reference(xd, stream)
@@ -350,7 +360,8 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "bf16xbf16->f32",
+                "data": "synthetic",
                 "config": {"workload": f"cfg{cfg.cid}: {cfg.note}", "chunks_per_step_per_gpu": B,
                            "frames_per_chunk": L, "frame": [cfg.h, cfg.w, cfg.c], "policy": policy,
                            "theta": [float(x) for x in ctl.thresholds()[:3]] + ["..."],

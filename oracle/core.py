@@ -46,6 +46,7 @@ def _load():
         lib.orc_run_chunk.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
                                       C.c_int, P, P, P, P, P, P, P]
         lib.orc_dilate.argtypes = [P] + [C.c_int] * 10 + [P]
+        lib.orc_set_precision.argtypes = [C.c_int]
         _lib = lib
     return _lib
 
@@ -94,9 +95,10 @@ def num_sites(net):
     return int(_load().orc_num_sites(_Spec(net).ptr, len(net.layers)))
 
 
-def dense_forward(net, frame):
+def dense_forward(net, frame, precision="fp32"):
     """Dense forward of one float32 frame [H][W][C]; list of per-layer outputs."""
     lib = _load()
+    lib.orc_set_precision(1 if precision == "bf16" else 0)
     sp = _Spec(net)
     shp = shapes(net)
     x = np.ascontiguousarray(frame, np.float32)
@@ -109,7 +111,7 @@ def dense_forward(net, frame):
 
 
 def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_deltas=False,
-              want_dense0=False, mask_layers=None, delta_layers=None):
+              want_dense0=False, mask_layers=None, delta_layers=None, precision="fp32"):
     """Run one chunk (frames float32 [L][H][W][C]) through dense + diff.
 
     Returns dict with
@@ -121,6 +123,7 @@ def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_
       in_mask   uint8 [L-1][H][W]   input-site mask; in_delta float32 [L-1][H][W][C]
     """
     lib = _load()
+    lib.orc_set_precision(1 if precision == "bf16" else 0)
     sp = _Spec(net)
     shp = shapes(net)
     fr = np.ascontiguousarray(frames, np.float32)

@@ -112,6 +112,22 @@ static float relu_f(float x) { return x > 0.0f ? x : 0.0f; }
 static float silu_f(float x) { return x / (1.0f + exp_r(-x)); }          /* R10 */
 static float sigm_f(float x) { return 1.0f / (1.0f + exp_r(-x)); }       /* R10 */
 
+/* Precision mode (R22-BF16).  0 = FP32 mode.  1 = BF16 mode: a
+ * convolution with groups == 1, c_in % 64 == 0 and c_out % 16 == 0 multiplies
+ * bf16-rounded (round-to-nearest-even) operands -- the weight and the input
+ * value -- and accumulates in fp32; everything else is unchanged. */
+static int g_bf16 = 0;
+void orc_set_precision(int bf16) { g_bf16 = bf16 ? 1 : 0; }
+
+static float bf16r(float v) {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    u &= 0xFFFF0000u;
+    memcpy(&v, &u, 4);
+    return v;
+}
+
 /* ------------------------------------------------------------ dense ops */
 
 /* Eq.(1): O[q][co] = sum_{dy,dx,ci} W[co][ci][dy][dx] * X[p(q,dy,dx)][g*cin_g+ci]
@@ -122,6 +138,7 @@ static void conv_apply(const orc_layer *l, shp si, shp so, const float *x, const
                        int with_bias, float *out) {
     const int cin_g = si.c / l->groups, cout_g = l->c_out / l->groups;
     const int No = so.h * so.w;
+    const int rb = g_bf16 && l->groups == 1 && si.c % 64 == 0 && l->c_out % 16 == 0;
 #pragma omp parallel for schedule(static)
     for (int q = 0; q < No; q++) {
         float *o = out + (size_t)q * so.c;
@@ -142,7 +159,7 @@ static void conv_apply(const orc_layer *l, shp si, shp so, const float *x, const
                     const float *xp = x + ((size_t)iy * si.w + ix) * si.c + (size_t)g * cin_g;
                     for (int ci = 0; ci < cin_g; ci++) {
                         const float wv = l->w[(((size_t)co * cin_g + ci) * l->k_h + dy) * l->k_w + dx];
-                        acc = fmaf(wv, xp[ci], acc);
+                        acc = rb ? fmaf(bf16r(wv), bf16r(xp[ci]), acc) : fmaf(wv, xp[ci], acc);
                     }
                 }
             }

@@ -28,10 +28,11 @@ namespace {
 
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
-              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_N = 14;
+              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_N = 16;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
-                              "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense"};
+                              "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
+                              "conv_tc_sparse", "conv_tc_dense"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -46,9 +47,11 @@ struct LayerRT {
     int site = 0;
     Geo geo{};
     bool depthwise = false;
+    bool tc = false;          // BF16 mode: tcgen05 tensor-core conv
     int n_consumers = 0, last_consumer = 0;
     // device weights (separate allocation)
     float *wk = nullptr, *bias = nullptr;
+    uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
     // buffer ids (-1 = none / alias)
     int b_y0 = -1, b_act = -1, b_slot = -1, b_pbase = -1, b_rows = -1, b_ridx = -1, b_out = -1;
     int alias_rows_of = -1;   // rows / slot / pbase borrowed from another tensor
@@ -83,6 +86,7 @@ struct st_encoder {
     int32_t *scan_tmp = nullptr;
     float *ref = nullptr;        // staged reference frames [B][N][C]
     float *weights_mem = nullptr;
+    uint16_t *wbf_mem = nullptr;
     // state
     int staged_chunks = 0;       // >0 after encode_reference
     int last_chunks = 0, last_ndiff = -1;
@@ -159,7 +163,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
         return ST_ERR_SHAPE;
     if (cfg->max_chunks < 1 || cfg->max_frames < 1) return ST_ERR_SHAPE;
     if (cfg->max_frames > 33) return ST_ERR_UNSUPPORTED;   // frame words hold L-1 <= 32 (R25)
-    if (cfg->precision != ST_FP32) return ST_ERR_UNSUPPORTED;
+    if (cfg->precision != ST_FP32 && cfg->precision != ST_BF16) return ST_ERR_UNSUPPORTED;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return ST_ERR_CUDA;
     cudaDeviceProp prop;
@@ -265,6 +269,38 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             o += (co + 63) / 64 * 64;
         }
         CUDA_OK(e.get(), cudaMemcpy(e->weights_mem, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    // ---- BF16 mode: tensor-core layers get bf16 [Cout][K] weights (RNE)
+    if (cfg->precision == ST_BF16) {
+        int64_t nbf = 0;
+        for (auto &l : e->L)
+            if (l.kind == ST_CONV && conv_tc_eligible(l.geo)) {
+                l.tc = true;
+                nbf += ((int64_t)l.spec.k_h * l.spec.k_w * l.geo.Cin * l.C + 127) / 128 * 128;
+            }
+        if (nbf) {
+            CUDA_OK(e.get(), cudaMalloc(&e->wbf_mem, nbf * 2));
+            std::vector<uint16_t> hb(nbf, 0);
+            int64_t o = 0;
+            for (auto &l : e->L) {
+                if (!l.tc) continue;
+                const int kh = l.spec.k_h, kw = l.spec.k_w, ci_n = l.geo.Cin, co = l.C;
+                const int64_t K = (int64_t)kh * kw * ci_n;
+                l.wbf = e->wbf_mem + o;
+                for (int c = 0; c < co; c++)
+                    for (int dy = 0; dy < kh; dy++)
+                        for (int dx = 0; dx < kw; dx++)
+                            for (int ci = 0; ci < ci_n; ci++) {
+                                float v = l.spec.w[(((int64_t)c * ci_n + ci) * kh + dy) * kw + dx];
+                                uint32_t u;
+                                std::memcpy(&u, &v, 4);
+                                u += 0x7FFFu + ((u >> 16) & 1u);   // round to nearest even
+                                hb[o + (int64_t)c * K + (dy * kw + dx) * ci_n + ci] = (uint16_t)(u >> 16);
+                            }
+                o += (K * co + 127) / 128 * 128;
+            }
+            CUDA_OK(e.get(), cudaMemcpy(e->wbf_mem, hb.data(), nbf * 2, cudaMemcpyHostToDevice));
+        }
     }
     for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
     st_status r = plan(e.get());
@@ -430,6 +466,7 @@ extern "C" void st_encoder_destroy(st_encoder *e) {
     cudaFree(e->smallmem);
     cudaFree(e->ref);
     cudaFree(e->weights_mem);
+    cudaFree(e->wbf_mem);
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     delete e;
 }
@@ -564,8 +601,8 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
-            LAUNCH(e, l.depthwise ? KC_DW_DENSE : KC_CONV_DENSE, i, s,
-                   l.depthwise ? launch_dwconv_f32(c, s) : launch_conv_f32(c, s));
+            LAUNCH(e, l.depthwise ? KC_DW_DENSE : (l.tc ? KC_TC_DENSE : KC_CONV_DENSE), i, s,
+                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.wbf, s) : launch_conv_f32(c, s)));
             if (F == 0) break;
             uint32_t *act = e->p<uint32_t>(l.b_act);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -579,8 +616,8 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             c.m_dev = e->totals + i;
             c.m_cap = (int64_t)B * F * N;
             c.out = e->p<float>(l.b_rows);
-            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : KC_CONV_SPARSE, i, s,
-                   l.depthwise ? launch_dwconv_f32(c, s) : launch_conv_f32(c, s));
+            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : (l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE), i, s,
+                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.wbf, s) : launch_conv_f32(c, s)));
             break;
         }
         case ST_RELU: case ST_SILU: {
@@ -826,20 +863,19 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
             cudaEventElapsedTime(&t, r.e0, r.e1);
             e->prof_ms[r.cls] += t;
             e->prof_n[r.cls] += 1;
-            if (r.layer >= 0 && (r.cls == KC_CONV_SPARSE || r.cls == KC_CONV_DENSE || r.cls == KC_DW_SPARSE ||
-                                 r.cls == KC_DW_DENSE)) {
+            const bool sparse = r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE || r.cls == KC_TC_SPARSE;
+            const bool dense = r.cls == KC_CONV_DENSE || r.cls == KC_DW_DENSE || r.cls == KC_TC_DENSE;
+            if (r.layer >= 0 && (sparse || dense)) {
                 const LayerRT &l = e->L[r.layer];
                 const int64_t K = (int64_t)l.geo.kh * l.geo.kw * (l.geo.Cin / l.geo.groups);
-                const int64_t M = (r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE)
-                                      ? rout[r.layer]
-                                      : (int64_t)e->last_chunks * l.H * l.W;
-                const int64_t Min = (r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE)
-                                        ? rin[r.layer]
-                                        : (int64_t)e->last_chunks * l.geo.Hin * l.geo.Win;
+                const int64_t M = sparse ? rout[r.layer] : (int64_t)e->last_chunks * l.H * l.W;
+                const int64_t Min = sparse ? rin[r.layer] : (int64_t)e->last_chunks * l.geo.Hin * l.geo.Win;
                 e->prof_flops[r.cls] += 2.0 * K * l.C * M;
-                // algorithmic bytes: each active input row once, each output row once, weights once
-                e->prof_bytes[r.cls] += 4.0 * ((double)Min * l.geo.Cin + (double)M * l.C + (double)K * l.C) +
-                                        ((r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE) ? 4.0 * M : 0.0);
+                // algorithmic bytes: each active input row once, each output row once (+ its
+                // 4-byte row index when sparse), weights once (bf16 on the tensor-core path)
+                const double wbytes = (r.cls == KC_TC_SPARSE || r.cls == KC_TC_DENSE) ? 2.0 : 4.0;
+                e->prof_bytes[r.cls] += 4.0 * ((double)Min * l.geo.Cin + (double)M * l.C) + wbytes * K * l.C +
+                                        (sparse ? 4.0 * M : 0.0);
             }
         }
         e->recs.clear();

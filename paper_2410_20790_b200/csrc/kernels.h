@@ -69,6 +69,9 @@ struct ConvCall {
 };
 void launch_conv_f32(const ConvCall &c, cudaStream_t s);
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s);
+// BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu); wbf = bf16 [Cout][K]
+bool conv_tc_eligible(const Geo &g);
+void launch_conv_tc(const ConvCall &c, const void *wbf, cudaStream_t s);
 
 // ---- sites, joins, accumulation (kernels_site.cu) ----
 enum Act { ACT_RELU = 0, ACT_SILU = 1 };

@@ -1,0 +1,361 @@
+// kernels_conv_tc.cu -- BF16 mode sparse / dense convolution on the 5th-gen
+// tensor cores (tcgen05, TMEM accumulators), sm_100a.
+//
+// Eq.(2) as a gathered implicit GEMM:
+//   D[M x Cout] = A[M x K] * B[K x Cout],  K = k_h*k_w*c_in in (dy, dx, ci) order,
+// A rows gathered from the compacted delta rows (sparse) or the dense
+// reference activations (dense), B = weights.  Used where the active-row
+// batch is a real dense contraction (c_in % 64 == 0: 3x3 convs of the CRNN
+// and ResNet encoders, 1x1 convs with wide inputs).
+//
+// Precision contract of BF16 mode (R22-BF16): A and B are rounded
+// to bf16 (RNE) when staged, products are exact in fp32, accumulation is fp32
+// in TMEM; rows/outputs stay fp32.
+//
+// CTA = 9 warps, persistent over (M tile, N tile):
+//   warps 0-3  producers: thread m gathers A row m of the tile (64 channels
+//              of one tap per k-block: 16 x LDG.128 fp32 -> cvt.bf16x2 ->
+//              8 x STS.128 in the 128B-swizzled K-major layout) and a share
+//              of the B tile (bf16 weights, LDG.128 -> STS.128), then
+//              fence.proxy.async + mbarrier arrive (full[s]);
+//   warp 4     MMA issuer: one elected lane issues 4 x tcgen05.mma
+//              (M=128, N=BN, K=16) per k-block, tcgen05.commit -> empty[s];
+//              after the last k-block commit -> tmem_full[acc];
+//   warps 5-8  epilogue: tcgen05.ld 32x32b (TMEM lane = tile row) -> fp32
+//              row stores (+bias in dense mode), arrive tmem_empty[acc].
+// Stages: 4-deep smem ring; TMEM: 2 accumulators x BN columns.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace st {
+
+namespace tc {
+
+constexpr int BM = 128, BK = 64, STAGES = 4, NPROD = 128, NTHREADS = 288;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// SWIZZLE_128B K-major smem descriptor (sm_100 version 1): start>>4 [0,14),
+// LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B
+// between 8-row core-matrix groups, version bits [46,48) = 1, layout
+// [61,64) = 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(16 >> 4) << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, K-major both, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+template <int BN>
+struct Smem {
+    static constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+    static constexpr int B_BYTES = BN * BK * 2;          // BN * 128 B
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int BAR_OFF = STAGES * STAGE;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers, + alignment slack
+};
+
+}  // namespace tc
+
+template <int BN>
+__global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __nv_bfloat16 *__restrict__ wbf) {
+    using namespace tc;
+    using S = Smem<BN>;
+    constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const Geo g = c.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
+    const int M = c.dense ? c.B * Nout : *c.m_dev;
+    const int K = g.kh * g.kw * g.Cin;
+    const int nkb = K / BK;
+    const int ntn = (g.Cout + BN - 1) / BN;
+    const int ntiles = ((M + BM - 1) / BM) * ntn;
+    const float *A = c.dense ? c.a_dense : c.a.rows;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full + s, NPROD);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; a++) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < 4) {
+        // ===================== producers =====================
+        const int m = threadIdx.x;   // tile row owned by this thread
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int mt = tile / ntn, nt = tile - mt * ntn;
+            const int r = mt * BM + m;
+            // decode the output row once per tile
+            int b = 0, q = 0, t1 = 0;
+            const bool rv = r < M;
+            if (rv) {
+                if (c.dense) {
+                    b = r / Nout;
+                    q = r - b * Nout;
+                } else {
+                    const int code = __ldg(c.ridx + r);
+                    const int gq = code >> 5;
+                    t1 = code & 31;
+                    b = gq / Nout;
+                    q = gq - b * Nout;
+                }
+            }
+            const int oy = q / g.Wout, ox = q - oy * g.Wout;
+            int cur_tap = -1;
+            const float *src = nullptr;
+            for (int kb = 0; kb < nkb; kb++) {
+                const int k0 = kb * BK;
+                const int tap = k0 / g.Cin, ci0 = k0 - tap * g.Cin;
+                if (tap != cur_tap) {
+                    cur_tap = tap;
+                    src = nullptr;
+                    if (rv) {
+                        const int dy = tap / g.kw, dx = tap - dy * g.kw;
+                        const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+                        if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                            const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
+                            if (c.dense) {
+                                src = A + bp * g.Cin;
+                            } else {
+                                const int row = row_of(c.a, bp, t1);
+                                if (row) src = A + (int64_t)row * g.Cin;
+                            }
+                        }
+                    }
+                }
+                mbar_wait(empty + stage, phase ^ 1);
+                unsigned char *sa = smem + stage * S::STAGE;
+                unsigned char *sb = sa + S::A_BYTES;
+                // ---- A row m: 64 fp32 -> 64 bf16 = 8 x 16 B chunks, swizzled
+                uint4 chunk[8];
+                if (src) {
+                    const float4 *p = reinterpret_cast<const float4 *>(src + ci0);
+                    float4 v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; i++) v[i] = __ldg(p + i);
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        chunk[j].x = pack_bf16x2(v[2 * j].x, v[2 * j].y);
+                        chunk[j].y = pack_bf16x2(v[2 * j].z, v[2 * j].w);
+                        chunk[j].z = pack_bf16x2(v[2 * j + 1].x, v[2 * j + 1].y);
+                        chunk[j].w = pack_bf16x2(v[2 * j + 1].z, v[2 * j + 1].w);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; j++) chunk[j] = make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                    *reinterpret_cast<uint4 *>(sa + m * 128 + ((j ^ (m & 7)) << 4)) = chunk[j];
+                // ---- B tile: BN rows x 8 chunks, bf16 weights [Cout][K]
+#pragma unroll
+                for (int cidx = m; cidx < BN * 8; cidx += NPROD) {
+                    const int n = cidx >> 3, j = cidx & 7;
+                    const int co = nt * BN + n;
+                    uint4 w = make_uint4(0, 0, 0, 0);
+                    if (co < g.Cout) w = __ldg(reinterpret_cast<const uint4 *>(wbf + (int64_t)co * K + k0) + j);
+                    *reinterpret_cast<uint4 *>(sb + n * 128 + ((j ^ (n & 7)) << 4)) = w;
+                }
+                fence_proxy_async();
+                mbar_arrive(full + stage);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 4) {
+        // ===================== MMA issuer =====================
+        constexpr uint32_t IDESC = idesc_bf16(BM, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            mbar_wait(tempty + acc, acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + acc * BN;
+            for (int kb = 0; kb < nkb; kb++) {
+                mbar_wait(full + stage, phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = smem_u32(smem + stage * S::STAGE);
+                    const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; k++)
+                        tc_mma(tmem_d, sdesc(sa + k * 32), sdesc(sb + k * 32), IDESC, (kb | k) != 0);
+                    tc_commit(empty + stage);
+                    if (kb == nkb - 1) tc_commit(tfull + acc);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue =====================
+        const int quarter = warp & 3;            // TMEM lane quarter accessible by this warp
+        const int row_in_tile = quarter * 32 + lane;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const int mt = tile / ntn, nt = tile - mt * ntn;
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            mbar_wait(tfull + acc, acc_phase);
+            tc_fence_after();
+            const int r = mt * BM + row_in_tile;
+            float *o = c.dense ? c.out + (int64_t)r * g.Cout : c.out + (int64_t)(r + 1) * g.Cout;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int n0 = nt * BN + c0;
+                if (r < M && n0 < g.Cout) {
+                    if (n0 + 32 <= g.Cout) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            float4 f;
+                            f.x = __uint_as_float(v[j]);
+                            f.y = __uint_as_float(v[j + 1]);
+                            f.z = __uint_as_float(v[j + 2]);
+                            f.w = __uint_as_float(v[j + 3]);
+                            if (c.dense) {
+                                f.x = __fadd_rn(f.x, __ldg(c.bias + n0 + j));
+                                f.y = __fadd_rn(f.y, __ldg(c.bias + n0 + j + 1));
+                                f.z = __fadd_rn(f.z, __ldg(c.bias + n0 + j + 2));
+                                f.w = __fadd_rn(f.w, __ldg(c.bias + n0 + j + 3));
+                            }
+                            *reinterpret_cast<float4 *>(o + n0 + j) = f;
+                        }
+                    } else {
+                        for (int j = 0; j < 32 && n0 + j < g.Cout; j++) {
+                            float f = __uint_as_float(v[j]);
+                            if (c.dense) f = __fadd_rn(f, __ldg(c.bias + n0 + j));
+                            o[n0 + j] = f;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty + acc);
+        }
+    }
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+template <int BN>
+static void launch_tc(const ConvCall &c, const __nv_bfloat16 *wbf, cudaStream_t s, int num_sms) {
+    using S = tc::Smem<BN>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+        attr = true;
+    }
+    const int ntn = (c.g.Cout + BN - 1) / BN;
+    const int64_t m_up = c.dense ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
+    const int64_t tiles = ((m_up + tc::BM - 1) / tc::BM) * ntn;
+    int grid = (int)std::min<int64_t>(tiles, num_sms);
+    if (grid < 1) grid = 1;
+    k_conv_tc<BN><<<grid, tc::NTHREADS, S::TOTAL, s>>>(c, wbf);
+}
+
+bool conv_tc_eligible(const Geo &g) {
+    return g.groups == 1 && g.Cin % tc::BK == 0 && g.Cout % 16 == 0;
+}
+
+void launch_conv_tc(const ConvCall &c, const void *wbf_v, cudaStream_t s) {
+    const __nv_bfloat16 *wbf = static_cast<const __nv_bfloat16 *>(wbf_v);
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (c.g.Cout >= 256) launch_tc<256>(c, wbf, s, num_sms);
+    else if (c.g.Cout >= 128) launch_tc<128>(c, wbf, s, num_sms);
+    else if (c.g.Cout >= 64) launch_tc<64>(c, wbf, s, num_sms);
+    else launch_tc<32>(c, wbf, s, num_sms);
+}
+
+}  // namespace st

@@ -16,12 +16,13 @@ import workloads as W
 REL, ABS = 1e-4, 1e-5   # north_star fp32 tolerance (reading R29)
 
 
-def gpu_run(net, frames_np, thresholds, debug=True, device=0, max_frames=None):
+def gpu_run(net, frames_np, thresholds, debug=True, device=0, max_frames=None, precision="fp32"):
     """frames_np float32 [B][L][H][W][C] -> (encoder, torch frames)."""
     import torch
     from paper_2410_20790_b200 import Encoder
     B, L = frames_np.shape[:2]
-    enc = Encoder(net, max_chunks=B, max_frames=max_frames or L, debug_retain=debug, device=device)
+    enc = Encoder(net, max_chunks=B, max_frames=max_frames or L, debug_retain=debug, device=device,
+                  precision=precision)
     fr = torch.from_numpy(np.ascontiguousarray(frames_np)).to(f"cuda:{device}")
     enc.encode_reference(fr[:, 0])
     enc.encode_diff(fr[:, 1:] if L > 1 else None, thresholds)
