@@ -28,11 +28,11 @@ namespace {
 
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
-              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_N = 16;
+              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16, KC_N = 17;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
                               "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
-                              "conv_tc_sparse", "conv_tc_dense"};
+                              "conv_tc_sparse", "conv_tc_dense", "se"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -52,6 +52,8 @@ struct LayerRT {
     // device weights (separate allocation)
     float *wk = nullptr, *bias = nullptr;
     uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
+    float *se_w1 = nullptr, *se_b1 = nullptr, *se_w2 = nullptr, *se_b2 = nullptr;   // SE MLP
+    int b_se = -1;            // SE scratch: sum0 [B][C] f64 | dsum [B][F][C] f64 | s_tab [B][F+1][C] | refresh [B]
     // buffer ids (-1 = none / alias)
     int b_y0 = -1, b_act = -1, b_slot = -1, b_pbase = -1, b_rows = -1, b_ridx = -1, b_out = -1;
     int alias_rows_of = -1;   // rows / slot / pbase borrowed from another tensor
@@ -220,7 +222,10 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             l.H = sh; l.W = sw; l.C = sc;
             break;
         case ST_SE:
-            return ST_ERR_UNSUPPORTED;
+            if (!layers[i].w || !layers[i].b || !layers[i].w2 || !layers[i].b2 || layers[i].se_hidden < 1)
+                return ST_ERR_ARG;
+            l.H = sh; l.W = sw; l.C = sc;
+            break;
         default:
             return ST_ERR_ARG;
         }
@@ -248,12 +253,29 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
         if (l.kind == ST_CONV) {
             const int cin_g = l.geo.Cin / l.spec.groups;
             wfloats += ((int64_t)l.spec.k_h * l.spec.k_w * cin_g * l.C + 63) / 64 * 64 + (l.C + 63) / 64 * 64;
+        } else if (l.kind == ST_SE) {
+            const int64_t hc = (int64_t)l.spec.se_hidden * l.C;
+            wfloats += 2 * ((hc + 63) / 64 * 64) + (l.spec.se_hidden + 63) / 64 * 64 + (l.C + 63) / 64 * 64;
         }
     CUDA_OK(e.get(), cudaMalloc(&e->weights_mem, std::max<int64_t>(wfloats, 1) * sizeof(float)));
     {
         std::vector<float> host(std::max<int64_t>(wfloats, 1));
         int64_t o = 0;
+        auto put = [&](const float *src, int64_t n) {
+            float *dst = e->weights_mem + o;
+            for (int64_t k = 0; k < n; k++) host[o + k] = src[k];
+            o += (n + 63) / 64 * 64;
+            return dst;
+        };
         for (auto &l : e->L) {
+            if (l.kind == ST_SE) {
+                const int64_t hc = (int64_t)l.spec.se_hidden * l.C;
+                l.se_w1 = put(l.spec.w, hc);
+                l.se_b1 = put(l.spec.b, l.spec.se_hidden);
+                l.se_w2 = put(l.spec.w2, hc);
+                l.se_b2 = put(l.spec.b2, l.C);
+                continue;
+            }
             if (l.kind != ST_CONV) continue;
             const int kh = l.spec.k_h, kw = l.spec.k_w, cin_g = l.geo.Cin / l.spec.groups, co = l.C;
             l.wk = e->weights_mem + o;
@@ -356,10 +378,12 @@ static st_status plan(st_encoder *e) {
             l.b_rows = add((l.rows_cap + 1) * l.C * 4, tdef, tlast);
             l.b_ridx = add(std::max<int64_t>(l.rows_cap, 1) * 4, tdef, tdef);
             break;
-        case ST_MAXPOOL: case ST_ADD:
+        case ST_MAXPOOL: case ST_ADD: case ST_SE:
             l.b_slot = add(B * N * 4, tdef, tlast);
             l.b_pbase = add(B * N * 4, tdef, tlast);
             l.b_rows = add((l.rows_cap + 1) * l.C * 4, tdef, tlast);
+            if (l.kind == ST_SE)   // sum0 | dsum | s_tab | refresh, used only while the layer runs
+                l.b_se = add(B * l.C * 8 + B * F * l.C * 8 + B * (F + 1) * l.C * 4 + B * 4 + 64, tdef, tdef);
             break;
         case ST_RELU: case ST_SILU: {
             // emitted rows go into the input's slot layout; in place when
@@ -660,6 +684,34 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_ADD, i, s, launch_add_rows(in, in2, slot, pb, B, (int)N, l.C, e->p<float>(l.b_rows), s));
             CUDA_OK(e, cudaMemcpyAsync(e->p<uint32_t>(l.b_act), slot, (size_t)B * N * 4, cudaMemcpyDeviceToDevice, s));
+            break;
+        }
+        case ST_SE: {
+            // reading R8: sums of x0 and of every frame's delta rows -> sequential
+            // gate schedule per chunk -> dense apply + pixel loop
+            char *sb = e->ptr(l.b_se);
+            double *sum0 = reinterpret_cast<double *>(sb);
+            double *dsum = sum0 + (int64_t)B * l.C;
+            float *s_tab = reinterpret_cast<float *>(dsum + (int64_t)B * F * l.C);
+            uint32_t *refresh = reinterpret_cast<uint32_t *>(s_tab + (int64_t)B * (F + 1) * l.C);
+            const int H = l.spec.se_hidden;
+            LAUNCH(e, KC_SE, i, s, launch_se_colsum(x_src, B, (int)N, l.C, sum0, s));
+            if (F > 0) LAUNCH(e, KC_SE, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, dsum, s));
+            LAUNCH(e, KC_SE, i, s,
+                   launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
+                                      thresholds[l.site], s_tab, refresh, s));
+            LAUNCH(e, KC_SE, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
+            if (F == 0) break;
+            uint32_t *slot = e->p<uint32_t>(l.b_slot);
+            int32_t *pb = e->p<int32_t>(l.b_pbase);
+            LAUNCH(e, KC_SE, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            LAUNCH(e, KC_SE, i, s,
+                   launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds[l.site], slot, pb,
+                                  e->p<uint32_t>(l.b_act), e->p<float>(l.b_rows), s));
+            LAUNCH(e, KC_COUNTS, i, s,
+                   launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
+                                       e->site_sum + l.site, nullptr, s));
             break;
         }
         case ST_OUTPUT: {

@@ -88,6 +88,16 @@ void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float t
 // residual add: out slot layout = act_a | act_b (already scanned into pbase)
 void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C,
                      float *out_rows, cudaStream_t s);
+// ---- squeeze-excitation site (kernels_se.cu, reading R8) ----
+void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s);
+void launch_se_delta_sums(DView in, int B, int N, int C, int F, double *dsum, cudaStream_t s);
+void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
+                        const float *b1, const float *w2, const float *b2, float theta, float *s_tab,
+                        uint32_t *refresh, cudaStream_t s);
+void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s);
+void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s);
+void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta,
+                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, float *out_rows, cudaStream_t s);
 // Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0)
 void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, float *out,
                        cudaStream_t s);

@@ -119,6 +119,34 @@ def test_cfg2_full_size_sampled():
         assert np.array_equal(act[b], r["counts"])
 
 
+@pytest.mark.parametrize("theta", [0.0, 0.01, 0.05])
+def test_se_site(theta):
+    """SE site (reading R8): gate refresh schedule, touched sets, values.
+    SiLU/sigmoid use (float)exp((double)x) on both sides (R10); the SE mean
+    is an fp64 sum in a different order on the GPU, so values are compared
+    at the fp32 tolerance and masks exactly (a rounding-order flip of the
+    fp32 mean would show up here)."""
+    n = Net(3, 12, 14)
+    x = n.silu(n.conv(-1, 24, 3))
+    s = n.se(x, 6)
+    n.output(n.conv(s, 16, 1, 1, 0))
+    init_weights(n, 21)
+    fr = np.stack([random_frames(40 + b, 9, 12, 14, 3, p_change=0.25, scale=0.3) for b in range(3)])
+    enc, _ = gpu_run(n, fr, theta)
+    for b in range(3):
+        compare_chunk(enc, n, fr[b], theta, b, exact=False)
+
+
+def test_efficientnet_small():
+    net = W.models.efficientnet_b0(64, 64)
+    init_weights(net, 13)
+    u8 = W.gen_video(2, 6, 64, 64, 3, 99, n_objects=4, size=(8, 24), speed=(1, 3), noise_q=0.1, noise_amp=2)
+    fr = W.to_float(u8)
+    enc, _ = gpu_run(net, fr, 0.05)
+    for b in range(2):
+        compare_chunk(enc, net, fr[b], 0.05, b, exact=False)
+
+
 def test_errors_and_state():
     from paper_2410_20790_b200 import Encoder, StError
     import torch
