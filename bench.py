@@ -206,30 +206,27 @@ def main():
                               cycle=cfg.cycle)
 
     # inputs: distinct synthetic batches per step (rank r owns global chunks r + world*j)
-    n_batches = max(1, min(cfg.steps, 4))
+    from paper_2410_20790_b200.sharding import shard
+    n_batches = max(1, min(cfg.steps, 4 if cfg.h * cfg.w <= 512 * 512 else 2))
     batches = []
     for s in range(n_batches):
-        u8 = np.stack([W.gen_chunk(cfg.video_seed(s * B * world + rank + world * j), L, cfg.h, cfg.w, cfg.c,
-                                   **cfg.video) for j in range(B)])
+        u8 = np.stack([W.gen_chunk(cfg.video_seed(cid), L, cfg.h, cfg.w, cfg.c, **cfg.video)
+                       for cid in shard(s, B * world, rank, world)])
         batches.append(torch.from_numpy(W.to_float(u8)).to(dev))
     frame_bytes = batches[0].numel() * 4
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    counts_dev = torch.zeros(2 * ns, dtype=torch.int64, device=dev)
-    gathered = torch.zeros(world * 2 * ns, dtype=torch.int64, device=dev) if world > 1 else None
+    from paper_2410_20790_b200.sharding import StatsExchange
+    ex = StatsExchange(ns, device=dev)
 
     def step(x):
         th = ctl.thresholds()
         enc.encode_reference(x[:, 0], stream)
         enc.encode_diff(x[:, 1:], th, stream)
         if policy != "fixed":
-            enc.copy_site_counts(counts_dev, stream)
-            if world > 1:
-                dist.all_gather_into_tensor(gathered, counts_dev)
-                tot = gathered.view(world, 2 * ns).sum(0).cpu().numpy()
-            else:
-                tot = counts_dev.cpu().numpy()
-            ctl.observe(tot[:ns], tot[ns:])
+            # the only collective: NCCL all-gather of int64 per-site counts
+            enc.copy_site_counts(ex.local, stream)
+            ctl.observe(*ex.exchange())
 
     for w in range(args.warmup):
         step(batches[w % n_batches])
