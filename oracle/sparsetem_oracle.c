@@ -112,10 +112,15 @@ static float relu_f(float x) { return x > 0.0f ? x : 0.0f; }
 static float silu_f(float x) { return x / (1.0f + exp_r(-x)); }          /* R10 */
 static float sigm_f(float x) { return 1.0f / (1.0f + exp_r(-x)); }       /* R10 */
 
-/* Precision mode (R22-BF16).  0 = FP32 mode.  1 = BF16 mode: a
- * convolution with groups == 1, c_in % 64 == 0 and c_out % 16 == 0 multiplies
- * bf16-rounded (round-to-nearest-even) operands -- the weight and the input
- * value -- and accumulates in fp32; everything else is unchanged. */
+/* Precision mode (R22-BF16).  0 = FP32 mode.  1 = BF16 mode:
+ *  - every emitted delta (input Subtraction, conv output, residual add, every
+ *    non-linear site) is stored rounded to bf16 (round-to-nearest-even); the
+ *    truncation decision is taken on the fp32 value, and the Subtraction
+ *    buffer S and each site's y_acc advance by the rounded (emitted) value;
+ *  - a convolution with groups == 1, c_in % 64 == 0 and c_out % 16 == 0
+ *    multiplies bf16-rounded operands (weight and input value) and
+ *    accumulates in fp32;
+ *  - dense reference activations, site states and outputs stay fp32. */
 static int g_bf16 = 0;
 void orc_set_precision(int bf16) { g_bf16 = bf16 ? 1 : 0; }
 
@@ -127,6 +132,7 @@ static float bf16r(float v) {
     memcpy(&v, &u, 4);
     return v;
 }
+static float emit_r(float v) { return g_bf16 ? bf16r(v) : v; }
 
 /* ------------------------------------------------------------ dense ops */
 
@@ -319,8 +325,9 @@ static void step_input(ctx_t *c, int t, const float *X, float *d, uint8_t *m) {
             m[p] = 1;
             cnt++;
             for (int ch = 0; ch < C; ch++) {
-                d[(size_t)p * C + ch] = raw[ch];
-                c->S[(size_t)p * C + ch] = c->S[(size_t)p * C + ch] + raw[ch];   /* R3 */
+                const float e = emit_r(raw[ch]);                   /* stored delta */
+                d[(size_t)p * C + ch] = e;
+                c->S[(size_t)p * C + ch] = c->S[(size_t)p * C + ch] + e;   /* R3 */
             }
         } else {
             m[p] = 0;
@@ -338,7 +345,11 @@ static int trunc_emit(const float *cand, int C, float th, float *ya, float *dout
         mx = a > mx ? a : mx;
     }
     if (mx > th) {
-        for (int ch = 0; ch < C; ch++) { ya[ch] = ya[ch] + cand[ch]; dout[ch] = cand[ch]; }
+        for (int ch = 0; ch < C; ch++) {
+            const float e = emit_r(cand[ch]);   /* stored delta; y_acc advances by it */
+            ya[ch] = ya[ch] + e;
+            dout[ch] = e;
+        }
         return 1;
     }
     for (int ch = 0; ch < C; ch++) dout[ch] = 0.0f;
@@ -356,12 +367,14 @@ static void step_layer(ctx_t *c, int i, int t, const float *d_a, const uint8_t *
     case ORC_CONV:
         dilate(m_a, si.h, si.w, l->k_h, l->k_w, l->s_h, l->s_w, l->p_h, l->p_w, so.h, so.w, m);
         conv_apply(l, si, so, d_a, m, 0, d);                        /* Eq.(2): no bias */
+        if (g_bf16)
+            for (size_t k = 0; k < (size_t)No * C; k++) d[k] = emit_r(d[k]);
         break;
     case ORC_ADD:
         for (int p = 0; p < No; p++) {
             m[p] = (uint8_t)(m_a[p] | m_b[p]);
             for (int ch = 0; ch < C; ch++)
-                d[(size_t)p * C + ch] = d_a[(size_t)p * C + ch] + d_b[(size_t)p * C + ch];
+                d[(size_t)p * C + ch] = emit_r(d_a[(size_t)p * C + ch] + d_b[(size_t)p * C + ch]);
         }
         break;
     case ORC_OUTPUT: {

@@ -2,11 +2,14 @@
 #pragma once
 #include <algorithm>
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "kernels.h"
 
 namespace st {
+
+typedef __nv_bfloat16 bf16;
 
 __device__ __forceinline__ uint32_t lowmask(int t1) { return (1u << t1) - 1u; }
 
@@ -15,6 +18,30 @@ __device__ __forceinline__ int row_of(const DView &v, int64_t bp, int t1) {
     const uint32_t a = __ldg(v.act + bp);
     if (!((a >> t1) & 1u)) return 0;
     return 1 + __ldg(v.pbase + bp) + __popc(__ldg(v.slot + bp) & lowmask(t1));
+}
+
+// ---- delta-row storage type T: float (FP32 mode) or bf16 (BF16 mode, R22-BF16)
+template <class T> __device__ __forceinline__ float ldr(const T *p);
+template <> __device__ __forceinline__ float ldr<float>(const float *p) { return *p; }
+template <> __device__ __forceinline__ float ldr<bf16>(const bf16 *p) { return __bfloat162float(*p); }
+template <class T> __device__ __forceinline__ void str(T *p, float v);
+template <> __device__ __forceinline__ void str<float>(float *p, float v) { *p = v; }
+template <> __device__ __forceinline__ void str<bf16>(bf16 *p, float v) { *p = __float2bfloat16_rn(v); }
+// the value as it will be stored (the emitted delta)
+template <class T> __device__ __forceinline__ float rnd(float v);
+template <> __device__ __forceinline__ float rnd<float>(float v) { return v; }
+template <> __device__ __forceinline__ float rnd<bf16>(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+// 4 consecutive elements -> float4 (p 4-element aligned)
+template <class T> __device__ __forceinline__ float4 ld4(const T *p);
+template <> __device__ __forceinline__ float4 ld4<float>(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+template <> __device__ __forceinline__ float4 ld4<bf16>(const bf16 *p) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
+    float4 f;
+    f.x = __uint_as_float(u.x << 16);
+    f.y = __uint_as_float(u.x & 0xFFFF0000u);
+    f.z = __uint_as_float(u.y << 16);
+    f.w = __uint_as_float(u.y & 0xFFFF0000u);
+    return f;
 }
 
 template <int G>
@@ -31,5 +58,17 @@ __device__ __forceinline__ float silu_f(float x) { return __fdiv_rn(x, __fadd_rn
 __device__ __forceinline__ float sigm_f(float x) { return __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_r(-x))); }
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// host-side dispatch on the row type
+#define ST_ROW_DISPATCH(bf, ...)            \
+    do {                                    \
+        if (bf) {                           \
+            typedef ::st::bf16 T;           \
+            __VA_ARGS__;                    \
+        } else {                            \
+            typedef float T;                \
+            __VA_ARGS__;                    \
+        }                                   \
+    } while (0)
 
 }  // namespace st

@@ -52,6 +52,7 @@ struct LayerRT {
     // device weights (separate allocation)
     float *wk = nullptr, *bias = nullptr;
     uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
+    alignas(64) unsigned char tmap[128] = {};   // CUtensorMap of wbf (tc layers)
     float *se_w1 = nullptr, *se_b1 = nullptr, *se_w2 = nullptr, *se_b2 = nullptr;   // SE MLP
     int b_se = -1;            // SE scratch: sum0 [B][C] f64 | dsum [B][F][C] f64 | s_tab [B][F+1][C] | refresh [B]
     // buffer ids (-1 = none / alias)
@@ -76,6 +77,8 @@ struct st_encoder {
     // input site tensor buffers
     int in_act = -1, in_pbase = -1, in_rows = -1;
     int64_t in_rows_cap = 0;
+    bool bf = false;             // BF16 mode: delta rows stored as bf16 (R22-BF16)
+    int esz = 4;                 // delta-row element size in bytes
     std::vector<Buf> bufs;
     char *arena = nullptr;
     int64_t arena_bytes = 0, persistent_bytes = 0, peak_transient = 0;
@@ -176,6 +179,8 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     e->in_C = cfg->in_c;
     e->B = cfg->max_chunks;
     e->F = cfg->max_frames - 1;
+    e->bf = cfg->precision == ST_BF16;
+    e->esz = e->bf ? 2 : 4;
     e->L.resize(n);
     // ---- validate + shapes
     for (int i = 0; i < n; i++) {
@@ -322,6 +327,9 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 o += (K * co + 127) / 128 * 128;
             }
             CUDA_OK(e.get(), cudaMemcpy(e->wbf_mem, hb.data(), nbf * 2, cudaMemcpyHostToDevice));
+            for (auto &l : e->L)
+                if (l.tc && !make_weight_tmap(l.tmap, l.wbf, l.spec.k_h * l.spec.k_w * l.geo.Cin, l.C))
+                    return fail(e.get(), ST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         }
     }
     for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
@@ -357,7 +365,8 @@ static st_status plan(st_encoder *e) {
     e->in_rows_cap = B * F * Nin;
     e->in_act = add(B * Nin * 4, 0, in_last);
     e->in_pbase = add(B * Nin * 4, 0, in_last);
-    e->in_rows = add((e->in_rows_cap + 1) * e->in_C * 4, 0, in_last);
+    const int64_t ES = e->esz;   // delta-row element size: 4 (FP32 mode) or 2 (BF16 mode)
+    e->in_rows = add((e->in_rows_cap + 1) * e->in_C * ES, 0, in_last);
     // per-layer tensors
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -375,13 +384,13 @@ static st_status plan(st_encoder *e) {
         switch (l.kind) {
         case ST_CONV:
             l.b_pbase = add(B * N * 4, tdef, tlast);
-            l.b_rows = add((l.rows_cap + 1) * l.C * 4, tdef, tlast);
+            l.b_rows = add((l.rows_cap + 1) * l.C * ES, tdef, tlast);
             l.b_ridx = add(std::max<int64_t>(l.rows_cap, 1) * 4, tdef, tdef);
             break;
         case ST_MAXPOOL: case ST_ADD: case ST_SE:
             l.b_slot = add(B * N * 4, tdef, tlast);
             l.b_pbase = add(B * N * 4, tdef, tlast);
-            l.b_rows = add((l.rows_cap + 1) * l.C * 4, tdef, tlast);
+            l.b_rows = add((l.rows_cap + 1) * l.C * ES, tdef, tlast);
             if (l.kind == ST_SE)   // sum0 | dsum | s_tab | refresh, used only while the layer runs
                 l.b_se = add(B * l.C * 8 + B * F * l.C * 8 + B * (F + 1) * l.C * 4 + B * 4 + 64, tdef, tdef);
             break;
@@ -395,7 +404,7 @@ static st_status plan(st_encoder *e) {
             } else {
                 l.alias_rows_of = l.src;   // slot/pbase still borrowed
                 const int64_t cap = sl ? sl->rows_cap : e->in_rows_cap;
-                l.b_rows = add((cap + 1) * l.C * 4, tdef, tlast);
+                l.b_rows = add((cap + 1) * l.C * ES, tdef, tlast);
             }
             break;
         }
@@ -526,7 +535,7 @@ static DView view_of(const st_encoder *e, int t) {
         v.act = e->p<uint32_t>(e->in_act);
         v.slot = v.act;
         v.pbase = e->p<int32_t>(e->in_pbase);
-        v.rows = e->p<float>(e->in_rows);
+        v.rows = e->ptr(e->in_rows);
         return v;
     }
     const LayerRT &l = e->L[t];
@@ -536,12 +545,12 @@ static DView view_of(const st_encoder *e, int t) {
         DView s = view_of(e, l.src);
         v.slot = s.slot;
         v.pbase = s.pbase;
-        v.rows = l.b_rows >= 0 ? e->p<float>(l.b_rows) : s.rows;
+        v.rows = l.b_rows >= 0 ? static_cast<const void *>(e->ptr(l.b_rows)) : s.rows;
         return v;
     }
     v.slot = l.b_slot >= 0 ? e->p<uint32_t>(l.b_slot) : v.act;
     v.pbase = e->p<int32_t>(l.b_pbase);
-    v.rows = e->p<float>(l.b_rows);
+    v.rows = e->ptr(l.b_rows);
     return v;
 }
 
@@ -584,22 +593,23 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
     CUDA_OK(e, cudaMemsetAsync(e->site_sum, 0, (size_t)e->n_sites * 8, s));
     const int64_t cstride = (int64_t)e->n_sites * 32;
     auto zero_row = [&](int buf, int C) {
-        if (buf >= 0) cudaMemsetAsync(e->ptr(buf), 0, (size_t)C * 4, s);
+        if (buf >= 0) cudaMemsetAsync(e->ptr(buf), 0, (size_t)C * e->esz, s);
     };
+    const bool bf = e->bf;
 
     // ---------------- input site: Subtraction + truncation + compaction (a2)
     if (F > 0) {
         uint32_t *act = e->p<uint32_t>(e->in_act);
         int32_t *pb = e->p<int32_t>(e->in_pbase);
-        float *rows = e->p<float>(e->in_rows);
+        void *rows = e->ptr(e->in_rows);
         const float *fr = frames_dev;
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds[0], act, s));
+               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds[0], bf, act, s));
         LAUNCH(e, KC_SCAN, -1, s,
                launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
         zero_row(e->in_rows, e->in_C);
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_rows(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, act, pb, rows, s));
+               launch_subtract_rows(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, act, pb, rows, bf, s));
         LAUNCH(e, KC_COUNTS, -1, s,
                launch_frame_counts(act, B, (int)Nin, e->counts, cstride, e->site_sum, nullptr, s));
     }
@@ -626,7 +636,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
             LAUNCH(e, l.depthwise ? KC_DW_DENSE : (l.tc ? KC_TC_DENSE : KC_CONV_DENSE), i, s,
-                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.wbf, s) : launch_conv_f32(c, s)));
+                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.tmap, s) : launch_conv_f32(c, s)));
             if (F == 0) break;
             uint32_t *act = e->p<uint32_t>(l.b_act);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -635,13 +645,14 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             LAUNCH(e, KC_ENUM, i, s, launch_enumerate(act, pb, B * N, e->p<int32_t>(l.b_ridx), s));
             zero_row(l.b_rows, l.C);
             c.dense = false;
+            c.bf = bf;
             c.a = in;
             c.ridx = e->p<int32_t>(l.b_ridx);
             c.m_dev = e->totals + i;
             c.m_cap = (int64_t)B * F * N;
-            c.out = e->p<float>(l.b_rows);
+            c.out = e->ptr(l.b_rows);
             LAUNCH(e, l.depthwise ? KC_DW_SPARSE : (l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE), i, s,
-                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.wbf, s) : launch_conv_f32(c, s)));
+                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.tmap, s) : launch_conv_f32(c, s)));
             break;
         }
         case ST_RELU: case ST_SILU: {
@@ -650,8 +661,8 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             if (F == 0) break;
             DView me = view_of(e, i);
             LAUNCH(e, KC_SITE_PW, i, s,
-                   launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds[l.site],
-                                         e->p<uint32_t>(l.b_act), const_cast<float *>(me.rows), s));
+                   launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds[l.site], bf,
+                                         e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
@@ -665,8 +676,8 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             LAUNCH(e, KC_SITE_MP, i, s,
-                   launch_site_maxpool(in, x_src, B, l.geo, thresholds[l.site], slot, pb, e->p<uint32_t>(l.b_act),
-                                       e->p<float>(l.b_rows), s));
+                   launch_site_maxpool(in, x_src, B, l.geo, thresholds[l.site], bf, slot, pb,
+                                       e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
@@ -682,7 +693,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             LAUNCH(e, KC_ADD, i, s, launch_or_words(in.act, in2.act, B * N, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             zero_row(l.b_rows, l.C);
-            LAUNCH(e, KC_ADD, i, s, launch_add_rows(in, in2, slot, pb, B, (int)N, l.C, e->p<float>(l.b_rows), s));
+            LAUNCH(e, KC_ADD, i, s, launch_add_rows(in, in2, slot, pb, B, (int)N, l.C, bf, e->ptr(l.b_rows), s));
             CUDA_OK(e, cudaMemcpyAsync(e->p<uint32_t>(l.b_act), slot, (size_t)B * N * 4, cudaMemcpyDeviceToDevice, s));
             break;
         }
@@ -696,7 +707,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             uint32_t *refresh = reinterpret_cast<uint32_t *>(s_tab + (int64_t)B * (F + 1) * l.C);
             const int H = l.spec.se_hidden;
             LAUNCH(e, KC_SE, i, s, launch_se_colsum(x_src, B, (int)N, l.C, sum0, s));
-            if (F > 0) LAUNCH(e, KC_SE, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, dsum, s));
+            if (F > 0) LAUNCH(e, KC_SE, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
             LAUNCH(e, KC_SE, i, s,
                    launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
                                       thresholds[l.site], s_tab, refresh, s));
@@ -707,8 +718,8 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             LAUNCH(e, KC_SE, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             LAUNCH(e, KC_SE, i, s,
-                   launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds[l.site], slot, pb,
-                                  e->p<uint32_t>(l.b_act), e->p<float>(l.b_rows), s));
+                   launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds[l.site], bf, slot, pb,
+                                  e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
@@ -717,7 +728,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
         case ST_OUTPUT: {
             DView v = F > 0 ? in : DView{};
             LAUNCH(e, KC_ACCUM, i, s,
-                   launch_accumulate(v, x_src, B, (int)N, l.C, F, e->p<float>(l.b_out), s));
+                   launch_accumulate(v, x_src, B, (int)N, l.C, F, bf, e->p<float>(l.b_out), s));
             break;
         }
         default:
@@ -863,7 +874,17 @@ extern "C" st_status st_debug_get_rows(st_encoder *e, int32_t layer, int32_t chu
         if (idx) idx[k] = (int32_t)p;
         if (rows) {
             const int64_t row = 1 + pb[p] + __builtin_popcount(slot[p] & ((1u << t1) - 1u));
-            CUDA_OK(e, cudaMemcpy(rows + k * C, v.rows + row * C, C * 4, cudaMemcpyDeviceToHost));
+            const char *src = static_cast<const char *>(v.rows) + row * C * e->esz;
+            if (e->esz == 4) {
+                CUDA_OK(e, cudaMemcpy(rows + k * C, src, C * 4, cudaMemcpyDeviceToHost));
+            } else {   // bf16 -> fp32 (exact)
+                std::vector<uint16_t> hb(C);
+                CUDA_OK(e, cudaMemcpy(hb.data(), src, C * 2, cudaMemcpyDeviceToHost));
+                for (int ch = 0; ch < C; ch++) {
+                    const uint32_t u = (uint32_t)hb[ch] << 16;
+                    std::memcpy(rows + k * C + ch, &u, 4);
+                }
+            }
         }
         k++;
     }

@@ -6,7 +6,8 @@
 //                        (pixel-major "frame words", so L-1 <= 32, R25)
 //   slot [B][N] uint32   frame bits that own a row (superset of act)
 //   pbase[B][N] int32    exclusive prefix over (b,p) of popc(slot)
-//   rows [1+cap][C] f32  packed delta rows in (b, p, t) order; row 0 = zeros
+//   rows [1+cap][C]      packed delta rows in (b, p, t) order; row 0 = zeros;
+//                        fp32 in FP32 mode, bf16 in BF16 mode (`bf` flags)
 // Row of (b,p,t) = 1 + pbase[b,p] + popc(slot[b,p] & ((1<<(t-1))-1)) when the
 // act bit is set, else row 0.  Consumers never read rows of inactive bits.
 #pragma once
@@ -19,7 +20,7 @@ struct DView {
     const uint32_t *act = nullptr;
     const uint32_t *slot = nullptr;
     const int32_t *pbase = nullptr;
-    const float *rows = nullptr;
+    const void *rows = nullptr;   // float or bf16 [1+cap][C]
 };
 
 struct Geo {   // conv / pool geometry
@@ -29,10 +30,10 @@ struct Geo {   // conv / pool geometry
 // ---- masks, compaction (kernels_mask.cu) ----
 // Subtraction pass 1 (site 0): act bits per pixel, sequential over frames.
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
-                          int B, int N, int C, int n_diff, float theta, uint32_t *act, cudaStream_t s);
+                          int B, int N, int C, int n_diff, float theta, bool bf, uint32_t *act, cudaStream_t s);
 // Subtraction pass 2: write emitted rows at the slots of `act`.
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
-                          int B, int N, int C, const uint32_t *act, const int32_t *pbase, float *rows,
+                          int B, int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
                           cudaStream_t s);
 // out[b][q] = OR of in[b][p] over the receptive field (dense amplification)
 void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaStream_t s);
@@ -55,7 +56,8 @@ void launch_or_words(const uint32_t *a, const uint32_t *b, int64_t n, uint32_t *
 struct ConvCall {
     Geo g;
     int B;
-    bool dense;             // reference-frame mode
+    bool dense;             // reference-frame mode (fp32 activations in and out)
+    bool bf;                // sparse mode: rows are bf16 (BF16 mode)
     // A operand
     const float *a_dense;   // dense: [B][Nin][Cin]
     DView a;                // sparse
@@ -65,13 +67,16 @@ struct ConvCall {
     // B operand / output
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only
-    float *out;             // dense: [B*Nout][Cout]; sparse: rows_out (row 1+r)
+    void *out;              // dense: float [B*Nout][Cout]; sparse: rows_out (row 1+r)
 };
 void launch_conv_f32(const ConvCall &c, cudaStream_t s);
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s);
-// BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu); wbf = bf16 [Cout][K]
+// BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu).  Weights bf16
+// [Cout][K] are read through a TMA descriptor (CUtensorMap, 128 bytes)
+// built once at create by make_weight_tmap.
 bool conv_tc_eligible(const Geo &g);
-void launch_conv_tc(const ConvCall &c, const void *wbf, cudaStream_t s);
+bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout);
+void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s);
 
 // ---- sites, joins, accumulation (kernels_site.cu) ----
 enum Act { ACT_RELU = 0, ACT_SILU = 1 };
@@ -79,27 +84,27 @@ void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t
 void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s);
 void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s);
 // pointwise site: emitted rows written into out_rows at the input slots
-void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta,
-                           uint32_t *out_act, float *out_rows, cudaStream_t s);
+void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta, bool bf,
+                           uint32_t *out_act, void *out_rows, cudaStream_t s);
 // maxpool site: touched layout (t_slot, t_pbase) = dilation of in.act
-void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta,
-                         const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act,
-                         float *out_rows, cudaStream_t s);
+void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta, bool bf,
+                         const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
+                         cudaStream_t s);
 // residual add: out slot layout = act_a | act_b (already scanned into pbase)
-void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C,
-                     float *out_rows, cudaStream_t s);
+void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C, bool bf,
+                     void *out_rows, cudaStream_t s);
 // ---- squeeze-excitation site (kernels_se.cu, reading R8) ----
 void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s);
-void launch_se_delta_sums(DView in, int B, int N, int C, int F, double *dsum, cudaStream_t s);
+void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double *dsum, cudaStream_t s);
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                         const float *b1, const float *w2, const float *b2, float theta, float *s_tab,
                         uint32_t *refresh, cudaStream_t s);
 void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s);
 void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s);
-void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta,
-                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, float *out_rows, cudaStream_t s);
+void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta, bool bf,
+                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s);
 // Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0)
-void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, float *out,
+void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, bool bf, float *out,
                        cudaStream_t s);
 
 }  // namespace st

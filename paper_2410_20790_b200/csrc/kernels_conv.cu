@@ -1,13 +1,16 @@
 // kernels_conv.cu -- convolution on compacted deltas and the
-// dense reference-frame convolution (a1), FP32 exact mode.
+// dense reference-frame convolution (a1) on CUDA cores.
 //
 // Eq.(2): Delta_out = W x Delta_in, bias absent (R5).
 // As an implicit GEMM: M = output rows (sparse: the dilated output mask's
 // (b, q, t) rows from `ridx`; dense: every reference pixel), N = c_out,
 // K = k_h*k_w*c_in in the fixed order (dy, dx, ci) (reading R18).  Each
 // output is one thread's sequential fmaf chain over K starting from +0.0f,
-// so results are bit-identical to the oracle; inactive taps read nothing
-// (fma(w, 0, acc) == acc, so skipping them is exact).
+// so FP32-mode results are bit-identical to the oracle; inactive taps read
+// nothing (fma(w, 0, acc) == acc, so skipping them is exact).  Used for every
+// conv in FP32 mode and, in BF16 mode, for convs the tensor-core kernel does
+// not take (small c_in such as the stems); delta rows are of type T (fp32 or
+// bf16; bf16 rows are exact fp32 values, outputs are rounded on store).
 //
 // Tile: 128 rows x BN cols x 8 k, 256 threads, 8 x (BN/16) outputs per
 // thread, register-prefetched double-buffered shared memory; per M tile a
@@ -20,7 +23,7 @@ namespace st {
 
 constexpr int CBM = 128, CBK = 8, CNT = 256, CAPAD = 4;
 
-template <int BN, bool CINV>
+template <int BN, bool CINV, class T>
 __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
     constexpr int TN = BN / 16;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -35,7 +38,8 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
     const int M = c.dense ? c.B * Nout : *c.m_dev;
     const int ntn = (g.Cout + BN - 1) / BN;
     const int ntiles = ((M + CBM - 1) / CBM) * ntn;
-    const float *A = c.dense ? c.a_dense : c.a.rows;
+    // dense launches are instantiated with T = float
+    const T *A = c.dense ? reinterpret_cast<const T *>(c.a_dense) : static_cast<const T *>(c.a.rows);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const bool bvec = (g.Cout & 3) == 0;
     const int nk = (K + CBK - 1) / CBK;
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                 const int m = tid >> 1, half = tid & 1;
                 const int idx = tab[m * ntaps + tap];
                 if (idx >= 0) {
-                    const float4 v = __ldg(reinterpret_cast<const float4 *>(A + (int64_t)idx * g.Cin + ci0 + half * 4));
+                    const float4 v = ld4<T>(A + (int64_t)idx * g.Cin + ci0 + half * 4);
                     ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
                 } else {
                     ra[0] = ra[1] = ra[2] = ra[3] = 0.0f;
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                     float v = 0.0f;
                     if (k < K) {
                         const int idx = tab[m * ntaps + tap];
-                        if (idx >= 0) v = __ldg(A + (int64_t)idx * g.Cin + ci);
+                        if (idx >= 0) v = ldr<T>(A + (int64_t)idx * g.Cin + ci);
                     }
                     ra[j] = v;
                 }
@@ -185,23 +189,32 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
         for (int i = 0; i < 8; i++) {
             const int r = m0 + ty * 8 + i;
             if (r >= M) continue;
-            float *o = c.dense ? c.out + (int64_t)r * g.Cout : c.out + (int64_t)(r + 1) * g.Cout;
+            if (c.dense) {
+                float *o = static_cast<float *>(c.out) + (int64_t)r * g.Cout;
 #pragma unroll
-            for (int j = 0; j < TN; j++) {
-                const int n = n0 + tx * TN + j;
-                if (n < g.Cout) o[n] = c.dense ? __fadd_rn(acc[i][j], __ldg(c.bias + n)) : acc[i][j];
+                for (int j = 0; j < TN; j++) {
+                    const int n = n0 + tx * TN + j;
+                    if (n < g.Cout) o[n] = __fadd_rn(acc[i][j], __ldg(c.bias + n));
+                }
+            } else {
+                T *o = static_cast<T *>(c.out) + (int64_t)(r + 1) * g.Cout;
+#pragma unroll
+                for (int j = 0; j < TN; j++) {
+                    const int n = n0 + tx * TN + j;
+                    if (n < g.Cout) str<T>(o + n, acc[i][j]);
+                }
             }
         }
     }
 }
 
-template <int BN, bool CINV>
+template <int BN, bool CINV, class T>
 static void launch_one(const ConvCall &c, cudaStream_t s) {
     const int ntaps = c.g.kh * c.g.kw;
     const size_t smem = (2 * CBK * (CBM + CAPAD) + 2 * CBK * BN) * sizeof(float) + CBM * ntaps * sizeof(int);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_conv_f32<BN, CINV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_conv_f32<BN, CINV, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         attr_set = true;
     }
     const int ntn = (c.g.Cout + BN - 1) / BN;
@@ -209,24 +222,30 @@ static void launch_one(const ConvCall &c, cudaStream_t s) {
     int64_t tiles = ((m_up + CBM - 1) / CBM) * ntn;
     int grid = (int)(tiles < 148 * 2 ? tiles : 148 * 2);
     if (grid < 1) grid = 1;
-    k_conv_f32<BN, CINV><<<grid, CNT, smem, s>>>(c);
+    k_conv_f32<BN, CINV, T><<<grid, CNT, smem, s>>>(c);
+}
+
+template <class T>
+static void launch_conv_t(const ConvCall &c, cudaStream_t s) {
+    const bool cinv = (c.g.Cin % CBK) == 0;
+    if (c.g.Cout > 64) {
+        cinv ? launch_one<128, true, T>(c, s) : launch_one<128, false, T>(c, s);
+    } else if (c.g.Cout > 32) {
+        cinv ? launch_one<64, true, T>(c, s) : launch_one<64, false, T>(c, s);
+    } else {
+        cinv ? launch_one<32, true, T>(c, s) : launch_one<32, false, T>(c, s);
+    }
 }
 
 void launch_conv_f32(const ConvCall &c, cudaStream_t s) {
-    const bool cinv = (c.g.Cin % CBK) == 0;
-    if (c.g.Cout > 64) {
-        cinv ? launch_one<128, true>(c, s) : launch_one<128, false>(c, s);
-    } else if (c.g.Cout > 32) {
-        cinv ? launch_one<64, true>(c, s) : launch_one<64, false>(c, s);
-    } else {
-        cinv ? launch_one<32, true>(c, s) : launch_one<32, false>(c, s);
-    }
+    if (c.dense || !c.bf) launch_conv_t<float>(c, s);
+    else launch_conv_t<bf16>(c, s);
 }
 
 // ------------------------------------------------------------- depthwise
 // groups == Cin == Cout (reading R9): per output row and channel,
-// acc = fmaf chain over (dy, dx); weights [C][kh][kw] (OIHW with I = 1).
-template <int CPL>
+// acc = fmaf chain over (dy, dx); weights [kh*kw][C] (K-major repack).
+template <int CPL, class T>
 __global__ void __launch_bounds__(256) k_dwconv_f32(ConvCall c) {
     const Geo g = c.g;
     const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
@@ -234,7 +253,7 @@ __global__ void __launch_bounds__(256) k_dwconv_f32(ConvCall c) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const float *A = c.dense ? c.a_dense : c.a.rows;
+    const T *A = c.dense ? reinterpret_cast<const T *>(c.a_dense) : static_cast<const T *>(c.a.rows);
     for (int64_t r = warp; r < M; r += nwarps) {
         int b, q, t1 = 0;
         if (c.dense) {
@@ -266,31 +285,41 @@ __global__ void __launch_bounds__(256) k_dwconv_f32(ConvCall c) {
                     if (!row) continue;
                     idx = row;
                 }
-                const float *ap = A + idx * g.Cin;
+                const T *ap = A + idx * g.Cin;
                 const int tap = dy * g.kw + dx;
 #pragma unroll
                 for (int i = 0; i < CPL; i++) {
                     const int ch = lane + 32 * i;
-                    if (ch < g.Cin) acc[i] = fmaf(__ldg(c.wk + (int64_t)tap * g.Cout + ch), __ldg(ap + ch), acc[i]);
+                    if (ch < g.Cin) acc[i] = fmaf(__ldg(c.wk + (int64_t)tap * g.Cout + ch), ldr<T>(ap + ch), acc[i]);
                 }
             }
         }
-        float *o = c.dense ? c.out + r * g.Cout : c.out + (r + 1) * g.Cout;
+        if (c.dense) {
+            float *o = static_cast<float *>(c.out) + r * g.Cout;
 #pragma unroll
-        for (int i = 0; i < CPL; i++) {
-            const int ch = lane + 32 * i;
-            if (ch < g.Cout) o[ch] = c.dense ? __fadd_rn(acc[i], __ldg(c.bias + ch)) : acc[i];
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + 32 * i;
+                if (ch < g.Cout) o[ch] = __fadd_rn(acc[i], __ldg(c.bias + ch));
+            }
+        } else {
+            T *o = static_cast<T *>(c.out) + (r + 1) * g.Cout;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + 32 * i;
+                if (ch < g.Cout) str<T>(o + ch, acc[i]);
+            }
         }
     }
 }
 
-void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
+template <class T>
+static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
     const int64_t m_up = c.dense ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
     int64_t blocks = (m_up * 32 + 255) / 256;
     int grid = (int)(blocks < 148 * 8 ? blocks : 148 * 8);
     if (grid < 1) grid = 1;
     const int cpl = (c.g.Cin + 31) / 32;
-#define DW(n) k_dwconv_f32<n><<<grid, 256, 0, s>>>(c)
+#define DW(n) k_dwconv_f32<n, T><<<grid, 256, 0, s>>>(c)
     if (cpl <= 1) DW(1);
     else if (cpl <= 2) DW(2);
     else if (cpl <= 3) DW(3);
@@ -300,6 +329,11 @@ void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
     else if (cpl <= 21) DW(21);
     else DW(36);
 #undef DW
+}
+
+void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
+    if (c.dense || !c.bf) launch_dw_t<float>(c, s);
+    else launch_dw_t<bf16>(c, s);
 }
 
 }  // namespace st

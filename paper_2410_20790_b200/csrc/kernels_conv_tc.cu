@@ -3,28 +3,34 @@
 //
 // Eq.(2) as a gathered implicit GEMM:
 //   D[M x Cout] = A[M x K] * B[K x Cout],  K = k_h*k_w*c_in in (dy, dx, ci) order,
-// A rows gathered from the compacted delta rows (sparse) or the dense
-// reference activations (dense), B = weights.  Used where the active-row
-// batch is a real dense contraction (c_in % 64 == 0: 3x3 convs of the CRNN
-// and ResNet encoders, 1x1 convs with wide inputs).
+// A rows gathered from the compacted bf16 delta rows (sparse) or the fp32
+// dense reference activations (dense), B = bf16 weights.  Used where the
+// active-row batch is a real dense contraction (c_in % 64 == 0: 3x3 convs of
+// the CRNN and ResNet encoders, 1x1 convs with wide inputs).
 //
-// Precision contract of BF16 mode (R22-BF16): A and B are rounded
-// to bf16 (RNE) when staged, products are exact in fp32, accumulation is fp32
-// in TMEM; rows/outputs stay fp32.
+// Precision contract of BF16 mode (R22-BF16): operands are bf16
+// (delta rows are stored bf16; dense activations and weights are rounded
+// RNE when staged), products are exact in fp32, accumulation is fp32 in TMEM;
+// sparse outputs are stored as bf16 delta rows, dense outputs as fp32 + bias.
 //
 // CTA = 9 warps, persistent over (M tile, N tile):
-//   warps 0-3  producers: thread m gathers A row m of the tile (64 channels
-//              of one tap per k-block: 16 x LDG.128 fp32 -> cvt.bf16x2 ->
-//              8 x STS.128 in the 128B-swizzled K-major layout) and a share
-//              of the B tile (bf16 weights, LDG.128 -> STS.128), then
-//              fence.proxy.async + mbarrier arrive (full[s]);
-//   warp 4     MMA issuer: one elected lane issues 4 x tcgen05.mma
-//              (M=128, N=BN, K=16) per k-block, tcgen05.commit -> empty[s];
-//              after the last k-block commit -> tmem_full[acc];
-//   warps 5-8  epilogue: tcgen05.ld 32x32b (TMEM lane = tile row) -> fp32
-//              row stores (+bias in dense mode), arrive tmem_empty[acc].
+//   warps 0-3  producers: thread m owns A row m of the tile.  Per k-block
+//              (64 channels of one tap): sparse -> 8 x cp.async 16 B of the
+//              bf16 row into the 128B-swizzled K-major layout (zero-fill for
+//              an inactive tap), completion tracked by
+//              cp.async.mbarrier.arrive.noinc; dense -> 16 x LDG.128 fp32 ->
+//              cvt.bf16x2 -> 8 x STS.128 + fence.proxy.async + arrive.
+//              Thread 0 also issues the B tile as one TMA 2D load
+//              (box 64 x BN, 128B swizzle) with expect_tx.
+//   warp 4     MMA issuer: one lane issues 4 x tcgen05.mma (M=128, N=BN,
+//              K=16) per k-block, tcgen05.commit -> empty[s]; after the last
+//              k-block commit -> tmem_full[acc].
+//   warps 5-8  epilogue: tcgen05.ld 32x32b (TMEM lane = tile row) -> row
+//              stores, arrive tmem_empty[acc].
 // Stages: 4-deep smem ring; TMEM: 2 accumulators x BN columns.
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 
@@ -54,6 +60,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+// 16-byte cp.async, zero-filled when src_bytes == 0
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
@@ -102,8 +128,8 @@ struct Smem {
 
 }  // namespace tc
 
-template <int BN>
-__global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __nv_bfloat16 *__restrict__ wbf) {
+template <int BN, bool DENSE>
+__global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b) {
     using namespace tc;
     using S = Smem<BN>;
     constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -118,16 +144,15 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     const Geo g = c.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
-    const int M = c.dense ? c.B * Nout : *c.m_dev;
+    const int M = DENSE ? c.B * Nout : *c.m_dev;
     const int K = g.kh * g.kw * g.Cin;
     const int nkb = K / BK;
     const int ntn = (g.Cout + BN - 1) / BN;
     const int ntiles = ((M + BM - 1) / BM) * ntn;
-    const float *A = c.dense ? c.a_dense : c.a.rows;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full + s, NPROD);
+            mbar_init(full + s, NPROD + 1);   // 128 producer arrivals + the TMA expect_tx arrival
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; a++) {
@@ -151,6 +176,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         const int m = threadIdx.x;   // tile row owned by this thread
         int stage = 0;
         uint32_t phase = 0;
+        const float *Ad = c.a_dense;
+        const bf16 *As = static_cast<const bf16 *>(c.a.rows);
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int mt = tile / ntn, nt = tile - mt * ntn;
             const int r = mt * BM + m;
@@ -158,7 +185,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             int b = 0, q = 0, t1 = 0;
             const bool rv = r < M;
             if (rv) {
-                if (c.dense) {
+                if (DENSE) {
                     b = r / Nout;
                     q = r - b * Nout;
                 } else {
@@ -171,23 +198,23 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             }
             const int oy = q / g.Wout, ox = q - oy * g.Wout;
             int cur_tap = -1;
-            const float *src = nullptr;
+            int64_t src = -1;   // element offset of the gathered row, -1 = zero
             for (int kb = 0; kb < nkb; kb++) {
                 const int k0 = kb * BK;
                 const int tap = k0 / g.Cin, ci0 = k0 - tap * g.Cin;
                 if (tap != cur_tap) {
                     cur_tap = tap;
-                    src = nullptr;
+                    src = -1;
                     if (rv) {
                         const int dy = tap / g.kw, dx = tap - dy * g.kw;
                         const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
                         if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
                             const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
-                            if (c.dense) {
-                                src = A + bp * g.Cin;
+                            if (DENSE) {
+                                src = bp * g.Cin;
                             } else {
                                 const int row = row_of(c.a, bp, t1);
-                                if (row) src = A + (int64_t)row * g.Cin;
+                                if (row) src = (int64_t)row * g.Cin;
                             }
                         }
                     }
@@ -195,41 +222,47 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 mbar_wait(empty + stage, phase ^ 1);
                 unsigned char *sa = smem + stage * S::STAGE;
                 unsigned char *sb = sa + S::A_BYTES;
-                // ---- A row m: 64 fp32 -> 64 bf16 = 8 x 16 B chunks, swizzled
-                uint4 chunk[8];
-                if (src) {
-                    const float4 *p = reinterpret_cast<const float4 *>(src + ci0);
-                    float4 v[16];
+                if (DENSE) {
+                    // ---- fp32 activations -> bf16 (RNE), 8 x 16 B chunks, swizzled
+                    uint4 chunk[8];
+                    if (src >= 0) {
+                        const float4 *p = reinterpret_cast<const float4 *>(Ad + src + ci0);
+                        float4 v[16];
 #pragma unroll
-                    for (int i = 0; i < 16; i++) v[i] = __ldg(p + i);
+                        for (int i = 0; i < 16; i++) v[i] = __ldg(p + i);
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        chunk[j].x = pack_bf16x2(v[2 * j].x, v[2 * j].y);
-                        chunk[j].y = pack_bf16x2(v[2 * j].z, v[2 * j].w);
-                        chunk[j].z = pack_bf16x2(v[2 * j + 1].x, v[2 * j + 1].y);
-                        chunk[j].w = pack_bf16x2(v[2 * j + 1].z, v[2 * j + 1].w);
+                        for (int j = 0; j < 8; j++) {
+                            chunk[j].x = pack_bf16x2(v[2 * j].x, v[2 * j].y);
+                            chunk[j].y = pack_bf16x2(v[2 * j].z, v[2 * j].w);
+                            chunk[j].z = pack_bf16x2(v[2 * j + 1].x, v[2 * j + 1].y);
+                            chunk[j].w = pack_bf16x2(v[2 * j + 1].z, v[2 * j + 1].w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; j++) chunk[j] = make_uint4(0, 0, 0, 0);
                     }
+#pragma unroll
+                    for (int j = 0; j < 8; j++)
+                        *reinterpret_cast<uint4 *>(sa + m * 128 + ((j ^ (m & 7)) << 4)) = chunk[j];
+                    fence_proxy_async();
+                    mbar_arrive(full + stage);
                 } else {
+                    // ---- bf16 delta row: 128 B = 8 x cp.async 16 B, zero-fill if inactive
+                    const bf16 *p = As + (src >= 0 ? src + ci0 : 0);
+                    const uint32_t nbytes = src >= 0 ? 16u : 0u;
 #pragma unroll
-                    for (int j = 0; j < 8; j++) chunk[j] = make_uint4(0, 0, 0, 0);
+                    for (int j = 0; j < 8; j++) cp_async16(sa + m * 128 + ((j ^ (m & 7)) << 4), p + j * 8, nbytes);
+                    cp_async_arrive_noinc(full + stage);
                 }
-#pragma unroll
-                for (int j = 0; j < 8; j++)
-                    *reinterpret_cast<uint4 *>(sa + m * 128 + ((j ^ (m & 7)) << 4)) = chunk[j];
-                // ---- B tile: BN rows x 8 chunks, bf16 weights [Cout][K]
-#pragma unroll
-                for (int cidx = m; cidx < BN * 8; cidx += NPROD) {
-                    const int n = cidx >> 3, j = cidx & 7;
-                    const int co = nt * BN + n;
-                    uint4 w = make_uint4(0, 0, 0, 0);
-                    if (co < g.Cout) w = __ldg(reinterpret_cast<const uint4 *>(wbf + (int64_t)co * K + k0) + j);
-                    *reinterpret_cast<uint4 *>(sb + n * 128 + ((j ^ (n & 7)) << 4)) = w;
+                // ---- B tile: one TMA 2D load by thread 0 (rows past Cout zero-filled)
+                if (m == 0) {
+                    mbar_arrive_tx(full + stage, S::B_BYTES);
+                    tma_load_2d(sb, &tmap_b, k0, nt * BN, full + stage);
                 }
-                fence_proxy_async();
-                mbar_arrive(full + stage);
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
+        if (!DENSE) asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == 4) {
         // ===================== MMA issuer =====================
         constexpr uint32_t IDESC = idesc_bf16(BM, BN);
@@ -270,7 +303,6 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             mbar_wait(tfull + acc, acc_phase);
             tc_fence_after();
             const int r = mt * BM + row_in_tile;
-            float *o = c.dense ? c.out + (int64_t)r * g.Cout : c.out + (int64_t)(r + 1) * g.Cout;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
@@ -287,29 +319,38 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 const int n0 = nt * BN + c0;
-                if (r < M && n0 < g.Cout) {
-                    if (n0 + 32 <= g.Cout) {
+                if (r >= M || n0 >= g.Cout) continue;
+                const bool full_chunk = n0 + 32 <= g.Cout;
+                if (DENSE) {
+                    float *o = static_cast<float *>(c.out) + (int64_t)r * g.Cout + n0;
+                    if (full_chunk) {
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
                             float4 f;
-                            f.x = __uint_as_float(v[j]);
-                            f.y = __uint_as_float(v[j + 1]);
-                            f.z = __uint_as_float(v[j + 2]);
-                            f.w = __uint_as_float(v[j + 3]);
-                            if (c.dense) {
-                                f.x = __fadd_rn(f.x, __ldg(c.bias + n0 + j));
-                                f.y = __fadd_rn(f.y, __ldg(c.bias + n0 + j + 1));
-                                f.z = __fadd_rn(f.z, __ldg(c.bias + n0 + j + 2));
-                                f.w = __fadd_rn(f.w, __ldg(c.bias + n0 + j + 3));
-                            }
-                            *reinterpret_cast<float4 *>(o + n0 + j) = f;
+                            f.x = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
+                            f.y = __fadd_rn(__uint_as_float(v[j + 1]), __ldg(c.bias + n0 + j + 1));
+                            f.z = __fadd_rn(__uint_as_float(v[j + 2]), __ldg(c.bias + n0 + j + 2));
+                            f.w = __fadd_rn(__uint_as_float(v[j + 3]), __ldg(c.bias + n0 + j + 3));
+                            *reinterpret_cast<float4 *>(o + j) = f;
                         }
                     } else {
-                        for (int j = 0; j < 32 && n0 + j < g.Cout; j++) {
-                            float f = __uint_as_float(v[j]);
-                            if (c.dense) f = __fadd_rn(f, __ldg(c.bias + n0 + j));
-                            o[n0 + j] = f;
+                        for (int j = 0; j < 32 && n0 + j < g.Cout; j++)
+                            o[j] = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
+                    }
+                } else {
+                    bf16 *o = static_cast<bf16 *>(c.out) + (int64_t)(r + 1) * g.Cout + n0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            uint4 u;
+                            u.x = pack_bf16x2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+                            u.y = pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                            u.z = pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+                            u.w = pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
+                            *reinterpret_cast<uint4 *>(o + j) = u;
                         }
+                    } else {
+                        for (int j = 0; j < 32 && n0 + j < g.Cout; j++) o[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
                     }
                 }
             }
@@ -324,38 +365,69 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     }
 }
 
-template <int BN>
-static void launch_tc(const ConvCall &c, const __nv_bfloat16 *wbf, cudaStream_t s, int num_sms) {
+template <int BN, bool DENSE>
+static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s, int num_sms) {
     using S = tc::Smem<BN>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+        cudaFuncSetAttribute(k_conv_tc<BN, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
         attr = true;
     }
     const int ntn = (c.g.Cout + BN - 1) / BN;
-    const int64_t m_up = c.dense ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
+    const int64_t m_up = DENSE ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
     const int64_t tiles = ((m_up + tc::BM - 1) / tc::BM) * ntn;
     int grid = (int)std::min<int64_t>(tiles, num_sms);
     if (grid < 1) grid = 1;
-    k_conv_tc<BN><<<grid, tc::NTHREADS, S::TOTAL, s>>>(c, wbf);
+    k_conv_tc<BN, DENSE><<<grid, tc::NTHREADS, S::TOTAL, s>>>(c, *tmap);
 }
 
 bool conv_tc_eligible(const Geo &g) {
     return g.groups == 1 && g.Cin % tc::BK == 0 && g.Cout % 16 == 0;
 }
 
-void launch_conv_tc(const ConvCall &c, const void *wbf_v, cudaStream_t s) {
-    const __nv_bfloat16 *wbf = static_cast<const __nv_bfloat16 *>(wbf_v);
+int conv_tc_bn(int cout) { return cout >= 256 ? 256 : cout >= 128 ? 128 : cout >= 64 ? 64 : 32; }
+
+// TMA descriptor of the bf16 weights [Cout][K] (K contiguous): box 64 x BN,
+// 128-byte swizzle matching the UMMA SWIZZLE_128B K-major smem layout,
+// out-of-bounds rows (Cout not a multiple of BN) zero-filled.
+bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const int BN = conv_tc_bn(Cout);
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)Cout};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)BN};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap *>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void *>(wbf), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+void launch_conv_tc(const ConvCall &c, const void *tmap_v, cudaStream_t s) {
+    const CUtensorMap *tmap = static_cast<const CUtensorMap *>(tmap_v);
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    if (c.g.Cout >= 256) launch_tc<256>(c, wbf, s, num_sms);
-    else if (c.g.Cout >= 128) launch_tc<128>(c, wbf, s, num_sms);
-    else if (c.g.Cout >= 64) launch_tc<64>(c, wbf, s, num_sms);
-    else launch_tc<32>(c, wbf, s, num_sms);
+#define TC_BN(BN_) (c.dense ? launch_tc<BN_, true>(c, tmap, s, num_sms) : launch_tc<BN_, false>(c, tmap, s, num_sms))
+    switch (conv_tc_bn(c.g.Cout)) {
+    case 256: TC_BN(256); break;
+    case 128: TC_BN(128); break;
+    case 64: TC_BN(64); break;
+    default: TC_BN(32); break;
+    }
+#undef TC_BN
 }
 
 }  // namespace st

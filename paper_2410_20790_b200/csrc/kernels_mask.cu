@@ -14,7 +14,7 @@
 namespace st {
 
 // ------------------------------------------------------------ subtraction
-template <int C>
+template <int C, class T>
 __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__ ref, int64_t ref_stride,
                                                        const float *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, int n_diff, float theta, uint32_t *__restrict__ act) {
@@ -39,18 +39,18 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
         }
         if (mx > theta) {                       // R1: strict comparison
 #pragma unroll
-            for (int c = 0; c < C; c++) S[c] = __fadd_rn(S[c], raw[c]);   // R3
+            for (int c = 0; c < C; c++) S[c] = __fadd_rn(S[c], rnd<T>(raw[c]));   // R3: S += emitted
             w |= 1u << t1;
         }
     }
     act[i] = w;
 }
 
-template <int C>
+template <int C, class T>
 __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__ ref, int64_t ref_stride,
                                                        const float *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, const uint32_t *__restrict__ act,
-                                                       const int32_t *__restrict__ pbase, float *__restrict__ rows) {
+                                                       const int32_t *__restrict__ pbase, T *__restrict__ rows) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     uint32_t w = act[i];
@@ -62,15 +62,15 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
     for (int c = 0; c < C; c++) S[c] = __ldg(r + c);
     const float *f = fr + b * fr_stride + (int64_t)p * C;
     const int64_t fs = (int64_t)N * C;
-    float *o = rows + (int64_t)(1 + pbase[i]) * C;
+    T *o = rows + (int64_t)(1 + pbase[i]) * C;
     while (w) {
         const int t1 = __ffs(w) - 1;
         w &= w - 1;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const float raw = __fsub_rn(__ldg(f + t1 * fs + c), S[c]);
-            S[c] = __fadd_rn(S[c], raw);
-            o[c] = raw;
+            const float e = rnd<T>(__fsub_rn(__ldg(f + t1 * fs + c), S[c]));   // emitted delta
+            S[c] = __fadd_rn(S[c], e);
+            str<T>(o + c, e);
         }
         o += C;
     }
@@ -78,23 +78,26 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
 
 #define SUB_DISPATCH(C_, KERNEL, ...)                                                    \
     switch (C_) {                                                                        \
-    case 1: KERNEL<1><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
-    case 2: KERNEL<2><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
-    case 3: KERNEL<3><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
-    case 4: KERNEL<4><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                          \
+    case 1: KERNEL<1, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
+    case 2: KERNEL<2, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
+    case 3: KERNEL<3, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
+    case 4: KERNEL<4, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
     default: break;                                                                      \
     }
 
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
-                          int N, int C, int n_diff, float theta, uint32_t *act, cudaStream_t s) {
+                          int N, int C, int n_diff, float theta, bool bf, uint32_t *act, cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
-    SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta, act);
+    ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta,
+                                     act));
 }
 
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
-                          int N, int C, const uint32_t *act, const int32_t *pbase, float *rows, cudaStream_t s) {
+                          int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
+                          cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
-    SUB_DISPATCH(C, k_subtract_rows, ref, ref_stride, frames, fr_stride, B, N, act, pbase, rows);
+    ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_rows, ref, ref_stride, frames, fr_stride, B, N, act, pbase,
+                                     static_cast<T *>(rows)));
 }
 
 // --------------------------------------------------------------- dilation

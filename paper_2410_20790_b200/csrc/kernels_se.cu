@@ -38,9 +38,11 @@ __global__ void __launch_bounds__(256) k_se_colsum(const float *__restrict__ x, 
 }
 
 // ---- (i-b) per-frame channel sums of the delta rows: dsum[b][t][c] (fp64)
+template <class T>
 __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, int F, int ppb,
                                                        double *__restrict__ dsum) {
     extern __shared__ double sacc[];   // [8 warps][32 frames][32 lanes]
+    const T *rows = static_cast<const T *>(in.rows);
     const int b = blockIdx.z, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.y * 32 + lane;
     double *my = sacc + w * 32 * 32;
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, i
             const int t1 = __ffs(a) - 1;
             a &= a - 1;
             const int64_t row = base + __popc(sl & lowmask(t1));
-            if (c < C) my[t1 * 32 + lane] += (double)in.rows[row * C + c];
+            if (c < C) my[t1 * 32 + lane] += (double)ldr<T>(rows + row * C + c);
         }
     }
     __syncthreads();
@@ -161,19 +163,20 @@ __global__ void k_se_slots(const uint32_t *__restrict__ act, const uint32_t *__r
 }
 
 // ---- (iii) SE site pixel loop
-template <int G, int CPL>
+template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restrict__ x0, const float *__restrict__ s_tab,
                                                  int N, int C, int F, int64_t BN, float theta,
                                                  const uint32_t *__restrict__ slot, const int32_t *__restrict__ pbase,
-                                                 uint32_t *__restrict__ out_act, float *__restrict__ out_rows) {
+                                                 uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+    const T *rows = static_cast<const T *>(in.rows);
     const int lane = threadIdx.x & (G - 1);
     unsigned mask = 0xffffffffu;
     if constexpr (G < 32) mask = ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
     for (int64_t bp = grp; bp < BN; bp += ngrp) {
-        const uint32_t T = __ldg(slot + bp);
-        if (!T) {
+        const uint32_t Tw = __ldg(slot + bp);
+        if (!Tw) {
             if (lane == 0) out_act[bp] = 0;
             continue;
         }
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
         const int ibase = a ? 1 + __ldg(in.pbase + bp) : 0;
         const uint32_t isl = a ? __ldg(in.slot + bp) : 0u;
         const int obase = 1 + __ldg(pbase + bp);
-        uint32_t bits = T, emit = 0;
+        uint32_t bits = Tw, emit = 0;
         while (bits) {
             const int t1 = __ffs(bits) - 1;
             bits &= bits - 1;
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
                 const int ch = lane + G * i;
                 cand[i] = 0.0f;
                 if (ch < C) {
-                    if (act) xa[i] = __fadd_rn(xa[i], in.rows[irow * C + ch]);
+                    if (act) xa[i] = __fadd_rn(xa[i], ldr<T>(rows + irow * C + ch));
                     cand[i] = __fsub_rn(__fmul_rn(xa[i], __ldg(s_now + ch)), ya[i]);
                     mx = fmaxf(mx, fabsf(cand[i]));
                 }
@@ -212,13 +215,14 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(mask, mx, o, G));
             if (mx > theta) {
-                const int64_t orow = obase + __popc(T & lowmask(t1));
+                const int64_t orow = obase + __popc(Tw & lowmask(t1));
 #pragma unroll
                 for (int i = 0; i < CPL; i++) {
                     const int ch = lane + G * i;
                     if (ch < C) {
-                        ya[i] = __fadd_rn(ya[i], cand[i]);
-                        out_rows[orow * C + ch] = cand[i];
+                        const float e = rnd<T>(cand[i]);
+                        ya[i] = __fadd_rn(ya[i], e);
+                        str<T>(out_rows + orow * C + ch, e);
                     }
                 }
                 emit |= 1u << t1;
@@ -253,16 +257,22 @@ void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int
     if (grid > 0) k_se_dense_apply<<<grid, 256, 0, s>>>(x, s_tab, N, C, F, n, y);
 }
 
-void launch_se_delta_sums(DView in, int B, int N, int C, int F, double *dsum, cudaStream_t s) {
-    cudaMemsetAsync(dsum, 0, (size_t)B * F * C * 8, s);
+template <class T>
+static void se_delta_sums_t(DView in, int B, int N, int C, int F, double *dsum, cudaStream_t s) {
     const int ppb = 1024;
     dim3 grid(cdiv(N, ppb), cdiv(C, 32), B);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_se_delta_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 32 * 8);
+        cudaFuncSetAttribute(k_se_delta_sums<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 32 * 8);
         attr = true;
     }
-    k_se_delta_sums<<<grid, 256, 8 * 32 * 32 * 8, s>>>(in, N, C, F, ppb, dsum);
+    k_se_delta_sums<T><<<grid, 256, 8 * 32 * 32 * 8, s>>>(in, N, C, F, ppb, dsum);
+}
+
+void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double *dsum, cudaStream_t s) {
+    cudaMemsetAsync(dsum, 0, (size_t)B * F * C * 8, s);
+    if (bf) se_delta_sums_t<bf16>(in, B, N, C, F, dsum, s);
+    else se_delta_sums_t<float>(in, B, N, C, F, dsum, s);
 }
 
 void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s) {
@@ -270,24 +280,28 @@ void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N,
     k_se_slots<<<cdiv(n, 256), 256, 0, s>>>(act, refresh, N, n, slot);
 }
 
-void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta,
-                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, float *out_rows, cudaStream_t s) {
+void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta, bool bf,
+                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
     auto grid_for = [&](int G) {
         return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(BN * G, 256), 148 * 8));
     };
-#define L_SE(G_, CPL_) \
-    k_se_site<G_, CPL_><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, out_rows)
-    if (C <= 8) L_SE(8, 1);
-    else if (C <= 16) L_SE(16, 1);
-    else if (C <= 32) L_SE(32, 1);
-    else if (C <= 64) L_SE(32, 2);
-    else if (C <= 96) L_SE(32, 3);
-    else if (C <= 160) L_SE(32, 5);
-    else if (C <= 256) L_SE(32, 8);
-    else if (C <= 480) L_SE(32, 15);
-    else if (C <= 672) L_SE(32, 21);
+#define L_SE(G_, CPL_)                                                                                      \
+    k_se_site<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \
+                                                        static_cast<T *>(out_rows))
+#define SE_CH                          \
+    if (C <= 8) L_SE(8, 1);            \
+    else if (C <= 16) L_SE(16, 1);     \
+    else if (C <= 32) L_SE(32, 1);     \
+    else if (C <= 64) L_SE(32, 2);     \
+    else if (C <= 96) L_SE(32, 3);     \
+    else if (C <= 160) L_SE(32, 5);    \
+    else if (C <= 256) L_SE(32, 8);    \
+    else if (C <= 480) L_SE(32, 15);   \
+    else if (C <= 672) L_SE(32, 21);   \
     else L_SE(32, 36);
+    ST_ROW_DISPATCH(bf, SE_CH);
+#undef SE_CH
 #undef L_SE
 }
 

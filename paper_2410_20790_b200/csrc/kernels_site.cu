@@ -8,11 +8,12 @@
 // kept in HBM):
 //     x_acc += Delta_t;  c = f(x_acc) - y_acc;
 //     emit iff max_c |c| > theta (pixel granularity, R1/R2);
-//     y_acc += c when emitted.
+//     e = c as stored (fp32, or bf16-rounded in BF16 mode); y_acc += e.
 // A pixel is owned by a group of G lanes (G = 32 for C >= 32, else the next
 // power of two >= C), each lane holding CPL channels; the channel max is a
 // group shuffle reduction.  Emitted rows are written in the input's slot
 // layout (in place), so no compaction pass is needed after a site.
+// Delta rows are of type T (float in FP32 mode, bf16 in BF16 mode).
 #include <math_constants.h>
 
 #include "common.cuh"
@@ -95,13 +96,14 @@ void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaS
 }
 
 // ------------------------------------------------------- pointwise site
-template <int G, int CPL, int ACT>
+template <int G, int CPL, int ACT, class T>
 __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
-                                                 float theta, uint32_t *__restrict__ out_act, float *out_rows) {
+                                                 float theta, uint32_t *__restrict__ out_act, T *out_rows) {
     const int lane = threadIdx.x & (G - 1);
     const unsigned mask = group_mask<G>();
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    const T *rows = static_cast<const T *>(in.rows);
     for (int64_t bp = grp; bp < BN; bp += ngrp) {
         uint32_t a = __ldg(in.act + bp);
         if (!a) {
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
             for (int i = 0; i < CPL; i++) {
                 const int ch = lane + G * i;
                 if (ch < C) {
-                    xa[i] = __fadd_rn(xa[i], in.rows[row * C + ch]);       // reconstruct x (Eq.3)
+                    xa[i] = __fadd_rn(xa[i], ldr<T>(rows + row * C + ch));   // reconstruct x (Eq.3)
                     cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);          // restore the delta
                     mx = fmaxf(mx, fabsf(cand[i]));
                 } else {
@@ -141,8 +143,9 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
                 for (int i = 0; i < CPL; i++) {
                     const int ch = lane + G * i;
                     if (ch < C) {
-                        ya[i] = __fadd_rn(ya[i], cand[i]);
-                        out_rows[row * C + ch] = cand[i];
+                        const float e = rnd<T>(cand[i]);
+                        ya[i] = __fadd_rn(ya[i], e);
+                        str<T>(out_rows + row * C + ch, e);
                     }
                 }
                 emit |= 1u << t1;
@@ -174,29 +177,31 @@ static int groups_grid(int64_t n_groups, int G) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(threads, 256), 148 * 8));
 }
 
-void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta, uint32_t *out_act,
-                           float *out_rows, cudaStream_t s) {
+void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta, bool bf,
+                           uint32_t *out_act, void *out_rows, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
-#define L_PW(G_, CPL_)                                                                                   \
-    {                                                                                                    \
-        const int grid = groups_grid(BN, G_);                                                            \
-        if (act == ACT_RELU)                                                                             \
-            k_site_pw<G_, CPL_, ACT_RELU><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act, out_rows); \
-        else                                                                                             \
-            k_site_pw<G_, CPL_, ACT_SILU><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act, out_rows); \
+#define L_PW(G_, CPL_)                                                                                 \
+    {                                                                                                  \
+        const int grid = groups_grid(BN, G_);                                                          \
+        if (act == ACT_RELU)                                                                           \
+            k_site_pw<G_, CPL_, ACT_RELU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
+                                                                  static_cast<T *>(out_rows));         \
+        else                                                                                           \
+            k_site_pw<G_, CPL_, ACT_SILU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
+                                                                  static_cast<T *>(out_rows));         \
     }
-    CH_DISPATCH(C, L_PW)
+    ST_ROW_DISPATCH(bf, CH_DISPATCH(C, L_PW));
 #undef L_PW
 }
 
 // --------------------------------------------------------- maxpool site
 // Touched set T = footprint dilation of the input mask (R7);
 // each touched window is re-evaluated from x_acc of its input pixels.
-template <int G, int CPL, int KMAX>
+template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__restrict__ x0, int B, Geo g,
                                                       float theta, const uint32_t *__restrict__ t_slot,
                                                       const int32_t *__restrict__ t_pbase,
-                                                      uint32_t *__restrict__ out_act, float *__restrict__ out_rows) {
+                                                      uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
     const int lane = threadIdx.x & (G - 1);
     const unsigned mask = group_mask<G>();
     const int C = g.Cin;
@@ -204,9 +209,10 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
     const int64_t BN = (int64_t)B * No;
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    const T *rows = static_cast<const T *>(in.rows);
     for (int64_t bq = grp; bq < BN; bq += ngrp) {
-        const uint32_t T = __ldg(t_slot + bq);
-        if (!T) {
+        const uint32_t Tw = __ldg(t_slot + bq);
+        if (!Tw) {
             if (lane == 0) out_act[bq] = 0;
             continue;
         }
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
             ya[i] = m;
         }
         const int base = 1 + __ldg(t_pbase + bq);
-        uint32_t bits = T, emit = 0;
+        uint32_t bits = Tw, emit = 0;
         while (bits) {
             const int t1 = __ffs(bits) - 1;
             bits &= bits - 1;
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
 #pragma unroll
                 for (int i = 0; i < CPL; i++) {
                     const int ch = lane + G * i;
-                    if (ch < C) xa[w][i] = __fadd_rn(xa[w][i], in.rows[(int64_t)row * C + ch]);
+                    if (ch < C) xa[w][i] = __fadd_rn(xa[w][i], ldr<T>(rows + (int64_t)row * C + ch));
                 }
             }
             float cand[CPL];
@@ -266,13 +272,14 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
             }
             mx = gmax<G>(mx, mask);
             if (mx > theta) {
-                const int64_t orow = base + __popc(T & lowmask(t1));
+                const int64_t orow = base + __popc(Tw & lowmask(t1));
 #pragma unroll
                 for (int i = 0; i < CPL; i++) {
                     const int ch = lane + G * i;
                     if (ch < C) {
-                        ya[i] = __fadd_rn(ya[i], cand[i]);
-                        out_rows[orow * C + ch] = cand[i];
+                        const float e = rnd<T>(cand[i]);
+                        ya[i] = __fadd_rn(ya[i], e);
+                        str<T>(out_rows + orow * C + ch, e);
                     }
                 }
                 emit |= 1u << t1;
@@ -282,32 +289,35 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
     }
 }
 
-void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta, const uint32_t *t_slot,
-                         const int32_t *t_pbase, uint32_t *out_act, float *out_rows, cudaStream_t s) {
+void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta, bool bf,
+                         const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
+                         cudaStream_t s) {
     const int64_t BN = (int64_t)B * g.Hout * g.Wout;
     const int kk = g.kh * g.kw;
-#define L_MP(G_, CPL_)                                                                                         \
-    {                                                                                                          \
-        const int grid = groups_grid(BN, G_);                                                                  \
-        if (kk <= 4)                                                                                           \
-            k_site_maxpool<G_, CPL_, 4><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase, out_act,    \
-                                                             out_rows);                                        \
-        else                                                                                                   \
-            k_site_maxpool<G_, CPL_, 9><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase, out_act,    \
-                                                             out_rows);                                        \
+#define L_MP(G_, CPL_)                                                                                       \
+    {                                                                                                        \
+        const int grid = groups_grid(BN, G_);                                                                \
+        if (kk <= 4)                                                                                         \
+            k_site_maxpool<G_, CPL_, 4, T><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase,        \
+                                                                out_act, static_cast<T *>(out_rows));        \
+        else                                                                                                 \
+            k_site_maxpool<G_, CPL_, 9, T><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase,        \
+                                                                out_act, static_cast<T *>(out_rows));        \
     }
-    CH_DISPATCH(g.Cin, L_MP)
+    ST_ROW_DISPATCH(bf, CH_DISPATCH(g.Cin, L_MP));
 #undef L_MP
 }
 
 // ---------------------------------------------------------- residual add
-template <int G, int CPL>
+template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32_t *__restrict__ slot,
                                                   const int32_t *__restrict__ pbase, int64_t BN, int C,
-                                                  float *__restrict__ out) {
+                                                  T *__restrict__ out) {
     const int lane = threadIdx.x & (G - 1);
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    const T *ra_rows = static_cast<const T *>(a.rows);
+    const T *rb_rows = static_cast<const T *>(b.rows);
     for (int64_t bp = grp; bp < BN; bp += ngrp) {
         uint32_t w = __ldg(slot + bp);
         if (!w) continue;
@@ -320,9 +330,9 @@ __global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32
             for (int i = 0; i < CPL; i++) {
                 const int ch = lane + G * i;
                 if (ch < C) {
-                    const float va = ra ? a.rows[(int64_t)ra * C + ch] : 0.0f;
-                    const float vb = rb ? b.rows[(int64_t)rb * C + ch] : 0.0f;
-                    out[row * C + ch] = __fadd_rn(va, vb);
+                    const float va = ra ? ldr<T>(ra_rows + (int64_t)ra * C + ch) : 0.0f;
+                    const float vb = rb ? ldr<T>(rb_rows + (int64_t)rb * C + ch) : 0.0f;
+                    str<T>(out + row * C + ch, __fadd_rn(va, vb));
                 }
             }
             row++;
@@ -330,17 +340,18 @@ __global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32
     }
 }
 
-void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C,
-                     float *out_rows, cudaStream_t s) {
+void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C, bool bf,
+                     void *out_rows, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
-#define L_ADD(G_, CPL_) k_add_rows<G_, CPL_><<<groups_grid(BN, G_), 256, 0, s>>>(a, b, slot, pbase, BN, C, out_rows);
-    CH_DISPATCH(C, L_ADD)
+#define L_ADD(G_, CPL_) \
+    k_add_rows<G_, CPL_, T><<<groups_grid(BN, G_), 256, 0, s>>>(a, b, slot, pbase, BN, C, static_cast<T *>(out_rows));
+    ST_ROW_DISPATCH(bf, CH_DISPATCH(C, L_ADD));
 #undef L_ADD
 }
 
 // ---------------------------------------------------------- accumulation
 // O_t = O_{t-1} + Delta_t, dense per-frame outputs [B][L][N][C].
-template <int G, int CPL>
+template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__restrict__ y0, int B, int N, int C,
                                                     int n_diff, float *__restrict__ out) {
     const int lane = threadIdx.x & (G - 1);
@@ -348,6 +359,7 @@ __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__res
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
     const int64_t fstride = (int64_t)N * C;
+    const T *rows = static_cast<const T *>(in.rows);
     for (int64_t bq = grp; bq < BN; bq += ngrp) {
         const int b = (int)(bq / N), q = (int)(bq % N);
         const uint32_t a = n_diff ? __ldg(in.act + bq) : 0u;
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__res
 #pragma unroll
                 for (int i = 0; i < CPL; i++) {
                     const int ch = lane + G * i;
-                    if (ch < C) O[i] = __fadd_rn(O[i], in.rows[row * C + ch]);
+                    if (ch < C) O[i] = __fadd_rn(O[i], ldr<T>(rows + row * C + ch));
                 }
             }
 #pragma unroll
@@ -380,10 +392,11 @@ __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__res
     }
 }
 
-void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, float *out, cudaStream_t s) {
+void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, bool bf, float *out,
+                       cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
-#define L_ACC(G_, CPL_) k_accumulate<G_, CPL_><<<groups_grid(BN, G_), 256, 0, s>>>(in, y0, B, N, C, n_diff, out);
-    CH_DISPATCH(C, L_ACC)
+#define L_ACC(G_, CPL_) k_accumulate<G_, CPL_, T><<<groups_grid(BN, G_), 256, 0, s>>>(in, y0, B, N, C, n_diff, out);
+    ST_ROW_DISPATCH(bf, CH_DISPATCH(C, L_ACC));
 #undef L_ACC
 }
 
