@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--policy", default=None, choices=[None, "fixed", "bst", "ibst"])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"],
+    ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"],
                     help="fp32: exact CUDA-core path; bf16: tcgen05 tensor-core convs (R22-BF16)")
     ap.add_argument("--no-dense", action="store_true", help="skip the own-dense-path reference timing")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -350,6 +350,28 @@ def main():
                  "diff_fps_excl_reference": diff_frames / max((ms_step - ref_ms) / 1e3, 1e-9)}
         del denc
 
+    mem = enc.memory_report()
+    # ---- the bit-exact FP32 mode on the same batches (context for the BF16 headline)
+    fp32_exact = None
+    if args.precision == "bf16":
+        del enc
+        fenc = Encoder(net, max_chunks=B, max_frames=L, device=local, precision="fp32")
+        th = ctl.thresholds()
+        fms = 0.0
+        for k in range(4):
+            flush.fill_(float(k))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fenc.encode_reference(batches[k % n_batches][:, 0], stream)
+            fenc.encode_diff(batches[k % n_batches][:, 1:], th, stream)
+            e1.record(stream)
+            e1.synchronize()
+            if k:
+                fms += e0.elapsed_time(e1)
+        fp32_exact = {"value": diff_frames / (fms / 3 / 1e3), "ms_per_step": fms / 3,
+                      "note": "FP32 mode (bit-exact with the oracle), CUDA-core convs"}
+        enc = fenc
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg)
@@ -373,7 +395,7 @@ def main():
                 "site_sparsity": site_sparsity,
                 "conv_rows_out": int(sum(lc["rows_out"][i] for i, l in enumerate(net.layers) if l["kind"] == W.CONV)),
                 "kernel_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in kt.items() if v["launches"]},
-                "memory": enc.memory_report()}
+                "memory": mem, "fp32_exact": fp32_exact}
         if dense:
             line.update(dense)
         print(json.dumps(line))

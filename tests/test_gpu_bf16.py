@@ -71,8 +71,8 @@ def test_tc_conv_kernel_unit(cin, cout, k, s):
             exp = r["deltas"][conv][t - 1].reshape(-1, cout)[idx]
             # both sides store bf16(fp32 accumulator); the accumulators differ
             # only in summation order, so the stored values differ by at most
-            # one bf16 ulp (2^-8 relative) where a rounding boundary is crossed
-            ok, e = _rel_ok(rows, exp, 2.0 ** -8, 1e-4)
+            # one bf16 ulp (<= 2^-7 relative) where a rounding boundary is crossed
+            ok, e = _rel_ok(rows, exp, 2.0 ** -7, 1e-4)
             assert ok, f"sparse tc conv rows err {e} (chunk {b} frame {t})"
 
 
