@@ -96,7 +96,12 @@ def main():
     summ = json.load(open(summ_p)) if os.path.exists(summ_p) else {"kernels": {}}
     for spec in a.full:
         cls, path = spec.split("=", 1)
+        pat = None
+        if "@" in path:   # cls=path@regex: keep kernels whose name matches regex
+            path, pat = path.split("@", 1)
         res = full(path)
+        if pat:
+            res = [d for d in res if re.search(pat, d["kernel"])]
         with open(f"profiles/{a.round}_ncu_{cls}.txt", "w") as f:
             f.write(f"# {a.round} ncu --set full --clock-control none ({os.path.basename(path)})\n")
             for d in res:
@@ -104,11 +109,14 @@ def main():
                 for k in KEYS:
                     if k in d:
                         f.write(f"  {k:70s} {d[k][0]} {d[k][1]}\n")
-        d = res[0]
-        rd = to_bytes(*d["dram__bytes_read.sum"])
-        wr = to_bytes(*d["dram__bytes_write.sum"])
-        summ["kernels"][cls] = {"round": a.round, "kernel": d["kernel"], "dram_bytes_per_launch": rd + wr,
-                                "dram_read": rd, "dram_write": wr, "source": os.path.basename(path)}
+        rd = sum(to_bytes(*d["dram__bytes_read.sum"]) for d in res) / len(res)
+        wr = sum(to_bytes(*d["dram__bytes_write.sum"]) for d in res) / len(res)
+        ten = [float(d[k][0]) for d in res for k in ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",)
+               if k in d and d[k][0] not in ("", "n/a")]
+        summ["kernels"][cls] = {"round": a.round, "kernel": res[0]["kernel"], "launches_averaged": len(res),
+                                "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                                "tensor_pipe_active_pct_mean": (sum(ten) / len(ten)) if ten else None,
+                                "source": os.path.basename(path)}
     json.dump(summ, open(summ_p, "w"), indent=1)
 
 
