@@ -10,13 +10,17 @@
 //     emit iff max_c |c| > theta (pixel granularity, R1/R2);
 //     e = c as stored (fp32, or bf16-rounded in BF16 mode); y_acc += e.
 // A pixel is owned by a group of G lanes (G = 32 for C >= 32, else the next
-// power of two >= C), each lane holding CPL channels; the channel max is a
-// group shuffle reduction.  Emitted rows are written in the input's slot
-// layout (in place), so no compaction pass is needed after a site.
-// Delta rows are of type T (float in FP32 mode, bf16 in BF16 mode).
+// power of two >= C); lane l holds channels [l*CPL, (l+1)*CPL) and moves
+// them with 16-byte vectors (rowio.cuh); the channel max is a group shuffle
+// reduction.  The frame loop is serial in its arithmetic but not in its
+// loads: rows of the next P active frames are fetched together (P = frames
+// prefetched per batch, sized so ~16 values per lane are in flight), which
+// turns a chain of dependent DRAM round trips into batches.  Emitted rows
+// are written in the input's slot layout (in place), so no compaction pass
+// follows a site.  Delta rows are of type T (fp32 / bf16).
 #include <math_constants.h>
 
-#include "common.cuh"
+#include "rowio.cuh"
 
 namespace st {
 
@@ -41,6 +45,8 @@ template <int ACT>
 __device__ __forceinline__ float actf(float x) {
     return ACT == ACT_RELU ? relu_f(x) : silu_f(x);
 }
+
+constexpr int prefetch_depth(int cpl) { return cpl <= 2 ? 8 : cpl <= 4 ? 4 : cpl <= 8 ? 2 : 1; }
 
 // ---------------------------------------------------------------- dense ops
 template <int ACT>
@@ -99,7 +105,10 @@ void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaS
 template <int G, int CPL, int ACT, class T>
 __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
                                                  float theta, uint32_t *__restrict__ out_act, T *out_rows) {
+    constexpr int P = prefetch_depth(CPL);
     const int lane = threadIdx.x & (G - 1);
+    const int c0 = lane * CPL;
+    const bool full = (C % 8 == 0) && (c0 + CPL <= C);
     const unsigned mask = group_mask<G>();
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
@@ -111,44 +120,48 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
             continue;
         }
         float xa[CPL], ya[CPL];
+        row_load<float, CPL>(x0 + bp * C, c0, C, full, xa);
 #pragma unroll
-        for (int i = 0; i < CPL; i++) {
-            const int ch = lane + G * i;
-            xa[i] = ch < C ? __ldg(x0 + bp * C + ch) : 0.0f;
-            ya[i] = actf<ACT>(xa[i]);
-        }
+        for (int i = 0; i < CPL; i++) ya[i] = actf<ACT>(xa[i]);
         const int base = 1 + __ldg(in.pbase + bp);
         const uint32_t sl = __ldg(in.slot + bp);
         uint32_t emit = 0;
         while (a) {
-            const int t1 = __ffs(a) - 1;
-            a &= a - 1;
-            const int64_t row = base + __popc(sl & lowmask(t1));
-            float cand[CPL];
-            float mx = 0.0f;
+            int t1s[P];
+            int64_t rws[P];
+            float v[P][CPL];
 #pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int ch = lane + G * i;
-                if (ch < C) {
-                    xa[i] = __fadd_rn(xa[i], ldr<T>(rows + row * C + ch));   // reconstruct x (Eq.3)
-                    cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);          // restore the delta
-                    mx = fmaxf(mx, fabsf(cand[i]));
-                } else {
-                    cand[i] = 0.0f;
+            for (int j = 0; j < P; j++) {            // issue the next P frames' row loads
+                t1s[j] = -1;
+                if (a) {
+                    const int t1 = __ffs(a) - 1;
+                    a &= a - 1;
+                    t1s[j] = t1;
+                    rws[j] = base + __popc(sl & lowmask(t1));
+                    row_load<T, CPL>(rows + rws[j] * C, c0, C, full, v[j]);
                 }
             }
-            mx = gmax<G>(mx, mask);
-            if (mx > theta) {                                              // truncation
+#pragma unroll
+            for (int j = 0; j < P; j++) {            // then step the frames in order
+                if (t1s[j] < 0) continue;
+                float cand[CPL];
+                float mx = 0.0f;
 #pragma unroll
                 for (int i = 0; i < CPL; i++) {
-                    const int ch = lane + G * i;
-                    if (ch < C) {
-                        const float e = rnd<T>(cand[i]);
-                        ya[i] = __fadd_rn(ya[i], e);
-                        str<T>(out_rows + row * C + ch, e);
-                    }
+                    xa[i] = __fadd_rn(xa[i], v[j][i]);                 // reconstruct x (Eq.3)
+                    cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);      // restore the delta
+                    mx = fmaxf(mx, fabsf(cand[i]));
                 }
-                emit |= 1u << t1;
+                mx = gmax<G>(mx, mask);
+                if (mx > theta) {                                      // truncation
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        cand[i] = rnd<T>(cand[i]);
+                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                    }
+                    row_store<T, CPL>(out_rows + rws[j] * C, c0, C, full, cand);
+                    emit |= 1u << t1s[j];
+                }
             }
         }
         if (lane == 0) out_act[bp] = emit;
@@ -196,15 +209,20 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
 
 // --------------------------------------------------------- maxpool site
 // Touched set T = footprint dilation of the input mask (R7);
-// each touched window is re-evaluated from x_acc of its input pixels.
+// each touched window is re-evaluated from x_acc of its input pixels.  The
+// window pixels' frame words are read once per output pixel; the rows of
+// the next P touched frames are fetched together.
 template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__restrict__ x0, int B, Geo g,
                                                       float theta, const uint32_t *__restrict__ t_slot,
                                                       const int32_t *__restrict__ t_pbase,
                                                       uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+    constexpr int P = CPL <= 2 ? 4 : CPL <= 4 ? 2 : 1;
     const int lane = threadIdx.x & (G - 1);
-    const unsigned mask = group_mask<G>();
     const int C = g.Cin;
+    const int c0 = lane * CPL;
+    const bool full = (C % 8 == 0) && (c0 + CPL <= C);
+    const unsigned mask = group_mask<G>();
     const int Nin = g.Hin * g.Win, No = g.Hout * g.Wout;
     const int64_t BN = (int64_t)B * No;
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
@@ -218,19 +236,29 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
         }
         const int b = (int)(bq / No), q = (int)(bq % No);
         const int oy = q / g.Wout, ox = q % g.Wout;
-        int64_t wp[KMAX];
+        uint32_t wa[KMAX], wsl[KMAX];
+        int wbase[KMAX];
+        uint32_t valid = 0;
         float xa[KMAX][CPL];
 #pragma unroll
         for (int w = 0; w < KMAX; w++) {
-            wp[w] = -1;
             const int dy = w / g.kw, dx = w % g.kw;
             const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
-            if (w < g.kh * g.kw && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win)
-                wp[w] = (int64_t)b * Nin + iy * g.Win + ix;
+            wa[w] = 0;
+            wsl[w] = 0;
+            wbase[w] = 0;
+            if (w < g.kh * g.kw && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                const int64_t p = (int64_t)b * Nin + iy * g.Win + ix;
+                valid |= 1u << w;
+                wa[w] = __ldg(in.act + p);
+                if (wa[w]) {
+                    wsl[w] = __ldg(in.slot + p);
+                    wbase[w] = 1 + __ldg(in.pbase + p);
+                }
+                row_load<float, CPL>(x0 + p * C, c0, C, full, xa[w]);
+            } else {
 #pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int ch = lane + G * i;
-                xa[w][i] = (wp[w] >= 0 && ch < C) ? __ldg(x0 + wp[w] * C + ch) : -CUDART_INF_F;
+                for (int i = 0; i < CPL; i++) xa[w][i] = -CUDART_INF_F;
             }
         }
         float ya[CPL];
@@ -239,50 +267,63 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
             float m = -CUDART_INF_F;
 #pragma unroll
             for (int w = 0; w < KMAX; w++)
-                if (wp[w] >= 0) m = xa[w][i] > m ? xa[w][i] : m;
+                if ((valid >> w) & 1u) m = xa[w][i] > m ? xa[w][i] : m;
             ya[i] = m;
         }
         const int base = 1 + __ldg(t_pbase + bq);
         uint32_t bits = Tw, emit = 0;
         while (bits) {
-            const int t1 = __ffs(bits) - 1;
-            bits &= bits - 1;
+            int t1s[P];
+            uint32_t has[P];
+            float v[P][KMAX][CPL];
 #pragma unroll
-            for (int w = 0; w < KMAX; w++) {
-                if (wp[w] < 0) continue;
-                const int row = row_of(in, wp[w], t1);
-                if (!row) continue;
+            for (int j = 0; j < P; j++) {
+                t1s[j] = -1;
+                has[j] = 0;
+                if (bits) {
+                    const int t1 = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    t1s[j] = t1;
 #pragma unroll
-                for (int i = 0; i < CPL; i++) {
-                    const int ch = lane + G * i;
-                    if (ch < C) xa[w][i] = __fadd_rn(xa[w][i], ldr<T>(rows + (int64_t)row * C + ch));
-                }
-            }
-            float cand[CPL];
-            float mx = 0.0f;
-#pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                float m = -CUDART_INF_F;
-#pragma unroll
-                for (int w = 0; w < KMAX; w++)
-                    if (wp[w] >= 0) m = xa[w][i] > m ? xa[w][i] : m;
-                cand[i] = __fsub_rn(m, ya[i]);
-                const int ch = lane + G * i;
-                if (ch < C) mx = fmaxf(mx, fabsf(cand[i]));
-            }
-            mx = gmax<G>(mx, mask);
-            if (mx > theta) {
-                const int64_t orow = base + __popc(Tw & lowmask(t1));
-#pragma unroll
-                for (int i = 0; i < CPL; i++) {
-                    const int ch = lane + G * i;
-                    if (ch < C) {
-                        const float e = rnd<T>(cand[i]);
-                        ya[i] = __fadd_rn(ya[i], e);
-                        str<T>(out_rows + orow * C + ch, e);
+                    for (int w = 0; w < KMAX; w++) {
+                        if ((wa[w] >> t1) & 1u) {
+                            has[j] |= 1u << w;
+                            const int64_t row = wbase[w] + __popc(wsl[w] & lowmask(t1));
+                            row_load<T, CPL>(rows + row * C, c0, C, full, v[j][w]);
+                        }
                     }
                 }
-                emit |= 1u << t1;
+            }
+#pragma unroll
+            for (int j = 0; j < P; j++) {
+                if (t1s[j] < 0) continue;
+#pragma unroll
+                for (int w = 0; w < KMAX; w++)
+                    if ((has[j] >> w) & 1u)
+#pragma unroll
+                        for (int i = 0; i < CPL; i++) xa[w][i] = __fadd_rn(xa[w][i], v[j][w][i]);
+                float cand[CPL];
+                float mx = 0.0f;
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    float m = -CUDART_INF_F;
+#pragma unroll
+                    for (int w = 0; w < KMAX; w++)
+                        if ((valid >> w) & 1u) m = xa[w][i] > m ? xa[w][i] : m;
+                    cand[i] = c0 + i < C ? __fsub_rn(m, ya[i]) : 0.0f;
+                    mx = fmaxf(mx, fabsf(cand[i]));
+                }
+                mx = gmax<G>(mx, mask);
+                if (mx > theta) {
+                    const int64_t orow = base + __popc(Tw & lowmask(t1s[j]));
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        cand[i] = rnd<T>(cand[i]);
+                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                    }
+                    row_store<T, CPL>(out_rows + orow * C, c0, C, full, cand);
+                    emit |= 1u << t1s[j];
+                }
             }
         }
         if (lane == 0) out_act[bq] = emit;
@@ -314,6 +355,8 @@ __global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32
                                                   const int32_t *__restrict__ pbase, int64_t BN, int C,
                                                   T *__restrict__ out) {
     const int lane = threadIdx.x & (G - 1);
+    const int c0 = lane * CPL;
+    const bool full = (C % 8 == 0) && (c0 + CPL <= C);
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
     const T *ra_rows = static_cast<const T *>(a.rows);
@@ -326,15 +369,18 @@ __global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32
             const int t1 = __ffs(w) - 1;
             w &= w - 1;
             const int ra = row_of(a, bp, t1), rb = row_of(b, bp, t1);
+            float va[CPL], vb[CPL];
+            if (ra) row_load<T, CPL>(ra_rows + (int64_t)ra * C, c0, C, full, va);
+            else
 #pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int ch = lane + G * i;
-                if (ch < C) {
-                    const float va = ra ? ldr<T>(ra_rows + (int64_t)ra * C + ch) : 0.0f;
-                    const float vb = rb ? ldr<T>(rb_rows + (int64_t)rb * C + ch) : 0.0f;
-                    str<T>(out + row * C + ch, __fadd_rn(va, vb));
-                }
-            }
+                for (int i = 0; i < CPL; i++) va[i] = 0.0f;
+            if (rb) row_load<T, CPL>(rb_rows + (int64_t)rb * C, c0, C, full, vb);
+            else
+#pragma unroll
+                for (int i = 0; i < CPL; i++) vb[i] = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) va[i] = __fadd_rn(va[i], vb[i]);
+            row_store<T, CPL>(out + row * C, c0, C, full, va);
             row++;
         }
     }
@@ -355,6 +401,8 @@ template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__restrict__ y0, int B, int N, int C,
                                                     int n_diff, float *__restrict__ out) {
     const int lane = threadIdx.x & (G - 1);
+    const int c0 = lane * CPL;
+    const bool full = (C % 8 == 0) && (c0 + CPL <= C);
     const int64_t BN = (int64_t)B * N;
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
@@ -367,27 +415,18 @@ __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__res
         const uint32_t sl = a ? __ldg(in.slot + bq) : 0u;
         float O[CPL];
         float *o = out + (int64_t)b * (n_diff + 1) * fstride + (int64_t)q * C;
-#pragma unroll
-        for (int i = 0; i < CPL; i++) {
-            const int ch = lane + G * i;
-            O[i] = ch < C ? __ldg(y0 + bq * C + ch) : 0.0f;
-            if (ch < C) o[ch] = O[i];
-        }
+        row_load<float, CPL>(y0 + bq * C, c0, C, full, O);
+        row_store<float, CPL>(o, c0, C, full, O);
         for (int t1 = 0; t1 < n_diff; t1++) {
             o += fstride;
             if ((a >> t1) & 1u) {
                 const int64_t row = base + __popc(sl & lowmask(t1));
+                float v[CPL];
+                row_load<T, CPL>(rows + row * C, c0, C, full, v);
 #pragma unroll
-                for (int i = 0; i < CPL; i++) {
-                    const int ch = lane + G * i;
-                    if (ch < C) O[i] = __fadd_rn(O[i], ldr<T>(rows + row * C + ch));
-                }
+                for (int i = 0; i < CPL; i++) O[i] = __fadd_rn(O[i], v[i]);
             }
-#pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int ch = lane + G * i;
-                if (ch < C) o[ch] = O[i];
-            }
+            row_store<float, CPL>(o, c0, C, full, O);
         }
     }
 }
