@@ -113,34 +113,56 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
     const T *rows = static_cast<const T *>(in.rows);
-    for (int64_t bp = grp; bp < BN; bp += ngrp) {
-        uint32_t a = __ldg(in.act + bp);
+    // software pipeline over this group's pixels: while pixel k runs, the
+    // frame word of pixel k+2 and the metadata + x0 of pixel k+1 are in flight
+    int64_t bp = grp;
+    uint32_t a_nx = bp < BN ? __ldg(in.act + bp) : 0u;                      // pixel k
+    int base_nx = 0;
+    uint32_t sl_nx = 0;
+    float x_nx[CPL];
+    if (a_nx) {
+        base_nx = 1 + __ldg(in.pbase + bp);
+        sl_nx = __ldg(in.slot + bp);
+        row_load<float, CPL>(x0 + bp * C, c0, C, full, x_nx);
+    }
+    uint32_t a_nn = bp + ngrp < BN ? __ldg(in.act + bp + ngrp) : 0u;         // pixel k+1
+    for (; bp < BN; bp += ngrp) {
+        uint32_t a = a_nx;
+        const int base = base_nx;
+        const uint32_t sl = sl_nx;
+        float xa[CPL], ya[CPL];
+#pragma unroll
+        for (int i = 0; i < CPL; i++) xa[i] = x_nx[i];
+        // prefetch: metadata + x0 of pixel k+1, frame word of pixel k+2
+        const int64_t b1 = bp + ngrp;
+        a_nx = a_nn;
+        if (a_nx) {
+            base_nx = 1 + __ldg(in.pbase + b1);
+            sl_nx = __ldg(in.slot + b1);
+            row_load<float, CPL>(x0 + b1 * C, c0, C, full, x_nx);
+        }
+        a_nn = b1 + ngrp < BN ? __ldg(in.act + b1 + ngrp) : 0u;
         if (!a) {
             if (lane == 0) out_act[bp] = 0;
             continue;
         }
-        float xa[CPL], ya[CPL];
-        row_load<float, CPL>(x0 + bp * C, c0, C, full, xa);
 #pragma unroll
         for (int i = 0; i < CPL; i++) ya[i] = actf<ACT>(xa[i]);
-        const int base = 1 + __ldg(in.pbase + bp);
-        const uint32_t sl = __ldg(in.slot + bp);
         uint32_t emit = 0;
         while (a) {
             int t1s[P];
             int64_t rws[P];
             float v[P][CPL];
 #pragma unroll
-            for (int j = 0; j < P; j++) {            // issue the next P frames' row loads
-                t1s[j] = -1;
-                if (a) {
-                    const int t1 = __ffs(a) - 1;
-                    a &= a - 1;
-                    t1s[j] = t1;
-                    rws[j] = base + __popc(sl & lowmask(t1));
-                    row_load<T, CPL>(rows + rws[j] * C, c0, C, full, v[j]);
-                }
+            for (int j = 0; j < P; j++) {            // the next P frames (absent: row 0 = zeros)
+                const int t1 = __ffs(a) - 1;         // -1 when a == 0
+                t1s[j] = t1;
+                rws[j] = t1 >= 0 ? base + __popc(sl & lowmask(t1)) : 0;
+                a &= a - 1;
             }
+#pragma unroll
+            for (int j = 0; j < P; j++)              // issue all P row loads before any use
+                row_load<T, CPL>(rows + rws[j] * C, c0, C, full, v[j]);
 #pragma unroll
             for (int j = 0; j < P; j++) {            // then step the frames in order
                 if (t1s[j] < 0) continue;
@@ -185,6 +207,33 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
     else if ((C_) <= 672) { LAUNCH(32, 21); }                      \
     else { LAUNCH(32, 36); }
 
+// Pixel-group shape for the site / join / accumulate kernels: 8 channels
+// (16 bytes of bf16) per lane when C % 8 == 0, so narrow layers put several
+// pixels in one warp (C = 64 -> 8 lanes per pixel, 4 pixels per warp) and a
+// lane always moves whole 16-byte vectors; wide layers use 32 lanes.
+#define SITE_DISPATCH(C_, LAUNCH)                                  \
+    if ((C_) % 8 != 0 || (C_) <= 8) {                              \
+        if ((C_) <= 1) { LAUNCH(1, 1); }                           \
+        else if ((C_) <= 2) { LAUNCH(2, 1); }                      \
+        else if ((C_) <= 4) { LAUNCH(4, 1); }                      \
+        else if ((C_) <= 8) { LAUNCH(8, 1); }                      \
+        else if ((C_) <= 16) { LAUNCH(16, 1); }                    \
+        else if ((C_) <= 32) { LAUNCH(32, 1); }                    \
+        else if ((C_) <= 64) { LAUNCH(32, 2); }                    \
+        else if ((C_) <= 128) { LAUNCH(32, 4); }                   \
+        else if ((C_) <= 256) { LAUNCH(32, 8); }                   \
+        else if ((C_) <= 512) { LAUNCH(32, 16); }                  \
+        else if ((C_) <= 768) { LAUNCH(32, 24); }                  \
+        else { LAUNCH(32, 40); }                                   \
+    } else if ((C_) <= 16) { LAUNCH(2, 8); }                       \
+    else if ((C_) <= 32) { LAUNCH(4, 8); }                         \
+    else if ((C_) <= 64) { LAUNCH(8, 8); }                         \
+    else if ((C_) <= 128) { LAUNCH(16, 8); }                       \
+    else if ((C_) <= 256) { LAUNCH(32, 8); }                       \
+    else if ((C_) <= 512) { LAUNCH(32, 16); }                      \
+    else if ((C_) <= 768) { LAUNCH(32, 24); }                      \
+    else { LAUNCH(32, 40); }
+
 static int groups_grid(int64_t n_groups, int G) {
     const int64_t threads = n_groups * G;
     return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(threads, 256), 148 * 8));
@@ -203,7 +252,7 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
             k_site_pw<G_, CPL_, ACT_SILU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
                                                                   static_cast<T *>(out_rows));         \
     }
-    ST_ROW_DISPATCH(bf, CH_DISPATCH(C, L_PW));
+    ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_PW));
 #undef L_PW
 }
 
@@ -276,24 +325,24 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
             int t1s[P];
             uint32_t has[P];
             float v[P][KMAX][CPL];
+            int64_t wrow[P][KMAX];
 #pragma unroll
-            for (int j = 0; j < P; j++) {
-                t1s[j] = -1;
+            for (int j = 0; j < P; j++) {            // the next P touched frames
+                const int t1 = __ffs(bits) - 1;      // -1 when bits == 0
+                bits &= bits - 1;
+                t1s[j] = t1;
                 has[j] = 0;
-                if (bits) {
-                    const int t1 = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    t1s[j] = t1;
 #pragma unroll
-                    for (int w = 0; w < KMAX; w++) {
-                        if ((wa[w] >> t1) & 1u) {
-                            has[j] |= 1u << w;
-                            const int64_t row = wbase[w] + __popc(wsl[w] & lowmask(t1));
-                            row_load<T, CPL>(rows + row * C, c0, C, full, v[j][w]);
-                        }
-                    }
+                for (int w = 0; w < KMAX; w++) {
+                    const bool on = t1 >= 0 && ((wa[w] >> t1) & 1u);
+                    has[j] |= (uint32_t)on << w;
+                    wrow[j][w] = on ? wbase[w] + __popc(wsl[w] & lowmask(t1)) : 0;   // row 0 = zeros
                 }
             }
+#pragma unroll
+            for (int j = 0; j < P; j++)              // issue every window row load before any use
+#pragma unroll
+                for (int w = 0; w < KMAX; w++) row_load<T, CPL>(rows + wrow[j][w] * C, c0, C, full, v[j][w]);
 #pragma unroll
             for (int j = 0; j < P; j++) {
                 if (t1s[j] < 0) continue;
@@ -345,7 +394,7 @@ void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float t
             k_site_maxpool<G_, CPL_, 9, T><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase,        \
                                                                 out_act, static_cast<T *>(out_rows));        \
     }
-    ST_ROW_DISPATCH(bf, CH_DISPATCH(g.Cin, L_MP));
+    ST_ROW_DISPATCH(bf, SITE_DISPATCH(g.Cin, L_MP));
 #undef L_MP
 }
 
@@ -391,7 +440,7 @@ void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbas
     const int64_t BN = (int64_t)B * N;
 #define L_ADD(G_, CPL_) \
     k_add_rows<G_, CPL_, T><<<groups_grid(BN, G_), 256, 0, s>>>(a, b, slot, pbase, BN, C, static_cast<T *>(out_rows));
-    ST_ROW_DISPATCH(bf, CH_DISPATCH(C, L_ADD));
+    ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_ADD));
 #undef L_ADD
 }
 
@@ -435,7 +484,7 @@ void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_dif
                        cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
 #define L_ACC(G_, CPL_) k_accumulate<G_, CPL_, T><<<groups_grid(BN, G_), 256, 0, s>>>(in, y0, B, N, C, n_diff, out);
-    ST_ROW_DISPATCH(bf, CH_DISPATCH(C, L_ACC));
+    ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_ACC));
 #undef L_ACC
 }
 
