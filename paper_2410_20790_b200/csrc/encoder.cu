@@ -66,6 +66,20 @@ struct LaunchRec {
     cudaEvent_t e0, e1;
 };
 
+struct GraphKey {
+    const float *frames;
+    int64_t stride;
+    int n_diff, chunks;
+    bool operator==(const GraphKey &o) const {
+        return frames == o.frames && stride == o.stride && n_diff == o.n_diff && chunks == o.chunks;
+    }
+};
+struct GraphEnt {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int launches;
+};
+
 }  // namespace
 
 struct st_encoder {
@@ -92,6 +106,13 @@ struct st_encoder {
     float *ref = nullptr;        // staged reference frames [B][N][C]
     float *weights_mem = nullptr;
     uint16_t *wbf_mem = nullptr;
+    // thresholds: pinned host staging -> device (a graph node), one fp32 per site
+    float *thr_dev = nullptr, *thr_host = nullptr;
+    cudaEvent_t thr_ev = nullptr;
+    bool thr_pending = false;
+    // CUDA graphs of whole steps, keyed by (frames, stride, n_diff, chunks)
+    bool use_graphs = true;
+    std::vector<GraphEnt> graphs;
     // state
     int staged_chunks = 0;       // >0 after encode_reference
     int last_chunks = 0, last_ndiff = -1;
@@ -478,7 +499,7 @@ static st_status plan(st_encoder *e) {
     int64_t max_words = B * Nin;
     for (auto &l : e->L) max_words = std::max<int64_t>(max_words, B * l.H * l.W);
     const int64_t small = (n + 1) * 4 + B * e->n_sites * 32 * 8 + (n + 1) * 3 * 8 + e->n_sites * 8 +
-                          scan_tmp_ints(max_words) * 4 + B * Nin * e->in_C * 4 + 1024;
+                          scan_tmp_ints(max_words) * 4 + e->n_sites * 4 + 8 * 256;
     CUDA_OK(e, cudaMalloc(&e->smallmem, small));
     char *p = e->smallmem;
     auto take = [&](int64_t bytes) { char *r = p; p += (bytes + 255) / 256 * 256; return r; };
@@ -487,6 +508,11 @@ static st_status plan(st_encoder *e) {
     e->stats = (long long *)take((n + 1) * 3 * 8);
     e->site_sum = (long long *)take(e->n_sites * 8);
     e->scan_tmp = (int32_t *)take(scan_tmp_ints(max_words) * 4);
+    e->thr_dev = (float *)take(e->n_sites * 4);
+    CUDA_OK(e, cudaMallocHost(&e->thr_host, e->n_sites * 4));
+    CUDA_OK(e, cudaEventCreateWithFlags(&e->thr_ev, cudaEventDisableTiming));
+    const char *ng = getenv("ST_NO_GRAPHS");
+    e->use_graphs = !(ng && ng[0] == '1');
     (void)take(0);
     CUDA_OK(e, cudaMalloc(&e->ref, B * Nin * e->in_C * 4));
     // zero rows (row 0 of every rows buffer) are written per step (arena reuse)
@@ -500,6 +526,10 @@ extern "C" void st_encoder_destroy(st_encoder *e) {
     cudaFree(e->ref);
     cudaFree(e->weights_mem);
     cudaFree(e->wbf_mem);
+    for (auto &g : e->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (e->thr_host) cudaFreeHost(e->thr_host);
+    if (e->thr_ev) cudaEventDestroy(e->thr_ev);
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     delete e;
 }
@@ -568,6 +598,12 @@ static int64_t rows_cap_of(const st_encoder *e, int t) {
     return l.rows_cap;
 }
 
+// Enqueue one SparseBatch step on stream s (everything st_encode_diff does on
+// the device).  Thresholds are read by the kernels from e->thr_dev, which the
+// first node refreshes from the pinned host staging buffer, so the same
+// captured graph serves every step.
+static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64_t fstride, cudaStream_t s);
+
 extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int32_t n_diff, int64_t chunk_stride,
                                     const float *thresholds, void *stream) {
     if (!e) return ST_ERR_ARG;
@@ -579,15 +615,57 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
         if (!(thresholds[i] >= 0.0f)) return fail(e, ST_ERR_ARG, "threshold %d is negative or NaN", i);
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_OK(e, cudaSetDevice(e->cfg.device));
-    const int B = e->staged_chunks, F = n_diff, n = (int)e->L.size();
+    const int64_t per = (int64_t)e->in_H * e->in_W * e->in_C;
+    const int64_t fstride = chunk_stride ? chunk_stride : (int64_t)n_diff * per;
+    // the previous step's threshold copy must have consumed the staging buffer
+    if (e->thr_pending) CUDA_OK(e, cudaEventSynchronize(e->thr_ev));
+    std::memcpy(e->thr_host, thresholds, sizeof(float) * e->n_sites);
+    e->last_chunks = e->staged_chunks;
+    e->last_ndiff = n_diff;
+    e->last_stream = s;
+    const bool graphs = e->use_graphs && !e->prof && !e->cfg.debug_retain;
+    if (!graphs) {
+        st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
+        if (r) return r;
+    } else {
+        GraphKey key{frames_dev, fstride, n_diff, e->staged_chunks};
+        GraphEnt *ent = nullptr;
+        for (auto &g : e->graphs)
+            if (g.key == key) ent = &g;
+        if (!ent) {   // first sight: run eagerly (lazy kernel attributes get set), capture next time
+            e->graphs.push_back(GraphEnt{key, nullptr, 0});
+            st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
+            if (r) return r;
+        } else {
+            if (!ent->exec) {
+                cudaGraph_t g = nullptr;
+                CUDA_OK(e, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
+                cudaError_t ce = cudaStreamEndCapture(s, &g);
+                if (r) return r;
+                if (ce != cudaSuccess) return fail(e, ST_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+                CUDA_OK(e, cudaGraphInstantiate(&ent->exec, g, 0));
+                cudaGraphDestroy(g);
+                ent->launches = e->launches;
+            }
+            CUDA_OK(e, cudaGraphLaunch(ent->exec, s));
+            e->launches = ent->launches;
+        }
+    }
+    CUDA_OK(e, cudaEventRecord(e->thr_ev, s));
+    e->thr_pending = true;
+    CUDA_OK(e, cudaGetLastError());
+    return ST_OK;
+}
+
+static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64_t fstride, cudaStream_t s) {
+    const int B = e->staged_chunks, n = (int)e->L.size();
     const int64_t Nin = (int64_t)e->in_H * e->in_W;
     const int64_t per = Nin * e->in_C;
-    const int64_t fstride = chunk_stride ? chunk_stride : (int64_t)F * per;
     e->launches = 0;
-    e->last_chunks = B;
-    e->last_ndiff = F;
-    e->last_stream = s;
     if (e->prof) { e->recs.clear(); e->ev_used = 0; }
+    CUDA_OK(e, cudaMemcpyAsync(e->thr_dev, e->thr_host, sizeof(float) * e->n_sites, cudaMemcpyHostToDevice, s));
+    const float *thresholds = e->thr_dev;   // device copy, one fp32 per site
     CUDA_OK(e, cudaMemsetAsync(e->counts, 0, (size_t)e->B * e->n_sites * 32 * 8, s));
     CUDA_OK(e, cudaMemsetAsync(e->stats, 0, (size_t)(n + 1) * 3 * 8, s));
     CUDA_OK(e, cudaMemsetAsync(e->site_sum, 0, (size_t)e->n_sites * 8, s));
@@ -604,7 +682,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
         void *rows = e->ptr(e->in_rows);
         const float *fr = frames_dev;
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds[0], bf, act, s));
+               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act, s));
         LAUNCH(e, KC_SCAN, -1, s,
                launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
         zero_row(e->in_rows, e->in_C);
@@ -661,7 +739,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             if (F == 0) break;
             DView me = view_of(e, i);
             LAUNCH(e, KC_SITE_PW, i, s,
-                   launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds[l.site], bf,
+                   launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
                                          e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
@@ -676,7 +754,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             LAUNCH(e, KC_SITE_MP, i, s,
-                   launch_site_maxpool(in, x_src, B, l.geo, thresholds[l.site], bf, slot, pb,
+                   launch_site_maxpool(in, x_src, B, l.geo, thresholds + l.site, bf, slot, pb,
                                        e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
@@ -710,7 +788,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             if (F > 0) LAUNCH(e, KC_SE, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
             LAUNCH(e, KC_SE, i, s,
                    launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
-                                      thresholds[l.site], s_tab, refresh, s));
+                                      thresholds + l.site, s_tab, refresh, s));
             LAUNCH(e, KC_SE, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
@@ -718,7 +796,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             LAUNCH(e, KC_SE, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             LAUNCH(e, KC_SE, i, s,
-                   launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds[l.site], bf, slot, pb,
+                   launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds + l.site, bf, slot, pb,
                                   e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,

@@ -27,10 +27,12 @@ struct Geo {   // conv / pool geometry
     int Hin, Win, Cin, Hout, Wout, Cout, kh, kw, sh, sw, ph, pw, groups;
 };
 
+// Thresholds are read by the kernels from device memory (theta points at one
+// fp32 site threshold), so a captured CUDA graph serves every step.
 // ---- masks, compaction (kernels_mask.cu) ----
 // Subtraction pass 1 (site 0): act bits per pixel, sequential over frames.
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
-                          int B, int N, int C, int n_diff, float theta, bool bf, uint32_t *act, cudaStream_t s);
+                          int B, int N, int C, int n_diff, const float *theta, bool bf, uint32_t *act, cudaStream_t s);
 // Subtraction pass 2: write emitted rows at the slots of `act`.
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
                           int B, int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
@@ -84,10 +86,10 @@ void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t
 void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s);
 void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s);
 // pointwise site: emitted rows written into out_rows at the input slots
-void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta, bool bf,
+void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
                            uint32_t *out_act, void *out_rows, cudaStream_t s);
 // maxpool site: touched layout (t_slot, t_pbase) = dilation of in.act
-void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta, bool bf,
+void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
                          cudaStream_t s);
 // residual add: out slot layout = act_a | act_b (already scanned into pbase)
@@ -97,11 +99,11 @@ void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbas
 void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s);
 void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double *dsum, cudaStream_t s);
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
-                        const float *b1, const float *w2, const float *b2, float theta, float *s_tab,
+                        const float *b1, const float *w2, const float *b2, const float *theta, float *s_tab,
                         uint32_t *refresh, cudaStream_t s);
 void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s);
 void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s);
-void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta, bool bf,
+void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, const float *theta, bool bf,
                     const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s);
 // Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0)
 void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, bool bf, float *out,

@@ -17,7 +17,9 @@ namespace st {
 template <int C, class T>
 __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__ ref, int64_t ref_stride,
                                                        const float *__restrict__ fr, int64_t fr_stride, int B,
-                                                       int N, int n_diff, float theta, uint32_t *__restrict__ act) {
+                                                       int N, int n_diff, const float *__restrict__ theta_p,
+                                                       uint32_t *__restrict__ act) {
+    const float theta = __ldg(theta_p);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     const int b = (int)(i / N), p = (int)(i % N);
@@ -86,9 +88,9 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
     }
 
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
-                          int N, int C, int n_diff, float theta, bool bf, uint32_t *act, cudaStream_t s) {
+                          int N, int C, int n_diff, const float *theta_p, bool bf, uint32_t *act, cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
-    ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta,
+    ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta_p,
                                      act));
 }
 

@@ -92,8 +92,10 @@ __device__ void se_gate_block(const float *m, int C, int H, const float *w1, con
 // force at frame t (t = 0: reference gate); refresh[b] bit t-1 = refresh at t.
 __global__ void __launch_bounds__(256) k_se_schedule(const double *__restrict__ sum0, const double *__restrict__ dsum,
                                                      int N, int C, int H, int F, const float *w1, const float *b1,
-                                                     const float *w2, const float *b2, float theta,
+                                                     const float *w2, const float *b2,
+                                                     const float *__restrict__ theta_p,
                                                      float *__restrict__ s_tab, uint32_t *__restrict__ refresh) {
+    const float theta = __ldg(theta_p);
     extern __shared__ float sm[];
     float *mean = sm;            // [C]
     float *gate = mean + C;      // [C]
@@ -165,9 +167,10 @@ __global__ void k_se_slots(const uint32_t *__restrict__ act, const uint32_t *__r
 // ---- (iii) SE site pixel loop
 template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restrict__ x0, const float *__restrict__ s_tab,
-                                                 int N, int C, int F, int64_t BN, float theta,
+                                                 int N, int C, int F, int64_t BN, const float *__restrict__ theta_p,
                                                  const uint32_t *__restrict__ slot, const int32_t *__restrict__ pbase,
                                                  uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+    const float theta = __ldg(theta_p);
     const T *rows = static_cast<const T *>(in.rows);
     const int lane = threadIdx.x & (G - 1);
     unsigned mask = 0xffffffffu;
@@ -240,7 +243,7 @@ void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStr
 }
 
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
-                        const float *b1, const float *w2, const float *b2, float theta, float *s_tab,
+                        const float *b1, const float *w2, const float *b2, const float *theta, float *s_tab,
                         uint32_t *refresh, cudaStream_t s) {
     const size_t smem = (size_t)(3 * C + ((H + 1) & ~1)) * 4 + (size_t)C * 8 + 64;
     static size_t attr = 0;
@@ -280,7 +283,7 @@ void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N,
     k_se_slots<<<cdiv(n, 256), 256, 0, s>>>(act, refresh, N, n, slot);
 }
 
-void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, float theta, bool bf,
+void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, const float *theta, bool bf,
                     const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
     auto grid_for = [&](int G) {

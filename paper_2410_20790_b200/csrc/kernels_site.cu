@@ -104,7 +104,9 @@ void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaS
 // ------------------------------------------------------- pointwise site
 template <int G, int CPL, int ACT, class T>
 __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
-                                                 float theta, uint32_t *__restrict__ out_act, T *out_rows) {
+                                                 const float *__restrict__ theta_p, uint32_t *__restrict__ out_act,
+                                                 T *out_rows) {
+    const float theta = __ldg(theta_p);
     constexpr int P = prefetch_depth(CPL);
     const int lane = threadIdx.x & (G - 1);
     const int c0 = lane * CPL;
@@ -239,7 +241,7 @@ static int groups_grid(int64_t n_groups, int G) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(threads, 256), 148 * 8));
 }
 
-void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, float theta, bool bf,
+void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
                            uint32_t *out_act, void *out_rows, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
 #define L_PW(G_, CPL_)                                                                                 \
@@ -263,9 +265,11 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
 // the next P touched frames are fetched together.
 template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__restrict__ x0, int B, Geo g,
-                                                      float theta, const uint32_t *__restrict__ t_slot,
+                                                      const float *__restrict__ theta_p,
+                                                      const uint32_t *__restrict__ t_slot,
                                                       const int32_t *__restrict__ t_pbase,
                                                       uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+    const float theta = __ldg(theta_p);
     constexpr int P = CPL <= 2 ? 4 : CPL <= 4 ? 2 : 1;
     const int lane = threadIdx.x & (G - 1);
     const int C = g.Cin;
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
     }
 }
 
-void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, float theta, bool bf,
+void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
                          cudaStream_t s) {
     const int64_t BN = (int64_t)B * g.Hout * g.Wout;

@@ -147,6 +147,38 @@ def test_efficientnet_small():
         compare_chunk(enc, net, fr[b], 0.05, b, exact=False)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_graph_replay_matches_eager(precision, monkeypatch):
+    """Steps replayed from a captured CUDA graph (thresholds refreshed from
+    device memory each step) are bit-identical to eager launches, and the
+    FP32 ones to the oracle."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    cfg = W.get_config(2)
+    net = cfg.build_net()
+    fr_np = make_frames(cfg, 4, L=9)
+    fr = torch.from_numpy(fr_np).cuda()
+    thetas = [0.05, 0.03, 0.08, 0.05]
+    outs = {}
+    for mode in ("graph", "eager"):
+        if mode == "eager":
+            monkeypatch.setenv("ST_NO_GRAPHS", "1")
+        enc = Encoder(net, 4, 9, precision=precision)
+        res = []
+        for th in thetas:
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append((enc.outputs(enc.taps[0]).cpu().numpy().copy(), enc.get_sparsity()[0].copy()))
+        outs[mode] = res
+        enc.close()
+    for (og, cg), (oe, ce) in zip(outs["graph"], outs["eager"]):
+        assert np.array_equal(og, oe) and np.array_equal(cg, ce)
+    if precision == "fp32":
+        r = oracle.run_chunk(net, fr_np[2], thetas[3], want_masks=False)
+        assert np.array_equal(outs["graph"][3][0][2], r["taps"][max(r["taps"])])
+
+
 def test_errors_and_state():
     from paper_2410_20790_b200 import Encoder, StError
     import torch
