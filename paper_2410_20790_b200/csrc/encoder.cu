@@ -113,6 +113,8 @@ struct st_encoder {
     // CUDA graphs of whole steps, keyed by (frames, stride, n_diff, chunks)
     bool use_graphs = true;
     std::vector<GraphEnt> graphs;
+    cudaStream_t gstream = nullptr;            // capture / replay stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // state
     int staged_chunks = 0;       // >0 after encode_reference
     int last_chunks = 0, last_ndiff = -1;
@@ -513,6 +515,9 @@ static st_status plan(st_encoder *e) {
     CUDA_OK(e, cudaEventCreateWithFlags(&e->thr_ev, cudaEventDisableTiming));
     const char *ng = getenv("ST_NO_GRAPHS");
     e->use_graphs = !(ng && ng[0] == '1');
+    CUDA_OK(e, cudaStreamCreateWithFlags(&e->gstream, cudaStreamNonBlocking));
+    CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     (void)take(0);
     CUDA_OK(e, cudaMalloc(&e->ref, B * Nin * e->in_C * 4));
     // zero rows (row 0 of every rows buffer) are written per step (arena reuse)
@@ -530,6 +535,9 @@ extern "C" void st_encoder_destroy(st_encoder *e) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (e->thr_host) cudaFreeHost(e->thr_host);
     if (e->thr_ev) cudaEventDestroy(e->thr_ev);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
+    if (e->gstream) cudaStreamDestroy(e->gstream);
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     delete e;
 }
@@ -637,18 +645,25 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
             if (r) return r;
         } else {
+            // capture and replay on the encoder's own stream, forked from / joined
+            // back to the caller's stream (the legacy default stream cannot be captured)
+            cudaStream_t g_s = e->gstream;
             if (!ent->exec) {
                 cudaGraph_t g = nullptr;
-                CUDA_OK(e, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-                st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
-                cudaError_t ce = cudaStreamEndCapture(s, &g);
+                CUDA_OK(e, cudaStreamBeginCapture(g_s, cudaStreamCaptureModeThreadLocal));
+                st_status r = issue_step(e, frames_dev, n_diff, fstride, g_s);
+                cudaError_t ce = cudaStreamEndCapture(g_s, &g);
                 if (r) return r;
                 if (ce != cudaSuccess) return fail(e, ST_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
                 CUDA_OK(e, cudaGraphInstantiate(&ent->exec, g, 0));
                 cudaGraphDestroy(g);
                 ent->launches = e->launches;
             }
-            CUDA_OK(e, cudaGraphLaunch(ent->exec, s));
+            CUDA_OK(e, cudaEventRecord(e->ev_fork, s));
+            CUDA_OK(e, cudaStreamWaitEvent(g_s, e->ev_fork, 0));
+            CUDA_OK(e, cudaGraphLaunch(ent->exec, g_s));
+            CUDA_OK(e, cudaEventRecord(e->ev_join, g_s));
+            CUDA_OK(e, cudaStreamWaitEvent(s, e->ev_join, 0));
             e->launches = ent->launches;
         }
     }
