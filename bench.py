@@ -230,6 +230,10 @@ def main():
 
     for w in range(args.warmup):
         step(batches[w % n_batches])
+    # every input batch seen twice before timing: the library captures a CUDA
+    # graph of the step on the second sight of a (frames, shape) key
+    for w in range(2 * n_batches):
+        step(batches[w % n_batches])
     torch.cuda.synchronize(dev)
     launches_per_step = enc.last_launch_count()
 
@@ -270,6 +274,10 @@ def main():
     out_view = enc.outputs(tap)
     host_out = torch.empty(out_view.shape, dtype=torch.float32).pin_memory()
     dev_in = torch.empty_like(batches[0])
+    for _ in range(2):   # graph capture of the e2e input buffer's key (untimed)
+        dev_in.copy_(host_in[0], non_blocking=True)
+        step(dev_in)
+    torch.cuda.synchronize(dev)
     e2e_ms = 0.0
     e2e_steps = max(3, min(args.steps, 10))
     for k in range(e2e_steps):
