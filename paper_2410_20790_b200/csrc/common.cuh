@@ -56,6 +56,10 @@ __device__ __forceinline__ float relu_f(float x) { return x > 0.0f ? x : 0.0f; }
 __device__ __forceinline__ float exp_r(float v) { return (float)exp((double)v); }
 __device__ __forceinline__ float silu_f(float x) { return __fdiv_rn(x, __fadd_rn(1.0f, exp_r(-x))); }
 __device__ __forceinline__ float sigm_f(float x) { return __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_r(-x))); }
+// BF16 mode (tolerance parity, R22-BF16): single-precision MUFU exp and
+// approximate division -- within a few fp32 ulp of the exact form, far below
+// the bf16 rounding of every emitted delta.
+__device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 

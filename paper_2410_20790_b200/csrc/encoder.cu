@@ -750,7 +750,10 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         }
         case ST_RELU: case ST_SILU: {
             const int act_kind = l.kind == ST_RELU ? ACT_RELU : ACT_SILU;
-            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, act_kind, s));
+            // the dense reference activation uses the same SiLU form as the site (fast in BF16 mode)
+            const int dense_kind = (act_kind == ACT_SILU && bf) ? ACT_SILU_FAST : act_kind;
+            LAUNCH(e, KC_DENSE_MISC, i, s,
+                   launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, s));
             if (F == 0) break;
             DView me = view_of(e, i);
             LAUNCH(e, KC_SITE_PW, i, s,

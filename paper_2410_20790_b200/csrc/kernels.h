@@ -81,7 +81,7 @@ bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout);
 void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s);
 
 // ---- sites, joins, accumulation (kernels_site.cu) ----
-enum Act { ACT_RELU = 0, ACT_SILU = 1 };
+enum Act { ACT_RELU = 0, ACT_SILU = 1, ACT_SILU_FAST = 2 };   // FAST: BF16 mode only
 void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t s);
 void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s);
 void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s);

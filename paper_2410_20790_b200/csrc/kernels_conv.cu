@@ -242,98 +242,4 @@ void launch_conv_f32(const ConvCall &c, cudaStream_t s) {
     else launch_conv_t<bf16>(c, s);
 }
 
-// ------------------------------------------------------------- depthwise
-// groups == Cin == Cout (reading R9): per output row and channel,
-// acc = fmaf chain over (dy, dx); weights [kh*kw][C] (K-major repack).
-template <int CPL, class T>
-__global__ void __launch_bounds__(256) k_dwconv_f32(ConvCall c) {
-    const Geo g = c.g;
-    const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
-    const int M = c.dense ? c.B * Nout : *c.m_dev;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const T *A = c.dense ? reinterpret_cast<const T *>(c.a_dense) : static_cast<const T *>(c.a.rows);
-    for (int64_t r = warp; r < M; r += nwarps) {
-        int b, q, t1 = 0;
-        if (c.dense) {
-            b = (int)(r / Nout);
-            q = (int)(r - (int64_t)b * Nout);
-        } else {
-            const int code = __ldg(c.ridx + r);
-            const int gq = code >> 5;
-            t1 = code & 31;
-            b = gq / Nout;
-            q = gq - b * Nout;
-        }
-        const int oy = q / g.Wout, ox = q - oy * g.Wout;
-        float acc[CPL];
-#pragma unroll
-        for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
-        for (int dy = 0; dy < g.kh; dy++) {
-            const int iy = oy * g.sh - g.ph + dy;
-            if (iy < 0 || iy >= g.Hin) continue;
-            for (int dx = 0; dx < g.kw; dx++) {
-                const int ix = ox * g.sw - g.pw + dx;
-                if (ix < 0 || ix >= g.Win) continue;
-                const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
-                int64_t idx;
-                if (c.dense) {
-                    idx = bp;
-                } else {
-                    const int row = row_of(c.a, bp, t1);
-                    if (!row) continue;
-                    idx = row;
-                }
-                const T *ap = A + idx * g.Cin;
-                const int tap = dy * g.kw + dx;
-#pragma unroll
-                for (int i = 0; i < CPL; i++) {
-                    const int ch = lane + 32 * i;
-                    if (ch < g.Cin) acc[i] = fmaf(__ldg(c.wk + (int64_t)tap * g.Cout + ch), ldr<T>(ap + ch), acc[i]);
-                }
-            }
-        }
-        if (c.dense) {
-            float *o = static_cast<float *>(c.out) + r * g.Cout;
-#pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int ch = lane + 32 * i;
-                if (ch < g.Cout) o[ch] = __fadd_rn(acc[i], __ldg(c.bias + ch));
-            }
-        } else {
-            T *o = static_cast<T *>(c.out) + (r + 1) * g.Cout;
-#pragma unroll
-            for (int i = 0; i < CPL; i++) {
-                const int ch = lane + 32 * i;
-                if (ch < g.Cout) str<T>(o + ch, acc[i]);
-            }
-        }
-    }
-}
-
-template <class T>
-static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
-    const int64_t m_up = c.dense ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
-    int64_t blocks = (m_up * 32 + 255) / 256;
-    int grid = (int)(blocks < 148 * 8 ? blocks : 148 * 8);
-    if (grid < 1) grid = 1;
-    const int cpl = (c.g.Cin + 31) / 32;
-#define DW(n) k_dwconv_f32<n, T><<<grid, 256, 0, s>>>(c)
-    if (cpl <= 1) DW(1);
-    else if (cpl <= 2) DW(2);
-    else if (cpl <= 3) DW(3);
-    else if (cpl <= 5) DW(5);
-    else if (cpl <= 8) DW(8);
-    else if (cpl <= 15) DW(15);
-    else if (cpl <= 21) DW(21);
-    else DW(36);
-#undef DW
-}
-
-void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
-    if (c.dense || !c.bf) launch_dw_t<float>(c, s);
-    else launch_dw_t<bf16>(c, s);
-}
-
 }  // namespace st

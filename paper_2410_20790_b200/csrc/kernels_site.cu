@@ -43,7 +43,7 @@ __device__ __forceinline__ float gmax(float v, unsigned mask) {
 
 template <int ACT>
 __device__ __forceinline__ float actf(float x) {
-    return ACT == ACT_RELU ? relu_f(x) : silu_f(x);
+    return ACT == ACT_RELU ? relu_f(x) : ACT == ACT_SILU ? silu_f(x) : silu_fast(x);
 }
 
 constexpr int prefetch_depth(int cpl) { return cpl <= 2 ? 8 : cpl <= 4 ? 4 : cpl <= 8 ? 2 : 1; }
@@ -59,7 +59,8 @@ void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t
     const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
     if (grid <= 0) return;
     if (act == ACT_RELU) k_dense_act<ACT_RELU><<<grid, 256, 0, s>>>(x, y, n);
-    else k_dense_act<ACT_SILU><<<grid, 256, 0, s>>>(x, y, n);
+    else if (act == ACT_SILU) k_dense_act<ACT_SILU><<<grid, 256, 0, s>>>(x, y, n);
+    else k_dense_act<ACT_SILU_FAST><<<grid, 256, 0, s>>>(x, y, n);
 }
 
 __global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g) {
@@ -250,9 +251,9 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
         if (act == ACT_RELU)                                                                           \
             k_site_pw<G_, CPL_, ACT_RELU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
                                                                   static_cast<T *>(out_rows));         \
-        else                                                                                           \
-            k_site_pw<G_, CPL_, ACT_SILU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
-                                                                  static_cast<T *>(out_rows));         \
+        else /* SiLU: exact (double exp) in FP32 mode, fast in BF16 mode */                            \
+            k_site_pw<G_, CPL_, (sizeof(T) == 4 ? ACT_SILU : ACT_SILU_FAST), T><<<grid, 256, 0, s>>>(  \
+                in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows));                            \
     }
     ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_PW));
 #undef L_PW
