@@ -5,24 +5,24 @@
 // kxk taps (dy, dx ascending) of W[c][dy][dx] * Delta_in[c], bias absent;
 // dense mode adds the bias last.  Depthwise work is HBM-bound (1.8-12.5
 // flop/B), so the kernel is organised around memory
-// parallelism: one output row per group of G lanes, lane l owning channels
-// [l*CPL, (l+1)*CPL) moved as 16-byte vectors; all tap row indices of the
-// row are resolved first and every tap's input vector is loaded before any
-// FMA (up to KMAX independent loads in flight per lane).  FP32-mode results
-// are bit-identical to the oracle (fmaf chain in tap order from +0).
+// parallelism: one output row per group of G lanes; the tap row indices of
+// the row are resolved once (32-bit, into registers), then the channels are
+// walked in chunks of G*8 -- lane l owns 8 channels of a chunk, moved as one
+// 16-byte bf16 vector (two float4 in FP32 mode) -- and a batch of tap loads
+// is issued before its FMAs.  FP32-mode results are bit-identical to the
+// oracle (fmaf chain in tap order from +0).
 #include "rowio.cuh"
 
 namespace st {
 
 template <int G, int CPL, int KMAX, class T>
-__global__ void __launch_bounds__(256) k_dwconv(ConvCall c) {
+__global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
+    constexpr int TB = KMAX > 9 ? 5 : 3;      // taps per load batch
     const Geo g = c.g;
-    const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
+    const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
     const int M = c.dense ? c.B * Nout : *c.m_dev;
     const int C = g.Cin;
     const int lane = threadIdx.x & (G - 1);
-    const int c0 = lane * CPL;
-    const bool full = (C % 8 == 0) && (c0 + CPL <= C);
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
     const int ntaps = g.kh * g.kw;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_dwconv(ConvCall c) {
             q = gq - b * Nout;
         }
         const int oy = q / g.Wout, ox = q - oy * g.Wout;
-        int64_t idx[KMAX];
+        int idx[KMAX];                         // input row per tap, -1 = zero
 #pragma unroll
         for (int tap = 0; tap < KMAX; tap++) {
             idx[tap] = -1;
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) k_dwconv(ConvCall c) {
                 if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
                     const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
                     if (c.dense) {
-                        idx[tap] = bp;
+                        idx[tap] = (int)bp;
                     } else {
                         const int row = row_of(c.a, bp, t1);
                         if (row) idx[tap] = row;
@@ -58,66 +58,64 @@ __global__ void __launch_bounds__(256) k_dwconv(ConvCall c) {
                 }
             }
         }
-        float acc[CPL];
+        for (int cb = 0; cb < C; cb += G * CPL) {
+            const int c0 = cb + lane * CPL;
+            const bool full = (C % 8 == 0) && (c0 + CPL <= C);
+            float acc[CPL];
 #pragma unroll
-        for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
-        // taps in batches of TB: every load of a batch is issued before its FMAs
-        constexpr int TB = KMAX > 9 ? 5 : KMAX;
+            for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
 #pragma unroll
-        for (int t0 = 0; t0 < KMAX; t0 += TB) {
-            float v[TB][CPL];
+            for (int t0 = 0; t0 < KMAX; t0 += TB) {
+                float v[TB][CPL];
 #pragma unroll
-            for (int j = 0; j < TB; j++)
-                if (idx[t0 + j] >= 0) row_load<T, CPL>(A + idx[t0 + j] * C, c0, C, full, v[j]);
+                for (int j = 0; j < TB; j++)
+                    if (t0 + j < KMAX && idx[t0 + j] >= 0)
+                        row_load<T, CPL>(A + (int64_t)idx[t0 + j] * C, c0, C, full, v[j]);
 #pragma unroll
-            for (int j = 0; j < TB; j++) {
-                if (idx[t0 + j] < 0) continue;
-                float w[CPL];
-                row_load<float, CPL>(c.wk + (int64_t)(t0 + j) * C, c0, C, full, w);
+                for (int j = 0; j < TB; j++) {
+                    if (t0 + j >= KMAX || idx[t0 + j] < 0) continue;
+                    float w[CPL];
+                    row_load<float, CPL>(c.wk + (int64_t)(t0 + j) * C, c0, C, full, w);
 #pragma unroll
-                for (int i = 0; i < CPL; i++) acc[i] = fmaf(w[i], v[j][i], acc[i]);
+                    for (int i = 0; i < CPL; i++) acc[i] = fmaf(w[i], v[j][i], acc[i]);
+                }
             }
-        }
-        if (c.dense) {
-            float bb[CPL];
-            row_load<float, CPL>(c.bias, c0, C, full, bb);
+            if (c0 >= C) continue;
+            if (c.dense) {
+                float bb[CPL];
+                row_load<float, CPL>(c.bias, c0, C, full, bb);
 #pragma unroll
-            for (int i = 0; i < CPL; i++) acc[i] = __fadd_rn(acc[i], bb[i]);
-            row_store<float, CPL>(static_cast<float *>(c.out) + r * C, c0, C, full, acc);
-        } else {
-            row_store<T, CPL>(static_cast<T *>(c.out) + (r + 1) * C, c0, C, full, acc);
+                for (int i = 0; i < CPL; i++) acc[i] = __fadd_rn(acc[i], bb[i]);
+                row_store<float, CPL>(static_cast<float *>(c.out) + r * C, c0, C, full, acc);
+            } else {
+                row_store<T, CPL>(static_cast<T *>(c.out) + (r + 1) * C, c0, C, full, acc);
+            }
         }
     }
 }
 
+// lanes per row: 8 channels per lane when C % 8 == 0 (G*8 channels per chunk)
 #define DW_SHAPE(C_, L)                                            \
-    if ((C_) % 8 != 0 || (C_) <= 8) {                              \
+    if ((C_) % 8 != 0) {                                           \
         if ((C_) <= 1) { L(1, 1); }                                \
         else if ((C_) <= 2) { L(2, 1); }                           \
         else if ((C_) <= 4) { L(4, 1); }                           \
         else if ((C_) <= 8) { L(8, 1); }                           \
         else if ((C_) <= 16) { L(16, 1); }                         \
-        else if ((C_) <= 32) { L(32, 1); }                         \
-        else if ((C_) <= 64) { L(32, 2); }                         \
-        else if ((C_) <= 128) { L(32, 4); }                        \
-        else if ((C_) <= 256) { L(32, 8); }                        \
-        else if ((C_) <= 512) { L(32, 16); }                       \
-        else { L(32, 40); }                                        \
-    } else if ((C_) <= 16) { L(2, 8); }                            \
+        else { L(32, 1); }                                         \
+    } else if ((C_) <= 8) { L(1, 8); }                             \
+    else if ((C_) <= 16) { L(2, 8); }                              \
     else if ((C_) <= 32) { L(4, 8); }                              \
     else if ((C_) <= 64) { L(8, 8); }                              \
     else if ((C_) <= 128) { L(16, 8); }                            \
-    else if ((C_) <= 256) { L(32, 8); }                            \
-    else if ((C_) <= 512) { L(32, 16); }                           \
-    else if ((C_) <= 768) { L(32, 24); }                           \
-    else { L(32, 40); }
+    else { L(32, 8); }
 
 template <class T>
 static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
     const int64_t m_up = c.dense ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
     const int kk = c.g.kh * c.g.kw;
     auto grid_for = [&](int G) {
-        return (int)std::max<int64_t>(1, std::min<int64_t>((m_up * G + 255) / 256, 148 * 8));
+        return (int)std::max<int64_t>(1, std::min<int64_t>((m_up * G + 255) / 256, 148 * 16));
     };
 #define L_DW(G_, CPL_)                                                                   \
     {                                                                                    \
