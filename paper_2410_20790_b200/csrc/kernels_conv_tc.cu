@@ -39,6 +39,7 @@ namespace st {
 namespace tc {
 
 constexpr int BM = 128, BK = 64, STAGES = 4, NPROD = 128, NTHREADS = 288;
+constexpr int TAPS = 9;   // max k_h*k_w taken by the tensor-core path (1x1, 2x2, 3x3)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -178,6 +179,14 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         uint32_t phase = 0;
         const float *Ad = c.a_dense;
         const bf16 *As = static_cast<const bf16 *>(c.a.rows);
+        const int ntaps = g.kh * g.kw;   // <= TAPS (conv_tc_eligible)
+        // row code of this thread's row in its first tile (sparse); the next
+        // tile's code is prefetched while the current tile streams
+        int code_nx = 0;
+        if (!DENSE && blockIdx.x < ntiles) {
+            const int r0 = (blockIdx.x / ntn) * BM + m;
+            if (r0 < M) code_nx = __ldg(c.ridx + r0);
+        }
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int mt = tile / ntn, nt = tile - mt * ntn;
             const int r = mt * BM + m;
@@ -189,36 +198,50 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     b = r / Nout;
                     q = r - b * Nout;
                 } else {
-                    const int code = __ldg(c.ridx + r);
+                    const int code = code_nx;
                     const int gq = code >> 5;
                     t1 = code & 31;
                     b = gq / Nout;
                     q = gq - b * Nout;
                 }
             }
+            if (!DENSE) {   // prefetch the next tile's row code
+                const int tn = tile + gridDim.x;
+                const int rn = (tn / ntn) * BM + m;
+                code_nx = (tn < ntiles && rn < M) ? __ldg(c.ridx + rn) : 0;
+            }
+            // resolve the input row of every tap up front: the lookups are
+            // independent loads, so one memory round trip per tile instead of
+            // one per tap change
             const int oy = q / g.Wout, ox = q - oy * g.Wout;
-            int cur_tap = -1;
-            int64_t src = -1;   // element offset of the gathered row, -1 = zero
-            for (int kb = 0; kb < nkb; kb++) {
-                const int k0 = kb * BK;
-                const int tap = k0 / g.Cin, ci0 = k0 - tap * g.Cin;
-                if (tap != cur_tap) {
-                    cur_tap = tap;
-                    src = -1;
-                    if (rv) {
-                        const int dy = tap / g.kw, dx = tap - dy * g.kw;
-                        const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
-                        if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
-                            const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
-                            if (DENSE) {
-                                src = bp * g.Cin;
-                            } else {
-                                const int row = row_of(c.a, bp, t1);
-                                if (row) src = (int64_t)row * g.Cin;
-                            }
+            int tapidx[TAPS];
+#pragma unroll
+            for (int t = 0; t < TAPS; t++) {
+                tapidx[t] = -1;
+                if (rv && t < ntaps) {
+                    const int dy = t / g.kw, dx = t - dy * g.kw;
+                    const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+                    if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                        const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
+                        if (DENSE) {
+                            tapidx[t] = (int)bp;
+                        } else {
+                            const uint32_t a = __ldg(c.a.act + bp);
+                            const int pb = __ldg(c.a.pbase + bp);
+                            const uint32_t sl = __ldg(c.a.slot + bp);
+                            tapidx[t] = ((a >> t1) & 1u) ? 1 + pb + __popc(sl & lowmask(t1)) : -1;
                         }
                     }
                 }
+            }
+            for (int kb = 0; kb < nkb; kb++) {
+                const int k0 = kb * BK;
+                const int tap = k0 / g.Cin, ci0 = k0 - tap * g.Cin;
+                int idx = -1;
+#pragma unroll
+                for (int t = 0; t < TAPS; t++)
+                    if (t == tap) idx = tapidx[t];
+                const int64_t src = idx >= 0 ? (int64_t)idx * g.Cin : -1;   // element offset, -1 = zero
                 mbar_wait(empty + stage, phase ^ 1);
                 unsigned char *sa = smem + stage * S::STAGE;
                 unsigned char *sb = sa + S::A_BYTES;
@@ -382,7 +405,7 @@ static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s
 }
 
 bool conv_tc_eligible(const Geo &g) {
-    return g.groups == 1 && g.Cin % tc::BK == 0 && g.Cout % 16 == 0;
+    return g.groups == 1 && g.Cin % tc::BK == 0 && g.Cout % 16 == 0 && g.kh * g.kw <= tc::TAPS;
 }
 
 int conv_tc_bn(int cout) { return cout >= 256 ? 256 : cout >= 128 ? 128 : cout >= 64 ? 64 : 32; }
