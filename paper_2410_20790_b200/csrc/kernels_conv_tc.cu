@@ -73,6 +73,24 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA 2D load multicast to the CTAs of `mask` (same smem offsets in each;
+// complete_tx lands on the barrier at the same offset in each destination)
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // 16-byte cp.async, zero-filled when src_bytes == 0
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
@@ -86,6 +104,14 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+// commit arriving on the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
@@ -149,12 +175,18 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     const int K = g.kh * g.kw * g.Cin;
     const int nkb = K / BK;
     const int ntn = (g.Cout + BN - 1) / BN;
-    const int ntiles = ((M + BM - 1) / BM) * ntn;
+    // 2-CTA cluster along M: work item w = (M-tile pair, N tile); this CTA
+    // takes M tile 2*pair + rank.  Both CTAs need the same weight tile, so
+    // each loads half of it and multicasts the half to both (B traffic / 2).
+    const uint32_t rank = cluster_rank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int mtiles = (M + BM - 1) / BM;
+    const int nwork = ((mtiles + 1) >> 1) * ntn;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full + s, NPROD + 1);   // 128 producer arrivals + the TMA expect_tx arrival
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, 2);          // this CTA's and the peer's MMA commit (shared B stage)
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(tfull + a, 1);
@@ -168,7 +200,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();   // peer barriers initialised before any multicast targets them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -183,12 +215,12 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         // row code of this thread's row in its first tile (sparse); the next
         // tile's code is prefetched while the current tile streams
         int code_nx = 0;
-        if (!DENSE && blockIdx.x < ntiles) {
-            const int r0 = (blockIdx.x / ntn) * BM + m;
+        if (!DENSE && cid < nwork) {
+            const int r0 = (2 * (cid / ntn) + (int)rank) * BM + m;
             if (r0 < M) code_nx = __ldg(c.ridx + r0);
         }
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int mt = tile / ntn, nt = tile - mt * ntn;
+        for (int w = cid; w < nwork; w += ncl) {
+            const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
             const int r = mt * BM + m;
             // decode the output row once per tile
             int b = 0, q = 0, t1 = 0;
@@ -206,9 +238,9 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 }
             }
             if (!DENSE) {   // prefetch the next tile's row code
-                const int tn = tile + gridDim.x;
-                const int rn = (tn / ntn) * BM + m;
-                code_nx = (tn < ntiles && rn < M) ? __ldg(c.ridx + rn) : 0;
+                const int wn = w + ncl;
+                const int rn = (2 * (wn / ntn) + (int)rank) * BM + m;
+                code_nx = (wn < nwork && rn < M) ? __ldg(c.ridx + rn) : 0;
             }
             // resolve the input row of every tap up front: the lookups are
             // independent loads, so one memory round trip per tile instead of
@@ -278,9 +310,10 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     cp_async_arrive_noinc(full + stage);
                 }
                 // ---- B tile: one TMA 2D load by thread 0 (rows past Cout zero-filled)
-                if (m == 0) {
+                if (m == 0) {   // expect both halves; load ours into both CTAs
                     mbar_arrive_tx(full + stage, S::B_BYTES);
-                    tma_load_2d(sb, &tmap_b, k0, nt * BN, full + stage);
+                    tma_load_2d_mc(sb + rank * (S::B_BYTES / 2), &tmap_b, k0, nt * BN + (int)rank * (BN / 2),
+                                   full + stage, 0x3);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
@@ -292,7 +325,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        for (int w = cid; w < nwork; w += ncl, it++) {
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(tempty + acc, acc_phase ^ 1);
@@ -307,7 +340,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
 #pragma unroll
                     for (int k = 0; k < BK / 16; k++)
                         tc_mma(tmem_d, sdesc(sa + k * 32), sdesc(sb + k * 32), IDESC, (kb | k) != 0);
-                    tc_commit(empty + stage);
+                    tc_commit_mc(empty + stage, 0x3);   // stage reusable only when both CTAs consumed it
                     if (kb == nkb - 1) tc_commit(tfull + acc);
                 }
                 __syncwarp();
@@ -319,8 +352,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         const int quarter = warp & 3;            // TMEM lane quarter accessible by this warp
         const int row_in_tile = quarter * 32 + lane;
         int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-            const int mt = tile / ntn, nt = tile - mt * ntn;
+        for (int w = cid; w < nwork; w += ncl, it++) {
+            const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(tfull + acc, acc_phase);
@@ -381,7 +414,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             mbar_arrive(tempty + acc);
         }
     }
-    __syncthreads();
+    tc_fence_before();
+    cluster_sync();   // no CTA leaves while its peer may still multicast into it
     if (warp == 4) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
@@ -398,10 +432,22 @@ static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s
     }
     const int ntn = (c.g.Cout + BN - 1) / BN;
     const int64_t m_up = DENSE ? (int64_t)c.B * c.g.Hout * c.g.Wout : c.m_cap;
-    const int64_t tiles = ((m_up + tc::BM - 1) / tc::BM) * ntn;
-    int grid = (int)std::min<int64_t>(tiles, num_sms);
-    if (grid < 1) grid = 1;
-    k_conv_tc<BN, DENSE><<<grid, tc::NTHREADS, S::TOTAL, s>>>(c, *tmap);
+    const int64_t work = ((m_up + 2 * tc::BM - 1) / (2 * tc::BM)) * ntn;   // (M-tile pair, N tile)
+    int grid = 2 * (int)std::min<int64_t>(work, num_sms / 2);              // whole 2-CTA clusters
+    if (grid < 2) grid = 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.dynamicSmemBytes = S::TOTAL;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE>, c, *tmap);
 }
 
 bool conv_tc_eligible(const Geo &g) {
@@ -426,7 +472,7 @@ bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout) {
     const int BN = conv_tc_bn(Cout);
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)Cout};
     cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)BN};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)(BN / 2)};   // half tile per CTA of a pair
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(reinterpret_cast<CUtensorMap *>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                         const_cast<void *>(wbf), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
