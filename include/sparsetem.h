@@ -124,8 +124,10 @@ st_status st_get_sparsity(st_encoder *enc, int64_t *active, int64_t *site_active
  * device buffer (for the NCCL all-gather of the statistics). */
 st_status st_copy_site_counts(st_encoder *enc, int64_t *dst_dev, void *stream);
 /* Step totals per layer (synchronizes): rows_in = active input rows read,
- * rows_out = output rows produced (conv: dilated mask), touched = pixels x
- * frames visited.  host [n_layers] each (any may be NULL).  Used for the
+ * rows_out = output rows produced (conv: dilated mask; site: emitted),
+ * touched = pixels with any active input frame.  host [n_layers] each (any
+ * may be NULL).  rows_in / touched are collected only while profiling is on
+ * (st_set_profiling; 0 otherwise), rows_out always.  Used for the
  * algorithmic bytes/flops of the roofline. */
 st_status st_get_layer_counts(st_encoder *enc, int64_t *rows_in, int64_t *rows_out,
                               int64_t *touched);

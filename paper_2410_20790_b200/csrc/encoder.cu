@@ -90,6 +90,7 @@ struct st_encoder {
     int B = 0, F = 0;   // max chunks, max diff frames
     // input site tensor buffers
     int in_act = -1, in_pbase = -1, in_rows = -1;
+    int in_dd = -1;              // dense per-frame input delta for CUDA-core convs on the input
     int64_t in_rows_cap = 0;
     bool bf = false;             // BF16 mode: delta rows stored as bf16 (R22-BF16)
     int esz = 4;                 // delta-row element size in bytes
@@ -390,6 +391,13 @@ static st_status plan(st_encoder *e) {
     e->in_pbase = add(B * Nin * 4, 0, in_last);
     const int64_t ES = e->esz;   // delta-row element size: 4 (FP32 mode) or 2 (BF16 mode)
     e->in_rows = add((e->in_rows_cap + 1) * e->in_C * ES, 0, in_last);
+    // convs reading the network input on CUDA cores (c_in <= 4 stems) gather
+    // from a dense per-frame delta written by the Subtraction pass instead of
+    // resolving every tap through the frame words
+    bool want_dd = false;
+    for (auto &l : e->L)
+        if (l.kind == ST_CONV && l.src == -1 && !l.depthwise && !l.tc) want_dd = true;
+    if (want_dd) e->in_dd = add(B * F * Nin * e->in_C * ES, 0, in_last);
     // per-layer tensors
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -697,7 +705,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         void *rows = e->ptr(e->in_rows);
         const float *fr = frames_dev;
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act, s));
+               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act,
+                                    e->in_dd >= 0 ? e->ptr(e->in_dd) : nullptr, s));
         LAUNCH(e, KC_SCAN, -1, s,
                launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
         zero_row(e->in_rows, e->in_C);
@@ -716,7 +725,9 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         const float *x_src = dense_of(e, l.src);
         long long *st = e->stats + 3 * i;
         DView in = F > 0 ? view_of(e, l.src) : DView{};
-        if (F > 0 && l.kind != ST_OUTPUT)   // rows_in / touched of this layer
+        // rows_in / touched of this layer: roofline accounting only, collected
+        // when profiling is on (st_set_profiling) so the timed step skips them
+        if (F > 0 && l.kind != ST_OUTPUT && e->prof)
             LAUNCH(e, KC_COUNTS, i, s, launch_frame_counts(in.act, B, (int)Ns, nullptr, 0, st, st + 2, s));
         switch (l.kind) {
         case ST_CONV: {
@@ -741,6 +752,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.bf = bf;
             c.a = in;
             c.ridx = e->p<int32_t>(l.b_ridx);
+            c.F = F;
+            c.ddelta = (l.src == -1 && !l.depthwise && !l.tc && e->in_dd >= 0) ? e->ptr(e->in_dd) : nullptr;
             c.m_dev = e->totals + i;
             c.m_cap = (int64_t)B * F * N;
             c.out = e->ptr(l.b_rows);

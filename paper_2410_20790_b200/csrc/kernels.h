@@ -30,9 +30,12 @@ struct Geo {   // conv / pool geometry
 // Thresholds are read by the kernels from device memory (theta points at one
 // fp32 site threshold), so a captured CUDA graph serves every step.
 // ---- masks, compaction (kernels_mask.cu) ----
-// Subtraction pass 1 (site 0): act bits per pixel, sequential over frames.
+// Subtraction pass 1 (site 0): act bits per pixel, sequential over frames;
+// optionally also the dense per-frame emitted delta ddelta [B][n_diff][N][C]
+// (zeros where truncated; row type) for convs reading the input directly.
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
-                          int B, int N, int C, int n_diff, const float *theta, bool bf, uint32_t *act, cudaStream_t s);
+                          int B, int N, int C, int n_diff, const float *theta, bool bf, uint32_t *act, void *ddelta,
+                          cudaStream_t s);
 // Subtraction pass 2: write emitted rows at the slots of `act`.
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
                           int B, int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
@@ -66,6 +69,8 @@ struct ConvCall {
     const int32_t *ridx;    // sparse: M-row list
     const int32_t *m_dev;   // sparse: device M
     int64_t m_cap;          // sparse: upper bound of M (grid sizing)
+    const void *ddelta;     // sparse, optional: dense per-frame input delta [B][F][Nin][Cin]
+    int F;                  // diff frames (ddelta indexing)
     // B operand / output
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only

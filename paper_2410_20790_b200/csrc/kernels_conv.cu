@@ -39,7 +39,11 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
     const int ntn = (g.Cout + BN - 1) / BN;
     const int ntiles = ((M + CBM - 1) / CBM) * ntn;
     // dense launches are instantiated with T = float
-    const T *A = c.dense ? reinterpret_cast<const T *>(c.a_dense) : static_cast<const T *>(c.a.rows);
+    // sparse mode reads either the compacted rows (via the frame-word lookup)
+    // or, for convs on the network input, the dense per-frame delta
+    const bool dd = !c.dense && c.ddelta != nullptr;
+    const T *A = c.dense ? reinterpret_cast<const T *>(c.a_dense)
+                         : dd ? static_cast<const T *>(c.ddelta) : static_cast<const T *>(c.a.rows);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const bool bvec = (g.Cout & 3) == 0;
     const int nk = (K + CBK - 1) / CBK;
@@ -72,6 +76,8 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                     const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
                     if (c.dense) {
                         idx = (int)bp;
+                    } else if (dd) {   // zeros where the input was truncated: no lookup
+                        idx = (int)(((int64_t)b * c.F + t1) * Nin + iy * g.Win + ix);
                     } else {
                         const int row = row_of(c.a, bp, t1);
                         idx = row ? row : -1;

@@ -18,7 +18,7 @@ template <int C, class T>
 __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__ ref, int64_t ref_stride,
                                                        const float *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, int n_diff, const float *__restrict__ theta_p,
-                                                       uint32_t *__restrict__ act) {
+                                                       uint32_t *__restrict__ act, T *__restrict__ ddelta) {
     const float theta = __ldg(theta_p);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
@@ -29,6 +29,9 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
     for (int c = 0; c < C; c++) S[c] = __ldg(r + c);
     const float *f = fr + b * fr_stride + (int64_t)p * C;
     const int64_t fs = (int64_t)N * C;
+    // optional dense per-frame copy of the emitted delta [B][n_diff][N][C]
+    // (zeros where truncated) for convs that read the input directly
+    T *dd = ddelta ? ddelta + ((int64_t)b * n_diff * N + p) * C : nullptr;
     uint32_t w = 0;
 #pragma unroll 4
     for (int t1 = 0; t1 < n_diff; ++t1) {
@@ -39,11 +42,14 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
             raw[c] = __fsub_rn(__ldg(f + t1 * fs + c), S[c]);
             mx = fmaxf(mx, fabsf(raw[c]));
         }
-        if (mx > theta) {                       // R1: strict comparison
+        const bool on = mx > theta;             // R1: strict comparison
 #pragma unroll
-            for (int c = 0; c < C; c++) S[c] = __fadd_rn(S[c], rnd<T>(raw[c]));   // R3: S += emitted
-            w |= 1u << t1;
+        for (int c = 0; c < C; c++) {
+            const float e = on ? rnd<T>(raw[c]) : 0.0f;
+            if (on) S[c] = __fadd_rn(S[c], e);  // R3: S += emitted
+            if (dd) str<T>(dd + t1 * fs + c, e);
         }
+        if (on) w |= 1u << t1;
     }
     act[i] = w;
 }
@@ -88,10 +94,11 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
     }
 
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
-                          int N, int C, int n_diff, const float *theta_p, bool bf, uint32_t *act, cudaStream_t s) {
+                          int N, int C, int n_diff, const float *theta_p, bool bf, uint32_t *act, void *ddelta,
+                          cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
     ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta_p,
-                                     act));
+                                     act, static_cast<T *>(ddelta)));
 }
 
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
