@@ -48,6 +48,7 @@ struct LayerRT {
     Geo geo{};
     bool depthwise = false;
     bool tc = false;          // BF16 mode: tcgen05 tensor-core conv
+    bool tc_small = false;    // BF16 mode: tcgen05 stem on the network input (c_in <= 4)
     int n_consumers = 0, last_consumer = 0;
     // device weights (separate allocation)
     float *wk = nullptr, *bias = nullptr;
@@ -323,20 +324,27 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     }
     // ---- BF16 mode: tensor-core layers get bf16 [Cout][K] weights (RNE)
     if (cfg->precision == ST_BF16) {
+        // weight K per tc layer: kh*kw*Cin in (dy, dx, ci) order; stems pack
+        // each tap as a 4-channel piece (zero pad) and round K up to 64
+        auto tc_k = [](const LayerRT &l) -> int64_t {
+            return l.tc_small ? conv_tc_small_k(l.geo) : (int64_t)l.spec.k_h * l.spec.k_w * l.geo.Cin;
+        };
         int64_t nbf = 0;
-        for (auto &l : e->L)
-            if (l.kind == ST_CONV && conv_tc_eligible(l.geo)) {
-                l.tc = true;
-                nbf += ((int64_t)l.spec.k_h * l.spec.k_w * l.geo.Cin * l.C + 127) / 128 * 128;
-            }
+        for (auto &l : e->L) {
+            if (l.kind != ST_CONV) continue;
+            if (conv_tc_eligible(l.geo)) l.tc = true;
+            else if (l.src == -1 && conv_tc_small_eligible(l.geo)) l.tc_small = true;
+            if (l.tc || l.tc_small) nbf += (tc_k(l) * l.C + 127) / 128 * 128;
+        }
         if (nbf) {
             CUDA_OK(e.get(), cudaMalloc(&e->wbf_mem, nbf * 2));
             std::vector<uint16_t> hb(nbf, 0);
             int64_t o = 0;
             for (auto &l : e->L) {
-                if (!l.tc) continue;
+                if (!l.tc && !l.tc_small) continue;
                 const int kh = l.spec.k_h, kw = l.spec.k_w, ci_n = l.geo.Cin, co = l.C;
-                const int64_t K = (int64_t)kh * kw * ci_n;
+                const int64_t K = tc_k(l);
+                const int cstep = l.tc_small ? 4 : ci_n;   // elements per tap in the K layout
                 l.wbf = e->wbf_mem + o;
                 for (int c = 0; c < co; c++)
                     for (int dy = 0; dy < kh; dy++)
@@ -346,13 +354,13 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                                 uint32_t u;
                                 std::memcpy(&u, &v, 4);
                                 u += 0x7FFFu + ((u >> 16) & 1u);   // round to nearest even
-                                hb[o + (int64_t)c * K + (dy * kw + dx) * ci_n + ci] = (uint16_t)(u >> 16);
+                                hb[o + (int64_t)c * K + (dy * kw + dx) * cstep + ci] = (uint16_t)(u >> 16);
                             }
                 o += (K * co + 127) / 128 * 128;
             }
             CUDA_OK(e.get(), cudaMemcpy(e->wbf_mem, hb.data(), nbf * 2, cudaMemcpyHostToDevice));
             for (auto &l : e->L)
-                if (l.tc && !make_weight_tmap(l.tmap, l.wbf, l.spec.k_h * l.spec.k_w * l.geo.Cin, l.C))
+                if ((l.tc || l.tc_small) && !make_weight_tmap(l.tmap, l.wbf, (int)tc_k(l), l.C))
                     return fail(e.get(), ST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         }
     }
@@ -396,8 +404,8 @@ static st_status plan(st_encoder *e) {
     // resolving every tap through the frame words
     bool want_dd = false;
     for (auto &l : e->L)
-        if (l.kind == ST_CONV && l.src == -1 && !l.depthwise && !l.tc) want_dd = true;
-    if (want_dd) e->in_dd = add(B * F * Nin * e->in_C * ES, 0, in_last);
+        if (l.kind == ST_CONV && l.src == -1 && !l.depthwise && !l.tc) want_dd = true;   // incl. tc_small
+    if (want_dd) e->in_dd = add(B * F * Nin * 4 * ES, 0, in_last);   // pixels padded to 4 channels
     // per-layer tensors
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -739,8 +747,11 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
-            LAUNCH(e, l.depthwise ? KC_DW_DENSE : (l.tc ? KC_TC_DENSE : KC_CONV_DENSE), i, s,
-                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.tmap, s) : launch_conv_f32(c, s)));
+            LAUNCH(e, l.depthwise ? KC_DW_DENSE : ((l.tc || l.tc_small) ? KC_TC_DENSE : KC_CONV_DENSE), i, s,
+                   l.depthwise  ? launch_dwconv_f32(c, s)
+                   : l.tc       ? launch_conv_tc(c, l.tmap, s)
+                   : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
+                                : launch_conv_f32(c, s));
             if (F == 0) break;
             uint32_t *act = e->p<uint32_t>(l.b_act);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -757,8 +768,11 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.m_dev = e->totals + i;
             c.m_cap = (int64_t)B * F * N;
             c.out = e->ptr(l.b_rows);
-            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : (l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE), i, s,
-                   l.depthwise ? launch_dwconv_f32(c, s) : (l.tc ? launch_conv_tc(c, l.tmap, s) : launch_conv_f32(c, s)));
+            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : ((l.tc || l.tc_small) ? KC_TC_SPARSE : KC_CONV_SPARSE), i, s,
+                   l.depthwise  ? launch_dwconv_f32(c, s)
+                   : l.tc       ? launch_conv_tc(c, l.tmap, s)
+                   : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
+                                : launch_conv_f32(c, s));
             break;
         }
         case ST_RELU: case ST_SILU: {

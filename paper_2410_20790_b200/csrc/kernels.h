@@ -84,6 +84,11 @@ void launch_dwconv_f32(const ConvCall &c, cudaStream_t s);
 bool conv_tc_eligible(const Geo &g);
 bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout);
 void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s);
+// stems on tensor cores: the network input (c_in <= 4); sparse mode reads the
+// 4-channel-padded dense input delta (c.ddelta), dense mode the fp32 frames
+bool conv_tc_small_eligible(const Geo &g);
+int conv_tc_small_k(const Geo &g);
+void launch_conv_tc_small(const ConvCall &c, const void *tmap, cudaStream_t s);
 
 // ---- sites, joins, accumulation (kernels_site.cu) ----
 enum Act { ACT_RELU = 0, ACT_SILU = 1, ACT_SILU_FAST = 2 };   // FAST: BF16 mode only

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
     const bool dd = !c.dense && c.ddelta != nullptr;
     const T *A = c.dense ? reinterpret_cast<const T *>(c.a_dense)
                          : dd ? static_cast<const T *>(c.ddelta) : static_cast<const T *>(c.a.rows);
+    const int astride = dd ? 4 : g.Cin;   // ddelta pixels are padded to 4 channels
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const bool bvec = (g.Cout & 3) == 0;
     const int nk = (K + CBK - 1) / CBK;
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                     if (c.dense) {
                         idx = (int)bp;
                     } else if (dd) {   // zeros where the input was truncated: no lookup
+                        // (4-channel-padded pixel pieces: element offset = idx * 4)
                         idx = (int)(((int64_t)b * c.F + t1) * Nin + iy * g.Win + ix);
                     } else {
                         const int row = row_of(c.a, bp, t1);
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                 const int m = tid >> 1, half = tid & 1;
                 const int idx = tab[m * ntaps + tap];
                 if (idx >= 0) {
-                    const float4 v = ld4<T>(A + (int64_t)idx * g.Cin + ci0 + half * 4);
+                    const float4 v = ld4<T>(A + (int64_t)idx * astride + ci0 + half * 4);
                     ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
                 } else {
                     ra[0] = ra[1] = ra[2] = ra[3] = 0.0f;
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                     float v = 0.0f;
                     if (k < K) {
                         const int idx = tab[m * ntaps + tap];
-                        if (idx >= 0) v = ldr<T>(A + (int64_t)idx * g.Cin + ci);
+                        if (idx >= 0) v = ldr<T>(A + (int64_t)idx * astride + ci);
                     }
                     ra[j] = v;
                 }

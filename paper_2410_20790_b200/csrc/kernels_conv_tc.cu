@@ -96,6 +96,11 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                  : "memory");
 }
+// 8-byte cp.async (.ca), zero-filled when src_bytes == 0
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -155,7 +160,14 @@ struct Smem {
 
 }  // namespace tc
 
-template <int BN, bool DENSE>
+// SMALL: convs on the network input with c_in <= 4 (stems).  The input delta
+// is the dense per-frame array padded to 4 channels (one aligned 8-byte bf16
+// piece per pixel), so a 64-wide k-block holds 16 taps x 4 channels and is
+// gathered with 16 x 8-byte cp.async per row -- no frame-word lookups (the
+// dense array holds zeros where the Subtraction truncated).  Dense mode
+// packs the fp32 reference frame's <= 4 channels into the same layout.
+// Weights are [Cout][ceil(taps/16)*64] with tap-major 4-channel pieces.
+template <int BN, bool DENSE, bool SMALL = false>
 __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b) {
     using namespace tc;
     using S = Smem<BN>;
@@ -173,7 +185,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
     const int M = DENSE ? c.B * Nout : *c.m_dev;
     const int K = g.kh * g.kw * g.Cin;
-    const int nkb = K / BK;
+    const int nkb = SMALL ? (g.kh * g.kw + 15) / 16 : K / BK;
     const int ntn = (g.Cout + BN - 1) / BN;
     // 2-CTA cluster along M: work item w = (M-tile pair, N tile); this CTA
     // takes M tile 2*pair + rank.  Both CTAs need the same weight tile, so
@@ -204,7 +216,74 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp < 4) {
+    if (SMALL && warp < 4) {
+        // ===================== producers (stem, c_in <= 4) =====================
+        const int m = threadIdx.x;
+        int stage = 0;
+        uint32_t phase = 0;
+        const int ntaps = g.kh * g.kw;
+        const bf16 *dd = static_cast<const bf16 *>(c.ddelta);
+        for (int w = cid; w < nwork; w += ncl) {
+            const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
+            const int r = mt * BM + m;
+            int b = 0, q = 0, t1 = 0;
+            const bool rv = r < M;
+            if (rv) {
+                if (DENSE) {
+                    b = r / Nout;
+                    q = r - b * Nout;
+                } else {
+                    const int code = __ldg(c.ridx + r);
+                    t1 = code & 31;
+                    b = (code >> 5) / Nout;
+                    q = (code >> 5) - b * Nout;
+                }
+            }
+            const int oy = q / g.Wout, ox = q - oy * g.Wout;
+            for (int kb = 0; kb < nkb; kb++) {
+                mbar_wait(empty + stage, phase ^ 1);
+                unsigned char *sa = smem + stage * S::STAGE;
+                unsigned char *sb = sa + S::A_BYTES;
+#pragma unroll 4
+                for (int j = 0; j < 16; j++) {
+                    const int tap = kb * 16 + j;
+                    unsigned char *dst = sa + m * 128 + ((((j >> 1) ^ (m & 7)) << 4) | ((j & 1) << 3));
+                    bool valid = false;
+                    int64_t pix = 0;
+                    if (rv && tap < ntaps) {
+                        const int dy = tap / g.kw, dx = tap - dy * g.kw;
+                        const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+                        valid = iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
+                        pix = iy * g.Win + ix;
+                    }
+                    if (DENSE) {
+                        float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                        if (valid) {
+                            const float *p = c.a_dense + ((int64_t)b * Nin + pix) * g.Cin;
+                            for (int ci = 0; ci < g.Cin; ci++) v[ci] = __ldg(p + ci);
+                        }
+                        *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
+                    } else {
+                        const bf16 *p = dd + (valid ? (((int64_t)b * c.F + t1) * Nin + pix) * 4 : 0);
+                        cp_async8(dst, p, valid ? 8u : 0u);
+                    }
+                }
+                if (DENSE) {
+                    fence_proxy_async();
+                    mbar_arrive(full + stage);
+                } else {
+                    cp_async_arrive_noinc(full + stage);
+                }
+                if (m == 0) {
+                    mbar_arrive_tx(full + stage, S::B_BYTES);
+                    tma_load_2d_mc(sb + rank * (S::B_BYTES / 2), &tmap_b, kb * BK, nt * BN + (int)rank * (BN / 2),
+                                   full + stage, 0x3);
+                }
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+        if (!DENSE) asm volatile("cp.async.wait_all;" ::: "memory");
+    } else if (warp < 4) {
         // ===================== producers =====================
         const int m = threadIdx.x;   // tile row owned by this thread
         int stage = 0;
@@ -422,12 +501,12 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     }
 }
 
-template <int BN, bool DENSE>
+template <int BN, bool DENSE, bool SMALL = false>
 static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s, int num_sms) {
     using S = tc::Smem<BN>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_conv_tc<BN, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+        cudaFuncSetAttribute(k_conv_tc<BN, DENSE, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
         attr = true;
     }
     const int ntn = (c.g.Cout + BN - 1) / BN;
@@ -447,12 +526,19 @@ static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE>, c, *tmap);
+    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE, SMALL>, c, *tmap);
 }
 
 bool conv_tc_eligible(const Geo &g) {
     return g.groups == 1 && g.Cin % tc::BK == 0 && g.Cout % 16 == 0 && g.kh * g.kw <= tc::TAPS;
 }
+
+// stems: the network input (c_in <= 4) on tensor cores, taps packed 16 per
+// 64-wide k-block (kernel SMALL variant); weights K = ceil(taps/16)*64
+bool conv_tc_small_eligible(const Geo &g) {
+    return g.groups == 1 && g.Cin <= 4 && g.Cout % 16 == 0 && g.kh * g.kw <= 64;
+}
+int conv_tc_small_k(const Geo &g) { return (g.kh * g.kw + 15) / 16 * tc::BK; }
 
 int conv_tc_bn(int cout) { return cout >= 256 ? 256 : cout >= 128 ? 128 : cout >= 64 ? 64 : 32; }
 
@@ -499,4 +585,25 @@ void launch_conv_tc(const ConvCall &c, const void *tmap_v, cudaStream_t s) {
 #undef TC_BN
 }
 
+}  // namespace st
+
+namespace st {
+void launch_conv_tc_small(const ConvCall &c, const void *tmap_v, cudaStream_t s) {
+    const CUtensorMap *tmap = static_cast<const CUtensorMap *>(tmap_v);
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+#define TC_BN(BN_) \
+    (c.dense ? launch_tc<BN_, true, true>(c, tmap, s, num_sms) : launch_tc<BN_, false, true>(c, tmap, s, num_sms))
+    switch (conv_tc_bn(c.g.Cout)) {
+    case 256: TC_BN(256); break;
+    case 128: TC_BN(128); break;
+    case 64: TC_BN(64); break;
+    default: TC_BN(32); break;
+    }
+#undef TC_BN
+}
 }  // namespace st

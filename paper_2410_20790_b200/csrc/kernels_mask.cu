@@ -31,7 +31,10 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
     const int64_t fs = (int64_t)N * C;
     // optional dense per-frame copy of the emitted delta [B][n_diff][N][C]
     // (zeros where truncated) for convs that read the input directly
-    T *dd = ddelta ? ddelta + ((int64_t)b * n_diff * N + p) * C : nullptr;
+    // channel-padded to 4 (one aligned 8-byte bf16 piece per pixel; zeros in
+    // the pad channels) so tensor-core stems gather a tap with one copy
+    T *dd = ddelta ? ddelta + ((int64_t)b * n_diff * N + p) * 4 : nullptr;
+    const int64_t dfs = (int64_t)N * 4;
     uint32_t w = 0;
 #pragma unroll 4
     for (int t1 = 0; t1 < n_diff; ++t1) {
@@ -43,12 +46,16 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
             mx = fmaxf(mx, fabsf(raw[c]));
         }
         const bool on = mx > theta;             // R1: strict comparison
+        float e4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int c = 0; c < C; c++) {
             const float e = on ? rnd<T>(raw[c]) : 0.0f;
             if (on) S[c] = __fadd_rn(S[c], e);  // R3: S += emitted
-            if (dd) str<T>(dd + t1 * fs + c, e);
+            e4[c] = e;
         }
+        if (dd)
+#pragma unroll
+            for (int c = 0; c < 4; c++) str<T>(dd + t1 * dfs + c, e4[c]);
         if (on) w |= 1u << t1;
     }
     act[i] = w;

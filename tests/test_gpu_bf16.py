@@ -76,6 +76,29 @@ def test_tc_conv_kernel_unit(cin, cout, k, s):
             assert ok, f"sparse tc conv rows err {e} (chunk {b} frame {t})"
 
 
+@pytest.mark.parametrize("cin,cout,k,s", [(3, 64, 7, 2), (1, 64, 3, 1), (3, 32, 3, 2), (3, 48, 5, 1)])
+def test_tc_stem_kernel_unit(cin, cout, k, s):
+    """Tensor-core stem (network input, c_in <= 4): sparse rows from the
+    4-channel-padded dense input delta, dense reference from the fp32 frames."""
+    n = Net(cin, 30, 38)
+    conv = n.conv(-1, cout, k, s, k // 2)
+    n.output(conv)
+    init_weights(n, cin * 7 + k)
+    B, L = 2, 6
+    fr = np.stack([random_frames(b + 11, L, 30, 38, cin, p_change=0.3) for b in range(B)])
+    th = np.array([0.02], np.float32)
+    enc, _ = gpu_run(n, fr, th, precision="bf16")
+    for b in range(B):
+        r = oracle.run_chunk(n, fr[b], th, want_deltas=True, want_dense0=True, precision="bf16")
+        ok, e = _rel_ok(enc.debug_dense0(conv, b), r["dense0"][conv], 1e-4, 1e-4)
+        assert ok, f"dense stem err {e}"
+        for t in range(1, L):
+            assert np.array_equal(enc.debug_mask(conv, b, t), r["masks"][conv][t - 1])
+            idx, rows = enc.debug_rows(conv, b, t)
+            ok, e = _rel_ok(rows, r["deltas"][conv][t - 1].reshape(-1, cout)[idx], 2.0 ** -7, 1e-4)
+            assert ok, f"sparse stem rows err {e} (chunk {b} frame {t})"
+
+
 def test_crnn_bf16_theta0():
     cfg = W.get_config(2)
     net = cfg.build_net()
