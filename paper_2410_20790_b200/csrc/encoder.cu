@@ -28,11 +28,13 @@ namespace {
 
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
-              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16, KC_N = 17;
+              KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16,
+              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_N = 19;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
                               "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
-                              "conv_tc_sparse", "conv_tc_dense", "se"};
+                              "conv_tc_sparse", "conv_tc_dense", "se", "conv_tc_stem_sparse",
+                              "conv_tc_stem_dense"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -747,7 +749,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
-            LAUNCH(e, l.depthwise ? KC_DW_DENSE : ((l.tc || l.tc_small) ? KC_TC_DENSE : KC_CONV_DENSE), i, s,
+            LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
                    l.depthwise  ? launch_dwconv_f32(c, s)
                    : l.tc       ? launch_conv_tc(c, l.tmap, s)
                    : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
@@ -768,7 +770,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.m_dev = e->totals + i;
             c.m_cap = (int64_t)B * F * N;
             c.out = e->ptr(l.b_rows);
-            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : ((l.tc || l.tc_small) ? KC_TC_SPARSE : KC_CONV_SPARSE), i, s,
+            LAUNCH(e, l.depthwise ? KC_DW_SPARSE : l.tc ? KC_TC_SPARSE : l.tc_small ? KC_STEM_SPARSE : KC_CONV_SPARSE, i, s,
                    l.depthwise  ? launch_dwconv_f32(c, s)
                    : l.tc       ? launch_conv_tc(c, l.tmap, s)
                    : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
@@ -1059,8 +1061,10 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
             cudaEventElapsedTime(&t, r.e0, r.e1);
             e->prof_ms[r.cls] += t;
             e->prof_n[r.cls] += 1;
-            const bool sparse = r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE || r.cls == KC_TC_SPARSE;
-            const bool dense = r.cls == KC_CONV_DENSE || r.cls == KC_DW_DENSE || r.cls == KC_TC_DENSE;
+            const bool sparse = r.cls == KC_CONV_SPARSE || r.cls == KC_DW_SPARSE || r.cls == KC_TC_SPARSE ||
+                                r.cls == KC_STEM_SPARSE;
+            const bool dense = r.cls == KC_CONV_DENSE || r.cls == KC_DW_DENSE || r.cls == KC_TC_DENSE ||
+                               r.cls == KC_STEM_DENSE;
             if (r.layer >= 0 && (sparse || dense)) {
                 const LayerRT &l = e->L[r.layer];
                 const int64_t K = (int64_t)l.geo.kh * l.geo.kw * (l.geo.Cin / l.geo.groups);
@@ -1069,7 +1073,8 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 e->prof_flops[r.cls] += 2.0 * K * l.C * M;
                 // algorithmic bytes: each active input row once, each output row once (+ its
                 // 4-byte row index when sparse), weights once (bf16 on the tensor-core path)
-                const double wbytes = (r.cls == KC_TC_SPARSE || r.cls == KC_TC_DENSE) ? 2.0 : 4.0;
+                const double wbytes = (r.cls == KC_TC_SPARSE || r.cls == KC_TC_DENSE || r.cls == KC_STEM_SPARSE ||
+                                       r.cls == KC_STEM_DENSE) ? 2.0 : 4.0;
                 e->prof_bytes[r.cls] += 4.0 * ((double)Min * l.geo.Cin + (double)M * l.C) + wbytes * K * l.C +
                                         (sparse ? 4.0 * M : 0.0);
             }
