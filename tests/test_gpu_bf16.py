@@ -61,7 +61,8 @@ def test_tc_conv_kernel_unit(cin, cout, k, s):
     net, conv = _tc_net(cin, cout, k, s, seed=cin + cout)
     B, L = 3, 6
     fr = np.stack([random_frames(b + 1, L, net.in_h, net.in_w, 3, p_change=0.3) for b in range(B)])
-    th = np.array([0.02, 0.0], np.float32)
+    th = np.zeros(oracle.num_sites(net), np.float32)
+    th[0] = 0.02
     enc, _ = gpu_run(net, fr, th, precision="bf16")
     for b in range(B):
         r = oracle.run_chunk(net, fr[b], th, want_deltas=True, want_dense0=True, precision="bf16")
