@@ -46,6 +46,8 @@ __device__ __forceinline__ float actf(float x) {
     return ACT == ACT_RELU ? relu_f(x) : ACT == ACT_SILU ? silu_f(x) : silu_fast(x);
 }
 
+// frames whose rows are fetched per batch (~16 prefetched values per lane:
+// deeper batches cost more registers than they save in latency -- measured)
 constexpr int prefetch_depth(int cpl) { return cpl <= 2 ? 8 : cpl <= 4 ? 4 : cpl <= 8 ? 2 : 1; }
 
 // ---------------------------------------------------------------- dense ops
