@@ -117,10 +117,10 @@ static float sigm_f(float x) { return 1.0f / (1.0f + exp_r(-x)); }       /* R10 
  *    non-linear site) is stored rounded to bf16 (round-to-nearest-even); the
  *    truncation decision is taken on the fp32 value, and the Subtraction
  *    buffer S and each site's y_acc advance by the rounded (emitted) value;
- *  - a convolution with groups == 1, c_out % 16 == 0 and either c_in % 64 == 0
- *    with at most 9 taps, or reading the network input with c_in <= 4 and at
- *    most 64 taps, multiplies bf16-rounded operands (weight and input value)
- *    and accumulates in fp32;
+ *  - a convolution with groups == 1 and either c_in % 8 == 0, c_out % 8 == 0
+ *    and at most 9 taps, or reading the network input with c_in <= 4,
+ *    c_out % 16 == 0 and at most 64 taps, multiplies bf16-rounded operands
+ *    (weight and input value) and accumulates in fp32;
  *  - dense reference activations, site states and outputs stay fp32. */
 static int g_bf16 = 0;
 void orc_set_precision(int bf16) { g_bf16 = bf16 ? 1 : 0; }
@@ -145,11 +145,13 @@ static void conv_apply(const orc_layer *l, shp si, shp so, const float *x, const
                        int with_bias, float *out) {
     const int cin_g = si.c / l->groups, cout_g = l->c_out / l->groups;
     const int No = so.h * so.w;
-    /* BF16 mode: tensor-core convs (R22-BF16) -- c_in % 64 == 0 with at most
-     * 9 taps, or a stem on the network input with c_in <= 4 and <= 64 taps */
+    /* BF16 mode: tensor-core convs (R22-BF16) -- c_in, c_out % 8 == 0 with at
+     * most 9 taps, or a stem on the network input with c_in <= 4, c_out % 16
+     * == 0 and <= 64 taps */
     const int taps = l->k_h * l->k_w;
-    const int rb = g_bf16 && l->groups == 1 && l->c_out % 16 == 0 &&
-                   ((si.c % 64 == 0 && taps <= 9) || (l->src == -1 && si.c <= 4 && taps <= 64));
+    const int rb = g_bf16 && l->groups == 1 &&
+                   ((si.c % 8 == 0 && l->c_out % 8 == 0 && taps <= 9) ||
+                    (l->src == -1 && si.c <= 4 && l->c_out % 16 == 0 && taps <= 64));
 #pragma omp parallel for schedule(static)
     for (int q = 0; q < No; q++) {
         float *o = out + (size_t)q * so.c;

@@ -116,6 +116,8 @@ struct st_encoder {
     bool thr_pending = false;
     // CUDA graphs of whole steps, keyed by (frames, stride, n_diff, chunks)
     bool use_graphs = true;
+    bool dw_rowmajor = false;
+    bool prof_trace = false;
     std::vector<GraphEnt> graphs;
     cudaStream_t gstream = nullptr;            // capture / replay stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -326,10 +328,11 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     }
     // ---- BF16 mode: tensor-core layers get bf16 [Cout][K] weights (RNE)
     if (cfg->precision == ST_BF16) {
-        // weight K per tc layer: kh*kw*Cin in (dy, dx, ci) order; stems pack
-        // each tap as a 4-channel piece (zero pad) and round K up to 64
+        // weight K per tc layer: kh*kw*Cpad in (dy, dx, ci) order, each tap's
+        // channels zero-padded to a multiple of 64; stems pack each tap as a
+        // 4-channel piece (zero pad) and round K up to 64
         auto tc_k = [](const LayerRT &l) -> int64_t {
-            return l.tc_small ? conv_tc_small_k(l.geo) : (int64_t)l.spec.k_h * l.spec.k_w * l.geo.Cin;
+            return l.tc_small ? conv_tc_small_k(l.geo) : (int64_t)l.spec.k_h * l.spec.k_w * conv_tc_cpad(l.geo.Cin);
         };
         int64_t nbf = 0;
         for (auto &l : e->L) {
@@ -346,7 +349,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 if (!l.tc && !l.tc_small) continue;
                 const int kh = l.spec.k_h, kw = l.spec.k_w, ci_n = l.geo.Cin, co = l.C;
                 const int64_t K = tc_k(l);
-                const int cstep = l.tc_small ? 4 : ci_n;   // elements per tap in the K layout
+                const int cstep = l.tc_small ? 4 : conv_tc_cpad(ci_n);   // elements per tap in the K layout
                 l.wbf = e->wbf_mem + o;
                 for (int c = 0; c < co; c++)
                     for (int dy = 0; dy < kh; dy++)
@@ -433,7 +436,7 @@ static st_status plan(st_encoder *e) {
             l.b_pbase = add(B * N * 4, tdef, tlast);
             l.b_rows = add((l.rows_cap + 1) * l.C * ES, tdef, tlast);
             if (l.kind == ST_SE)   // sum0 | dsum | s_tab | refresh, used only while the layer runs
-                l.b_se = add(B * l.C * 8 + B * F * l.C * 8 + B * (F + 1) * l.C * 4 + B * 4 + 64, tdef, tdef);
+                l.b_se = add(B * l.C * 8 + B * F * l.C * 8 + 2 * B * (F + 1) * l.C * 4 + B * 4 + 128, tdef, tdef);
             break;
         case ST_RELU: case ST_SILU: {
             // emitted rows go into the input's slot layout; in place when
@@ -533,6 +536,10 @@ static st_status plan(st_encoder *e) {
     CUDA_OK(e, cudaEventCreateWithFlags(&e->thr_ev, cudaEventDisableTiming));
     const char *ng = getenv("ST_NO_GRAPHS");
     e->use_graphs = !(ng && ng[0] == '1');
+    const char *dr = getenv("ST_DW_ROWMAJOR");   // A/B switch: the M-row depthwise kernel
+    e->dw_rowmajor = dr && dr[0] == '1';
+    const char *pt = getenv("ST_PROF_TRACE");    // per-launch profile lines on stderr
+    e->prof_trace = pt && pt[0] == '1';
     CUDA_OK(e, cudaStreamCreateWithFlags(&e->gstream, cudaStreamNonBlocking));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
@@ -759,7 +766,9 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, act, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(act, B * N, pb, e->totals + i, e->scan_tmp, st + 1, s));
-            LAUNCH(e, KC_ENUM, i, s, launch_enumerate(act, pb, B * N, e->p<int32_t>(l.b_ridx), s));
+            const bool dw_pm = l.depthwise && !e->dw_rowmajor;   // pixel-major depthwise needs no M-row list
+            if (!dw_pm)
+                LAUNCH(e, KC_ENUM, i, s, launch_enumerate(act, pb, B * N, e->p<int32_t>(l.b_ridx), s));
             zero_row(l.b_rows, l.C);
             c.dense = false;
             c.bf = bf;
@@ -771,7 +780,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.m_cap = (int64_t)B * F * N;
             c.out = e->ptr(l.b_rows);
             LAUNCH(e, l.depthwise ? KC_DW_SPARSE : l.tc ? KC_TC_SPARSE : l.tc_small ? KC_STEM_SPARSE : KC_CONV_SPARSE, i, s,
-                   l.depthwise  ? launch_dwconv_f32(c, s)
+                   dw_pm        ? launch_dwconv_pm(c, act, pb, s)
+                   : l.depthwise ? launch_dwconv_f32(c, s)
                    : l.tc       ? launch_conv_tc(c, l.tmap, s)
                    : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
                                 : launch_conv_f32(c, s));
@@ -830,12 +840,13 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             double *dsum = sum0 + (int64_t)B * l.C;
             float *s_tab = reinterpret_cast<float *>(dsum + (int64_t)B * F * l.C);
             uint32_t *refresh = reinterpret_cast<uint32_t *>(s_tab + (int64_t)B * (F + 1) * l.C);
+            float *gate_tab = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(refresh + B) + 63) & ~uintptr_t(63));
             const int H = l.spec.se_hidden;
             LAUNCH(e, KC_SE, i, s, launch_se_colsum(x_src, B, (int)N, l.C, sum0, s));
             if (F > 0) LAUNCH(e, KC_SE, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
             LAUNCH(e, KC_SE, i, s,
                    launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
-                                      thresholds + l.site, s_tab, refresh, s));
+                                      thresholds + l.site, gate_tab, s_tab, refresh, s));
             LAUNCH(e, KC_SE, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
@@ -1075,8 +1086,15 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 // 4-byte row index when sparse), weights once (bf16 on the tensor-core path)
                 const double wbytes = (r.cls == KC_TC_SPARSE || r.cls == KC_TC_DENSE || r.cls == KC_STEM_SPARSE ||
                                        r.cls == KC_STEM_DENSE) ? 2.0 : 4.0;
-                e->prof_bytes[r.cls] += 4.0 * ((double)Min * l.geo.Cin + (double)M * l.C) + wbytes * K * l.C +
-                                        (sparse ? 4.0 * M : 0.0);
+                const double ebytes = sparse && e->cfg.precision == ST_BF16 ? 2.0 : 4.0;   // row element size
+                const double b = ebytes * ((double)Min * l.geo.Cin + (double)M * l.C) + wbytes * K * l.C +
+                                 (sparse && r.cls != KC_DW_SPARSE ? 4.0 * M : 0.0);
+                e->prof_bytes[r.cls] += b;
+                if (e->prof_trace)
+                    fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f M=%lld Min=%lld K=%lld C=%d GBps=%.1f\n",
+                            (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, (long long)M, (long long)Min, (long long)K, l.C, t > 0 ? b / t * 1e-6 : 0.0);
+            } else if (e->prof_trace) {
+                fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f\n", (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t);
             }
         }
         e->recs.clear();

@@ -78,10 +78,13 @@ struct ConvCall {
 };
 void launch_conv_f32(const ConvCall &c, cudaStream_t s);
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s);
+// sparse depthwise, pixel-major over the output frame words (no M-row list)
+void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, cudaStream_t s);
 // BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu).  Weights bf16
 // [Cout][K] are read through a TMA descriptor (CUtensorMap, 128 bytes)
 // built once at create by make_weight_tmap.
 bool conv_tc_eligible(const Geo &g);
+int conv_tc_cpad(int cin);   // per-tap channel stride of the bf16 weight K layout (zero padded)
 bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout);
 void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s);
 // stems on tensor cores: the network input (c_in <= 4); sparse mode reads the
@@ -109,8 +112,8 @@ void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbas
 void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s);
 void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double *dsum, cudaStream_t s);
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
-                        const float *b1, const float *w2, const float *b2, const float *theta, float *s_tab,
-                        uint32_t *refresh, cudaStream_t s);
+                        const float *b1, const float *w2, const float *b2, const float *theta, float *gate_tab,
+                        float *s_tab, uint32_t *refresh, cudaStream_t s);
 void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s);
 void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s);
 void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, const float *theta, bool bf,

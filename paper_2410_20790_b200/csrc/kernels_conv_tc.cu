@@ -5,8 +5,9 @@
 //   D[M x Cout] = A[M x K] * B[K x Cout],  K = k_h*k_w*c_in in (dy, dx, ci) order,
 // A rows gathered from the compacted bf16 delta rows (sparse) or the fp32
 // dense reference activations (dense), B = bf16 weights.  Used where the
-// active-row batch is a real dense contraction (c_in % 64 == 0: 3x3 convs of
-// the CRNN and ResNet encoders, 1x1 convs with wide inputs).
+// active-row batch is a real dense contraction (3x3 convs of the CRNN and
+// ResNet encoders, EfficientNet 1x1 expand/project convs; c_in % 8 == 0, each
+// tap's channels zero-padded to a multiple of the 64-wide k-block).
 //
 // Precision contract of BF16 mode (R22-BF16): operands are bf16
 // (delta rows are stored bf16; dense activations and weights are rounded
@@ -184,8 +185,10 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
     const int M = DENSE ? c.B * Nout : *c.m_dev;
-    const int K = g.kh * g.kw * g.Cin;
-    const int nkb = SMALL ? (g.kh * g.kw + 15) / 16 : K / BK;
+    // K layout (dy, dx, ci) with each tap's channels zero-padded to Cpad, a
+    // multiple of the 64-wide k-block (Cpad == c_in when c_in % 64 == 0)
+    const int Cpad = (g.Cin + BK - 1) / BK * BK;
+    const int nkb = SMALL ? (g.kh * g.kw + 15) / 16 : g.kh * g.kw * Cpad / BK;
     const int ntn = (g.Cout + BN - 1) / BN;
     // 2-CTA cluster along M: work item w = (M-tile pair, N tile); this CTA
     // takes M tile 2*pair + rank.  Both CTAs need the same weight tile, so
@@ -347,7 +350,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             }
             for (int kb = 0; kb < nkb; kb++) {
                 const int k0 = kb * BK;
-                const int tap = k0 / g.Cin, ci0 = k0 - tap * g.Cin;
+                const int tap = k0 / Cpad, ci0 = k0 - tap * Cpad;
+                const int nval = min(8, (g.Cin - ci0) >> 3);   // real 8-channel chunks (c_in % 8 == 0)
                 int idx = -1;
 #pragma unroll
                 for (int t = 0; t < TAPS; t++)
@@ -363,7 +367,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                         const float4 *p = reinterpret_cast<const float4 *>(Ad + src + ci0);
                         float4 v[16];
 #pragma unroll
-                        for (int i = 0; i < 16; i++) v[i] = __ldg(p + i);
+                        for (int i = 0; i < 16; i++)
+                            v[i] = (i >> 1) < nval ? __ldg(p + i) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
                         for (int j = 0; j < 8; j++) {
                             chunk[j].x = pack_bf16x2(v[2 * j].x, v[2 * j].y);
@@ -383,9 +388,10 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 } else {
                     // ---- bf16 delta row: 128 B = 8 x cp.async 16 B, zero-fill if inactive
                     const bf16 *p = As + (src >= 0 ? src + ci0 : 0);
-                    const uint32_t nbytes = src >= 0 ? 16u : 0u;
+                    const int nv = src >= 0 ? nval : 0;
 #pragma unroll
-                    for (int j = 0; j < 8; j++) cp_async16(sa + m * 128 + ((j ^ (m & 7)) << 4), p + j * 8, nbytes);
+                    for (int j = 0; j < 8; j++)
+                        cp_async16(sa + m * 128 + ((j ^ (m & 7)) << 4), j < nv ? p + j * 8 : As, j < nv ? 16u : 0u);
                     cp_async_arrive_noinc(full + stage);
                 }
                 // ---- B tile: one TMA 2D load by thread 0 (rows past Cout zero-filled)
@@ -529,9 +535,12 @@ static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s
     cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE, SMALL>, c, *tmap);
 }
 
+// c_in % 8 == 0 (16-byte bf16 row pieces; each tap zero-padded to a multiple
+// of 64 channels), c_out % 8 == 0 (the TMA zero-fills weight rows past c_out)
 bool conv_tc_eligible(const Geo &g) {
-    return g.groups == 1 && g.Cin % tc::BK == 0 && g.Cout % 16 == 0 && g.kh * g.kw <= tc::TAPS;
+    return g.groups == 1 && g.Cin % 8 == 0 && g.Cout % 8 == 0 && g.kh * g.kw <= tc::TAPS;
 }
+int conv_tc_cpad(int cin) { return (cin + tc::BK - 1) / tc::BK * tc::BK; }
 
 // stems: the network input (c_in <= 4) on tensor cores, taps packed 16 per
 // 64-wide k-block (kernel SMALL variant); weights K = ceil(taps/16)*64

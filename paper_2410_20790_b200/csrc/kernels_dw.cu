@@ -94,6 +94,97 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
     }
 }
 
+// Sparse mode, pixel-major: one group per OUTPUT PIXEL.  Its output rows are
+// its active frames, consecutive in the (b, p, t) row order (base = 1 +
+// out_pbase, j-th set bit -> row base + j), and every tap's frame word,
+// slot word and row base are read once per pixel instead of once per
+// (output row, tap); per frame the active taps' rows are loaded in a batch.
+// The tap metadata (frame word, slot word, row base) is gathered by the
+// group's lanes in parallel (lane j: taps j, j+G, ...) into shared memory,
+// then read back as one 16-byte broadcast per tap, so 5x5 kernels keep the
+// register budget of two CTAs per SM.
+template <int G, int CPL, int KMAX, class T>
+__global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t *__restrict__ out_act,
+                                                      const int32_t *__restrict__ out_pbase) {
+    constexpr int TB = KMAX > 9 ? 5 : 3;
+    extern __shared__ int4 dw_meta[];   // [256/G groups][KMAX] {act, slot, 1 + pbase, 0}
+    const Geo g = c.g;
+    const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
+    const int C = g.Cin;
+    const int lane = threadIdx.x & (G - 1);
+    const uint32_t gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    int4 *meta = dw_meta + (threadIdx.x / G) * KMAX;
+    const int64_t BNo = (int64_t)c.B * Nout;
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int ntaps = g.kh * g.kw;
+    const T *A = static_cast<const T *>(c.a.rows);
+    T *O = static_cast<T *>(c.out);
+    for (int64_t bq = grp; bq < BNo; bq += ngrp) {
+        uint32_t w = __ldg(out_act + bq);
+        if (!w) continue;
+        const int b = (int)(bq / Nout), q = (int)(bq - (int64_t)b * Nout);
+        const int oy = q / g.Wout, ox = q - oy * g.Wout;
+        __syncwarp(gmask);   // previous pixel's metadata fully consumed
+        for (int tap = lane; tap < KMAX; tap += G) {
+            int4 m = make_int4(0, 0, 0, 0);
+            if (tap < ntaps) {
+                const int dy = tap / g.kw, dx = tap - dy * g.kw;
+                const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+                if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                    const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
+                    m.x = (int)__ldg(c.a.act + bp);
+                    m.y = (int)__ldg(c.a.slot + bp);
+                    m.z = 1 + __ldg(c.a.pbase + bp);
+                }
+            }
+            meta[tap] = m;
+        }
+        __syncwarp(gmask);
+        int64_t orow = 1 + __ldg(out_pbase + bq);
+        while (w) {
+            const int t1 = __ffs(w) - 1;
+            w &= w - 1;
+            const uint32_t lm = lowmask(t1);
+            for (int cb = 0; cb < C; cb += G * CPL) {
+                const int c0 = cb + lane * CPL;
+                const bool full = (C % 8 == 0) && (c0 + CPL <= C);
+                float acc[CPL];
+#pragma unroll
+                for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
+#pragma unroll
+                for (int t0 = 0; t0 < KMAX; t0 += TB) {
+                    float v[TB][CPL];
+                    bool on[TB];
+#pragma unroll
+                    for (int j = 0; j < TB; j++) {
+                        const int tap = t0 + j;
+                        on[j] = false;
+                        if (tap < KMAX) {
+                            const int4 m = meta[tap];
+                            on[j] = ((uint32_t)m.x >> t1) & 1u;
+                            if (on[j]) {
+                                const int64_t row = m.z + __popc((uint32_t)m.y & lm);
+                                row_load<T, CPL>(A + row * C, c0, C, full, v[j]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < TB; j++) {
+                        if (!on[j]) continue;
+                        float wv[CPL];
+                        row_load<float, CPL>(c.wk + (int64_t)(t0 + j) * C, c0, C, full, wv);
+#pragma unroll
+                        for (int i = 0; i < CPL; i++) acc[i] = fmaf(wv[i], v[j][i], acc[i]);
+                    }
+                }
+                if (c0 < C) row_store<T, CPL>(O + orow * C, c0, C, full, acc);
+            }
+            orow++;
+        }
+    }
+}
+
 // lanes per row: 8 channels per lane when C % 8 == 0 (G*8 channels per chunk)
 #define DW_SHAPE(C_, L)                                            \
     if ((C_) % 8 != 0) {                                           \
@@ -129,6 +220,37 @@ static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
     if (c.dense || !c.bf) launch_dw_t<float>(c, s);
     else launch_dw_t<bf16>(c, s);
+}
+
+template <int G, int CPL, int KMAX, class T>
+static void launch_dw_pm_k(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, int64_t BNo,
+                           cudaStream_t s) {
+    constexpr int smem = (256 / G) * KMAX * 16;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dwconv_pm<G, CPL, KMAX, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo * G + 255) / 256, 148 * 16));
+    k_dwconv_pm<G, CPL, KMAX, T><<<grid, 256, smem, s>>>(c, out_act, out_pbase);
+}
+
+template <class T>
+static void launch_dw_pm_t(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, cudaStream_t s) {
+    const int64_t BNo = (int64_t)c.B * c.g.Hout * c.g.Wout;
+    const int kk = c.g.kh * c.g.kw;
+#define L_DWPM(G_, CPL_)                                                                 \
+    {                                                                                    \
+        if (kk <= 9) launch_dw_pm_k<G_, CPL_, 9, T>(c, out_act, out_pbase, BNo, s);      \
+        else launch_dw_pm_k<G_, CPL_, 25, T>(c, out_act, out_pbase, BNo, s);             \
+    }
+    DW_SHAPE(c.g.Cin, L_DWPM);
+#undef L_DWPM
+}
+
+void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, cudaStream_t s) {
+    if (!c.bf) launch_dw_pm_t<float>(c, out_act, out_pbase, s);
+    else launch_dw_pm_t<bf16>(c, out_act, out_pbase, s);
 }
 
 }  // namespace st

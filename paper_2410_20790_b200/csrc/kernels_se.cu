@@ -18,17 +18,29 @@
 
 namespace st {
 
-// ---- (i-a) dense channel sums: sums[b][c] += sum_p x[b][p][c]  (fp64)
+// ---- (i-a) dense channel sums: sums[b][c] += sum_p x[b][p][c]  (fp64;
+// four independent partial sums per lane keep four loads in flight)
 __global__ void __launch_bounds__(256) k_se_colsum(const float *__restrict__ x, int N, int C, int ppb,
                                                    double *__restrict__ sums) {
     const int b = blockIdx.z, c = blockIdx.y * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
     const int p0 = blockIdx.x * ppb;
     const int p1 = min(N, p0 + ppb);
-    double acc = 0.0;
-    if (c < C)
-        for (int p = p0 + w; p < p1; p += 8) acc += (double)__ldg(x + ((int64_t)b * N + p) * C + c);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (c < C) {
+        const float *xb = x + (int64_t)b * N * C + c;
+        int p = p0 + w;
+        for (; p + 24 < p1; p += 32) {
+            const float v0 = __ldg(xb + (int64_t)p * C), v1 = __ldg(xb + (int64_t)(p + 8) * C);
+            const float v2 = __ldg(xb + (int64_t)(p + 16) * C), v3 = __ldg(xb + (int64_t)(p + 24) * C);
+            a0 += (double)v0;
+            a1 += (double)v1;
+            a2 += (double)v2;
+            a3 += (double)v3;
+        }
+        for (; p < p1; p += 8) a0 += (double)__ldg(xb + (int64_t)p * C);
+    }
     __shared__ double red[8][32];
-    red[w][threadIdx.x & 31] = acc;
+    red[w][threadIdx.x & 31] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (w == 0 && c < C) {
         double s = 0.0;
@@ -37,7 +49,9 @@ __global__ void __launch_bounds__(256) k_se_colsum(const float *__restrict__ x, 
     }
 }
 
-// ---- (i-b) per-frame channel sums of the delta rows: dsum[b][t][c] (fp64)
+// ---- (i-b) per-frame channel sums of the delta rows: dsum[b][t][c] (fp64).
+// Each warp reads 32 frame words at once and walks the active pixels of the
+// ballot (lanes = 32 channels of the block's channel slice).
 template <class T>
 __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, int F, int ppb,
                                                        double *__restrict__ dsum) {
@@ -48,17 +62,25 @@ __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, i
     double *my = sacc + w * 32 * 32;
     for (int t = 0; t < 32; t++) my[t * 32 + lane] = 0.0;
     const int p0 = blockIdx.x * ppb, p1 = min(N, p0 + ppb);
-    for (int p = p0 + w; p < p1; p += 8) {
+    for (int pw = p0 + w * 32; pw < p1; pw += 8 * 32) {
+        const int p = pw + lane;
         const int64_t bp = (int64_t)b * N + p;
-        uint32_t a = __ldg(in.act + bp);
-        if (!a) continue;
-        const int base = 1 + __ldg(in.pbase + bp);
-        const uint32_t sl = __ldg(in.slot + bp);
-        while (a) {
-            const int t1 = __ffs(a) - 1;
-            a &= a - 1;
-            const int64_t row = base + __popc(sl & lowmask(t1));
-            if (c < C) my[t1 * 32 + lane] += (double)ldr<T>(rows + row * C + c);
+        const uint32_t a_l = p < p1 ? __ldg(in.act + bp) : 0u;
+        uint32_t bal = __ballot_sync(0xffffffffu, a_l != 0);
+        const int base_l = a_l ? 1 + __ldg(in.pbase + bp) : 0;
+        const uint32_t sl_l = a_l ? __ldg(in.slot + bp) : 0u;
+        while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            uint32_t a = __shfl_sync(0xffffffffu, a_l, src);
+            const int base = __shfl_sync(0xffffffffu, base_l, src);
+            const uint32_t sl = __shfl_sync(0xffffffffu, sl_l, src);
+            while (a) {
+                const int t1 = __ffs(a) - 1;
+                a &= a - 1;
+                const int64_t row = base + __popc(sl & lowmask(t1));
+                if (c < C) my[t1 * 32 + lane] += (double)ldr<T>(rows + row * C + c);
+            }
         }
     }
     __syncthreads();
@@ -88,45 +110,49 @@ __device__ void se_gate_block(const float *m, int C, int H, const float *w1, con
     __syncthreads();
 }
 
-// ---- (ii) gate schedule, one CTA per chunk.  s_tab[b][t][c] = s_emit in
-// force at frame t (t = 0: reference gate); refresh[b] bit t-1 = refresh at t.
-__global__ void __launch_bounds__(256) k_se_schedule(const double *__restrict__ sum0, const double *__restrict__ dsum,
-                                                     int N, int C, int H, int F, const float *w1, const float *b1,
-                                                     const float *w2, const float *b2,
-                                                     const float *__restrict__ theta_p,
-                                                     float *__restrict__ s_tab, uint32_t *__restrict__ refresh) {
-    const float theta = __ldg(theta_p);
+// ---- (ii-a) gates of every frame, one CTA per (frame t, chunk b): the means
+// mean_t = (sum0 + dsum_1 + ... + dsum_t) / N do not depend on the refresh
+// decisions, so the F+1 gate evaluations run in parallel.  The running sum
+// is accumulated in frame order (as the sequential schedule would).
+__global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum0, const double *__restrict__ dsum,
+                                                  int N, int C, int H, int F, const float *w1, const float *b1,
+                                                  const float *w2, const float *b2, float *__restrict__ gate_tab) {
     extern __shared__ float sm[];
-    float *mean = sm;            // [C]
-    float *gate = mean + C;      // [C]
-    float *semit = gate + C;     // [C]
-    float *hid = semit + C;      // [H]
-    double *run = reinterpret_cast<double *>(
-        (reinterpret_cast<uintptr_t>(hid + H) + 7) & ~uintptr_t(7));   // [C], 8-byte aligned
+    float *mean = sm;          // [C]
+    float *hid = mean + C;     // [H]
+    const int t = blockIdx.x, b = blockIdx.y;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        double run = sum0[(int64_t)b * C + c];
+        for (int t1 = 0; t1 < t; t1++) run += dsum[((int64_t)b * F + t1) * C + c];
+        mean[c] = (float)(run / (double)N);
+    }
+    __syncthreads();
+    se_gate_block(mean, C, H, w1, b1, w2, b2, hid, gate_tab + ((int64_t)b * (F + 1) + t) * C);
+}
+
+// ---- (ii-b) refresh schedule, one CTA per chunk (frames sequential):
+// s_tab[b][t][c] = s_emit in force at frame t (t = 0: reference gate);
+// refresh[b] bit t-1 = refresh at t.
+__global__ void __launch_bounds__(256) k_se_schedule(const float *__restrict__ gate_tab, int C, int F,
+                                                     const float *__restrict__ theta_p, float *__restrict__ s_tab,
+                                                     uint32_t *__restrict__ refresh) {
+    const float theta = __ldg(theta_p);
+    extern __shared__ float semit[];   // [C]
     __shared__ float red[8];
     __shared__ int do_refresh;
     const int b = blockIdx.x;
+    const float *gt = gate_tab + (int64_t)b * (F + 1) * C;
+    float *st = s_tab + (int64_t)b * (F + 1) * C;
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
-        run[c] = sum0[(int64_t)b * C + c];
-        mean[c] = (float)(run[c] / (double)N);
-    }
-    __syncthreads();
-    se_gate_block(mean, C, H, w1, b1, w2, b2, hid, gate);
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-        semit[c] = gate[c];
-        s_tab[(int64_t)b * (F + 1) * C + c] = gate[c];
+        semit[c] = gt[c];
+        st[c] = gt[c];
     }
     uint32_t bits = 0;
     for (int t1 = 0; t1 < F; t1++) {
         __syncthreads();
-        for (int c = threadIdx.x; c < C; c += blockDim.x) {
-            run[c] += dsum[((int64_t)b * F + t1) * C + c];
-            mean[c] = (float)(run[c] / (double)N);
-        }
-        __syncthreads();
-        se_gate_block(mean, C, H, w1, b1, w2, b2, hid, gate);
+        const float *g = gt + (int64_t)(t1 + 1) * C;
         float mx = 0.0f;
-        for (int c = threadIdx.x; c < C; c += blockDim.x) mx = fmaxf(mx, fabsf(__fsub_rn(gate[c], semit[c])));
+        for (int c = threadIdx.x; c < C; c += blockDim.x) mx = fmaxf(mx, fabsf(__fsub_rn(g[c], semit[c])));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -139,21 +165,40 @@ __global__ void __launch_bounds__(256) k_se_schedule(const double *__restrict__ 
         __syncthreads();
         if (do_refresh) {
             bits |= 1u << t1;
-            for (int c = threadIdx.x; c < C; c += blockDim.x) semit[c] = gate[c];
+            for (int c = threadIdx.x; c < C; c += blockDim.x) semit[c] = g[c];
         }
         __syncthreads();
-        for (int c = threadIdx.x; c < C; c += blockDim.x) s_tab[((int64_t)b * (F + 1) + t1 + 1) * C + c] = semit[c];
+        for (int c = threadIdx.x; c < C; c += blockDim.x) st[(int64_t)(t1 + 1) * C + c] = semit[c];
     }
     if (threadIdx.x == 0) refresh[b] = bits;
 }
 
-// dense reference SE: y0 = x0 * s_tab[b][0]
+// dense reference SE: y0 = x0 * s_tab[b][0]; grid (pixel blocks, chunk),
+// float4 over channels when C % 4 == 0
 __global__ void k_se_dense_apply(const float *__restrict__ x, const float *__restrict__ s_tab, int N, int C, int F,
-                                 int64_t n, float *__restrict__ y) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i % C);
-        const int b = (int)(i / ((int64_t)N * C));
-        y[i] = __fmul_rn(x[i], s_tab[(int64_t)b * (F + 1) * C + c]);
+                                 float *__restrict__ y) {
+    const int b = blockIdx.y;
+    const float *sb = s_tab + (int64_t)b * (F + 1) * C;
+    const int64_t n = (int64_t)N * C;
+    const float *xb = x + (int64_t)b * n;
+    float *yb = y + (int64_t)b * n;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if ((C & 3) == 0) {
+        const int64_t n4 = n >> 2;
+        const int C4 = C >> 2;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+            const int c = (int)(i % C4) * 4;
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(xb) + i);
+            float4 o;
+            o.x = __fmul_rn(v.x, __ldg(sb + c));
+            o.y = __fmul_rn(v.y, __ldg(sb + c + 1));
+            o.z = __fmul_rn(v.z, __ldg(sb + c + 2));
+            o.w = __fmul_rn(v.w, __ldg(sb + c + 3));
+            reinterpret_cast<float4 *>(yb)[i] = o;
+        }
+    } else {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+            yb[i] = __fmul_rn(xb[i], __ldg(sb + (int)(i % C)));
     }
 }
 
@@ -237,32 +282,39 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
 
 void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s) {
     cudaMemsetAsync(sum0, 0, (size_t)B * C * 8, s);
-    const int ppb = 2048;
+    const int ppb = 1024;
     dim3 grid(cdiv(N, ppb), cdiv(C, 32), B);
     k_se_colsum<<<grid, 256, 0, s>>>(x, N, C, ppb, sum0);
 }
 
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
-                        const float *b1, const float *w2, const float *b2, const float *theta, float *s_tab,
-                        uint32_t *refresh, cudaStream_t s) {
-    const size_t smem = (size_t)(3 * C + ((H + 1) & ~1)) * 4 + (size_t)C * 8 + 64;
+                        const float *b1, const float *w2, const float *b2, const float *theta, float *gate_tab,
+                        float *s_tab, uint32_t *refresh, cudaStream_t s) {
+    const size_t smem = (size_t)(C + H) * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
-        cudaFuncSetAttribute(k_se_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    k_se_schedule<<<B, 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, theta, s_tab, refresh);
+    k_se_gates<<<dim3(F + 1, B), 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, gate_tab);
+    static size_t attr2 = 0;
+    const size_t smem2 = (size_t)C * 4;
+    if (smem2 > 48 * 1024 && smem2 > attr2) {
+        cudaFuncSetAttribute(k_se_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        attr2 = smem2;
+    }
+    k_se_schedule<<<B, 256, smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
 }
 
 void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s) {
-    const int64_t n = (int64_t)B * N * C;
-    const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
-    if (grid > 0) k_se_dense_apply<<<grid, 256, 0, s>>>(x, s_tab, N, C, F, n, y);
+    const int64_t n = (int64_t)N * C / ((C & 3) == 0 ? 4 : 1);
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16 / std::max(B, 1) + 1));
+    if (n > 0 && B > 0) k_se_dense_apply<<<dim3(gx, B), 256, 0, s>>>(x, s_tab, N, C, F, y);
 }
 
 template <class T>
 static void se_delta_sums_t(DView in, int B, int N, int C, int F, double *dsum, cudaStream_t s) {
-    const int ppb = 1024;
+    const int ppb = 2048;
     dim3 grid(cdiv(N, ppb), cdiv(C, 32), B);
     static bool attr = false;
     if (!attr) {

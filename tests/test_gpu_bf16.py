@@ -1,6 +1,6 @@
 """BF16 mode (tcgen05 tensor-core convolution) parity (-m gpu).
 
-Contract (R22-BF16): convolutions with c_in % 64 == 0 multiply
+Contract (R22-BF16): convolutions with c_in, c_out % 8 == 0 multiply
 bf16-rounded operands with fp32 accumulation; the oracle's BF16 mode applies
 the same rounding with its sequential fmaf chain, so the two differ only in
 the fp32 summation order inside the tensor core.  Checks:
@@ -43,11 +43,11 @@ def _rel_ok(a, b, rel, rms_frac):
 
 
 def _tc_net(cin, cout, k, s=1, h=20, w=28, seed=0):
-    # upstream convs stay on the exact CUDA-core path (c_out = 8 is not a
-    # tensor-core shape, c_in = 8 < 64), so the conv under test receives
+    # upstream convs stay on the exact CUDA-core path (c_out = 12 and c_in = 12
+    # are not tensor-core shapes), so the conv under test receives
     # bit-identical input deltas on both sides
     n = Net(3, h, w)
-    x = n.relu(n.conv(-1, 8, 3))
+    x = n.relu(n.conv(-1, 12, 3))
     x = n.relu(n.conv(x, cin, 3))
     y = n.conv(x, cout, k, s, k // 2)
     n.output(y)
@@ -56,7 +56,10 @@ def _tc_net(cin, cout, k, s=1, h=20, w=28, seed=0):
 
 
 @pytest.mark.parametrize("cin,cout,k,s", [(64, 64, 3, 1), (64, 128, 3, 1), (128, 256, 3, 2), (64, 512, 1, 1),
-                                          (192, 96, 3, 1), (64, 32, 3, 1)])
+                                          (192, 96, 3, 1), (64, 32, 3, 1),
+                                          # channel-padded k-blocks (c_in % 64 != 0), ragged c_out tiles
+                                          (16, 96, 1, 1), (24, 40, 1, 1), (40, 24, 3, 1), (144, 24, 1, 1),
+                                          (8, 16, 3, 2), (112, 672, 1, 1)])
 def test_tc_conv_kernel_unit(cin, cout, k, s):
     net, conv = _tc_net(cin, cout, k, s, seed=cin + cout)
     B, L = 3, 6

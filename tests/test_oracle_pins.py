@@ -406,11 +406,12 @@ def test_pin16_se_zero_threshold(oracle_lib):
 
 
 # ------------------------------------------------ BF16-mode conv contract
-@pytest.mark.parametrize("cin,cout", [(64, 16), (128, 32), (32, 16)])
+@pytest.mark.parametrize("cin,cout", [(64, 16), (128, 32), (32, 16), (24, 40), (12, 16), (16, 12)])
 def test_bf16_mode_conv_matches_rounded_fp64(oracle_lib, cin, cout):
-    """BF16 mode (R22-BF16): eligible convs (c_in % 64 == 0) equal the fp64
-    convolution of bf16-rounded weights and inputs (torch bfloat16 casts);
-    ineligible ones (c_in = 32) are unchanged from FP32 mode."""
+    """BF16 mode (R22-BF16): eligible convs (c_in % 8 == 0, c_out % 8 == 0)
+    equal the fp64 convolution of bf16-rounded weights and inputs (torch
+    bfloat16 casts); ineligible ones (c_in = 12, c_out = 12) are unchanged
+    from FP32 mode."""
     n = Net(cin, 7, 9)
     c = n.conv(-1, cout, 3)
     n.output(c)
@@ -418,7 +419,7 @@ def test_bf16_mode_conv_matches_rounded_fp64(oracle_lib, cin, cout):
     x = np.random.default_rng(cin).standard_normal((7, 9, cin)).astype(np.float32)
     got = oracle.dense_forward(n, x, precision="bf16")[c]
     rb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64)
-    if cin % 64 == 0:
+    if cin % 8 == 0 and cout % 8 == 0:
         xw = rb(x).permute(2, 0, 1).unsqueeze(0)
         ww = rb(n.layers[c]["w"])
         ref = F.conv2d(xw, ww, torch.from_numpy(n.layers[c]["b"].astype(np.float64)), padding=1)[0].permute(1, 2, 0).numpy()
