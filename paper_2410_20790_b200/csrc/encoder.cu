@@ -795,6 +795,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
                    launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, s));
             if (F == 0) break;
             DView me = view_of(e, i);
+            if (l.b_rows >= 0) zero_row(l.b_rows, l.C);   // own buffer (not in place)
             LAUNCH(e, KC_SITE_PW, i, s,
                    launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
                                          e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), s));
@@ -810,6 +811,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SITE_MP, i, s,
                    launch_site_maxpool(in, x_src, B, l.geo, thresholds + l.site, bf, slot, pb,
                                        e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
@@ -853,6 +855,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_SE, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SE, i, s,
                    launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds + l.site, bf, slot, pb,
                                   e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
