@@ -304,18 +304,32 @@ def main():
         enc.kernel_times(reset=False)
     kt = enc.kernel_times(reset=True)
     enc.set_profiling(False)
+    kt.pop("prof_stats", None)   # roofline-only statistics launched by the profiled pass, not part of a step
     step_kernel_ms = sum(v["ms"] for v in kt.values()) / args.steps
     dom = max(kt, key=lambda k: kt[k]["ms"])
     peaks, peak_src = measured_peaks()
+    # per-class achieved rate vs its roofline (algorithmic bytes / flops)
+    kroof = {}
+    for k, v in kt.items():
+        if not v["launches"] or v["ms"] <= 0:
+            continue
+        if v["flops"] > 0 and k.startswith("conv_tc"):
+            tf = v["flops"] / (v["ms"] / 1e3) / 1e12
+            kroof[k] = {"TFLOP/s": round(tf, 1), "frac": round(tf / float(peaks.get("bf16_tflops", 1590.0)), 3),
+                        "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)}
+        elif v["bytes"] > 0:
+            gb = v["bytes"] / (v["ms"] / 1e3) / 1e9
+            kroof[k] = {"GB/s": round(gb, 1), "frac": round(gb / float(peaks["hbm_gbs"]), 3)}
     d = kt[dom]
     nl = max(d["launches"], 1)
     if d["flops"] > 0 and dom.startswith("conv_tc"):
         # tcgen05 bf16: measured cuBLAS bf16 peak, sustained figure (kernel timed inside a long step)
-        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+        peak_key = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
+        peak = float(peaks.get(peak_key, 1590.0))
         ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                 "traffic": ncu_traffic(dom), "kernel": dom,
-                "peak_source": f"{peak_src} bf16_tflops_sustained",
+                "peak_source": f"{peak_src} {peak_key}",
                 "share_of_step": d["ms"] / args.steps / step_kernel_ms}
     elif d["flops"] > 0 and dom.startswith("conv"):
         # FP32 CUDA-core FFMA: 148 SMs x 128 lanes x 2 flop x max SM clock
@@ -403,6 +417,7 @@ def main():
                 "site_sparsity": site_sparsity,
                 "conv_rows_out": int(sum(lc["rows_out"][i] for i, l in enumerate(net.layers) if l["kind"] == W.CONV)),
                 "kernel_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in kt.items() if v["launches"]},
+                "kernel_roofline": kroof,
                 "memory": mem, "fp32_exact": fp32_exact}
         if dense:
             line.update(dense)

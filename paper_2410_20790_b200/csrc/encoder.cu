@@ -29,12 +29,12 @@ namespace {
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
               KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16,
-              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_N = 19;
+              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_N = 20;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
                               "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
                               "conv_tc_sparse", "conv_tc_dense", "se", "conv_tc_stem_sparse",
-                              "conv_tc_stem_dense"};
+                              "conv_tc_stem_dense", "prof_stats"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -112,6 +112,7 @@ struct st_encoder {
     uint16_t *wbf_mem = nullptr;
     // thresholds: pinned host staging -> device (a graph node), one fp32 per site
     float *thr_dev = nullptr, *thr_host = nullptr;
+    float *zeros = nullptr;   // 1 KiB of device zeros (gather source of absent taps)
     cudaEvent_t thr_ev = nullptr;
     bool thr_pending = false;
     // CUDA graphs of whole steps, keyed by (frames, stride, n_diff, chunks)
@@ -522,7 +523,7 @@ static st_status plan(st_encoder *e) {
     int64_t max_words = B * Nin;
     for (auto &l : e->L) max_words = std::max<int64_t>(max_words, B * l.H * l.W);
     const int64_t small = (n + 1) * 4 + B * e->n_sites * 32 * 8 + (n + 1) * 3 * 8 + e->n_sites * 8 +
-                          scan_tmp_ints(max_words) * 4 + e->n_sites * 4 + 8 * 256;
+                          scan_tmp_ints(max_words) * 4 + e->n_sites * 4 + 1024 + 8 * 256;
     CUDA_OK(e, cudaMalloc(&e->smallmem, small));
     char *p = e->smallmem;
     auto take = [&](int64_t bytes) { char *r = p; p += (bytes + 255) / 256 * 256; return r; };
@@ -532,6 +533,8 @@ static st_status plan(st_encoder *e) {
     e->site_sum = (long long *)take(e->n_sites * 8);
     e->scan_tmp = (int32_t *)take(scan_tmp_ints(max_words) * 4);
     e->thr_dev = (float *)take(e->n_sites * 4);
+    e->zeros = (float *)take(1024);
+    CUDA_OK(e, cudaMemset(e->zeros, 0, 1024));
     CUDA_OK(e, cudaMallocHost(&e->thr_host, e->n_sites * 4));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->thr_ev, cudaEventDisableTiming));
     const char *ng = getenv("ST_NO_GRAPHS");
@@ -745,7 +748,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         // rows_in / touched of this layer: roofline accounting only, collected
         // when profiling is on (st_set_profiling) so the timed step skips them
         if (F > 0 && l.kind != ST_OUTPUT && e->prof)
-            LAUNCH(e, KC_COUNTS, i, s, launch_frame_counts(in.act, B, (int)Ns, nullptr, 0, st, st + 2, s));
+            LAUNCH(e, KC_PROF_STATS, i, s, launch_frame_counts(in.act, B, (int)Ns, nullptr, 0, st, st + 2, s));
         switch (l.kind) {
         case ST_CONV: {
             ConvCall c{};
@@ -753,6 +756,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.B = B;
             c.dense = true;
             c.a_dense = x_src;
+            c.zeros = e->zeros;
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
@@ -1096,6 +1100,26 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 if (e->prof_trace)
                     fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f M=%lld Min=%lld K=%lld C=%d GBps=%.1f\n",
                             (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, (long long)M, (long long)Min, (long long)K, l.C, t > 0 ? b / t * 1e-6 : 0.0);
+            } else if (r.layer >= 0 && e->last_ndiff > 0 &&
+                       (r.cls == KC_SITE_PW || r.cls == KC_SITE_MP || r.cls == KC_ACCUM)) {
+                // algorithmic bytes of the HBM-bound per-pixel kernels:
+                // input delta rows once, x0 of the touched input pixels once, emitted
+                // rows once, frame words in/out; Accumulation writes the dense outputs
+                const LayerRT &l = e->L[r.layer];
+                const double eb = e->cfg.precision == ST_BF16 ? 2.0 : 4.0;
+                const double C = l.C, Bc = e->last_chunks, F = e->last_ndiff;
+                const double Nout = (double)l.H * l.W;
+                const double Nin = l.src < 0 ? (double)e->in_H * e->in_W : (double)e->L[l.src].H * e->L[l.src].W;
+                double b = 0;
+                if (r.cls == KC_ACCUM)
+                    b = 4.0 * Bc * (F + 1) * Nout * C + 4.0 * Bc * Nout * C + eb * rin[r.layer] * C + 4.0 * Bc * Nin;
+                else
+                    b = eb * ((double)rin[r.layer] + (double)rout[r.layer]) * C + 4.0 * tch[r.layer] * C +
+                        12.0 * tch[r.layer] + 4.0 * Bc * (Nin + Nout);
+                e->prof_bytes[r.cls] += b;
+                if (e->prof_trace)
+                    fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f GBps=%.1f\n",
+                            (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, t > 0 ? b / t * 1e-6 : 0.0);
             } else if (e->prof_trace) {
                 fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f\n", (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t);
             }

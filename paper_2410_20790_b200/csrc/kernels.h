@@ -65,6 +65,7 @@ struct ConvCall {
     bool bf;                // sparse mode: rows are bf16 (BF16 mode)
     // A operand
     const float *a_dense;   // dense: [B][Nin][Cin]
+    const float *zeros;     // >= 1 KiB of device zeros (source of absent taps / padding)
     DView a;                // sparse
     const int32_t *ridx;    // sparse: M-row list
     const int32_t *m_dev;   // sparse: device M

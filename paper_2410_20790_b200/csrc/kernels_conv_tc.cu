@@ -144,6 +144,26 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// 8 independent 16-byte read-only loads issued back to back in one asm
+// block (ptxas otherwise chains them through one destination register)
+__device__ __forceinline__ void ldg4x8(const float *const (&p)[8], float4 (&v)[8]) {
+    asm volatile(
+        "ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%32];\n\t"
+        "ld.global.nc.v4.f32 {%4,%5,%6,%7}, [%33];\n\t"
+        "ld.global.nc.v4.f32 {%8,%9,%10,%11}, [%34];\n\t"
+        "ld.global.nc.v4.f32 {%12,%13,%14,%15}, [%35];\n\t"
+        "ld.global.nc.v4.f32 {%16,%17,%18,%19}, [%36];\n\t"
+        "ld.global.nc.v4.f32 {%20,%21,%22,%23}, [%37];\n\t"
+        "ld.global.nc.v4.f32 {%24,%25,%26,%27}, [%38];\n\t"
+        "ld.global.nc.v4.f32 {%28,%29,%30,%31}, [%39];"
+        : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[0].z), "=f"(v[0].w), "=f"(v[1].x), "=f"(v[1].y), "=f"(v[1].z),
+          "=f"(v[1].w), "=f"(v[2].x), "=f"(v[2].y), "=f"(v[2].z), "=f"(v[2].w), "=f"(v[3].x), "=f"(v[3].y),
+          "=f"(v[3].z), "=f"(v[3].w), "=f"(v[4].x), "=f"(v[4].y), "=f"(v[4].z), "=f"(v[4].w), "=f"(v[5].x),
+          "=f"(v[5].y), "=f"(v[5].z), "=f"(v[5].w), "=f"(v[6].x), "=f"(v[6].y), "=f"(v[6].z), "=f"(v[6].w),
+          "=f"(v[7].x), "=f"(v[7].y), "=f"(v[7].z), "=f"(v[7].w)
+        : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]), "l"(p[4]), "l"(p[5]), "l"(p[6]), "l"(p[7]));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -226,49 +246,60 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         uint32_t phase = 0;
         const int ntaps = g.kh * g.kw;
         const bf16 *dd = static_cast<const bf16 *>(c.ddelta);
+        // warp-cooperative gather: lane l stages tap (l & 15) of rows 2i + (l >> 4)
+        // of its warp's 32 rows, so the 16 lanes of a row read the row's
+        // receptive field as k_w-pixel contiguous runs (few lines per
+        // instruction) instead of 32 scattered rows per instruction
+        const int wrow0 = warp * 32, j = lane & 15;
         for (int w = cid; w < nwork; w += ncl) {
             const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
             const int r = mt * BM + m;
-            int b = 0, q = 0, t1 = 0;
-            const bool rv = r < M;
-            if (rv) {
+            // this thread's row: input plane (chunk, or chunk x frame) and the
+            // receptive-field origin; invalid rows get an origin no tap reaches
+            int plane = 0, iy0 = -(1 << 20), ix0 = -(1 << 20);
+            if (r < M) {
+                int b, q;
                 if (DENSE) {
                     b = r / Nout;
                     q = r - b * Nout;
+                    plane = b;
                 } else {
                     const int code = __ldg(c.ridx + r);
-                    t1 = code & 31;
                     b = (code >> 5) / Nout;
                     q = (code >> 5) - b * Nout;
+                    plane = b * c.F + (code & 31);
                 }
+                const int oy = q / g.Wout, ox = q - oy * g.Wout;
+                iy0 = oy * g.sh - g.ph;
+                ix0 = ox * g.sw - g.pw;
             }
-            const int oy = q / g.Wout, ox = q - oy * g.Wout;
             for (int kb = 0; kb < nkb; kb++) {
+                const int tap = kb * 16 + j;
+                const bool tv = tap < ntaps;
+                const int dy = tv ? tap / g.kw : 0, dx = tv ? tap - (tap / g.kw) * g.kw : 0;
                 mbar_wait(empty + stage, phase ^ 1);
                 unsigned char *sa = smem + stage * S::STAGE;
                 unsigned char *sb = sa + S::A_BYTES;
 #pragma unroll 4
-                for (int j = 0; j < 16; j++) {
-                    const int tap = kb * 16 + j;
-                    unsigned char *dst = sa + m * 128 + ((((j >> 1) ^ (m & 7)) << 4) | ((j & 1) << 3));
-                    bool valid = false;
-                    int64_t pix = 0;
-                    if (rv && tap < ntaps) {
-                        const int dy = tap / g.kw, dx = tap - dy * g.kw;
-                        const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
-                        valid = iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
-                        pix = iy * g.Win + ix;
-                    }
+                for (int i = 0; i < 16; i++) {
+                    const int rl = 2 * i + (lane >> 4), row = wrow0 + rl;
+                    const int pl = __shfl_sync(0xffffffffu, plane, rl);
+                    const int iy = __shfl_sync(0xffffffffu, iy0, rl) + dy;
+                    const int ix = __shfl_sync(0xffffffffu, ix0, rl) + dx;
+                    const bool valid = tv && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
+                    const int64_t pix = (int64_t)pl * Nin + iy * g.Win + ix;
+                    unsigned char *dst = sa + row * 128 + ((((j >> 1) ^ (row & 7)) << 4) | ((j & 1) << 3));
                     if (DENSE) {
                         float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                         if (valid) {
-                            const float *p = c.a_dense + ((int64_t)b * Nin + pix) * g.Cin;
-                            for (int ci = 0; ci < g.Cin; ci++) v[ci] = __ldg(p + ci);
+                            const float *p = c.a_dense + pix * g.Cin;
+#pragma unroll
+                            for (int ci = 0; ci < 4; ci++)
+                                if (ci < g.Cin) v[ci] = __ldg(p + ci);
                         }
                         *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
                     } else {
-                        const bf16 *p = dd + (valid ? (((int64_t)b * c.F + t1) * Nin + pix) * 4 : 0);
-                        cp_async8(dst, p, valid ? 8u : 0u);
+                        cp_async8(dst, dd + (valid ? pix * 4 : 0), valid ? 8u : 0u);
                     }
                 }
                 if (DENSE) {
@@ -360,38 +391,48 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 mbar_wait(empty + stage, phase ^ 1);
                 unsigned char *sa = smem + stage * S::STAGE;
                 unsigned char *sb = sa + S::A_BYTES;
+                // Warp-cooperative, coalesced staging: the warp's 32 rows are
+                // moved a few rows per instruction (lanes split a row's
+                // 128-byte k-block slice), each row's source index taken from
+                // its owner lane by shuffle.  One row per thread would touch
+                // 32 lines per instruction (8x the L1tex wavefronts).
+                const int wrow0 = warp * 32;
                 if (DENSE) {
-                    // ---- fp32 activations -> bf16 (RNE), 8 x 16 B chunks, swizzled
-                    uint4 chunk[8];
-                    if (src >= 0) {
-                        const float4 *p = reinterpret_cast<const float4 *>(Ad + src + ci0);
-                        float4 v[16];
+                    // ---- fp32 activations -> bf16 (RNE): 2 rows x 16 float4 per instruction,
+                    // two batches of 8 unconditional loads (an invalid source reads a safe
+                    // address and is zeroed after), so the loads issue back to back
+                    // an absent tap / padding chunk reads the zero block, so no
+                    // per-load validity has to stay live (8+ live predicates make
+                    // ptxas serialise the loads)
+                    float4 v[16];
+                    const float *pp[16];
 #pragma unroll
-                        for (int i = 0; i < 16; i++)
-                            v[i] = (i >> 1) < nval ? __ldg(p + i) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll
-                        for (int j = 0; j < 8; j++) {
-                            chunk[j].x = pack_bf16x2(v[2 * j].x, v[2 * j].y);
-                            chunk[j].y = pack_bf16x2(v[2 * j].z, v[2 * j].w);
-                            chunk[j].z = pack_bf16x2(v[2 * j + 1].x, v[2 * j + 1].y);
-                            chunk[j].w = pack_bf16x2(v[2 * j + 1].z, v[2 * j + 1].w);
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 8; j++) chunk[j] = make_uint4(0, 0, 0, 0);
+                    for (int i = 0; i < 16; i++) {
+                        const int rl = 2 * i + (lane >> 4), j4 = lane & 15;
+                        const int64_t si = __shfl_sync(0xffffffffu, src, rl);
+                        pp[i] = (si >= 0 && (j4 >> 1) < nval) ? Ad + si + ci0 + 4 * j4 : c.zeros + 4 * j4;
                     }
+                    ldg4x8(*reinterpret_cast<const float *const(*)[8]>(pp), *reinterpret_cast<float4(*)[8]>(v));
+                    ldg4x8(*reinterpret_cast<const float *const(*)[8]>(pp + 8), *reinterpret_cast<float4(*)[8]>(v + 8));
 #pragma unroll
-                    for (int j = 0; j < 8; j++)
-                        *reinterpret_cast<uint4 *>(sa + m * 128 + ((j ^ (m & 7)) << 4)) = chunk[j];
+                    for (int i = 0; i < 16; i++) {
+                        const int row = wrow0 + 2 * i + (lane >> 4), j4 = lane & 15;
+                        *reinterpret_cast<uint2 *>(sa + row * 128 + ((((j4 >> 1) ^ (row & 7)) << 4) | ((j4 & 1) << 3))) =
+                            make_uint2(pack_bf16x2(v[i].x, v[i].y), pack_bf16x2(v[i].z, v[i].w));
+                    }
                     fence_proxy_async();
                     mbar_arrive(full + stage);
                 } else {
-                    // ---- bf16 delta row: 128 B = 8 x cp.async 16 B, zero-fill if inactive
-                    const bf16 *p = As + (src >= 0 ? src + ci0 : 0);
-                    const int nv = src >= 0 ? nval : 0;
+                    // ---- bf16 delta rows: 4 rows x 8 x 16 B cp.async per instruction, zero-fill if inactive
 #pragma unroll
-                    for (int j = 0; j < 8; j++)
-                        cp_async16(sa + m * 128 + ((j ^ (m & 7)) << 4), j < nv ? p + j * 8 : As, j < nv ? 16u : 0u);
+                    for (int i = 0; i < 8; i++) {
+                        const int rl = 4 * i + (lane >> 3), j = lane & 7;
+                        const int64_t si = __shfl_sync(0xffffffffu, src, rl);
+                        const int row = wrow0 + rl;
+                        const bool ok = si >= 0 && j < nval;
+                        cp_async16(sa + row * 128 + ((j ^ (row & 7)) << 4), ok ? As + si + ci0 + j * 8 : As,
+                                   ok ? 16u : 0u);
+                    }
                     cp_async_arrive_noinc(full + stage);
                 }
                 // ---- B tile: one TMA 2D load by thread 0 (rows past Cout zero-filled)
@@ -475,8 +516,9 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                             *reinterpret_cast<float4 *>(o + j) = f;
                         }
                     } else {
-                        for (int j = 0; j < 32 && n0 + j < g.Cout; j++)
-                            o[j] = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
+#pragma unroll
+                        for (int j = 0; j < 32; j++)   // unrolled: v[] stays in registers
+                            if (n0 + j < g.Cout) o[j] = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
                     }
                 } else {
                     bf16 *o = static_cast<bf16 *>(c.out) + (int64_t)(r + 1) * g.Cout + n0;
@@ -491,7 +533,9 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                             *reinterpret_cast<uint4 *>(o + j) = u;
                         }
                     } else {
-                        for (int j = 0; j < 32 && n0 + j < g.Cout; j++) o[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+#pragma unroll
+                        for (int j = 0; j < 32; j++)
+                            if (n0 + j < g.Cout) o[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
                     }
                 }
             }

@@ -261,26 +261,42 @@ void launch_enumerate(const uint32_t *slot, const int32_t *pbase, int64_t n, int
 
 // ----------------------------------------------------------------- counts
 constexpr int CNT_E = 8;
+// Per-frame popcounts by bit transposition: for each frame bit t a warp
+// ballots bit t of its 32 words, so lane t accumulates popc(ballot) -- one
+// ballot per word and no per-bit atomics (dense words would otherwise
+// serialise on 31 shared counters).
 __global__ void __launch_bounds__(256) k_frame_counts(const uint32_t *__restrict__ act, int N, long long *counts,
                                                       int64_t cstride, long long *stat, long long *stat_nz) {
     __shared__ int cnt[32];
     __shared__ int nz;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) nz = 0;
     __syncthreads();
     const int b = blockIdx.y;
-    const int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * CNT_E;
     const uint32_t *a = act + (int64_t)b * N;
+    // block covers 256 * CNT_E consecutive words; warp w takes CNT_E runs of 32
+    const int64_t base = (int64_t)blockIdx.x * 256 * CNT_E + (int64_t)warp * 32 * CNT_E;
+    uint32_t w[CNT_E];
+#pragma unroll
     for (int e = 0; e < CNT_E; e++) {
-        if (p0 + e >= N) break;
-        uint32_t w = __ldg(a + p0 + e);
-        if (w) atomicAdd(&nz, 1);
-        while (w) {
-            const int t1 = __ffs(w) - 1;
-            w &= w - 1;
-            atomicAdd(&cnt[t1], 1);
+        const int64_t p = base + e * 32 + lane;
+        w[e] = p < N ? __ldg(a + p) : 0u;
+    }
+    int mine = 0, nzw = 0;
+#pragma unroll
+    for (int e = 0; e < CNT_E; e++) {
+        nzw += __popc(__ballot_sync(0xffffffffu, w[e] != 0u));
+        uint32_t any = __reduce_or_sync(0xffffffffu, w[e]);
+        while (any) {   // only frames with at least one active pixel in these 32 words
+            const int t = __ffs(any) - 1;
+            any &= any - 1;
+            const int cbit = __popc(__ballot_sync(0xffffffffu, (w[e] >> t) & 1u));
+            if (lane == t) mine += cbit;
         }
     }
+    if (mine) atomicAdd(&cnt[lane], mine);
+    if (lane == 0 && nzw) atomicAdd(&nz, nzw);
     __syncthreads();
     if (threadIdx.x < 32) {
         const int v = cnt[threadIdx.x];

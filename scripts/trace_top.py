@@ -1,6 +1,9 @@
 """Summarise ST_PROF_TRACE=1 stderr lines (bf16 encoder) per (kernel class, layer)."""
 import collections
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import oracle
 import workloads as W
