@@ -60,6 +60,7 @@ struct LayerRT {
     int b_se = -1;            // SE scratch: sum0 [B][C] f64 | dsum [B][F][C] f64 | s_tab [B][F+1][C] | refresh [B]
     // buffer ids (-1 = none / alias)
     int b_y0 = -1, b_act = -1, b_slot = -1, b_pbase = -1, b_rows = -1, b_ridx = -1, b_out = -1;
+    int b_ybf = -1;           // bf16 shadow of y0 (BF16 mode: feeds a tcgen05 conv in dense mode)
     int alias_rows_of = -1;   // rows / slot / pbase borrowed from another tensor
     int64_t rows_cap = 0;     // rows excluding the zero row
 };
@@ -457,6 +458,18 @@ static st_status plan(st_encoder *e) {
             break;
         }
     }
+    // bf16 shadows of dense activations read by tcgen05 convs in dense mode
+    // (same live interval as the fp32 y0 they shadow)
+    for (int i = 0; i < n; i++) {
+        const LayerRT &c = e->L[i];
+        if (c.kind != ST_CONV || !c.tc || c.src < 0) continue;
+        int o = c.src;
+        while (o >= 0 && e->L[o].kind == ST_OUTPUT) o = e->L[o].src;
+        if (o < 0 || e->L[o].b_y0 < 0 || e->L[o].b_ybf >= 0) continue;
+        const LayerRT &ol = e->L[o];
+        const Buf &yb = e->bufs[ol.b_y0];
+        e->L[o].b_ybf = add(B * (int64_t)ol.H * ol.W * ol.C * 2, yb.first, yb.last);
+    }
     // aliases extend the lifetime of the borrowed buffers
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -620,6 +633,12 @@ static DView view_of(const st_encoder *e, int t) {
     return v;
 }
 
+static void *ybf_of(st_encoder *e, int t) { return e->L[t].b_ybf >= 0 ? e->ptr(e->L[t].b_ybf) : nullptr; }
+// bf16 shadow of the dense tensor a layer reads (through OUTPUT taps), or null
+static const void *dense_bf_of(st_encoder *e, int t) {
+    while (t >= 0 && e->L[t].kind == ST_OUTPUT) t = e->L[t].src;
+    return t >= 0 ? ybf_of(e, t) : nullptr;
+}
 static const float *dense_of(const st_encoder *e, int t) {
     if (t < 0) return e->ref;
     const LayerRT &l = e->L[t];
@@ -757,6 +776,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.dense = true;
             c.a_dense = x_src;
             c.zeros = e->zeros;
+            c.a_dense_bf = l.tc ? dense_bf_of(e, l.src) : nullptr;
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
@@ -765,6 +785,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
                    : l.tc       ? launch_conv_tc(c, l.tmap, s)
                    : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
                                 : launch_conv_f32(c, s));
+            if (l.b_ybf >= 0)
+                LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
             if (F == 0) break;
             uint32_t *act = e->p<uint32_t>(l.b_act);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -796,7 +818,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             // the dense reference activation uses the same SiLU form as the site (fast in BF16 mode)
             const int dense_kind = (act_kind == ACT_SILU && bf) ? ACT_SILU_FAST : act_kind;
             LAUNCH(e, KC_DENSE_MISC, i, s,
-                   launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, s));
+                   launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
             if (F == 0) break;
             DView me = view_of(e, i);
             if (l.b_rows >= 0) zero_row(l.b_rows, l.C);   // own buffer (not in place)
@@ -809,7 +831,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             break;
         }
         case ST_MAXPOOL: {
-            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_maxpool(x_src, e->p<float>(l.b_y0), B, l.geo, s));
+            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_maxpool(x_src, e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), s));
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -826,7 +848,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         }
         case ST_ADD: {
             const float *x2 = dense_of(e, l.src2);
-            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, s));
+            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, ybf_of(e, i), s));
             if (F == 0) break;
             DView in2 = view_of(e, l.src2);
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
@@ -854,6 +876,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
                    launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
                                       thresholds + l.site, gate_tab, s_tab, refresh, s));
             LAUNCH(e, KC_SE, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
+            if (l.b_ybf >= 0)
+                LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);

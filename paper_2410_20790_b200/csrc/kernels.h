@@ -66,6 +66,7 @@ struct ConvCall {
     // A operand
     const float *a_dense;   // dense: [B][Nin][Cin]
     const float *zeros;     // >= 1 KiB of device zeros (source of absent taps / padding)
+    const void *a_dense_bf; // dense, optional: bf16 shadow of a_dense (tcgen05 path gathers it with cp.async)
     DView a;                // sparse
     const int32_t *ridx;    // sparse: M-row list
     const int32_t *m_dev;   // sparse: device M
@@ -96,9 +97,12 @@ void launch_conv_tc_small(const ConvCall &c, const void *tmap, cudaStream_t s);
 
 // ---- sites, joins, accumulation (kernels_site.cu) ----
 enum Act { ACT_RELU = 0, ACT_SILU = 1, ACT_SILU_FAST = 2 };   // FAST: BF16 mode only
-void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t s);
-void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s);
-void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s);
+// dense reference-frame ops; ybf (optional, may be null): bf16 (RNE) shadow
+// of y for a tensor-core conv that consumes y in dense mode
+void launch_dense_act(const float *x, float *y, int64_t n, int act, void *ybf, cudaStream_t s);
+void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s);
+void launch_dense_add(const float *a, const float *b, float *y, int64_t n, void *ybf, cudaStream_t s);
+void launch_to_bf16(const float *x, void *ybf, int64_t n, cudaStream_t s);
 // pointwise site: emitted rows written into out_rows at the input slots
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
                            uint32_t *out_act, void *out_rows, cudaStream_t s);

@@ -323,7 +323,10 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         int stage = 0;
         uint32_t phase = 0;
         const float *Ad = c.a_dense;
-        const bf16 *As = static_cast<const bf16 *>(c.a.rows);
+        // bf16 rows gathered with cp.async: the delta rows (sparse), or the bf16
+        // shadow of the dense activation when the producer wrote one (dense)
+        const bool async_a = !DENSE || c.a_dense_bf != nullptr;
+        const bf16 *As = static_cast<const bf16 *>(DENSE ? c.a_dense_bf : c.a.rows);
         const int ntaps = g.kh * g.kw;   // <= TAPS (conv_tc_eligible)
         // row code of this thread's row in its first tile (sparse); the next
         // tile's code is prefetched while the current tile streams
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 // its owner lane by shuffle.  One row per thread would touch
                 // 32 lines per instruction (8x the L1tex wavefronts).
                 const int wrow0 = warp * 32;
-                if (DENSE) {
+                if (!async_a) {
                     // ---- fp32 activations -> bf16 (RNE): 2 rows x 16 float4 per instruction,
                     // two batches of 8 unconditional loads (an invalid source reads a safe
                     // address and is zeroed after), so the loads issue back to back
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
-        if (!DENSE) asm volatile("cp.async.wait_all;" ::: "memory");
+        if (async_a) asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == 4) {
         // ===================== MMA issuer =====================
         constexpr uint32_t IDESC = idesc_bf16(BM, BN);

@@ -51,21 +51,28 @@ __device__ __forceinline__ float actf(float x) {
 constexpr int prefetch_depth(int cpl) { return cpl <= 2 ? 8 : cpl <= 4 ? 4 : cpl <= 8 ? 2 : 1; }
 
 // ---------------------------------------------------------------- dense ops
-template <int ACT>
-__global__ void k_dense_act(const float *__restrict__ x, float *__restrict__ y, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = actf<ACT>(x[i]);
+__device__ __forceinline__ void put_bf(void *ybf, int64_t i, float v) {
+    if (ybf) static_cast<bf16 *>(ybf)[i] = __float2bfloat16_rn(v);
 }
 
-void launch_dense_act(const float *x, float *y, int64_t n, int act, cudaStream_t s) {
+template <int ACT>
+__global__ void k_dense_act(const float *__restrict__ x, float *__restrict__ y, int64_t n, void *ybf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = actf<ACT>(x[i]);
+        y[i] = v;
+        put_bf(ybf, i, v);
+    }
+}
+
+void launch_dense_act(const float *x, float *y, int64_t n, int act, void *ybf, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
     if (grid <= 0) return;
-    if (act == ACT_RELU) k_dense_act<ACT_RELU><<<grid, 256, 0, s>>>(x, y, n);
-    else if (act == ACT_SILU) k_dense_act<ACT_SILU><<<grid, 256, 0, s>>>(x, y, n);
-    else k_dense_act<ACT_SILU_FAST><<<grid, 256, 0, s>>>(x, y, n);
+    if (act == ACT_RELU) k_dense_act<ACT_RELU><<<grid, 256, 0, s>>>(x, y, n, ybf);
+    else if (act == ACT_SILU) k_dense_act<ACT_SILU><<<grid, 256, 0, s>>>(x, y, n, ybf);
+    else k_dense_act<ACT_SILU_FAST><<<grid, 256, 0, s>>>(x, y, n, ybf);
 }
 
-__global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g) {
+__global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g, void *ybf) {
     const int No = g.Hout * g.Wout;
     const int64_t n = (int64_t)B * No * g.Cin;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -85,23 +92,49 @@ __global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__
             }
         }
         y[i] = m;
+        put_bf(ybf, i, m);
     }
 }
 
-void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, cudaStream_t s) {
+void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s) {
     const int64_t n = (int64_t)B * g.Hout * g.Wout * g.Cin;
     const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
-    if (grid > 0) k_dense_maxpool<<<grid, 256, 0, s>>>(x, y, B, g);
+    if (grid > 0) k_dense_maxpool<<<grid, 256, 0, s>>>(x, y, B, g, ybf);
 }
 
-__global__ void k_dense_add(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ y, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = __fadd_rn(a[i], b[i]);
+__global__ void k_dense_add(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ y, int64_t n,
+                            void *ybf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = __fadd_rn(a[i], b[i]);
+        y[i] = v;
+        put_bf(ybf, i, v);
+    }
 }
 
-void launch_dense_add(const float *a, const float *b, float *y, int64_t n, cudaStream_t s) {
+void launch_dense_add(const float *a, const float *b, float *y, int64_t n, void *ybf, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
-    if (grid > 0) k_dense_add<<<grid, 256, 0, s>>>(a, b, y, n);
+    if (grid > 0) k_dense_add<<<grid, 256, 0, s>>>(a, b, y, n, ybf);
+}
+
+// bf16 shadow of a dense activation produced by another kernel (4 per thread)
+__global__ void k_to_bf16(const float *__restrict__ x, bf16 *__restrict__ y, int64_t n) {
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < n;
+         i += (int64_t)gridDim.x * blockDim.x * 4) {
+        if (i + 4 <= n) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i));
+            uint2 u;
+            u.x = RowIO<bf16, 2>::pack(v.x, v.y);
+            u.y = RowIO<bf16, 2>::pack(v.z, v.w);
+            *reinterpret_cast<uint2 *>(y + i) = u;
+        } else {
+            for (int64_t j = i; j < n; j++) y[j] = __float2bfloat16_rn(x[j]);
+        }
+    }
+}
+
+void launch_to_bf16(const float *x, void *ybf, int64_t n, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(cdiv(n, 1024), 148 * 16);
+    if (grid > 0) k_to_bf16<<<grid, 256, 0, s>>>(x, static_cast<bf16 *>(ybf), n);
 }
 
 // ------------------------------------------------------- pointwise site
@@ -247,6 +280,7 @@ static int groups_grid(int64_t n_groups, int G) {
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
                            uint32_t *out_act, void *out_rows, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
+
 #define L_PW(G_, CPL_)                                                                                 \
     {                                                                                                  \
         const int grid = groups_grid(BN, G_);                                                          \
@@ -386,11 +420,268 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
     }
 }
 
+// Tile-resident variant (C = G*CPL, G a power of two <= 32).  A CTA owns
+// a TOH x TOW tile of output pixels of one chunk; the x_acc state of the
+// tile's input footprint lives in shared memory (one fp32 row per input
+// pixel, shared by the overlapping windows instead of one register copy per
+// window), the y_acc of each output in the registers of its lane group.
+// Frames of the tile's union word run in order.  Each thread owns fixed
+// (footprint pixel, lane chunk) units; the delta pieces of its units for the
+// frame MP_NS-1 ahead are staged with cp.async into a ring of MP_NS frame
+// stages (thread-private slots, so a per-thread cp.async.wait_group is the
+// only completion needed), so DRAM latency overlaps the frames in between.
+// Per frame: x_acc += Delta_t at the active footprint pixels, then every
+// touched output re-evaluates its window max (R7).  Per-pixel
+// arithmetic is identical to k_site_maxpool (x_acc += Delta in frame order,
+// max over the valid window, c = max - y_acc), so FP32 mode stays bit-exact.
+constexpr int MP_NS = 4;    // frame stages in flight
+constexpr int MP_KU = 4;    // units per thread (footprint pixels x G <= 1024)
+
+template <int G, int CPL, int OPT, class T>
+__global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *__restrict__ x0, int B, Geo g,
+                                                        int TOH, int TOW, const float *__restrict__ theta_p,
+                                                        const uint32_t *__restrict__ t_slot,
+                                                        const int32_t *__restrict__ t_pbase,
+                                                        uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+    constexpr int NGR = 256 / G;                          // output groups per CTA
+    constexpr int PIECES = CPL * (int)sizeof(T) / 16;     // 16-byte pieces per unit
+    extern __shared__ __align__(16) unsigned char smem_mp[];
+    const int C = G * CPL;
+    const float theta = __ldg(theta_p);
+    const int tid = threadIdx.x, lane = tid & (G - 1), gr = tid / G;
+    const unsigned gmask = group_mask<G>();
+    const int Nin = g.Hin * g.Win, No = g.Hout * g.Wout;
+    const int ntx = (g.Wout + TOW - 1) / TOW, nty = (g.Hout + TOH - 1) / TOH;
+    const int b = blockIdx.x / (ntx * nty);
+    const int tr = blockIdx.x - b * ntx * nty;
+    const int ty = tr / ntx, tx = tr - ty * ntx;
+    const int FH = (TOH - 1) * g.sh + g.kh, FW = (TOW - 1) * g.sw + g.kw, FP = FH * FW;
+    const int fy0 = ty * TOH * g.sh - g.ph, fx0 = tx * TOW * g.sw - g.pw;
+    float *xs = reinterpret_cast<float *>(smem_mp);
+    T *stg = reinterpret_cast<T *>(xs + (size_t)FP * C);                // [MP_NS][ku][256][CPL]
+    uint32_t *u_word = reinterpret_cast<uint32_t *>(stg + (size_t)MP_NS * ((FP * G + 255) / 256) * 256 * CPL);
+    const T *rows = static_cast<const T *>(in.rows);
+    if (tid == 0) *u_word = 0u;
+    // ---- this thread's units: metadata in registers, x0 into x_acc (-inf outside the map, R11)
+    uint32_t u_act[MP_KU], u_sl[MP_KU];
+    int u_r1[MP_KU], u_off[MP_KU];
+    uint32_t uw = 0;
+#pragma unroll
+    for (int k = 0; k < MP_KU; k++) {
+        const int u = tid + k * 256;
+        const int p = u / G, l = u - (u / G) * G;
+        u_act[k] = 0;
+        u_sl[k] = 0;
+        u_r1[k] = 0;
+        u_off[k] = p * C + l * CPL;
+        if (p < FP) {
+            const int iy = fy0 + p / FW, ix = fx0 + p % FW;
+            float v[CPL];
+            if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                const int64_t gp = (int64_t)b * Nin + iy * g.Win + ix;
+                u_act[k] = __ldg(in.act + gp);
+                if (u_act[k]) {
+                    u_sl[k] = __ldg(in.slot + gp);
+                    u_r1[k] = 1 + __ldg(in.pbase + gp);
+                }
+                RowIO<float, CPL>::load(x0 + gp * C + l * CPL, v);
+            } else {
+#pragma unroll
+                for (int i = 0; i < CPL; i++) v[i] = -CUDART_INF_F;
+            }
+            RowIO<float, CPL>::store(xs + u_off[k], v);
+            uw |= u_act[k];
+        }
+    }
+    uw = __reduce_or_sync(0xffffffffu, uw);
+    __syncthreads();
+    if ((tid & 31) == 0 && uw) atomicOr(u_word, uw);
+    __syncthreads();
+    // ---- outputs of this group: y_acc = window max of x0 (= y0)
+    int64_t ob[OPT];
+    uint32_t Tw[OPT], emit[OPT];
+    int obase[OPT], wo[OPT];   // wo: footprint index of the window's top-left pixel
+    float ya[OPT][CPL];
+#pragma unroll
+    for (int j = 0; j < OPT; j++) {
+        const int o = gr + j * NGR;
+        const int loy = o / TOW, lox = o - (o / TOW) * TOW;
+        const int oy = ty * TOH + loy, ox = tx * TOW + lox;
+        ob[j] = -1;
+        Tw[j] = 0;
+        emit[j] = 0;
+        obase[j] = 0;
+        wo[j] = loy * g.sh * FW + lox * g.sw;
+        if (o < TOH * TOW && oy < g.Hout && ox < g.Wout) {
+            ob[j] = (int64_t)b * No + oy * g.Wout + ox;
+            Tw[j] = __ldg(t_slot + ob[j]);
+            obase[j] = 1 + __ldg(t_pbase + ob[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < CPL; i++) ya[j][i] = -CUDART_INF_F;
+        if (ob[j] >= 0)
+            for (int dy = 0; dy < g.kh; dy++)
+                for (int dx = 0; dx < g.kw; dx++) {
+                    float w[CPL];
+                    RowIO<float, CPL>::load(xs + (size_t)(wo[j] + dy * FW + dx) * C + lane * CPL, w);
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) ya[j][i] = w[i] > ya[j][i] ? w[i] : ya[j][i];
+                }
+    }
+    __syncthreads();   // every window's y_acc taken from x0 before frame 1 updates x_acc
+    const uint32_t U = *u_word;
+    const int ku = (FP * G + 255) / 256;   // units per thread in use (<= MP_KU): stage stride
+    // stage the active units of frame bit t1 (t1 < 0: nothing) into ring slot st
+    auto issue = [&](int t1, int st) {
+        if (t1 < 0) return;
+#pragma unroll
+        for (int k = 0; k < MP_KU; k++)
+            if ((u_act[k] >> t1) & 1u) {
+                const int row = u_r1[k] + __popc(u_sl[k] & lowmask(t1));
+                const unsigned char *src =
+                    reinterpret_cast<const unsigned char *>(rows + (int64_t)row * C + (u_off[k] % C));
+                unsigned char *dst =
+                    reinterpret_cast<unsigned char *>(stg + ((size_t)(st * ku + k) * 256 + tid) * CPL);
+#pragma unroll
+                for (int q = 0; q < PIECES; q++)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(dst + 16 * q)),
+                                 "l"(src + 16 * q)
+                                 : "memory");
+            }
+    };
+    // prologue: frames 0 .. MP_NS-2 of U in flight
+    uint32_t Ui = U;   // frames not yet issued
+    for (int s = 0; s < MP_NS - 1; s++) {
+        const int t1 = Ui ? __ffs(Ui) - 1 : -1;
+        if (Ui) Ui &= Ui - 1;
+        issue(t1, s);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    uint32_t Uc = U;   // frames not yet consumed
+    int it = 0;
+    while (Uc) {
+        const int t1 = __ffs(Uc) - 1;
+        Uc &= Uc - 1;
+        {   // frame MP_NS-1 ahead into the slot consumed MP_NS-1 frames from now
+            const int tn = Ui ? __ffs(Ui) - 1 : -1;
+            if (Ui) Ui &= Ui - 1;
+            issue(tn, (it + MP_NS - 1) % MP_NS);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        asm volatile("cp.async.wait_group %0;" ::"n"(MP_NS - 1) : "memory");
+        // (a) x_acc += Delta_t at this thread's active units (own staged pieces)
+        const int st = it % MP_NS;
+#pragma unroll
+        for (int k = 0; k < MP_KU; k++)
+            if ((u_act[k] >> t1) & 1u) {
+                float v[CPL], w[CPL];
+                RowIO<T, CPL>::load(stg + ((size_t)(st * ku + k) * 256 + tid) * CPL, v);
+                RowIO<float, CPL>::load(xs + u_off[k], w);
+#pragma unroll
+                for (int i = 0; i < CPL; i++) w[i] = __fadd_rn(w[i], v[i]);
+                RowIO<float, CPL>::store(xs + u_off[k], w);
+            }
+        __syncthreads();
+        // (b) touched outputs: candidate = window max - y_acc, truncation
+#pragma unroll
+        for (int j = 0; j < OPT; j++) {
+            if (!((Tw[j] >> t1) & 1u)) continue;   // group-uniform
+            float m[CPL];
+#pragma unroll
+            for (int i = 0; i < CPL; i++) m[i] = -CUDART_INF_F;
+            for (int dy = 0; dy < g.kh; dy++)
+                for (int dx = 0; dx < g.kw; dx++) {
+                    float w[CPL];
+                    RowIO<float, CPL>::load(xs + (size_t)(wo[j] + dy * FW + dx) * C + lane * CPL, w);
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) m[i] = w[i] > m[i] ? w[i] : m[i];
+                }
+            float cand[CPL];
+            float mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                cand[i] = __fsub_rn(m[i], ya[j][i]);
+                mx = fmaxf(mx, fabsf(cand[i]));
+            }
+            mx = gmax<G>(mx, gmask);
+            if (mx > theta) {
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    cand[i] = rnd<T>(cand[i]);
+                    ya[j][i] = __fadd_rn(ya[j][i], cand[i]);
+                }
+                RowIO<T, CPL>::store(out_rows + (int64_t)(obase[j] + __popc(Tw[j] & lowmask(t1))) * C + lane * CPL,
+                                     cand);
+                emit[j] |= 1u << t1;
+            }
+        }
+        __syncthreads();
+        it++;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < OPT; j++)
+        if (ob[j] >= 0 && lane == 0) out_act[ob[j]] = emit[j];
+}
+
+// output tile for the tile-resident maxpool: the most outputs per CTA whose
+// input footprint's fp32 x_acc fits in 64 KiB
+static size_t mp_smem(int FP, int C, int G, int esz) {
+    return (size_t)FP * C * 4 + (size_t)MP_NS * ((FP * G + 255) / 256) * 256 * (C / G) * esz + 16;
+}
+static bool mp_tile(const Geo &g, int C, int G, int esz, int max_out, int &TOH, int &TOW) {
+    int fp_max = std::min(16384 / C, 256 * MP_KU / G);
+    while (fp_max > 1 && mp_smem(fp_max, C, G, esz) > 200 * 1024) fp_max--;
+    int best = 0;
+    TOH = TOW = 0;
+    for (int h = 1; h <= std::min(g.Hout, 32); h++)
+        for (int w = 1; w <= std::min(g.Wout, 64); w++) {
+            const int fp = ((h - 1) * g.sh + g.kh) * ((w - 1) * g.sw + g.kw);
+            if (h * w > max_out || fp > fp_max) continue;
+            // most outputs; ties: fewest footprint pixels
+            if (h * w > best || (h * w == best && fp < ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw))) {
+                best = h * w;
+                TOH = h;
+                TOW = w;
+            }
+        }
+    return best > 0;
+}
+
 void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
                          cudaStream_t s) {
     const int64_t BN = (int64_t)B * g.Hout * g.Wout;
     const int kk = g.kh * g.kw;
+    const int C = g.Cin;
+    // tile-resident kernel when C = G * CPL (G a power of two <= 32, 8 | CPL)
+    int TG = 0, TCPL = 0;
+    if (C % 8 == 0 && C >= 16) {
+        const int cpl = std::max(8, C / 32), gg = C / cpl;
+        if (gg * cpl == C && (gg & (gg - 1)) == 0 && (cpl == 8 || cpl == 16)) { TG = gg; TCPL = cpl; }
+    }
+    constexpr int OPT = 2;
+    int TOH = 0, TOW = 0;
+    if (TG && mp_tile(g, C, TG, bf ? 2 : 4, OPT * (256 / TG), TOH, TOW)) {
+        const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
+        const size_t sm = mp_smem(FP, C, TG, bf ? 2 : 4);
+        const int64_t tiles = (int64_t)B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW);
+#define L_MPT(G_, CPL_)                                                                                      \
+    {                                                                                                        \
+        auto kf = k_site_maxpool_t<G_, CPL_, OPT, T>;                                                        \
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                      \
+        kf<<<(unsigned)tiles, 256, sm, s>>>(in, x0, B, g, TOH, TOW, theta, t_slot, t_pbase, out_act,         \
+                                            static_cast<T *>(out_rows));                                     \
+    }
+#define L_MPT_C(...)                                                                                         \
+    if (TG == 2) L_MPT(2, 8) else if (TG == 4) L_MPT(4, 8) else if (TG == 8) L_MPT(8, 8)                     \
+    else if (TG == 16) L_MPT(16, 8) else if (TCPL == 8) L_MPT(32, 8) else L_MPT(32, 16)
+        ST_ROW_DISPATCH(bf, L_MPT_C());
+#undef L_MPT_C
+#undef L_MPT
+        return;
+    }
 #define L_MP(G_, CPL_)                                                                                       \
     {                                                                                                        \
         const int grid = groups_grid(BN, G_);                                                                \
