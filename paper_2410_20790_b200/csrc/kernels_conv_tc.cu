@@ -39,7 +39,8 @@ namespace st {
 
 namespace tc {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, NPROD = 128, NTHREADS = 288;
+constexpr int BM = 128, BK = 64, NPROD = 128, NTHREADS = 288;
+constexpr int SMEM_MAX = 232448;   // 227 KB opt-in dynamic shared memory per CTA
 constexpr int TAPS = 9;   // max k_h*k_w taken by the tensor-core path (1x1, 2x2, 3x3)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -119,6 +120,32 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+// 2-SM MMA (issued by the leader CTA of the pair): A rows 0-127 from the
+// leader's smem and 128-255 from the peer's, B rows (N) split likewise, D rows
+// 0-127 in the leader's TMEM and 128-255 in the peer's (same addresses)
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// completion of the leader's prior 2-SM MMAs -> barrier at this offset in both CTAs
+__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+// arrive (release, cluster scope) on the barrier at this offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(rank)
+        : "memory");
+}
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
     asm volatile(
@@ -172,9 +199,11 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 template <int BN>
 struct Smem {
-    static constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-    static constexpr int B_BYTES = BN * BK * 2;          // BN * 128 B
+    static constexpr int A_BYTES = BM * BK * 2;          // 16 KB: this CTA's 128 rows of the M=256 tile
+    static constexpr int B_BYTES = (BN / 2) * BK * 2;    // this CTA's half of the BN weight rows
     static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES_FIT = (SMEM_MAX - 256 - 1024) / STAGE;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int BAR_OFF = STAGES * STAGE;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers, + alignment slack
 };
@@ -192,11 +221,13 @@ template <int BN, bool DENSE, bool SMALL = false>
 __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b) {
     using namespace tc;
     using S = Smem<BN>;
+    constexpr int STAGES = S::STAGES;
     constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
-    uint64_t *empty = full + STAGES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);   // this CTA's stage landed
+    uint64_t *pfull = full + STAGES;     // leader only: the peer's stage landed (relayed)
+    uint64_t *empty = pfull + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
@@ -210,9 +241,11 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     const int Cpad = (g.Cin + BK - 1) / BK * BK;
     const int nkb = SMALL ? (g.kh * g.kw + 15) / 16 : g.kh * g.kw * Cpad / BK;
     const int ntn = (g.Cout + BN - 1) / BN;
-    // 2-CTA cluster along M: work item w = (M-tile pair, N tile); this CTA
-    // takes M tile 2*pair + rank.  Both CTAs need the same weight tile, so
-    // each loads half of it and multicasts the half to both (B traffic / 2).
+    // CTA pair (cta_group::2): work item w = (M-tile pair, N tile) is one
+    // M=256 x N=BN MMA tile; this CTA stages A rows of M tile 2*pair + rank and
+    // weight rows [rank*BN/2, (rank+1)*BN/2) of the N tile, the leader (rank 0)
+    // issues the MMAs over both CTAs' shared memory, each CTA's TMEM receives
+    // its own 128 rows.
     const uint32_t rank = cluster_rank();
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const int mtiles = (M + BM - 1) / BM;
@@ -221,18 +254,19 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full + s, NPROD + 1);   // 128 producer arrivals + the TMA expect_tx arrival
-            mbar_init(empty + s, 2);          // this CTA's and the peer's MMA commit (shared B stage)
+            mbar_init(pfull + s, 1);          // the peer's relay
+            mbar_init(empty + s, 1);          // the leader's multicast MMA commit
         }
         for (int a = 0; a < 2; a++) {
-            mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tfull + a, 1);          // the leader's multicast MMA commit
+            mbar_init(tempty + a, 2);         // both CTAs' epilogues drained the accumulator
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
     cluster_sync();   // peer barriers initialised before any multicast targets them
@@ -308,10 +342,9 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 } else {
                     cp_async_arrive_noinc(full + stage);
                 }
-                if (m == 0) {
+                if (m == 0) {   // this CTA's half of the weight tile
                     mbar_arrive_tx(full + stage, S::B_BYTES);
-                    tma_load_2d_mc(sb + rank * (S::B_BYTES / 2), &tmap_b, kb * BK, nt * BN + (int)rank * (BN / 2),
-                                   full + stage, 0x3);
+                    tma_load_2d(sb, &tmap_b, kb * BK, nt * BN + (int)rank * (BN / 2), full + stage);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
@@ -328,69 +361,82 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         const bool async_a = !DENSE || c.a_dense_bf != nullptr;
         const bf16 *As = static_cast<const bf16 *>(DENSE ? c.a_dense_bf : c.a.rows);
         const int ntaps = g.kh * g.kw;   // <= TAPS (conv_tc_eligible)
-        // row code of this thread's row in its first tile (sparse); the next
-        // tile's code is prefetched while the current tile streams
-        int code_nx = 0;
-        if (!DENSE && cid < nwork) {
-            const int r0 = (2 * (cid / ntn) + (int)rank) * BM + m;
-            if (r0 < M) code_nx = __ldg(c.ridx + r0);
-        }
-        for (int w = cid; w < nwork; w += ncl) {
-            const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
-            const int r = mt * BM + m;
-            // decode the output row once per tile
-            int b = 0, q = 0, t1 = 0;
-            const bool rv = r < M;
-            if (rv) {
-                if (DENSE) {
-                    b = r / Nout;
-                    q = r - b * Nout;
-                } else {
-                    const int code = code_nx;
-                    const int gq = code >> 5;
-                    t1 = code & 31;
-                    b = gq / Nout;
-                    q = gq - b * Nout;
-                }
-            }
-            if (!DENSE) {   // prefetch the next tile's row code
-                const int wn = w + ncl;
-                const int rn = (2 * (wn / ntn) + (int)rank) * BM + m;
-                code_nx = (wn < nwork && rn < M) ? __ldg(c.ridx + rn) : 0;
-            }
-            // resolve the input row of every tap up front: the lookups are
-            // independent loads, so one memory round trip per tile instead of
-            // one per tap change
+        // Sparse: a tile's tap lookups (frame word, base, slot of each of the
+        // <= 9 input pixels) are issued one tile ahead -- while the current
+        // tile streams -- and the row code two tiles ahead, so a tile boundary
+        // costs no dependent memory round trip (short-K layers have only a
+        // few k-blocks per tile).
+        uint32_t n_a[TAPS], n_sl[TAPS];
+        int n_pb[TAPS], n_t1 = 0;
+        auto fetch_taps = [&](int w, int code) {
+            const int r = (2 * (w / ntn) + (int)rank) * BM + m;
+            const bool ok = w < nwork && r < M;
+            const int gq = code >> 5;
+            const int b = gq / Nout, q = gq - (gq / Nout) * Nout;
             const int oy = q / g.Wout, ox = q - oy * g.Wout;
-            int tapidx[TAPS];
+            n_t1 = code & 31;
 #pragma unroll
             for (int t = 0; t < TAPS; t++) {
-                tapidx[t] = -1;
-                if (rv && t < ntaps) {
+                n_a[t] = 0;
+                n_sl[t] = 0;
+                n_pb[t] = 0;
+                if (ok && t < ntaps) {
                     const int dy = t / g.kw, dx = t - dy * g.kw;
                     const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
                     if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
                         const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
-                        if (DENSE) {
-                            tapidx[t] = (int)bp;
-                        } else {
-                            const uint32_t a = __ldg(c.a.act + bp);
-                            const int pb = __ldg(c.a.pbase + bp);
-                            const uint32_t sl = __ldg(c.a.slot + bp);
-                            tapidx[t] = ((a >> t1) & 1u) ? 1 + pb + __popc(sl & lowmask(t1)) : -1;
-                        }
+                        n_a[t] = __ldg(c.a.act + bp);
+                        n_pb[t] = __ldg(c.a.pbase + bp);
+                        n_sl[t] = __ldg(c.a.slot + bp);
                     }
                 }
             }
+        };
+        auto code_of = [&](int w) {
+            const int r = (2 * (w / ntn) + (int)rank) * BM + m;
+            return (w < nwork && r < M) ? __ldg(c.ridx + r) : 0;
+        };
+        int code_nx = 0;
+        if (!DENSE) {
+            fetch_taps(cid, code_of(cid));
+            code_nx = code_of(cid + ncl);
+        }
+        for (int w = cid; w < nwork; w += ncl) {
+            const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
+            const int r = mt * BM + m;
+            const bool rv = r < M;
+            int tapidx[TAPS];
+            if (DENSE) {
+                // dense rows are (chunk, pixel): taps are pixel indices
+                const int b = rv ? r / Nout : 0, q = rv ? r - b * Nout : 0;
+                const int oy = q / g.Wout, ox = q - oy * g.Wout;
+#pragma unroll
+                for (int t = 0; t < TAPS; t++) {
+                    tapidx[t] = -1;
+                    if (rv && t < ntaps) {
+                        const int dy = t / g.kw, dx = t - dy * g.kw;
+                        const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+                        if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) tapidx[t] = b * Nin + iy * g.Win + ix;
+                    }
+                }
+            } else {
+                // this tile's lookups (issued a tile ago) -> delta-row index per tap (-1 = zero)
+#pragma unroll
+                for (int t = 0; t < TAPS; t++)
+                    tapidx[t] = ((n_a[t] >> n_t1) & 1u) ? 1 + n_pb[t] + __popc(n_sl[t] & lowmask(n_t1)) : -1;
+                fetch_taps(w + ncl, code_nx);    // next tile's lookups in flight
+                code_nx = code_of(w + 2 * ncl);  // and the row code after that
+            }
+            // the K loop walks (tap, 64-channel block) without divisions
+            int tap = 0, ci0 = 0;
             for (int kb = 0; kb < nkb; kb++) {
-                const int k0 = kb * BK;
-                const int tap = k0 / Cpad, ci0 = k0 - tap * Cpad;
                 const int nval = min(8, (g.Cin - ci0) >> 3);   // real 8-channel chunks (c_in % 8 == 0)
                 int idx = -1;
 #pragma unroll
                 for (int t = 0; t < TAPS; t++)
                     if (t == tap) idx = tapidx[t];
                 const int64_t src = idx >= 0 ? (int64_t)idx * g.Cin : -1;   // element offset, -1 = zero
+                const int k0 = kb * BK;
                 mbar_wait(empty + stage, phase ^ 1);
                 unsigned char *sa = smem + stage * S::STAGE;
                 unsigned char *sb = sa + S::A_BYTES;
@@ -439,42 +485,57 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     cp_async_arrive_noinc(full + stage);
                 }
                 // ---- B tile: one TMA 2D load by thread 0 (rows past Cout zero-filled)
-                if (m == 0) {   // expect both halves; load ours into both CTAs
+                if (m == 0) {   // this CTA's half of the weight tile
                     mbar_arrive_tx(full + stage, S::B_BYTES);
-                    tma_load_2d_mc(sb + rank * (S::B_BYTES / 2), &tmap_b, k0, nt * BN + (int)rank * (BN / 2),
-                                   full + stage, 0x3);
+                    tma_load_2d(sb, &tmap_b, k0, nt * BN + (int)rank * (BN / 2), full + stage);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                ci0 += BK;
+                if (ci0 == Cpad) { ci0 = 0; tap++; }
             }
         }
         if (async_a) asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == 4) {
-        // ===================== MMA issuer =====================
-        constexpr uint32_t IDESC = idesc_bf16(BM, BN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int w = cid; w < nwork; w += ncl, it++) {
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(tempty + acc, acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t tmem_d = tmem_base + acc * BN;
-            for (int kb = 0; kb < nkb; kb++) {
-                mbar_wait(full + stage, phase);
+        if (rank == 0) {
+            // ===================== MMA issuer (leader) =====================
+            constexpr uint32_t IDESC = idesc_bf16(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int w = cid; w < nwork; w += ncl, it++) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                mbar_wait(tempty + acc, acc_phase ^ 1);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t sa = smem_u32(smem + stage * S::STAGE);
-                    const uint32_t sb = sa + S::A_BYTES;
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < nkb; kb++) {
+                    mbar_wait(full + stage, phase);
+                    mbar_wait(pfull + stage, phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sa = smem_u32(smem + stage * S::STAGE);
+                        const uint32_t sb = sa + S::A_BYTES;
 #pragma unroll
-                    for (int k = 0; k < BK / 16; k++)
-                        tc_mma(tmem_d, sdesc(sa + k * 32), sdesc(sb + k * 32), IDESC, (kb | k) != 0);
-                    tc_commit_mc(empty + stage, 0x3);   // stage reusable only when both CTAs consumed it
-                    if (kb == nkb - 1) tc_commit(tfull + acc);
+                        for (int k = 0; k < BK / 16; k++)
+                            tc_mma2(tmem_d, sdesc(sa + k * 32), sdesc(sb + k * 32), IDESC, (kb | k) != 0);
+                        tc_commit2_mc(empty + stage);                 // both CTAs' stage reusable
+                        if (kb == nkb - 1) tc_commit2_mc(tfull + acc);  // both CTAs' epilogues
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                __syncwarp();
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
+        } else if (lane == 0) {
+            // ===================== relay (peer) =====================
+            // forwards "this CTA's stage landed" to the leader's pfull barrier
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int w = cid; w < nwork; w += ncl)
+                for (int kb = 0; kb < nkb; kb++) {
+                    mbar_wait(full + stage, phase);
+                    mbar_arrive_remote(pfull + stage, 0);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
         }
     } else {
         // ===================== epilogue =====================
@@ -543,14 +604,16 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 }
             }
             tc_fence_before();
-            mbar_arrive(tempty + acc);
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // all 4 epilogue warps done with acc
+            if (warp == 5 && lane == 0) mbar_arrive_remote(tempty + acc, 0);
         }
     }
+    __syncwarp();     // reconverge role-divergent warps before the .aligned cluster barrier
     tc_fence_before();
-    cluster_sync();   // no CTA leaves while its peer may still multicast into it
+    cluster_sync();   // no CTA leaves while its peer may still signal it / its MMAs target it
     if (warp == 4) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
     }
 }
 

@@ -21,7 +21,7 @@ for d in recs:
     k = (int(d["cls"]), int(d["layer"]))
     agg[k].append(float(d["ms"]))
     info[k] = (d.get("M"), d.get("Min"), d.get("GBps"))
-n = max(len(v) for v in agg.values())
+n = int(os.environ.get("TRACE_STEPS", "0")) or max(len(v) for v in agg.values())
 tot = sum(sum(v) for v in agg.values()) / n
 print(f"cfg{cfgn}: {n} passes, {tot:.3f} ms per pass")
 for (c, li), v in sorted(agg.items(), key=lambda x: -sum(x[1]))[:top]:
