@@ -95,6 +95,7 @@ struct st_encoder {
     // input site tensor buffers
     int in_act = -1, in_pbase = -1, in_rows = -1;
     int in_dd = -1;              // dense per-frame input delta for CUDA-core convs on the input
+    int in_refbf = -1;           // reference frames as 4-channel-padded bf16 (tensor-core stems)
     int64_t in_rows_cap = 0;
     bool bf = false;             // BF16 mode: delta rows stored as bf16 (R22-BF16)
     int esz = 4;                 // delta-row element size in bytes
@@ -352,6 +353,8 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 const int kh = l.spec.k_h, kw = l.spec.k_w, ci_n = l.geo.Cin, co = l.C;
                 const int64_t K = tc_k(l);
                 const int cstep = l.tc_small ? 4 : conv_tc_cpad(ci_n);   // elements per tap in the K layout
+                int sr = 0, shift = 0;
+                if (l.tc_small) conv_tc_small_layout(l.geo, sr, shift);
                 l.wbf = e->wbf_mem + o;
                 for (int c = 0; c < co; c++)
                     for (int dy = 0; dy < kh; dy++)
@@ -361,7 +364,8 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                                 uint32_t u;
                                 std::memcpy(&u, &v, 4);
                                 u += 0x7FFFu + ((u >> 16) & 1u);   // round to nearest even
-                                hb[o + (int64_t)c * K + (dy * kw + dx) * cstep + ci] = (uint16_t)(u >> 16);
+                                const int slot = sr ? dy * sr + dx + shift : dy * kw + dx;
+                                hb[o + (int64_t)c * K + slot * cstep + ci] = (uint16_t)(u >> 16);
                             }
                 o += (K * co + 127) / 128 * 128;
             }
@@ -413,6 +417,10 @@ static st_status plan(st_encoder *e) {
     for (auto &l : e->L)
         if (l.kind == ST_CONV && l.src == -1 && !l.depthwise && !l.tc) want_dd = true;   // incl. tc_small
     if (want_dd) e->in_dd = add(B * F * Nin * 4 * ES, 0, in_last);   // pixels padded to 4 channels
+    bool want_refbf = false;   // stems on tensor cores read the reference frames as padded bf16
+    for (auto &l : e->L)
+        if (l.kind == ST_CONV && l.tc_small) want_refbf = true;
+    if (want_refbf) e->in_refbf = add(B * Nin * 4 * 2, 0, in_last);
     // per-layer tensors
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -755,6 +763,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
                launch_frame_counts(act, B, (int)Nin, e->counts, cstride, e->site_sum, nullptr, s));
     }
 
+    if (e->in_refbf >= 0)
+        LAUNCH(e, KC_DENSE_MISC, -1, s, launch_pad4_bf16(e->ref, (int64_t)B * Nin, e->in_C, e->ptr(e->in_refbf), s));
     // ---------------- layers in topological order, dense then diff ("N")
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -776,7 +786,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.dense = true;
             c.a_dense = x_src;
             c.zeros = e->zeros;
-            c.a_dense_bf = l.tc ? dense_bf_of(e, l.src) : nullptr;
+            c.a_dense_bf = l.tc ? dense_bf_of(e, l.src) : l.tc_small ? e->ptr(e->in_refbf) : nullptr;
+            if (l.tc_small) conv_tc_small_layout(l.geo, c.sr, c.shift);
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);

@@ -73,6 +73,7 @@ struct ConvCall {
     int64_t m_cap;          // sparse: upper bound of M (grid sizing)
     const void *ddelta;     // sparse, optional: dense per-frame input delta [B][F][Nin][Cin]
     int F;                  // diff frames (ddelta indexing)
+    int sr, shift;          // stems: paired K layout (sr > 0), see conv_tc_small_layout
     // B operand / output
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only
@@ -92,7 +93,14 @@ void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s);
 // stems on tensor cores: the network input (c_in <= 4); sparse mode reads the
 // 4-channel-padded dense input delta (c.ddelta), dense mode the fp32 frames
 bool conv_tc_small_eligible(const Geo &g);
+// stem K layout: "paired" for stride-2 stems on even-width maps (each kernel row
+// padded to sr tap slots, slot = dy*sr + dx + shift, so 16-byte pieces of two
+// 4-channel pixels land on 16-byte slot pairs); else 16 taps per 64-wide k-block.
+// slot_of gives the 4-channel slot of tap (dy, dx); K = conv_tc_small_k
+void conv_tc_small_layout(const Geo &g, int &sr, int &shift);
 int conv_tc_small_k(const Geo &g);
+// bf16 copy of the fp32 reference frames [n][C] padded to 4 channels [n][4]
+void launch_pad4_bf16(const float *x, int64_t n, int C, void *out, cudaStream_t s);
 void launch_conv_tc_small(const ConvCall &c, const void *tmap, cudaStream_t s);
 
 // ---- sites, joins, accumulation (kernels_site.cu) ----

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     // K layout (dy, dx, ci) with each tap's channels zero-padded to Cpad, a
     // multiple of the 64-wide k-block (Cpad == c_in when c_in % 64 == 0)
     const int Cpad = (g.Cin + BK - 1) / BK * BK;
-    const int nkb = SMALL ? (g.kh * g.kw + 15) / 16 : g.kh * g.kw * Cpad / BK;
+    const int nkb = SMALL ? ((c.sr > 0 ? g.kh * c.sr : g.kh * g.kw) + 15) / 16 : g.kh * g.kw * Cpad / BK;
     const int ntn = (g.Cout + BN - 1) / BN;
     // CTA pair (cta_group::2): work item w = (M-tile pair, N tile) is one
     // M=256 x N=BN MMA tile; this CTA stages A rows of M tile 2*pair + rank and
@@ -275,16 +275,14 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
 
     if (SMALL && warp < 4) {
         // ===================== producers (stem, c_in <= 4) =====================
+        // A source: the 4-channel-padded bf16 input delta per frame (sparse)
+        // or the padded bf16 reference frames (dense); 8 bytes per pixel
         const int m = threadIdx.x;
         int stage = 0;
         uint32_t phase = 0;
         const int ntaps = g.kh * g.kw;
-        const bf16 *dd = static_cast<const bf16 *>(c.ddelta);
-        // warp-cooperative gather: lane l stages tap (l & 15) of rows 2i + (l >> 4)
-        // of its warp's 32 rows, so the 16 lanes of a row read the row's
-        // receptive field as k_w-pixel contiguous runs (few lines per
-        // instruction) instead of 32 scattered rows per instruction
-        const int wrow0 = warp * 32, j = lane & 15;
+        const bf16 *dd = static_cast<const bf16 *>(DENSE ? c.a_dense_bf : c.ddelta);
+        const int wrow0 = warp * 32;
         for (int w = cid; w < nwork; w += ncl) {
             const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
             const int r = mt * BM + m;
@@ -308,40 +306,45 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 ix0 = ox * g.sw - g.pw;
             }
             for (int kb = 0; kb < nkb; kb++) {
-                const int tap = kb * 16 + j;
-                const bool tv = tap < ntaps;
-                const int dy = tv ? tap / g.kw : 0, dx = tv ? tap - (tap / g.kw) * g.kw : 0;
                 mbar_wait(empty + stage, phase ^ 1);
                 unsigned char *sa = smem + stage * S::STAGE;
                 unsigned char *sb = sa + S::A_BYTES;
-#pragma unroll 4
-                for (int i = 0; i < 16; i++) {
-                    const int rl = 2 * i + (lane >> 4), row = wrow0 + rl;
-                    const int pl = __shfl_sync(0xffffffffu, plane, rl);
-                    const int iy = __shfl_sync(0xffffffffu, iy0, rl) + dy;
-                    const int ix = __shfl_sync(0xffffffffu, ix0, rl) + dx;
-                    const bool valid = tv && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
-                    const int64_t pix = (int64_t)pl * Nin + iy * g.Win + ix;
-                    unsigned char *dst = sa + row * 128 + ((((j >> 1) ^ (row & 7)) << 4) | ((j & 1) << 3));
-                    if (DENSE) {
-                        float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-                        if (valid) {
-                            const float *p = c.a_dense + pix * g.Cin;
+                if (c.sr > 0) {
+                    // paired layout: lane (l & 7) stages the 16-byte slot pair
+                    // p of rows 4i + (l >> 3): pixels (ix, ix+1) of kernel row dy
+                    const int p = lane & 7;
+                    const int s0 = kb * 16 + 2 * p;
+                    const int dy = s0 / c.sr, dxp = s0 - dy * c.sr - c.shift;   // dx of the pair's first pixel
+                    const bool sv = dy < g.kh;
 #pragma unroll
-                            for (int ci = 0; ci < 4; ci++)
-                                if (ci < g.Cin) v[ci] = __ldg(p + ci);
-                        }
-                        *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
-                    } else {
-                        cp_async8(dst, dd + (valid ? pix * 4 : 0), valid ? 8u : 0u);
+                    for (int i = 0; i < 8; i++) {
+                        const int rl = 4 * i + (lane >> 3), row = wrow0 + rl;
+                        const int pl = __shfl_sync(0xffffffffu, plane, rl);
+                        const int iy = __shfl_sync(0xffffffffu, iy0, rl) + dy;
+                        const int ix = __shfl_sync(0xffffffffu, ix0, rl) + dxp;   // even
+                        const bool valid = sv && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
+                        const bf16 *src = dd + (valid ? ((int64_t)pl * Nin + iy * g.Win + ix) * 4 : 0);
+                        cp_async16(sa + row * 128 + ((p ^ (row & 7)) << 4), src, valid ? 16u : 0u);
+                    }
+                } else {
+                    // 16 taps per k-block: lane l stages tap (l & 15) of rows 2i + (l >> 4)
+                    const int j = lane & 15;
+                    const int tap = kb * 16 + j;
+                    const bool tv = tap < ntaps;
+                    const int dy = tv ? tap / g.kw : 0, dx = tv ? tap - (tap / g.kw) * g.kw : 0;
+#pragma unroll 4
+                    for (int i = 0; i < 16; i++) {
+                        const int rl = 2 * i + (lane >> 4), row = wrow0 + rl;
+                        const int pl = __shfl_sync(0xffffffffu, plane, rl);
+                        const int iy = __shfl_sync(0xffffffffu, iy0, rl) + dy;
+                        const int ix = __shfl_sync(0xffffffffu, ix0, rl) + dx;
+                        const bool valid = tv && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
+                        const int64_t pix = (int64_t)pl * Nin + iy * g.Win + ix;
+                        cp_async8(sa + row * 128 + ((((j >> 1) ^ (row & 7)) << 4) | ((j & 1) << 3)),
+                                  dd + (valid ? pix * 4 : 0), valid ? 8u : 0u);
                     }
                 }
-                if (DENSE) {
-                    fence_proxy_async();
-                    mbar_arrive(full + stage);
-                } else {
-                    cp_async_arrive_noinc(full + stage);
-                }
+                cp_async_arrive_noinc(full + stage);
                 if (m == 0) {   // this CTA's half of the weight tile
                     mbar_arrive_tx(full + stage, S::B_BYTES);
                     tma_load_2d(sb, &tmap_b, kb * BK, nt * BN + (int)rank * (BN / 2), full + stage);
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
-        if (!DENSE) asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp < 4) {
         // ===================== producers =====================
         const int m = threadIdx.x;   // tile row owned by this thread
@@ -657,7 +660,33 @@ int conv_tc_cpad(int cin) { return (cin + tc::BK - 1) / tc::BK * tc::BK; }
 bool conv_tc_small_eligible(const Geo &g) {
     return g.groups == 1 && g.Cin <= 4 && g.Cout % 16 == 0 && g.kh * g.kw <= 64;
 }
-int conv_tc_small_k(const Geo &g) { return (g.kh * g.kw + 15) / 16 * tc::BK; }
+void conv_tc_small_layout(const Geo &g, int &sr, int &shift) {
+    // stride 2 -> ix0 = 2*ox - pw has the parity of pw for every output
+    // pixel; even map width keeps pixel pairs 16-byte aligned in memory
+    sr = shift = 0;
+    if (g.sw == 2 && g.Win % 2 == 0 && g.kw + (g.pw & 1) <= 16) {
+        shift = g.pw & 1;
+        sr = (g.kw + shift + 1) / 2 * 2;
+    }
+}
+int conv_tc_small_k(const Geo &g) {
+    int sr, shift;
+    conv_tc_small_layout(g, sr, shift);
+    const int slots = sr ? g.kh * sr : g.kh * g.kw;
+    return (slots + 15) / 16 * tc::BK;
+}
+
+__global__ void k_pad4_bf16(const float *__restrict__ x, int64_t n, int C, uint2 *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int c = 0; c < C && c < 4; c++) v[c] = __ldg(x + i * C + c);
+        out[i] = make_uint2(tc::pack_bf16x2(v[0], v[1]), tc::pack_bf16x2(v[2], v[3]));
+    }
+}
+void launch_pad4_bf16(const float *x, int64_t n, int C, void *out, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (grid > 0) k_pad4_bf16<<<grid, 256, 0, s>>>(x, n, C, static_cast<uint2 *>(out));
+}
 
 int conv_tc_bn(int cout) { return cout >= 256 ? 256 : cout >= 128 ? 128 : cout >= 64 ? 64 : 32; }
 
