@@ -11,6 +11,8 @@
 // 16-byte bf16 vector (two float4 in FP32 mode) -- and a batch of tap loads
 // is issued before its FMAs.  FP32-mode results are bit-identical to the
 // oracle (fmaf chain in tap order from +0).
+#include <type_traits>
+
 #include "rowio.cuh"
 
 namespace st {
@@ -185,6 +187,213 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t
     }
 }
 
+// Tile-resident depthwise (C % 8 == 0).  A CTA owns an output tile of one
+// chunk and one channel slice (<= 64 channels).  Depthwise deltas are linear
+// per frame (Eq.2, no state across frames), so the CTA stages the footprint's
+// delta rows of a GROUP of frames at once -- [pixel][frame in group][slice]
+// in shared memory, only the rows that exist (active) are copied, with
+// cp.async 16-byte pieces -- then every active output of every frame of the
+// group reads its k x k taps from shared memory (absent taps = 0).  Each input
+// row is fetched once per (tile, slice) instead of once per tap of every
+// output that touches it, and one round trip serves a whole frame group.
+// DENSE (reference frame): fp32 activations in, fp32 + bias out, one frame.
+// FP32 mode keeps the oracle's fmaf chain over taps in (dy, dx) order from +0.
+constexpr int DWT_CS = 64;                 // max channels per slice
+constexpr int DWT_STG = 96 * 1024;         // staging bytes per CTA (two CTAs per SM)
+
+template <class TI>
+struct DwTile {
+    static constexpr int EPL = 16 / (int)sizeof(TI);   // elements per 16-byte piece
+    static size_t smem(int FP, int TO, int kk) {
+        return (size_t)kk * DWT_CS * 4 + (size_t)FP * 12 + (size_t)TO * 8 + DWT_STG + 64;
+    }
+};
+
+template <class T, bool DENSE>
+__global__ void __launch_bounds__(256) k_dw_tile(ConvCall c, const uint32_t *__restrict__ out_act,
+                                                 const int32_t *__restrict__ out_pbase, int TOH, int TOW) {
+    using TI = typename std::conditional<DENSE, float, T>::type;   // staged input element
+    using TO = typename std::conditional<DENSE, float, T>::type;   // output element
+    constexpr int EPL = DwTile<TI>::EPL;
+    extern __shared__ __align__(16) unsigned char dwt_smem[];
+    const Geo g = c.g;
+    const int C = g.Cin, kk = g.kh * g.kw;
+    const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
+    const int nsl = (C + DWT_CS - 1) / DWT_CS;
+    const int ntx = (g.Wout + TOW - 1) / TOW, nty = (g.Hout + TOH - 1) / TOH;
+    int bid = blockIdx.x;
+    const int sl = bid % nsl;
+    bid /= nsl;
+    const int tile = bid % (ntx * nty), b = bid / (ntx * nty);
+    const int ty = tile / ntx, tx = tile - ty * ntx;
+    const int cs0 = sl * DWT_CS, csw = min(DWT_CS, C - cs0);   // slice channels (multiple of 8)
+    const int FH = (TOH - 1) * g.sh + g.kh, FW = (TOW - 1) * g.sw + g.kw, FP = FH * FW, TOc = TOH * TOW;
+    const int fy0 = ty * TOH * g.sh - g.ph, fx0 = tx * TOW * g.sw - g.pw;
+    // frames per staged group: the whole [FP][FG][csw] block fits the staging area
+    const int FG = DENSE ? 1 : min(32, (int)(DWT_STG / ((size_t)FP * csw * sizeof(TI))));
+    float *w_s = reinterpret_cast<float *>(dwt_smem);                 // [kk][csw]
+    uint32_t *f_act = reinterpret_cast<uint32_t *>(w_s + kk * DWT_CS); // [FP]
+    uint32_t *f_sl = f_act + FP;
+    int32_t *f_row = reinterpret_cast<int32_t *>(f_sl + FP);          // sparse: 1 + pbase; dense: pixel; -1 outside
+    uint32_t *o_act = reinterpret_cast<uint32_t *>(f_row + FP);       // [TO]
+    int32_t *o_row = reinterpret_cast<int32_t *>(o_act + TOc);        // sparse: 1 + out pbase; dense: out pixel; -1
+    uintptr_t sp = reinterpret_cast<uintptr_t>(o_row + TOc);
+    TI *stg = reinterpret_cast<TI *>((sp + 15) & ~uintptr_t(15));     // [FP][FG][csw]
+    __shared__ uint32_t u_word;
+    const int tid = threadIdx.x;
+    if (tid == 0) u_word = 0u;
+    for (int i = tid; i < kk * csw; i += 256) {
+        const int tap = i / csw, j = i - tap * csw;
+        w_s[i] = __ldg(c.wk + (int64_t)tap * C + cs0 + j);
+    }
+    for (int p = tid; p < FP; p += 256) {
+        const int iy = fy0 + p / FW, ix = fx0 + p % FW;
+        uint32_t a = 0, sl2 = 0;
+        int row = -1;
+        if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+            const int64_t gp = (int64_t)b * Nin + iy * g.Win + ix;
+            if (DENSE) {
+                a = 1u;
+                row = (int)gp;
+            } else {
+                a = __ldg(c.a.act + gp);
+                if (a) {
+                    sl2 = __ldg(c.a.slot + gp);
+                    row = 1 + __ldg(c.a.pbase + gp);
+                }
+            }
+        }
+        f_act[p] = a;
+        f_sl[p] = sl2;
+        f_row[p] = row;
+    }
+    __syncthreads();
+    uint32_t uw = 0;
+    for (int o = tid; o < TOc; o += 256) {
+        const int oy = ty * TOH + o / TOW, ox = tx * TOW + o % TOW;
+        uint32_t a = 0;
+        int row = -1;
+        if (oy < g.Hout && ox < g.Wout) {
+            const int64_t bo = (int64_t)b * Nout + oy * g.Wout + ox;
+            if (DENSE) {
+                a = 1u;
+                row = (int)bo;
+            } else {
+                a = __ldg(out_act + bo);
+                row = 1 + __ldg(out_pbase + bo);
+            }
+        }
+        o_act[o] = a;
+        o_row[o] = row;
+        uw |= a;
+    }
+    uw = __reduce_or_sync(0xffffffffu, uw);
+    if ((tid & 31) == 0 && uw) atomicOr(&u_word, uw);
+    __syncthreads();
+    const uint32_t U = u_word;
+    const TI *src_base = DENSE ? reinterpret_cast<const TI *>(c.a_dense) : static_cast<const TI *>(c.a.rows);
+    const int ppp = csw / EPL;   // 16-byte pieces per staged row
+    const int ncg = csw / 8;     // 8-channel groups per output
+    uint32_t Ur = U;
+    while (Ur) {
+        const int ta = __ffs(Ur) - 1;                                   // group = frames [ta, ta + FG)
+        const uint32_t gmask = (ta + FG >= 32) ? ~lowmask(ta) : (lowmask(ta + FG) & ~lowmask(ta));
+        // ---- stage every existing row of the group (absent rows are never read)
+        for (int u = tid; u < FP * FG * ppp; u += 256) {
+            const int k = u % ppp, pj = u / ppp;
+            const int j = pj % FG, p = pj / FG;
+            const int t1 = ta + j;
+            if (t1 < 32 && f_row[p] >= 0 && ((f_act[p] >> t1) & 1u)) {
+                const int64_t row = DENSE ? (int64_t)f_row[p] : (int64_t)f_row[p] + __popc(f_sl[p] & lowmask(t1));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                                 stg + ((size_t)p * FG + j) * csw + k * EPL)),
+                             "l"(src_base + row * C + cs0 + k * EPL)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        // ---- every active output of every frame of the group
+        uint32_t Ug = U & gmask;
+        while (Ug) {
+            const int t1 = __ffs(Ug) - 1;
+            Ug &= Ug - 1;
+            const int j = t1 - ta;
+            for (int u = tid; u < TOc * ncg; u += 256) {
+                const int o = u / ncg, cg = u - (u / ncg) * ncg;
+                const uint32_t oa = o_act[o];
+                if (!((oa >> t1) & 1u)) continue;
+                const int loy = o / TOW, lox = o - (o / TOW) * TOW;
+                float acc[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) acc[i] = 0.0f;
+                for (int dy = 0; dy < g.kh; dy++)
+                    for (int dx = 0; dx < g.kw; dx++) {
+                        const int p = (loy * g.sh + dy) * FW + lox * g.sw + dx;
+                        float v[8], w[8];
+                        if (f_row[p] >= 0 && ((f_act[p] >> t1) & 1u)) {
+                            RowIO<TI, 8>::load(stg + ((size_t)p * FG + j) * csw + cg * 8, v);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; i++) v[i] = 0.0f;
+                        }
+                        RowIO<float, 8>::load(w_s + (dy * g.kw + dx) * csw + cg * 8, w);
+#pragma unroll
+                        for (int i = 0; i < 8; i++) acc[i] = fmaf(w[i], v[i], acc[i]);
+                    }
+                if (DENSE) {
+                    float bb[8];
+                    RowIO<float, 8>::load(c.bias + cs0 + cg * 8, bb);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) acc[i] = __fadd_rn(acc[i], bb[i]);
+                    RowIO<float, 8>::store(static_cast<float *>(c.out) + (int64_t)o_row[o] * C + cs0 + cg * 8, acc);
+                } else {
+                    const int64_t orow = (int64_t)o_row[o] + __popc(oa & lowmask(t1));
+                    RowIO<TO, 8>::store(static_cast<TO *>(c.out) + orow * C + cs0 + cg * 8, acc);
+                }
+            }
+        }
+        __syncthreads();   // staging area reused by the next group
+        Ur &= ~gmask;
+    }
+}
+
+// output tile of the tile-resident depthwise: most outputs whose footprint fits
+static bool dw_tile_dims(const Geo &g, int fp_max, int &TOH, int &TOW) {
+    int best = 0;
+    TOH = TOW = 0;
+    for (int h = 1; h <= std::min(g.Hout, 32); h++)
+        for (int w = 1; w <= std::min(g.Wout, 64); w++) {
+            const int fp = ((h - 1) * g.sh + g.kh) * ((w - 1) * g.sw + g.kw);
+            if (fp > fp_max || h * w > 256) continue;
+            if (h * w > best) { best = h * w; TOH = h; TOW = w; }
+        }
+    return best > 0;
+}
+
+template <class T, bool DENSE>
+static bool launch_dw_tile_t(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, cudaStream_t s) {
+    using TI = typename std::conditional<DENSE, float, T>::type;
+    const Geo &g = c.g;
+    if (g.Cin % 8 != 0) return false;
+    // footprint small enough that a group holds >= 4 frames (sparse) / 1 frame (dense)
+    const int csw = std::min(DWT_CS, g.Cin);
+    const int fp_max = std::min<int>(512, (int)(DWT_STG / ((DENSE ? 1 : 4) * csw * sizeof(TI))));
+    int TOH, TOW;
+    if (!dw_tile_dims(g, fp_max, TOH, TOW)) return false;
+    const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
+    const size_t sm = DwTile<TI>::smem(FP, TOH * TOW, g.kh * g.kw);
+    const int64_t grid = (int64_t)c.B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW) *
+                         ((g.Cin + DWT_CS - 1) / DWT_CS);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dw_tile<T, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+        attr = true;
+    }
+    k_dw_tile<T, DENSE><<<(unsigned)grid, 256, sm, s>>>(c, out_act, out_pbase, TOH, TOW);
+    return true;
+}
+
 // lanes per row: 8 channels per lane when C % 8 == 0 (G*8 channels per chunk)
 #define DW_SHAPE(C_, L)                                            \
     if ((C_) % 8 != 0) {                                           \
@@ -218,6 +427,7 @@ static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
 }
 
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
+    if (c.dense && launch_dw_tile_t<float, true>(c, nullptr, nullptr, s)) return;
     if (c.dense || !c.bf) launch_dw_t<float>(c, s);
     else launch_dw_t<bf16>(c, s);
 }
