@@ -14,7 +14,7 @@
 // with x_acc / y_acc in registers, like the pointwise site.
 #include <math_constants.h>
 
-#include "common.cuh"
+#include "rowio.cuh"
 
 namespace st {
 
@@ -91,6 +91,71 @@ __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, i
         for (int ww = 0; ww < 8; ww++) s += sacc[ww * 1024 + i];
         if (s != 0.0) atomicAdd(dsum + ((int64_t)b * F + t1) * C + cc, s);
     }
+}
+
+// ---- (i-b') the same sums, thread-per-(frame, 8-channel group): thread
+// (t, cg) accumulates frame t's rows of its 8 channels in fp64 registers
+// while the CTA sweeps its pixel range; the frame words / slots / row bases
+// of 256 pixels are staged in shared memory and every active (pixel, t) row
+// slice is one 16-byte vector load, consecutive threads reading consecutive
+// pieces of a row (rows of a pixel are contiguous), several pixels in flight.
+// Exact fp64 sums of bf16 / fp32 values do not depend on the order (R8).
+template <class T>
+__global__ void __launch_bounds__(256) k_se_delta_sums_v(DView in, int N, int C, int F, int ppb, int CS,
+                                                         double *__restrict__ dsum) {
+    __shared__ uint32_t m_act[256], m_sl[256];
+    __shared__ int32_t m_row[256];
+    const T *rows = static_cast<const T *>(in.rows);
+    const int b = blockIdx.z, ncg = CS / 8;
+    const int t = threadIdx.x / ncg, cg = threadIdx.x - (threadIdx.x / ncg) * ncg;
+    const int c0 = blockIdx.y * CS + cg * 8;
+    const bool mine = t < F && c0 < C;   // C % 8 == 0
+    const uint32_t tbit = mine ? 1u << t : 0u;
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc[i] = 0.0;
+    const int p0 = blockIdx.x * ppb, p1 = min(N, p0 + ppb);
+    for (int pb = p0; pb < p1; pb += 256) {
+        const int p = pb + threadIdx.x;
+        uint32_t a = 0, sl = 0;
+        int r1 = 0;
+        if (p < p1) {
+            const int64_t bp = (int64_t)b * N + p;
+            a = __ldg(in.act + bp);
+            if (a) {
+                sl = __ldg(in.slot + bp);
+                r1 = 1 + __ldg(in.pbase + bp);
+            }
+        }
+        m_act[threadIdx.x] = a;
+        m_sl[threadIdx.x] = sl;
+        m_row[threadIdx.x] = r1;
+        __syncthreads();
+        const int np = min(256, p1 - pb);
+        for (int k0 = 0; k0 < np; k0 += 8) {
+            float v[8][8];
+            uint32_t on = 0;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int k = k0 + u;
+                const bool o = k < np && (m_act[k] & tbit);
+                on |= (uint32_t)o << u;
+                const int64_t row = o ? m_row[k] + __popc(m_sl[k] & lowmask(t)) : 0;   // row 0 = zeros
+                RowIO<T, 8>::load(rows + row * C + (mine ? c0 : 0), v[u]);
+            }
+            if (on) {
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+#pragma unroll
+                    for (int i = 0; i < 8; i++) acc[i] += (double)v[u][i];   // zeros where off
+            }
+        }
+        __syncthreads();
+    }
+    if (mine)
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (acc[i] != 0.0) atomicAdd(dsum + ((int64_t)b * F + t) * C + c0 + i, acc[i]);
 }
 
 // gate of one chunk from fp32 means m[C] (block-wide; hid/gate in smem)
@@ -326,6 +391,15 @@ static void se_delta_sums_t(DView in, int B, int N, int C, int F, double *dsum, 
 
 void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double *dsum, cudaStream_t s) {
     cudaMemsetAsync(dsum, 0, (size_t)B * F * C * 8, s);
+    if (C % 8 == 0 && F >= 1 && F <= 32) {
+        // channel slice: as many 8-channel groups as fit 256 threads at F frames
+        const int CS = std::max(8, std::min((C + 7) / 8 * 8, (256 / F) * 8));
+        const int ppb = 2048;
+        dim3 grid(cdiv(N, ppb), cdiv(C, CS), B);
+        if (bf) k_se_delta_sums_v<bf16><<<grid, 256, 0, s>>>(in, N, C, F, ppb, CS, dsum);
+        else k_se_delta_sums_v<float><<<grid, 256, 0, s>>>(in, N, C, F, ppb, CS, dsum);
+        return;
+    }
     if (bf) se_delta_sums_t<bf16>(in, B, N, C, F, dsum, s);
     else se_delta_sums_t<float>(in, B, N, C, F, dsum, s);
 }
