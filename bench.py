@@ -77,7 +77,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -320,6 +320,19 @@ def main():
         elif v["bytes"] > 0:
             gb = v["bytes"] / (v["ms"] / 1e3) / 1e9
             kroof[k] = {"GB/s": round(gb, 1), "frac": round(gb / float(peaks["hbm_gbs"]), 3)}
+    # whole-step roofline: T_roof = sum over kernel classes of
+    # max(algorithmic bytes / BW, algorithmic flops / P_class), on the measured counts
+    bw = float(peaks["hbm_gbs"]) * 1e9
+    p_tc = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))) * 1e12
+    p_f32 = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    t_roof = 0.0
+    for k, v in kt.items():
+        p = p_tc if k.startswith("conv_tc") else p_f32
+        t_roof += max(v["bytes"] / bw, v["flops"] / p)
+    t_roof_ms = t_roof * 1e3 / args.steps
+    step_roof = {"t_roof_ms": t_roof_ms, "t_measured_ms": None, "frac": None,
+                 "note": "sum over kernel classes of max(alg bytes / HBM peak, alg flops / class peak); "
+                         "classes without a byte model (scan, counts, dense_misc) contribute 0"}
     d = kt[dom]
     nl = max(d["launches"], 1)
     if d["flops"] > 0 and dom.startswith("conv_tc"):
@@ -418,6 +431,7 @@ def main():
                 "conv_rows_out": int(sum(lc["rows_out"][i] for i, l in enumerate(net.layers) if l["kind"] == W.CONV)),
                 "kernel_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in kt.items() if v["launches"]},
                 "kernel_roofline": kroof,
+                "step_roofline": dict(step_roof, t_measured_ms=ms_step, frac=step_roof["t_roof_ms"] / ms_step),
                 "memory": mem, "fp32_exact": fp32_exact}
         if dense:
             line.update(dense)
