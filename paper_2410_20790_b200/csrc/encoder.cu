@@ -52,6 +52,8 @@ struct LayerRT {
     bool tc = false;          // BF16 mode: tcgen05 tensor-core conv
     bool tc_small = false;    // BF16 mode: tcgen05 stem on the network input (c_in <= 4)
     int n_consumers = 0, last_consumer = 0;
+    int fused_pool = -1;      // ReLU: the maxpool that runs this site in its own pass
+    int fused_relu = -1;      // MAXPOOL: the ReLU site folded into this layer's pass
     // device weights (separate allocation)
     float *wk = nullptr, *bias = nullptr;
     uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
@@ -284,6 +286,21 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             }
         }
     }
+    // ReLU -> maxpool pairs run as one tile-resident pass (the ReLU output is
+    // read only by the pool, its input is a conv tensor, windows cover the map)
+    {
+        const char *nf = getenv("ST_NO_FUSE");   // A/B switch
+        if (!(nf && nf[0] == '1'))
+            for (int i = 0; i < n; i++) {
+                LayerRT &p = e->L[i];
+                if (p.kind != ST_MAXPOOL || p.src < 0) continue;
+                LayerRT &r = e->L[p.src];
+                if (r.kind != ST_RELU || r.n_consumers != 1 || r.src < 0 || e->L[r.src].kind != ST_CONV) continue;
+                if (!site_relu_maxpool_fusable(p.geo, e->bf)) continue;
+                p.fused_relu = p.src;
+                r.fused_pool = i;
+            }
+    }
     // ---- weights (K-major repack: wk[(dy*kw+dx)*cin_g + ci][co], reading R18)
     int64_t wfloats = 0;
     for (auto &l : e->L)
@@ -496,6 +513,13 @@ static st_status plan(st_encoder *e) {
             break;
         }
     }
+    // a fused ReLU -> maxpool pass reads the conv's dense pre-activation (the
+    // ReLU's x0) at the pool's step time
+    for (int i = 0; i < n; i++)
+        if (e->L[i].fused_relu >= 0) {
+            const LayerRT &cv = e->L[e->L[e->L[i].fused_relu].src];
+            if (cv.b_y0 >= 0) e->bufs[cv.b_y0].last = std::max(e->bufs[cv.b_y0].last, t_of(i));
+        }
     // ---- first-fit arena assignment, largest first
     std::vector<int> order(e->bufs.size());
     for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
@@ -776,7 +800,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         DView in = F > 0 ? view_of(e, l.src) : DView{};
         // rows_in / touched of this layer: roofline accounting only, collected
         // when profiling is on (st_set_profiling) so the timed step skips them
-        if (F > 0 && l.kind != ST_OUTPUT && e->prof)
+        if (F > 0 && l.kind != ST_OUTPUT && e->prof && l.fused_relu < 0)
             LAUNCH(e, KC_PROF_STATS, i, s, launch_frame_counts(in.act, B, (int)Ns, nullptr, 0, st, st + 2, s));
         switch (l.kind) {
         case ST_CONV: {
@@ -833,6 +857,7 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             if (F == 0) break;
             DView me = view_of(e, i);
             if (l.b_rows >= 0) zero_row(l.b_rows, l.C);   // own buffer (not in place)
+            if (l.fused_pool >= 0) break;                 // runs inside the pool's pass
             LAUNCH(e, KC_SITE_PW, i, s,
                    launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
                                          e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), s));
@@ -846,6 +871,29 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
+            if (l.fused_relu >= 0) {
+                // ReLU site + pool in one pass; the pool's row capacity is the
+                // dilation of the conv mask (superset of the ReLU's emitted mask)
+                const LayerRT &r = e->L[l.fused_relu];
+                const DView cv = view_of(e, r.src);
+                LAUNCH(e, KC_DILATE, i, s, launch_dilate(cv.act, B, l.geo, slot, s));
+                LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+                zero_row(l.b_rows, l.C);
+                LAUNCH(e, KC_SITE_MP, i, s,
+                       launch_site_relu_maxpool(cv, dense_of(e, r.src), B, l.geo, thresholds + r.site,
+                                                thresholds + l.site, bf, slot, pb, e->p<uint32_t>(r.b_act),
+                                                r.b_rows >= 0 ? e->ptr(r.b_rows) : nullptr,
+                                                e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
+                LAUNCH(e, KC_COUNTS, l.fused_relu, s,
+                       launch_frame_counts(e->p<uint32_t>(r.b_act), B, (int)Ns, e->counts + r.site * 32, cstride,
+                                           e->site_sum + r.site, nullptr, s));
+                LAUNCH(e, KC_COUNTS, i, s,
+                       launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
+                                           e->site_sum + l.site, nullptr, s));
+                if (e->prof)
+                    LAUNCH(e, KC_PROF_STATS, i, s, launch_frame_counts(in.act, B, (int)Ns, nullptr, 0, st, st + 2, s));
+                break;
+            }
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             zero_row(l.b_rows, l.C);
@@ -1148,6 +1196,10 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 double b = 0;
                 if (r.cls == KC_ACCUM)
                     b = 4.0 * Bc * (F + 1) * Nout * C + 4.0 * Bc * Nout * C + eb * rin[r.layer] * C + 4.0 * Bc * Nin;
+                else if (l.fused_relu >= 0)   // ReLU + pool pass: conv rows in, x0 of the touched conv
+                    // pixels, pool rows out; the ReLU rows never leave the chip
+                    b = eb * ((double)rin[l.fused_relu] + (double)rout[r.layer]) * C + 4.0 * tch[l.fused_relu] * C +
+                        12.0 * tch[l.fused_relu] + 4.0 * Bc * (2 * Nin + Nout);
                 else
                     b = eb * ((double)rin[r.layer] + (double)rout[r.layer]) * C + 4.0 * tch[r.layer] * C +
                         12.0 * tch[r.layer] + 4.0 * Bc * (Nin + Nout);

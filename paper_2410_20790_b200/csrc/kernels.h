@@ -118,6 +118,15 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
 void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
                          cudaStream_t s);
+// ReLU site + maxpool site in one tile-resident pass (ReLU output consumed
+// only by the pool): conv = the conv's delta tensor, x0_conv its dense
+// pre-activation; (t_slot, t_pbase) = dilation of conv.act (row capacity of
+// the pool); writes the ReLU mask words r_act (+ its rows into r_rows at the
+// conv slots when r_rows != nullptr) and the pool's act / rows.
+bool site_relu_maxpool_fusable(const Geo &g, bool bf);
+void launch_site_relu_maxpool(DView conv, const float *x0_conv, int B, const Geo &g, const float *theta_r,
+                              const float *theta, bool bf, const uint32_t *t_slot, const int32_t *t_pbase,
+                              uint32_t *r_act, void *r_rows, uint32_t *out_act, void *out_rows, cudaStream_t s);
 // residual add: out slot layout = act_a | act_b (already scanned into pbase)
 void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C, bool bf,
                      void *out_rows, cudaStream_t s);

@@ -434,20 +434,39 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
 // touched output re-evaluates its window max (R7).  Per-pixel
 // arithmetic is identical to k_site_maxpool (x_acc += Delta in frame order,
 // max over the valid window, c = max - y_acc), so FP32 mode stays bit-exact.
+//
+// FUSE: the ReLU site that feeds the pool runs in the same pass (ReLU ->
+// maxpool with the ReLU output consumed only by the pool).  `in` is then the
+// CONV delta tensor and x0 the conv's dense pre-activation; each unit keeps
+// the ReLU x_acc in registers and the ReLU y_acc -- which is, bit for bit,
+// the pool's x_acc (both start from relu(x0) and advance by the same emitted
+// values) -- in shared memory.  Per frame a unit runs the pointwise site
+// step of k_site_pw (x += Delta; c = relu(x) - y; emit iff max_c |c| > theta_r;
+// y += rnd(c)), records the emission in a per-pixel word, and the pool's
+// touched set is the window-OR of those words (the footprint dilation of the
+// ReLU's emitted mask, R7).  The pool's row layout (t_slot, t_pbase) is the
+// dilation of the CONV mask, a superset of the touched frames (rows of
+// untouched frames stay unused).  The ReLU delta rows never go to HBM
+// (written only when r_rows != nullptr, debug); its mask words are written
+// for the statistics.  Requires every ReLU pixel to lie in some window.
 constexpr int MP_NS = 4;    // frame stages in flight
 constexpr int MP_KU = 4;    // units per thread (footprint pixels x G <= 1024)
 
-template <int G, int CPL, int OPT, class T>
+template <int G, int CPL, int OPT, class T, bool FUSE>
 __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *__restrict__ x0, int B, Geo g,
                                                         int TOH, int TOW, const float *__restrict__ theta_p,
                                                         const uint32_t *__restrict__ t_slot,
                                                         const int32_t *__restrict__ t_pbase,
-                                                        uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+                                                        uint32_t *__restrict__ out_act, T *__restrict__ out_rows,
+                                                        const float *__restrict__ theta_rp, uint32_t *__restrict__ r_act,
+                                                        T *__restrict__ r_rows) {
     constexpr int NGR = 256 / G;                          // output groups per CTA
     constexpr int PIECES = CPL * (int)sizeof(T) / 16;     // 16-byte pieces per unit
+    constexpr int XR = FUSE ? MP_KU : 1;                  // ReLU x_acc register rows
     extern __shared__ __align__(16) unsigned char smem_mp[];
     const int C = G * CPL;
     const float theta = __ldg(theta_p);
+    const float theta_r = FUSE ? __ldg(theta_rp) : 0.0f;
     const int tid = threadIdx.x, lane = tid & (G - 1), gr = tid / G;
     const unsigned gmask = group_mask<G>();
     const int Nin = g.Hin * g.Win, No = g.Hout * g.Wout;
@@ -460,11 +479,15 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
     float *xs = reinterpret_cast<float *>(smem_mp);
     T *stg = reinterpret_cast<T *>(xs + (size_t)FP * C);                // [MP_NS][ku][256][CPL]
     uint32_t *u_word = reinterpret_cast<uint32_t *>(stg + (size_t)MP_NS * ((FP * G + 255) / 256) * 256 * CPL);
+    uint32_t *r_em = u_word + 4;                                         // FUSE: [FP] ReLU emitted words
     const T *rows = static_cast<const T *>(in.rows);
     if (tid == 0) *u_word = 0u;
+    if (FUSE)
+        for (int p = tid; p < FP; p += 256) r_em[p] = 0u;
     // ---- this thread's units: metadata in registers, x0 into x_acc (-inf outside the map, R11)
-    uint32_t u_act[MP_KU], u_sl[MP_KU];
+    uint32_t u_act[MP_KU], u_sl[MP_KU], r_emit[MP_KU];
     int u_r1[MP_KU], u_off[MP_KU];
+    float xr[XR][CPL];
     uint32_t uw = 0;
 #pragma unroll
     for (int k = 0; k < MP_KU; k++) {
@@ -473,6 +496,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
         u_act[k] = 0;
         u_sl[k] = 0;
         u_r1[k] = 0;
+        r_emit[k] = 0;
         u_off[k] = p * C + l * CPL;
         if (p < FP) {
             const int iy = fy0 + p / FW, ix = fx0 + p % FW;
@@ -485,6 +509,13 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
                     u_r1[k] = 1 + __ldg(in.pbase + gp);
                 }
                 RowIO<float, CPL>::load(x0 + gp * C + l * CPL, v);
+                if constexpr (FUSE) {
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        xr[k][i] = v[i];
+                        v[i] = relu_f(v[i]);   // y0 of the ReLU = x0 of the pool
+                    }
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < CPL; i++) v[i] = -CUDART_INF_F;
@@ -570,23 +601,62 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         asm volatile("cp.async.wait_group %0;" ::"n"(MP_NS - 1) : "memory");
-        // (a) x_acc += Delta_t at this thread's active units (own staged pieces)
         const int st = it % MP_NS;
+        if constexpr (FUSE) {
+            // (a') ReLU site step at this thread's active units (pixel-uniform branch)
 #pragma unroll
-        for (int k = 0; k < MP_KU; k++)
-            if ((u_act[k] >> t1) & 1u) {
-                float v[CPL], w[CPL];
-                RowIO<T, CPL>::load(stg + ((size_t)(st * ku + k) * 256 + tid) * CPL, v);
-                RowIO<float, CPL>::load(xs + u_off[k], w);
+            for (int k = 0; k < MP_KU; k++)
+                if ((u_act[k] >> t1) & 1u) {
+                    float v[CPL], y[CPL], cand[CPL];
+                    RowIO<T, CPL>::load(stg + ((size_t)(st * ku + k) * 256 + tid) * CPL, v);
+                    RowIO<float, CPL>::load(xs + u_off[k], y);
+                    float mx = 0.0f;
 #pragma unroll
-                for (int i = 0; i < CPL; i++) w[i] = __fadd_rn(w[i], v[i]);
-                RowIO<float, CPL>::store(xs + u_off[k], w);
-            }
+                    for (int i = 0; i < CPL; i++) {
+                        xr[k][i] = __fadd_rn(xr[k][i], v[i]);
+                        cand[i] = __fsub_rn(relu_f(xr[k][i]), y[i]);
+                        mx = fmaxf(mx, fabsf(cand[i]));
+                    }
+                    mx = gmax<G>(mx, gmask);
+                    if (mx > theta_r) {
+#pragma unroll
+                        for (int i = 0; i < CPL; i++) {
+                            cand[i] = rnd<T>(cand[i]);
+                            y[i] = __fadd_rn(y[i], cand[i]);
+                        }
+                        RowIO<float, CPL>::store(xs + u_off[k], y);
+                        r_emit[k] |= 1u << t1;
+                        if ((tid & (G - 1)) == 0) r_em[(tid + k * 256) / G] |= 1u << t1;
+                        if (r_rows) {
+                            const int row = u_r1[k] + __popc(u_sl[k] & lowmask(t1));
+                            RowIO<T, CPL>::store(r_rows + (int64_t)row * C + (u_off[k] % C), cand);
+                        }
+                    }
+                }
+        } else {
+            // (a) x_acc += Delta_t at this thread's active units (own staged pieces)
+#pragma unroll
+            for (int k = 0; k < MP_KU; k++)
+                if ((u_act[k] >> t1) & 1u) {
+                    float v[CPL], w[CPL];
+                    RowIO<T, CPL>::load(stg + ((size_t)(st * ku + k) * 256 + tid) * CPL, v);
+                    RowIO<float, CPL>::load(xs + u_off[k], w);
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) w[i] = __fadd_rn(w[i], v[i]);
+                    RowIO<float, CPL>::store(xs + u_off[k], w);
+                }
+        }
         __syncthreads();
         // (b) touched outputs: candidate = window max - y_acc, truncation
 #pragma unroll
         for (int j = 0; j < OPT; j++) {
             if (!((Tw[j] >> t1) & 1u)) continue;   // group-uniform
+            if constexpr (FUSE) {   // touched iff some window pixel's ReLU emitted at t1
+                uint32_t tch = 0;
+                for (int dy = 0; dy < g.kh; dy++)
+                    for (int dx = 0; dx < g.kw; dx++) tch |= r_em[wo[j] + dy * FW + dx];
+                if (!((tch >> t1) & 1u)) continue;
+            }
             float m[CPL];
 #pragma unroll
             for (int i = 0; i < CPL; i++) m[i] = -CUDART_INF_F;
@@ -623,12 +693,23 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
 #pragma unroll
     for (int j = 0; j < OPT; j++)
         if (ob[j] >= 0 && lane == 0) out_act[ob[j]] = emit[j];
+    if constexpr (FUSE) {   // ReLU mask words of the footprint (halo pixels: identical duplicate writes)
+#pragma unroll
+        for (int k = 0; k < MP_KU; k++) {
+            const int u = tid + k * 256;
+            const int p = u / G;
+            if (p >= FP || (u & (G - 1))) continue;
+            const int iy = fy0 + p / FW, ix = fx0 + p % FW;
+            if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) r_act[(int64_t)b * Nin + iy * g.Win + ix] = r_emit[k];
+        }
+    }
 }
 
 // output tile for the tile-resident maxpool: the most outputs per CTA whose
 // input footprint's fp32 x_acc fits in 64 KiB
 static size_t mp_smem(int FP, int C, int G, int esz) {
-    return (size_t)FP * C * 4 + (size_t)MP_NS * ((FP * G + 255) / 256) * 256 * (C / G) * esz + 16;
+    // x_acc rows | cp.async frame ring | u_word (+pad) | FUSE: per-pixel ReLU emitted words
+    return (size_t)FP * C * 4 + (size_t)MP_NS * ((FP * G + 255) / 256) * 256 * (C / G) * esz + 16 + (size_t)FP * 4;
 }
 static bool mp_tile(const Geo &g, int C, int G, int esz, int max_out, int &TOH, int &TOW) {
     int fp_max = std::min(16384 / C, 256 * MP_KU / G);
@@ -649,37 +730,73 @@ static bool mp_tile(const Geo &g, int C, int G, int esz, int max_out, int &TOH, 
     return best > 0;
 }
 
+constexpr int MP_OPT = 2;   // outputs per lane group
+struct MpPlan {
+    int TG = 0, TCPL = 0, TOH = 0, TOW = 0;
+};
+// tile-resident kernel when C = G * CPL (G a power of two <= 32, CPL 8 or 16)
+static bool mp_plan(const Geo &g, bool bf, MpPlan &pl) {
+    const int C = g.Cin;
+    if (C % 8 != 0 || C < 16) return false;
+    const int cpl = std::max(8, C / 32), gg = C / cpl;
+    if (gg * cpl != C || (gg & (gg - 1)) != 0 || (cpl != 8 && cpl != 16)) return false;
+    pl.TG = gg;
+    pl.TCPL = cpl;
+    return mp_tile(g, C, gg, bf ? 2 : 4, MP_OPT * (256 / gg), pl.TOH, pl.TOW);
+}
+
+bool site_relu_maxpool_fusable(const Geo &g, bool bf) {
+    MpPlan pl;
+    if (!mp_plan(g, bf, pl)) return false;
+    // every input pixel inside some window (the fused pass runs the ReLU site
+    // only on window footprints): no gaps between windows, last window reaches the edge
+    auto covers = [](int in, int out, int k, int st, int pd) { return st <= k && (out - 1) * st - pd + k >= in; };
+    return covers(g.Hin, g.Hout, g.kh, g.sh, g.ph) && covers(g.Win, g.Wout, g.kw, g.sw, g.pw);
+}
+
+template <bool FUSE>
+static bool launch_mp_tile(const MpPlan &pl, DView in, const float *x0, int B, const Geo &g, const float *theta,
+                           bool bf, const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
+                           const float *theta_r, uint32_t *r_act, void *r_rows, cudaStream_t s) {
+    const int C = g.Cin, TG = pl.TG, TCPL = pl.TCPL, TOH = pl.TOH, TOW = pl.TOW;
+    const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
+    const size_t sm = mp_smem(FP, C, TG, bf ? 2 : 4);
+    const int64_t tiles = (int64_t)B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW);
+#define L_MPT(G_, CPL_)                                                                                      \
+    {                                                                                                        \
+        auto kf = k_site_maxpool_t<G_, CPL_, MP_OPT, T, FUSE>;                                               \
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                      \
+        kf<<<(unsigned)tiles, 256, sm, s>>>(in, x0, B, g, TOH, TOW, theta, t_slot, t_pbase, out_act,         \
+                                            static_cast<T *>(out_rows), theta_r, r_act,                      \
+                                            static_cast<T *>(r_rows));                                       \
+    }
+#define L_MPT_C(...)                                                                                         \
+    if (TG == 2) L_MPT(2, 8) else if (TG == 4) L_MPT(4, 8) else if (TG == 8) L_MPT(8, 8)                     \
+    else if (TG == 16) L_MPT(16, 8) else if (TCPL == 8) L_MPT(32, 8) else L_MPT(32, 16)
+    ST_ROW_DISPATCH(bf, L_MPT_C());
+#undef L_MPT_C
+#undef L_MPT
+    return true;
+}
+
+void launch_site_relu_maxpool(DView conv, const float *x0_conv, int B, const Geo &g, const float *theta_r,
+                              const float *theta, bool bf, const uint32_t *t_slot, const int32_t *t_pbase,
+                              uint32_t *r_act, void *r_rows, uint32_t *out_act, void *out_rows, cudaStream_t s) {
+    MpPlan pl;
+    if (!mp_plan(g, bf, pl)) return;   // callers check site_relu_maxpool_fusable first
+    launch_mp_tile<true>(pl, conv, x0_conv, B, g, theta, bf, t_slot, t_pbase, out_act, out_rows, theta_r, r_act,
+                         r_rows, s);
+}
+
 void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
                          cudaStream_t s) {
     const int64_t BN = (int64_t)B * g.Hout * g.Wout;
     const int kk = g.kh * g.kw;
-    const int C = g.Cin;
-    // tile-resident kernel when C = G * CPL (G a power of two <= 32, 8 | CPL)
-    int TG = 0, TCPL = 0;
-    if (C % 8 == 0 && C >= 16) {
-        const int cpl = std::max(8, C / 32), gg = C / cpl;
-        if (gg * cpl == C && (gg & (gg - 1)) == 0 && (cpl == 8 || cpl == 16)) { TG = gg; TCPL = cpl; }
-    }
-    constexpr int OPT = 2;
-    int TOH = 0, TOW = 0;
-    if (TG && mp_tile(g, C, TG, bf ? 2 : 4, OPT * (256 / TG), TOH, TOW)) {
-        const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
-        const size_t sm = mp_smem(FP, C, TG, bf ? 2 : 4);
-        const int64_t tiles = (int64_t)B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW);
-#define L_MPT(G_, CPL_)                                                                                      \
-    {                                                                                                        \
-        auto kf = k_site_maxpool_t<G_, CPL_, OPT, T>;                                                        \
-        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                      \
-        kf<<<(unsigned)tiles, 256, sm, s>>>(in, x0, B, g, TOH, TOW, theta, t_slot, t_pbase, out_act,         \
-                                            static_cast<T *>(out_rows));                                     \
-    }
-#define L_MPT_C(...)                                                                                         \
-    if (TG == 2) L_MPT(2, 8) else if (TG == 4) L_MPT(4, 8) else if (TG == 8) L_MPT(8, 8)                     \
-    else if (TG == 16) L_MPT(16, 8) else if (TCPL == 8) L_MPT(32, 8) else L_MPT(32, 16)
-        ST_ROW_DISPATCH(bf, L_MPT_C());
-#undef L_MPT_C
-#undef L_MPT
+    MpPlan pl;
+    if (mp_plan(g, bf, pl)) {
+        launch_mp_tile<false>(pl, in, x0, B, g, theta, bf, t_slot, t_pbase, out_act, out_rows, nullptr, nullptr,
+                              nullptr, s);
         return;
     }
 #define L_MP(G_, CPL_)                                                                                       \

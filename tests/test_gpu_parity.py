@@ -193,3 +193,61 @@ def test_errors_and_state():
     with pytest.raises(StError):            # negative threshold
         enc.encode_diff(fr, -1.0)
     enc.encode_diff(fr, 0.05)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("model", ["crnn", "resnet18"])
+def test_fused_relu_maxpool_matches_unfused(precision, model, monkeypatch):
+    """The ReLU -> maxpool pass (one tile-resident kernel, ReLU rows kept on
+    chip) gives bit-identical tap outputs and per-site counts to the separate
+    ReLU and maxpool site kernels (ST_NO_FUSE=1), in both modes."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    if model == "crnn":
+        cfg = W.get_config(2)
+        net = cfg.build_net()
+        fr_np = make_frames(cfg, 3, L=10)
+    else:
+        net = W.models.resnet18(72, 104)
+        init_weights(net, 12)
+        fr_np = W.to_float(W.gen_video(2, 9, 72, 104, 3, 78, n_objects=4, size=(8, 24), speed=(1, 3),
+                                       noise_q=0.1, noise_amp=2))
+    fr = torch.from_numpy(fr_np).cuda()
+    outs = {}
+    for mode in ("fused", "separate"):
+        if mode == "separate":
+            monkeypatch.setenv("ST_NO_FUSE", "1")
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.05, 0.0, 0.1):
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs[mode] = res
+        enc.close()
+    for (og, cg), (oe, ce) in zip(outs["fused"], outs["separate"]):
+        assert np.array_equal(cg, ce)
+        for a, b in zip(og, oe):
+            assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("C,k,s,p,h,w", [(16, 2, 2, 0, 20, 36), (32, 3, 2, 1, 23, 41), (64, 2, 1, 0, 9, 30),
+                                         (16, 3, 1, 1, 17, 17), (128, 2, 2, 0, 13, 21), (32, 3, 3, 0, 19, 26)])
+def test_relu_maxpool_geometries_exact(C, k, s, p, h, w):
+    """conv -> ReLU -> maxpool at tile-kernel widths over pool geometries with
+    and without full window coverage (odd maps, k < s gaps): FP32 bit-exact
+    against the oracle, fused or not."""
+    net = Net(3, h, w)
+    c1 = net.conv(-1, C, 3, 1, 1)
+    r1 = net.relu(c1)
+    mp = net.maxpool(r1, k, s, p)
+    c2 = net.conv(mp, 8, 3, 1, 1)
+    net.output(net.relu(c2))
+    init_weights(net, 100 + C + k)
+    fr = np.stack([random_frames(C + b, 6, h, w, 3) for b in range(2)])
+    for th in (0.0, 0.04):
+        enc, _ = gpu_run(net, fr, th)
+        for b in range(2):
+            compare_chunk(enc, net, fr[b], th, b)
+        enc.close()
