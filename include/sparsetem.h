@@ -85,6 +85,16 @@ typedef struct {
     int32_t precision;           /* st_precision                                  */
     int32_t device;              /* CUDA device ordinal                           */
     int32_t debug_retain;        /* 1: keep every layer's buffers for st_debug_*  */
+    int32_t streaming;           /* 1: streaming continuation:  *
+                                  * the per-site caches of the vanilla DeltaCNN   *
+                                  * schedule -- S, each site's x_acc /    *
+                                  * y_acc, each tap's last output -- are kept in  *
+                                  * persistent device buffers, so st_encode_diff  *
+                                  * called again without st_encode_reference      *
+                                  * continues every chunk from its last frame     *
+                                  * (chunks longer than max_frames, live video).  *
+                                  * Memory: those caches (st_memory_report).      *
+                                  * ST_ERR_UNSUPPORTED with SE layers.            */
 } st_encoder_config;
 
 /* Validate specs, infer shapes, number the sites, repack weights, plan the
@@ -106,7 +116,11 @@ st_status st_encode_reference(st_encoder *enc, const float *ref_dev, int32_t n_c
                               int64_t chunk_stride, void *stream);
 
 /* One SparseBatch pass over n_diff diff frames of every staged
- * chunk.  frames_dev: chunk c, diff frame t (1..n_diff) at frames_dev +
+ * chunk.  With cfg.streaming, a call after a previous st_encode_diff (no
+ * st_encode_reference in between) continues each chunk: its frame 0 is the
+ * previous call's last frame (state and outputs), the dense reference pass
+ * is skipped, and the results equal one call over all frames of the chunk.
+ * frames_dev: chunk c, diff frame t (1..n_diff) at frames_dev +
  * c*chunk_stride + (t-1)*H*W*C (chunk_stride 0 = packed n_diff*H*W*C).
  * thresholds: host [n_sites] fp32 truncation thresholds, constant for the
  * call (R15).  n_diff = 0 runs the dense pass only.  Errors: ST_ERR_STATE

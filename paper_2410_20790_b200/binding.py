@@ -34,7 +34,7 @@ class st_layer_spec(C.Structure):
 
 class st_encoder_config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("in_c", "in_h", "in_w", "max_chunks", "max_frames", "precision",
-                                         "device", "debug_retain")]
+                                         "device", "debug_retain", "streaming")]
 
 
 class st_ctl_config(C.Structure):
@@ -118,7 +118,8 @@ def _stream_handle(stream):
 class Encoder:
     """One encoder = one network on one device (st_encoder_create)."""
 
-    def __init__(self, net, max_chunks, max_frames, precision="fp32", device=0, debug_retain=False):
+    def __init__(self, net, max_chunks, max_frames, precision="fp32", device=0, debug_retain=False,
+                 streaming=False):
         L = lib()
         self.net = net
         self.n_layers = len(net.layers)
@@ -135,7 +136,7 @@ class Encoder:
                     keep.append(a)
                     setattr(s, f, a.ctypes.data_as(C.POINTER(C.c_float)))
         cfg = st_encoder_config(net.in_c, net.in_h, net.in_w, max_chunks, max_frames, PRECISION[precision],
-                                device, int(bool(debug_retain)))
+                                device, int(bool(debug_retain)), int(bool(streaming)))
         h = C.c_void_p()
         r = L.st_encoder_create(C.byref(cfg), C.cast(arr, C.c_void_p), self.n_layers, C.byref(h))
         if r != 0:

@@ -54,6 +54,10 @@ struct LayerRT {
     int n_consumers = 0, last_consumer = 0;
     int fused_pool = -1;      // ReLU: the maxpool that runs this site in its own pass
     int fused_relu = -1;      // MAXPOOL: the ReLU site folded into this layer's pass
+    // streaming state (N1, persistent): pointwise site sx[0]/sy[0] in place;
+    // maxpool sx[0..1] ping-pong x_acc + spy y_acc; fused pool (on the pool
+    // layer) sx[0..1] ReLU x_acc, sy[0..1] ReLU y_acc, spy pool y_acc; OUTPUT sx[0]
+    int sx[2] = {-1, -1}, sy[2] = {-1, -1}, spy = -1;
     // device weights (separate allocation)
     float *wk = nullptr, *bias = nullptr;
     uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
@@ -76,8 +80,10 @@ struct GraphKey {
     const float *frames;
     int64_t stride;
     int n_diff, chunks;
+    int smode;   // streaming: 0 off / first call after a reference, 1 + ping-pong parity on continuations
     bool operator==(const GraphKey &o) const {
-        return frames == o.frames && stride == o.stride && n_diff == o.n_diff && chunks == o.chunks;
+        return frames == o.frames && stride == o.stride && n_diff == o.n_diff && chunks == o.chunks &&
+               smode == o.smode;
     }
 };
 struct GraphEnt {
@@ -128,6 +134,11 @@ struct st_encoder {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // state
     int staged_chunks = 0;       // >0 after encode_reference
+    // streaming continuation (N1): cont = the chunks already ran a diff call
+    // since their reference; par = ping-pong parity of the shared-halo states
+    bool cont = false;
+    int par = 0;
+    int in_S = -1;               // Subtraction buffer S [B][N][C] (streaming)
     int last_chunks = 0, last_ndiff = -1;
     cudaStream_t last_stream = nullptr;
     std::string err;
@@ -286,6 +297,9 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             }
         }
     }
+    if (cfg->streaming)
+        for (auto &l : e->L)
+            if (l.kind == ST_SE) return ST_ERR_UNSUPPORTED;   // SE gate schedule spans the call (R8)
     // ReLU -> maxpool pairs run as one tile-resident pass (the ReLU output is
     // read only by the pool, its input is a conv tensor, windows cover the map)
     {
@@ -513,6 +527,26 @@ static st_status plan(st_encoder *e) {
             break;
         }
     }
+    // streaming state (N1): the vanilla schedule's persistent caches
+    if (e->cfg.streaming) {
+        e->in_S = add(B * Nin * e->in_C * 4, 0, END);
+        for (int i = 0; i < n; i++) {
+            LayerRT &l = e->L[i];
+            const int64_t No = (int64_t)l.H * l.W * l.C;
+            const int64_t Ni = l.src < 0 ? Nin * e->in_C : (int64_t)e->L[l.src].H * e->L[l.src].W * e->L[l.src].C;
+            if (l.kind == ST_OUTPUT) {
+                l.sx[0] = add(B * No * 4, 0, END);
+            } else if ((l.kind == ST_RELU || l.kind == ST_SILU) && l.fused_pool < 0) {
+                l.sx[0] = add(B * No * 4, 0, END);
+                l.sy[0] = add(B * No * 4, 0, END);
+            } else if (l.kind == ST_MAXPOOL) {
+                for (int k = 0; k < 2; k++) l.sx[k] = add(B * Ni * 4, 0, END);
+                if (l.fused_relu >= 0)
+                    for (int k = 0; k < 2; k++) l.sy[k] = add(B * Ni * 4, 0, END);
+                l.spy = add(B * No * 4, 0, END);
+            }
+        }
+    }
     // a fused ReLU -> maxpool pass reads the conv's dense pre-activation (the
     // ReLU's x0) at the pool's step time
     for (int i = 0; i < n; i++)
@@ -637,6 +671,8 @@ extern "C" st_status st_encode_reference(st_encoder *e, const float *ref_dev, in
     CUDA_OK(e, cudaSetDevice(e->cfg.device));
     CUDA_OK(e, cudaMemcpy2DAsync(e->ref, per * 4, ref_dev, stride * 4, per * 4, n_chunks, cudaMemcpyDeviceToDevice, s));
     e->staged_chunks = n_chunks;
+    e->cont = false;
+    e->par = 0;
     return ST_OK;
 }
 
@@ -715,7 +751,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
         st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
         if (r) return r;
     } else {
-        GraphKey key{frames_dev, fstride, n_diff, e->staged_chunks};
+        GraphKey key{frames_dev, fstride, n_diff, e->staged_chunks, e->cont ? 1 + e->par : 0};
         GraphEnt *ent = nullptr;
         for (auto &g : e->graphs)
             if (g.key == key) ent = &g;
@@ -748,6 +784,10 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
     }
     CUDA_OK(e, cudaEventRecord(e->thr_ev, s));
     e->thr_pending = true;
+    if (e->cfg.streaming) {   // the chunks continue from the saved state next call
+        e->cont = true;
+        e->par ^= 1;
+    }
     CUDA_OK(e, cudaGetLastError());
     return ST_OK;
 }
@@ -768,6 +808,15 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         if (buf >= 0) cudaMemsetAsync(e->ptr(buf), 0, (size_t)C * e->esz, s);
     };
     const bool bf = e->bf;
+    // streaming (N1): on a continuation the dense reference pass is skipped and
+    // every site starts from its saved state; par selects the ping-pong halves
+    const bool strm = e->cfg.streaming != 0, cont = strm && e->cont;
+    const int par = e->par;
+    auto fcopy = [&](int dst_buf, const float *src, int64_t n_floats) {
+        cudaMemcpyAsync(e->ptr(dst_buf), src, (size_t)n_floats * 4, cudaMemcpyDeviceToDevice, s);
+    };
+    const float *S0 = cont ? e->p<float>(e->in_S) : e->ref;   // Subtraction buffer at call start
+    if (strm && !cont) fcopy(e->in_S, e->ref, B * per);
 
     // ---------------- input site: Subtraction + truncation + compaction (a2)
     if (F > 0) {
@@ -776,18 +825,19 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         void *rows = e->ptr(e->in_rows);
         const float *fr = frames_dev;
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_mask(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act,
+               launch_subtract_mask(S0, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act,
                                     e->in_dd >= 0 ? e->ptr(e->in_dd) : nullptr, s));
         LAUNCH(e, KC_SCAN, -1, s,
                launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
         zero_row(e->in_rows, e->in_C);
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_rows(e->ref, per, fr, fstride, B, (int)Nin, e->in_C, act, pb, rows, bf, s));
+               launch_subtract_rows(S0, per, fr, fstride, B, (int)Nin, e->in_C, act, pb, rows, bf,
+                                    strm ? e->p<float>(e->in_S) : nullptr, s));
         LAUNCH(e, KC_COUNTS, -1, s,
                launch_frame_counts(act, B, (int)Nin, e->counts, cstride, e->site_sum, nullptr, s));
     }
 
-    if (e->in_refbf >= 0)
+    if (e->in_refbf >= 0 && !cont)
         LAUNCH(e, KC_DENSE_MISC, -1, s, launch_pad4_bf16(e->ref, (int64_t)B * Nin, e->in_C, e->ptr(e->in_refbf), s));
     // ---------------- layers in topological order, dense then diff ("N")
     for (int i = 0; i < n; i++) {
@@ -815,12 +865,13 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             c.wk = l.wk;
             c.bias = l.bias;
             c.out = e->p<float>(l.b_y0);
-            LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
-                   l.depthwise  ? launch_dwconv_f32(c, s)
-                   : l.tc       ? launch_conv_tc(c, l.tmap, s)
-                   : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
-                                : launch_conv_f32(c, s));
-            if (l.b_ybf >= 0)
+            if (!cont)
+                LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
+                       l.depthwise  ? launch_dwconv_f32(c, s)
+                       : l.tc       ? launch_conv_tc(c, l.tmap, s)
+                       : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
+                                    : launch_conv_f32(c, s));
+            if (l.b_ybf >= 0 && !cont)
                 LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
             if (F == 0) break;
             uint32_t *act = e->p<uint32_t>(l.b_act);
@@ -852,22 +903,61 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             const int act_kind = l.kind == ST_RELU ? ACT_RELU : ACT_SILU;
             // the dense reference activation uses the same SiLU form as the site (fast in BF16 mode)
             const int dense_kind = (act_kind == ACT_SILU && bf) ? ACT_SILU_FAST : act_kind;
-            LAUNCH(e, KC_DENSE_MISC, i, s,
-                   launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
+            if (!cont)
+                LAUNCH(e, KC_DENSE_MISC, i, s,
+                       launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
+            SiteState sst;
+            const float *x_init = x_src;
+            if (strm && l.sx[0] >= 0) {   // in-place state; first call: from the dense reference pass
+                if (!cont) {
+                    fcopy(l.sx[0], x_src, B * N * l.C);
+                    fcopy(l.sy[0], e->p<float>(l.b_y0), B * N * l.C);
+                }
+                x_init = e->p<float>(l.sx[0]);
+                sst.y_init = e->p<float>(l.sy[0]);
+                sst.x_save = e->p<float>(l.sx[0]);
+                sst.y_save = e->p<float>(l.sy[0]);
+            }
             if (F == 0) break;
             DView me = view_of(e, i);
             if (l.b_rows >= 0) zero_row(l.b_rows, l.C);   // own buffer (not in place)
             if (l.fused_pool >= 0) break;                 // runs inside the pool's pass
             LAUNCH(e, KC_SITE_PW, i, s,
-                   launch_site_pointwise(in, x_src, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
-                                         e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), s));
+                   launch_site_pointwise(in, x_init, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
+                                         e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), sst, s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
             break;
         }
         case ST_MAXPOOL: {
-            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_maxpool(x_src, e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), s));
+            if (!cont)
+                LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_maxpool(x_src, e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), s));
+            // streaming state: x_acc of the input pixels ping-pongs (windows of
+            // neighbouring tiles share pixels), y_acc of the outputs in place
+            SiteState sst;
+            const float *x_init = x_src;
+            const int64_t NiC = Ns * Cs;
+            if (strm) {
+                if (!cont) fcopy(l.spy, e->p<float>(l.b_y0), B * N * l.C);
+                sst.y_init = e->p<float>(l.spy);
+                sst.y_save = e->p<float>(l.spy);
+                if (l.fused_relu >= 0) {
+                    const LayerRT &r = e->L[l.fused_relu];
+                    x_init = cont ? e->p<float>(l.sx[par]) : dense_of(e, r.src);
+                    sst.ry_init = cont ? e->p<float>(l.sy[par]) : e->p<float>(r.b_y0);
+                    sst.rx_save = e->p<float>(l.sx[par ^ 1]);
+                    sst.ry_save = e->p<float>(l.sy[par ^ 1]);
+                    if (F == 0) {   // the pass writes every footprint pixel; without it, carry over
+                        fcopy(l.sx[par ^ 1], x_init, B * NiC);
+                        fcopy(l.sy[par ^ 1], sst.ry_init, B * NiC);
+                    }
+                } else {
+                    x_init = cont ? e->p<float>(l.sx[par]) : x_src;
+                    fcopy(l.sx[par ^ 1], x_init, B * NiC);   // the kernels save changed pixels only
+                    sst.x_save = e->p<float>(l.sx[par ^ 1]);
+                }
+            }
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -880,10 +970,10 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
                 LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
                 zero_row(l.b_rows, l.C);
                 LAUNCH(e, KC_SITE_MP, i, s,
-                       launch_site_relu_maxpool(cv, dense_of(e, r.src), B, l.geo, thresholds + r.site,
+                       launch_site_relu_maxpool(cv, strm ? x_init : dense_of(e, r.src), B, l.geo, thresholds + r.site,
                                                 thresholds + l.site, bf, slot, pb, e->p<uint32_t>(r.b_act),
                                                 r.b_rows >= 0 ? e->ptr(r.b_rows) : nullptr,
-                                                e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
+                                                e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), sst, s));
                 LAUNCH(e, KC_COUNTS, l.fused_relu, s,
                        launch_frame_counts(e->p<uint32_t>(r.b_act), B, (int)Ns, e->counts + r.site * 32, cstride,
                                            e->site_sum + r.site, nullptr, s));
@@ -898,8 +988,8 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SITE_MP, i, s,
-                   launch_site_maxpool(in, x_src, B, l.geo, thresholds + l.site, bf, slot, pb,
-                                       e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
+                   launch_site_maxpool(in, x_init, B, l.geo, thresholds + l.site, bf, slot, pb,
+                                       e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), sst, s));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
@@ -907,7 +997,9 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         }
         case ST_ADD: {
             const float *x2 = dense_of(e, l.src2);
-            LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, ybf_of(e, i), s));
+            if (!cont)
+                LAUNCH(e, KC_DENSE_MISC, i, s,
+                       launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, ybf_of(e, i), s));
             if (F == 0) break;
             DView in2 = view_of(e, l.src2);
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
@@ -953,8 +1045,10 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         }
         case ST_OUTPUT: {
             DView v = F > 0 ? in : DView{};
+            float *o_state = strm ? e->p<float>(l.sx[0]) : nullptr;   // last output = next call's frame 0
             LAUNCH(e, KC_ACCUM, i, s,
-                   launch_accumulate(v, x_src, B, (int)N, l.C, F, bf, e->p<float>(l.b_out), s));
+                   launch_accumulate(v, cont ? o_state : x_src, B, (int)N, l.C, F, bf, e->p<float>(l.b_out), o_state,
+                                     s));
             break;
         }
         default:

@@ -36,10 +36,13 @@ struct Geo {   // conv / pool geometry
 void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
                           int B, int N, int C, int n_diff, const float *theta, bool bf, uint32_t *act, void *ddelta,
                           cudaStream_t s);
-// Subtraction pass 2: write emitted rows at the slots of `act`.
+// Subtraction pass 2: write emitted rows at the slots of `act`; s_save
+// (streaming, nullable): final S of every pixel with an emission, [B][N][C]
+// (may alias ref when ref_stride == N*C: each pixel is read, then written, by
+// its own thread).
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
                           int B, int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
-                          cudaStream_t s);
+                          float *s_save, cudaStream_t s);
 // out[b][q] = OR of in[b][p] over the receptive field (dense amplification)
 void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaStream_t s);
 // pbase = exclusive prefix of popc(words) over n words; *total = sum; also
@@ -111,13 +114,28 @@ void launch_dense_act(const float *x, float *y, int64_t n, int act, void *ybf, c
 void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s);
 void launch_dense_add(const float *a, const float *b, float *y, int64_t n, void *ybf, cudaStream_t s);
 void launch_to_bf16(const float *x, void *ybf, int64_t n, cudaStream_t s);
+// Streaming state of a site (the per-site caches of the
+// vanilla DeltaCNN schedule, kept so st_encode_diff can continue a
+// chunk).  All pointers nullable (SparseBatch: none).  x0 passed to a site
+// launch is the x_acc at call start (dense reference activation on the
+// first call, the saved state on a continuation); y_init the y_acc at call
+// start (null: derived from x0).  Saves cover every pixel the call changed;
+// the encoder pre-fills save buffers that are not updated in place.
+struct SiteState {
+    const float *y_init = nullptr;   // y_acc at start [B][N_out][C]
+    float *x_save = nullptr;         // x_acc at end [B][N_in][C]
+    float *y_save = nullptr;         // y_acc at end [B][N_out][C]
+    const float *ry_init = nullptr;  // fused ReLU -> pool: ReLU y_acc at start [B][N_in][C]
+    float *rx_save = nullptr;        //                     ReLU x_acc at end
+    float *ry_save = nullptr;        //                     ReLU y_acc at end
+};
 // pointwise site: emitted rows written into out_rows at the input slots
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
-                           uint32_t *out_act, void *out_rows, cudaStream_t s);
+                           uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s);
 // maxpool site: touched layout (t_slot, t_pbase) = dilation of in.act
 void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
-                         cudaStream_t s);
+                         const SiteState &st, cudaStream_t s);
 // ReLU site + maxpool site in one tile-resident pass (ReLU output consumed
 // only by the pool): conv = the conv's delta tensor, x0_conv its dense
 // pre-activation; (t_slot, t_pbase) = dilation of conv.act (row capacity of
@@ -126,7 +144,8 @@ void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const f
 bool site_relu_maxpool_fusable(const Geo &g, bool bf);
 void launch_site_relu_maxpool(DView conv, const float *x0_conv, int B, const Geo &g, const float *theta_r,
                               const float *theta, bool bf, const uint32_t *t_slot, const int32_t *t_pbase,
-                              uint32_t *r_act, void *r_rows, uint32_t *out_act, void *out_rows, cudaStream_t s);
+                              uint32_t *r_act, void *r_rows, uint32_t *out_act, void *out_rows, const SiteState &st,
+                              cudaStream_t s);
 // residual add: out slot layout = act_a | act_b (already scanned into pbase)
 void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbase, int B, int N, int C, bool bf,
                      void *out_rows, cudaStream_t s);
@@ -140,8 +159,10 @@ void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int
 void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s);
 void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, const float *theta, bool bf,
                     const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s);
-// Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0)
+// Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0, the
+// start state [B][N][C]); o_save (streaming, nullable, may alias y0): the
+// last frame's output, the start of the next call
 void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, bool bf, float *out,
-                       cudaStream_t s);
+                       float *o_save, cudaStream_t s);
 
 }  // namespace st

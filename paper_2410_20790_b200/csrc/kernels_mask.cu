@@ -65,7 +65,8 @@ template <int C, class T>
 __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__ ref, int64_t ref_stride,
                                                        const float *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, const uint32_t *__restrict__ act,
-                                                       const int32_t *__restrict__ pbase, T *__restrict__ rows) {
+                                                       const int32_t *__restrict__ pbase, T *__restrict__ rows,
+                                                       float *s_save) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     uint32_t w = act[i];
@@ -89,6 +90,9 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
         }
         o += C;
     }
+    if (s_save)
+#pragma unroll
+        for (int c = 0; c < C; c++) s_save[i * C + c] = S[c];
 }
 
 #define SUB_DISPATCH(C_, KERNEL, ...)                                                    \
@@ -110,10 +114,10 @@ void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *fra
 
 void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
                           int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
-                          cudaStream_t s) {
+                          float *s_save, cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
     ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_rows, ref, ref_stride, frames, fr_stride, B, N, act, pbase,
-                                     static_cast<T *>(rows)));
+                                     static_cast<T *>(rows), s_save));
 }
 
 // --------------------------------------------------------------- dilation

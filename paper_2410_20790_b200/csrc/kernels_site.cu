@@ -141,7 +141,7 @@ void launch_to_bf16(const float *x, void *ybf, int64_t n, cudaStream_t s) {
 template <int G, int CPL, int ACT, class T>
 __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
                                                  const float *__restrict__ theta_p, uint32_t *__restrict__ out_act,
-                                                 T *out_rows) {
+                                                 T *out_rows, SiteState sst) {
     const float theta = __ldg(theta_p);
     constexpr int P = prefetch_depth(CPL);
     const int lane = threadIdx.x & (G - 1);
@@ -184,8 +184,11 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
             if (lane == 0) out_act[bp] = 0;
             continue;
         }
+        if (sst.y_init)   // streaming continuation: the saved y_acc
+            row_load<float, CPL>(sst.y_init + bp * C, c0, C, full, ya);
+        else
 #pragma unroll
-        for (int i = 0; i < CPL; i++) ya[i] = actf<ACT>(xa[i]);
+            for (int i = 0; i < CPL; i++) ya[i] = actf<ACT>(xa[i]);
         uint32_t emit = 0;
         while (a) {
             int t1s[P];
@@ -225,6 +228,10 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
             }
         }
         if (lane == 0) out_act[bp] = emit;
+        if (sst.x_save) {   // streaming: state of a touched pixel (in place)
+            row_store<float, CPL>(sst.x_save + bp * C, c0, C, full, xa);
+            row_store<float, CPL>(sst.y_save + bp * C, c0, C, full, ya);
+        }
     }
 }
 
@@ -278,7 +285,7 @@ static int groups_grid(int64_t n_groups, int G) {
 }
 
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
-                           uint32_t *out_act, void *out_rows, cudaStream_t s) {
+                           uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
 
 #define L_PW(G_, CPL_)                                                                                 \
@@ -286,10 +293,10 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
         const int grid = groups_grid(BN, G_);                                                          \
         if (act == ACT_RELU)                                                                           \
             k_site_pw<G_, CPL_, ACT_RELU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
-                                                                  static_cast<T *>(out_rows));         \
+                                                                  static_cast<T *>(out_rows), st);     \
         else /* SiLU: exact (double exp) in FP32 mode, fast in BF16 mode */                            \
             k_site_pw<G_, CPL_, (sizeof(T) == 4 ? ACT_SILU : ACT_SILU_FAST), T><<<grid, 256, 0, s>>>(  \
-                in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows));                            \
+                in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st);                        \
     }
     ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_PW));
 #undef L_PW
@@ -305,7 +312,8 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
                                                       const float *__restrict__ theta_p,
                                                       const uint32_t *__restrict__ t_slot,
                                                       const int32_t *__restrict__ t_pbase,
-                                                      uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+                                                      uint32_t *__restrict__ out_act, T *__restrict__ out_rows,
+                                                      SiteState sst) {
     const float theta = __ldg(theta_p);
     constexpr int P = CPL <= 2 ? 4 : CPL <= 4 ? 2 : 1;
     const int lane = threadIdx.x & (G - 1);
@@ -360,6 +368,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
                 if ((valid >> w) & 1u) m = xa[w][i] > m ? xa[w][i] : m;
             ya[i] = m;
         }
+        if (sst.y_init) row_load<float, CPL>(sst.y_init + bq * C, c0, C, full, ya);   // streaming continuation
         const int base = 1 + __ldg(t_pbase + bq);
         uint32_t bits = Tw, emit = 0;
         while (bits) {
@@ -417,6 +426,17 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
             }
         }
         if (lane == 0) out_act[bq] = emit;
+        if (sst.x_save) {   // streaming: x_acc of the window pixels that changed (overlapping
+                            // windows write identical values), y_acc of this output
+#pragma unroll
+            for (int w = 0; w < KMAX; w++)
+                if (wa[w]) {
+                    const int dy = w / g.kw, dx = w % g.kw;
+                    const int64_t p = (int64_t)b * Nin + (oy * g.sh - g.ph + dy) * g.Win + ox * g.sw - g.pw + dx;
+                    row_store<float, CPL>(sst.x_save + p * C, c0, C, full, xa[w]);
+                }
+            row_store<float, CPL>(sst.y_save + bq * C, c0, C, full, ya);
+        }
     }
 }
 
@@ -459,7 +479,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
                                                         const int32_t *__restrict__ t_pbase,
                                                         uint32_t *__restrict__ out_act, T *__restrict__ out_rows,
                                                         const float *__restrict__ theta_rp, uint32_t *__restrict__ r_act,
-                                                        T *__restrict__ r_rows) {
+                                                        T *__restrict__ r_rows, SiteState sst) {
     constexpr int NGR = 256 / G;                          // output groups per CTA
     constexpr int PIECES = CPL * (int)sizeof(T) / 16;     // 16-byte pieces per unit
     constexpr int XR = FUSE ? MP_KU : 1;                  // ReLU x_acc register rows
@@ -515,6 +535,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
                         xr[k][i] = v[i];
                         v[i] = relu_f(v[i]);   // y0 of the ReLU = x0 of the pool
                     }
+                    if (sst.ry_init) RowIO<float, CPL>::load(sst.ry_init + gp * C + l * CPL, v);   // continuation
                 }
             } else {
 #pragma unroll
@@ -558,6 +579,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
 #pragma unroll
                     for (int i = 0; i < CPL; i++) ya[j][i] = w[i] > ya[j][i] ? w[i] : ya[j][i];
                 }
+        if (sst.y_init && ob[j] >= 0) RowIO<float, CPL>::load(sst.y_init + ob[j] * C + lane * CPL, ya[j]);
     }
     __syncthreads();   // every window's y_acc taken from x0 before frame 1 updates x_acc
     const uint32_t U = *u_word;
@@ -693,6 +715,30 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
 #pragma unroll
     for (int j = 0; j < OPT; j++)
         if (ob[j] >= 0 && lane == 0) out_act[ob[j]] = emit[j];
+    if (sst.y_save) {   // streaming: pool y_acc of the outputs (in place), x_acc of the footprint
+#pragma unroll
+        for (int j = 0; j < OPT; j++)
+            if (ob[j] >= 0) RowIO<float, CPL>::store(sst.y_save + ob[j] * C + lane * CPL, ya[j]);
+#pragma unroll
+        for (int k = 0; k < MP_KU; k++) {
+            const int u = tid + k * 256;
+            const int p = u / G;
+            if (p >= FP) continue;
+            const int iy = fy0 + p / FW, ix = fx0 + p % FW;
+            if (iy < 0 || iy >= g.Hin || ix < 0 || ix >= g.Win) continue;
+            const int64_t o = ((int64_t)b * Nin + iy * g.Win + ix) * C + (u_off[k] % C);
+            if constexpr (FUSE) {   // every footprint pixel (ping-pong buffers, halo: identical writes)
+                float w[CPL];
+                RowIO<float, CPL>::load(xs + u_off[k], w);
+                RowIO<float, CPL>::store(sst.ry_save + o, w);
+                RowIO<float, CPL>::store(sst.rx_save + o, xr[k]);
+            } else if (u_act[k]) {  // pixels that changed (the rest was pre-copied)
+                float w[CPL];
+                RowIO<float, CPL>::load(xs + u_off[k], w);
+                RowIO<float, CPL>::store(sst.x_save + o, w);
+            }
+        }
+    }
     if constexpr (FUSE) {   // ReLU mask words of the footprint (halo pixels: identical duplicate writes)
 #pragma unroll
         for (int k = 0; k < MP_KU; k++) {
@@ -757,7 +803,8 @@ bool site_relu_maxpool_fusable(const Geo &g, bool bf) {
 template <bool FUSE>
 static bool launch_mp_tile(const MpPlan &pl, DView in, const float *x0, int B, const Geo &g, const float *theta,
                            bool bf, const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
-                           const float *theta_r, uint32_t *r_act, void *r_rows, cudaStream_t s) {
+                           const float *theta_r, uint32_t *r_act, void *r_rows, const SiteState &st,
+                           cudaStream_t s) {
     const int C = g.Cin, TG = pl.TG, TCPL = pl.TCPL, TOH = pl.TOH, TOW = pl.TOW;
     const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
     const size_t sm = mp_smem(FP, C, TG, bf ? 2 : 4);
@@ -768,7 +815,7 @@ static bool launch_mp_tile(const MpPlan &pl, DView in, const float *x0, int B, c
         cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                      \
         kf<<<(unsigned)tiles, 256, sm, s>>>(in, x0, B, g, TOH, TOW, theta, t_slot, t_pbase, out_act,         \
                                             static_cast<T *>(out_rows), theta_r, r_act,                      \
-                                            static_cast<T *>(r_rows));                                       \
+                                            static_cast<T *>(r_rows), st);                                   \
     }
 #define L_MPT_C(...)                                                                                         \
     if (TG == 2) L_MPT(2, 8) else if (TG == 4) L_MPT(4, 8) else if (TG == 8) L_MPT(8, 8)                     \
@@ -781,22 +828,23 @@ static bool launch_mp_tile(const MpPlan &pl, DView in, const float *x0, int B, c
 
 void launch_site_relu_maxpool(DView conv, const float *x0_conv, int B, const Geo &g, const float *theta_r,
                               const float *theta, bool bf, const uint32_t *t_slot, const int32_t *t_pbase,
-                              uint32_t *r_act, void *r_rows, uint32_t *out_act, void *out_rows, cudaStream_t s) {
+                              uint32_t *r_act, void *r_rows, uint32_t *out_act, void *out_rows, const SiteState &st,
+                              cudaStream_t s) {
     MpPlan pl;
     if (!mp_plan(g, bf, pl)) return;   // callers check site_relu_maxpool_fusable first
     launch_mp_tile<true>(pl, conv, x0_conv, B, g, theta, bf, t_slot, t_pbase, out_act, out_rows, theta_r, r_act,
-                         r_rows, s);
+                         r_rows, st, s);
 }
 
 void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
-                         cudaStream_t s) {
+                         const SiteState &st, cudaStream_t s) {
     const int64_t BN = (int64_t)B * g.Hout * g.Wout;
     const int kk = g.kh * g.kw;
     MpPlan pl;
     if (mp_plan(g, bf, pl)) {
         launch_mp_tile<false>(pl, in, x0, B, g, theta, bf, t_slot, t_pbase, out_act, out_rows, nullptr, nullptr,
-                              nullptr, s);
+                              nullptr, st, s);
         return;
     }
 #define L_MP(G_, CPL_)                                                                                       \
@@ -804,10 +852,10 @@ void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const f
         const int grid = groups_grid(BN, G_);                                                                \
         if (kk <= 4)                                                                                         \
             k_site_maxpool<G_, CPL_, 4, T><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase,        \
-                                                                out_act, static_cast<T *>(out_rows));        \
+                                                                out_act, static_cast<T *>(out_rows), st);    \
         else                                                                                                 \
             k_site_maxpool<G_, CPL_, 9, T><<<grid, 256, 0, s>>>(in, x0, B, g, theta, t_slot, t_pbase,        \
-                                                                out_act, static_cast<T *>(out_rows));        \
+                                                                out_act, static_cast<T *>(out_rows), st);    \
     }
     ST_ROW_DISPATCH(bf, SITE_DISPATCH(g.Cin, L_MP));
 #undef L_MP
@@ -862,8 +910,8 @@ void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbas
 // ---------------------------------------------------------- accumulation
 // O_t = O_{t-1} + Delta_t, dense per-frame outputs [B][L][N][C].
 template <int G, int CPL, class T>
-__global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__restrict__ y0, int B, int N, int C,
-                                                    int n_diff, float *__restrict__ out) {
+__global__ void __launch_bounds__(256) k_accumulate(DView in, const float *y0, int B, int N, int C,
+                                                    int n_diff, float *__restrict__ out, float *o_save) {
     const int lane = threadIdx.x & (G - 1);
     const int c0 = lane * CPL;
     const bool full = (C % 8 == 0) && (c0 + CPL <= C);
@@ -892,13 +940,15 @@ __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *__res
             }
             row_store<float, CPL>(o, c0, C, full, O);
         }
+        if (o_save) row_store<float, CPL>(o_save + bq * C, c0, C, full, O);   // streaming: next call's start
     }
 }
 
 void launch_accumulate(DView in, const float *y0, int B, int N, int C, int n_diff, bool bf, float *out,
-                       cudaStream_t s) {
+                       float *o_save, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
-#define L_ACC(G_, CPL_) k_accumulate<G_, CPL_, T><<<groups_grid(BN, G_), 256, 0, s>>>(in, y0, B, N, C, n_diff, out);
+#define L_ACC(G_, CPL_) \
+    k_accumulate<G_, CPL_, T><<<groups_grid(BN, G_), 256, 0, s>>>(in, y0, B, N, C, n_diff, out, o_save);
     ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_ACC));
 #undef L_ACC
 }
