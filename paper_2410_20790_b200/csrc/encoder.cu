@@ -583,6 +583,10 @@ static st_status plan(st_encoder *e) {
     for (auto &l : e->L)
         if (l.b_out >= 0) persistent += e->bufs[l.b_out].bytes;
     persistent += B * Nin * e->in_C * 4;   // staged reference (Subtraction buffer)
+    if (e->in_S >= 0) persistent += e->bufs[e->in_S].bytes;   // streaming caches (N1)
+    for (auto &l : e->L)
+        for (int id : {l.sx[0], l.sx[1], l.sy[0], l.sy[1], l.spy})
+            if (id >= 0) persistent += e->bufs[id].bytes;
     e->persistent_bytes = persistent;
     int64_t peak = 0;
     for (int t = 0; t <= END; t++) {
