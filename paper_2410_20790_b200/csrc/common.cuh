@@ -9,6 +9,17 @@
 
 namespace st {
 
+// Programmatic dependent launch: inside the captured step graph the edges
+// between consecutive kernels are programmatic (encoder.cu), so a kernel's
+// CTAs may be scheduled while its predecessor drains.  Every kernel calls
+// this first: wait until the prerequisite grids have completed and their
+// writes are visible (no global access precedes it), then allow our own
+// dependents to be scheduled.  Both are no-ops in a normal launch.
+__device__ __forceinline__ void st_pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 typedef __nv_bfloat16 bf16;
 
 __device__ __forceinline__ uint32_t lowmask(int t1) { return (1u << t1) - 1u; }

@@ -127,6 +127,7 @@ struct st_encoder {
     bool thr_pending = false;
     // CUDA graphs of whole steps, keyed by (frames, stride, n_diff, chunks)
     bool use_graphs = true;
+    bool use_pdl = false;        // programmatic kernel->kernel edges in captured steps (ST_PDL=1)
     bool dw_rowmajor = false;
     bool prof_trace = false;
     std::vector<GraphEnt> graphs;
@@ -622,6 +623,10 @@ static st_status plan(st_encoder *e) {
     CUDA_OK(e, cudaEventCreateWithFlags(&e->thr_ev, cudaEventDisableTiming));
     const char *ng = getenv("ST_NO_GRAPHS");
     e->use_graphs = !(ng && ng[0] == '1');
+    // programmatic edges measured neutral-to-slower on cfg2/cfg4 (592.9K vs
+    // 582.6K diff-frames/s, profiles/r01i_bench_cfg2_pdl.json): opt-in
+    const char *np = getenv("ST_PDL");
+    e->use_pdl = np && np[0] == '1';
     const char *dr = getenv("ST_DW_ROWMAJOR");   // A/B switch: the M-row depthwise kernel
     e->dw_rowmajor = dr && dr[0] == '1';
     const char *pt = getenv("ST_PROF_TRACE");    // per-launch profile lines on stderr
@@ -725,6 +730,41 @@ static int64_t rows_cap_of(const st_encoder *e, int t) {
     return l.rows_cap;
 }
 
+// Turn every kernel -> kernel edge of a captured step into a programmatic
+// dependency (PDL): the dependent kernel is scheduled while its predecessor
+// drains and blocks in griddepcontrol.wait (st_pdl_enter, the first statement
+// of every kernel) until the predecessor completed and its writes are
+// visible.  Edges touching memset / memcpy nodes stay full dependencies.  On
+// any API failure the graph keeps its plain edges.
+static void make_edges_programmatic(cudaGraph_t g) {
+    size_t ne = 0;
+    if (cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne) != cudaSuccess || ne == 0) {
+        cudaGetLastError();
+        return;
+    }
+    std::vector<cudaGraphNode_t> from(ne), to(ne);
+    std::vector<cudaGraphEdgeData> ed(ne);
+    if (cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    for (size_t i = 0; i < ne; i++) {
+        cudaGraphNodeType tf, tt;
+        if (cudaGraphNodeGetType(from[i], &tf) != cudaSuccess || cudaGraphNodeGetType(to[i], &tt) != cudaSuccess) break;
+        if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel) continue;
+        if (ed[i].type != cudaGraphDependencyTypeDefault) continue;
+        cudaGraphEdgeData pe{};
+        pe.from_port = cudaGraphKernelNodePortProgrammatic;
+        pe.type = cudaGraphDependencyTypeProgrammatic;
+        if (cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1) != cudaSuccess) break;
+        if (cudaGraphAddDependencies_v2(g, &from[i], &to[i], &pe, 1) != cudaSuccess) {
+            cudaGraphAddDependencies_v2(g, &from[i], &to[i], &ed[i], 1);   // restore the plain edge
+            break;
+        }
+    }
+    cudaGetLastError();
+}
+
 // Enqueue one SparseBatch step on stream s (everything st_encode_diff does on
 // the device).  Thresholds are read by the kernels from e->thr_dev, which the
 // first node refreshes from the pinned host staging buffer, so the same
@@ -774,6 +814,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
                 cudaError_t ce = cudaStreamEndCapture(g_s, &g);
                 if (r) return r;
                 if (ce != cudaSuccess) return fail(e, ST_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+                if (e->use_pdl) make_edges_programmatic(g);
                 CUDA_OK(e, cudaGraphInstantiate(&ent->exec, g, 0));
                 cudaGraphDestroy(g);
                 ent->launches = e->launches;

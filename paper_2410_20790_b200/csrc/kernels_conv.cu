@@ -25,6 +25,7 @@ constexpr int CBM = 128, CBK = 8, CNT = 256, CAPAD = 4;
 
 template <int BN, bool CINV, class T>
 __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
+    st_pdl_enter();
     constexpr int TN = BN / 16;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *As = reinterpret_cast<float *>(smem_raw);                 // [2][CBK][CBM+CAPAD]

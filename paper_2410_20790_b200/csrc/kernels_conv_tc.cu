@@ -219,6 +219,7 @@ struct Smem {
 // Weights are [Cout][ceil(taps/16)*64] with tap-major 4-channel pieces.
 template <int BN, bool DENSE, bool SMALL = false>
 __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b) {
+    st_pdl_enter();
     using namespace tc;
     using S = Smem<BN>;
     constexpr int STAGES = S::STAGES;
@@ -677,6 +678,7 @@ int conv_tc_small_k(const Geo &g) {
 }
 
 __global__ void k_pad4_bf16(const float *__restrict__ x, int64_t n, int C, uint2 *__restrict__ out) {
+    st_pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         for (int c = 0; c < C && c < 4; c++) v[c] = __ldg(x + i * C + c);

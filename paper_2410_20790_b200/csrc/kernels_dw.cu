@@ -19,6 +19,7 @@ namespace st {
 
 template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
+    st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 5 : 3;      // taps per load batch
     const Geo g = c.g;
     const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
 template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t *__restrict__ out_act,
                                                       const int32_t *__restrict__ out_pbase) {
+    st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 5 : 3;
     extern __shared__ int4 dw_meta[];   // [256/G groups][KMAX] {act, slot, 1 + pbase, 0}
     const Geo g = c.g;
@@ -212,6 +214,7 @@ struct DwTile {
 template <class T, bool DENSE>
 __global__ void __launch_bounds__(256) k_dw_tile(ConvCall c, const uint32_t *__restrict__ out_act,
                                                  const int32_t *__restrict__ out_pbase, int TOH, int TOW) {
+    st_pdl_enter();
     using TI = typename std::conditional<DENSE, float, T>::type;   // staged input element
     using TO = typename std::conditional<DENSE, float, T>::type;   // output element
     constexpr int EPL = DwTile<TI>::EPL;

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
                                                        const float *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, int n_diff, const float *__restrict__ theta_p,
                                                        uint32_t *__restrict__ act, T *__restrict__ ddelta) {
+    st_pdl_enter();
     const float theta = __ldg(theta_p);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
                                                        int N, const uint32_t *__restrict__ act,
                                                        const int32_t *__restrict__ pbase, T *__restrict__ rows,
                                                        float *s_save) {
+    st_pdl_enter();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     uint32_t w = act[i];
@@ -123,6 +125,7 @@ void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *fra
 // --------------------------------------------------------------- dilation
 __global__ void __launch_bounds__(256) k_dilate(const uint32_t *__restrict__ in, int B, Geo g,
                                                 uint32_t *__restrict__ out) {
+    st_pdl_enter();
     const int No = g.Hout * g.Wout;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * No) return;
@@ -179,6 +182,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int *warp_sums, int &block
 }
 
 __global__ void __launch_bounds__(SCAN_T) k_scan1(const uint32_t *__restrict__ w, int64_t n, int32_t *tmp) {
+    st_pdl_enter();
     __shared__ int ws[32];
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_E;
     int s = 0;
@@ -191,6 +195,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan1(const uint32_t *__restrict__ w
 }
 
 __global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *total, long long *stat) {
+    st_pdl_enter();
     __shared__ int ws[32];
     __shared__ int carry;
     if (threadIdx.x == 0) carry = 0;
@@ -213,6 +218,7 @@ __global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *t
 
 __global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w, int64_t n,
                                                   const int32_t *__restrict__ tmp, int32_t *__restrict__ pbase) {
+    st_pdl_enter();
     __shared__ int ws[32];
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_E;
     int c[SCAN_E];
@@ -246,6 +252,7 @@ void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t 
 // -------------------------------------------------------------- enumerate
 __global__ void __launch_bounds__(256) k_enumerate(const uint32_t *__restrict__ slot, const int32_t *__restrict__ pbase,
                                                    int64_t n, int32_t *__restrict__ ridx) {
+    st_pdl_enter();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint32_t w = slot[i];
@@ -271,6 +278,7 @@ constexpr int CNT_E = 8;
 // serialise on 31 shared counters).
 __global__ void __launch_bounds__(256) k_frame_counts(const uint32_t *__restrict__ act, int N, long long *counts,
                                                       int64_t cstride, long long *stat, long long *stat_nz) {
+    st_pdl_enter();
     __shared__ int cnt[32];
     __shared__ int nz;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -319,6 +327,7 @@ void launch_frame_counts(const uint32_t *act, int B, int N, long long *counts, i
 }
 
 __global__ void k_or_words(const uint32_t *a, const uint32_t *b, int64_t n, uint32_t *o) {
+    st_pdl_enter();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) o[i] = a[i] | b[i];
 }

@@ -22,6 +22,7 @@ namespace st {
 // four independent partial sums per lane keep four loads in flight)
 __global__ void __launch_bounds__(256) k_se_colsum(const float *__restrict__ x, int N, int C, int ppb,
                                                    double *__restrict__ sums) {
+    st_pdl_enter();
     const int b = blockIdx.z, c = blockIdx.y * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
     const int p0 = blockIdx.x * ppb;
     const int p1 = min(N, p0 + ppb);
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(256) k_se_colsum(const float *__restrict__ x, 
 template <class T>
 __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, int F, int ppb,
                                                        double *__restrict__ dsum) {
+    st_pdl_enter();
     extern __shared__ double sacc[];   // [8 warps][32 frames][32 lanes]
     const T *rows = static_cast<const T *>(in.rows);
     const int b = blockIdx.z, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(256) k_se_delta_sums(DView in, int N, int C, i
 template <class T>
 __global__ void __launch_bounds__(256) k_se_delta_sums_v(DView in, int N, int C, int F, int ppb, int CS,
                                                          double *__restrict__ dsum) {
+    st_pdl_enter();
     __shared__ uint32_t m_act[256], m_sl[256];
     __shared__ int32_t m_row[256];
     const T *rows = static_cast<const T *>(in.rows);
@@ -182,6 +185,7 @@ __device__ void se_gate_block(const float *m, int C, int H, const float *w1, con
 __global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum0, const double *__restrict__ dsum,
                                                   int N, int C, int H, int F, const float *w1, const float *b1,
                                                   const float *w2, const float *b2, float *__restrict__ gate_tab) {
+    st_pdl_enter();
     extern __shared__ float sm[];
     float *mean = sm;          // [C]
     float *hid = mean + C;     // [H]
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum
 __global__ void __launch_bounds__(256) k_se_schedule(const float *__restrict__ gate_tab, int C, int F,
                                                      const float *__restrict__ theta_p, float *__restrict__ s_tab,
                                                      uint32_t *__restrict__ refresh) {
+    st_pdl_enter();
     const float theta = __ldg(theta_p);
     extern __shared__ float semit[];   // [C]
     __shared__ float red[8];
@@ -242,6 +247,7 @@ __global__ void __launch_bounds__(256) k_se_schedule(const float *__restrict__ g
 // float4 over channels when C % 4 == 0
 __global__ void k_se_dense_apply(const float *__restrict__ x, const float *__restrict__ s_tab, int N, int C, int F,
                                  float *__restrict__ y) {
+    st_pdl_enter();
     const int b = blockIdx.y;
     const float *sb = s_tab + (int64_t)b * (F + 1) * C;
     const int64_t n = (int64_t)N * C;
@@ -270,6 +276,7 @@ __global__ void k_se_dense_apply(const float *__restrict__ x, const float *__res
 // slot[b][p] = act[b][p] | refresh[b]
 __global__ void k_se_slots(const uint32_t *__restrict__ act, const uint32_t *__restrict__ refresh, int N, int64_t n,
                            uint32_t *__restrict__ slot) {
+    st_pdl_enter();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) slot[i] = act[i] | refresh[i / N];
 }
@@ -280,6 +287,7 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
                                                  int N, int C, int F, int64_t BN, const float *__restrict__ theta_p,
                                                  const uint32_t *__restrict__ slot, const int32_t *__restrict__ pbase,
                                                  uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+    st_pdl_enter();
     const float theta = __ldg(theta_p);
     const T *rows = static_cast<const T *>(in.rows);
     const int lane = threadIdx.x & (G - 1);

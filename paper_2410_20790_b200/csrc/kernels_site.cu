@@ -57,6 +57,7 @@ __device__ __forceinline__ void put_bf(void *ybf, int64_t i, float v) {
 
 template <int ACT>
 __global__ void k_dense_act(const float *__restrict__ x, float *__restrict__ y, int64_t n, void *ybf) {
+    st_pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float v = actf<ACT>(x[i]);
         y[i] = v;
@@ -73,6 +74,7 @@ void launch_dense_act(const float *x, float *y, int64_t n, int act, void *ybf, c
 }
 
 __global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g, void *ybf) {
+    st_pdl_enter();
     const int No = g.Hout * g.Wout;
     const int64_t n = (int64_t)B * No * g.Cin;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -104,6 +106,7 @@ void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *y
 
 __global__ void k_dense_add(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ y, int64_t n,
                             void *ybf) {
+    st_pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float v = __fadd_rn(a[i], b[i]);
         y[i] = v;
@@ -118,6 +121,7 @@ void launch_dense_add(const float *a, const float *b, float *y, int64_t n, void 
 
 // bf16 shadow of a dense activation produced by another kernel (4 per thread)
 __global__ void k_to_bf16(const float *__restrict__ x, bf16 *__restrict__ y, int64_t n) {
+    st_pdl_enter();
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < n;
          i += (int64_t)gridDim.x * blockDim.x * 4) {
         if (i + 4 <= n) {
@@ -142,6 +146,7 @@ template <int G, int CPL, int ACT, class T>
 __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
                                                  const float *__restrict__ theta_p, uint32_t *__restrict__ out_act,
                                                  T *out_rows, SiteState sst) {
+    st_pdl_enter();
     const float theta = __ldg(theta_p);
     constexpr int P = prefetch_depth(CPL);
     const int lane = threadIdx.x & (G - 1);
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool(DView in, const float *__r
                                                       const int32_t *__restrict__ t_pbase,
                                                       uint32_t *__restrict__ out_act, T *__restrict__ out_rows,
                                                       SiteState sst) {
+    st_pdl_enter();
     const float theta = __ldg(theta_p);
     constexpr int P = CPL <= 2 ? 4 : CPL <= 4 ? 2 : 1;
     const int lane = threadIdx.x & (G - 1);
@@ -480,6 +486,7 @@ __global__ void __launch_bounds__(256) k_site_maxpool_t(DView in, const float *_
                                                         uint32_t *__restrict__ out_act, T *__restrict__ out_rows,
                                                         const float *__restrict__ theta_rp, uint32_t *__restrict__ r_act,
                                                         T *__restrict__ r_rows, SiteState sst) {
+    st_pdl_enter();
     constexpr int NGR = 256 / G;                          // output groups per CTA
     constexpr int PIECES = CPL * (int)sizeof(T) / 16;     // 16-byte pieces per unit
     constexpr int XR = FUSE ? MP_KU : 1;                  // ReLU x_acc register rows
@@ -866,6 +873,7 @@ template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_add_rows(DView a, DView b, const uint32_t *__restrict__ slot,
                                                   const int32_t *__restrict__ pbase, int64_t BN, int C,
                                                   T *__restrict__ out) {
+    st_pdl_enter();
     const int lane = threadIdx.x & (G - 1);
     const int c0 = lane * CPL;
     const bool full = (C % 8 == 0) && (c0 + CPL <= C);
@@ -912,6 +920,7 @@ void launch_add_rows(DView a, DView b, const uint32_t *slot, const int32_t *pbas
 template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_accumulate(DView in, const float *y0, int B, int N, int C,
                                                     int n_diff, float *__restrict__ out, float *o_save) {
+    st_pdl_enter();
     const int lane = threadIdx.x & (G - 1);
     const int c0 = lane * CPL;
     const bool full = (C % 8 == 0) && (c0 + CPL <= C);
