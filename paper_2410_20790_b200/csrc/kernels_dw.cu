@@ -110,7 +110,7 @@ template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t *__restrict__ out_act,
                                                       const int32_t *__restrict__ out_pbase) {
     st_pdl_enter();
-    constexpr int TB = KMAX > 9 ? 5 : 3;
+    constexpr int TB = KMAX > 9 ? 4 : 3;   // active taps loaded per batch
     extern __shared__ int4 dw_meta[];   // [256/G groups][KMAX] {act, slot, 1 + pbase, 0}
     const Geo g = c.g;
     const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
@@ -145,6 +145,16 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t
             meta[tap] = m;
         }
         __syncwarp(gmask);
+        // live taps (active in some frame of this step), ascending, into meta[k].w
+        int nlive = 0;
+        for (int r = 0; r < KMAX; r += G) {
+            const int tap = r + lane;
+            const bool live = tap < KMAX && meta[tap].x != 0;
+            const uint32_t bal = __ballot_sync(gmask, live) >> ((threadIdx.x & 31) & ~(G - 1));
+            if (live) meta[nlive + __popc(bal & ((1u << lane) - 1u))].w = tap;
+            nlive += __popc(bal);
+        }
+        __syncwarp(gmask);
         int64_t orow = 1 + __ldg(out_pbase + bq);
         while (w) {
             const int t1 = __ffs(w) - 1;
@@ -156,28 +166,32 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t
                 float acc[CPL];
 #pragma unroll
                 for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
-#pragma unroll
-                for (int t0 = 0; t0 < KMAX; t0 += TB) {
+                // batches of TB taps ACTIVE in frame t1 (found by walking the live
+                // list), loaded together; fmaf chain in ascending tap order
+                int k = 0;
+                while (k < nlive) {
+                    int tp[TB];
                     float v[TB][CPL];
-                    bool on[TB];
 #pragma unroll
                     for (int j = 0; j < TB; j++) {
-                        const int tap = t0 + j;
-                        on[j] = false;
-                        if (tap < KMAX) {
+                        tp[j] = -1;
+                        while (k < nlive) {
+                            const int tap = meta[k].w;
+                            k++;
                             const int4 m = meta[tap];
-                            on[j] = ((uint32_t)m.x >> t1) & 1u;
-                            if (on[j]) {
+                            if (((uint32_t)m.x >> t1) & 1u) {
+                                tp[j] = tap;
                                 const int64_t row = m.z + __popc((uint32_t)m.y & lm);
                                 row_load<T, CPL>(A + row * C, c0, C, full, v[j]);
+                                break;
                             }
                         }
                     }
 #pragma unroll
                     for (int j = 0; j < TB; j++) {
-                        if (!on[j]) continue;
+                        if (tp[j] < 0) continue;
                         float wv[CPL];
-                        row_load<float, CPL>(c.wk + (int64_t)(t0 + j) * C, c0, C, full, wv);
+                        row_load<float, CPL>(c.wk + (int64_t)tp[j] * C, c0, C, full, wv);
 #pragma unroll
                         for (int i = 0; i < CPL; i++) acc[i] = fmaf(wv[i], v[j][i], acc[i]);
                     }
