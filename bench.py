@@ -218,8 +218,10 @@ def main():
     for s in range(n_batches):
         u8 = np.stack([W.gen_chunk(cfg.video_seed(cid), L, cfg.h, cfg.w, cfg.c, **cfg.video)
                        for cid in shard(s, B * world, rank, world)])
-        batches.append(torch.from_numpy(W.to_float(u8)).to(dev))
-    frame_bytes = batches[0].numel() * 4
+        # uint8 frames, the camera / decoder format (v / 255 inside the
+        # Subtraction kernels, reading R20; bit-identical to fp32 frames)
+        batches.append(torch.from_numpy(np.ascontiguousarray(u8)).to(dev))
+    frame_bytes = batches[0].numel() * batches[0].element_size()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     from paper_2410_20790_b200.sharding import StatsExchange
@@ -458,7 +460,7 @@ def main():
                            "frames_per_chunk": L, "frame": [cfg.h, cfg.w, cfg.c], "policy": policy,
                            "theta": [float(x) for x in ctl.thresholds()[:3]] + ["..."],
                            "parallelism": f"chunk-sharded dp{world}", "l2": "flushed between timed steps",
-                           "input_bytes_per_step": frame_bytes},
+                           "input_bytes_per_step": frame_bytes, "frames": "uint8 (v/255, R20)"},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": frame_bytes,
                         "d2h_bytes_per_step": int(host_out[0].numel() * 4), "steps": e2e_steps,
                         "pipelined": "H2D of step k+1 and D2H of step k on copy streams overlap compute"},

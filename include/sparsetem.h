@@ -128,6 +128,17 @@ st_status st_encode_reference(st_encoder *enc, const float *ref_dev, int32_t n_c
 st_status st_encode_diff(st_encoder *enc, const float *frames_dev, int32_t n_diff,
                          int64_t chunk_stride, const float *thresholds, void *stream);
 
+/* uint8 video frames (the camera / decoder format; 4x fewer bytes over PCIe
+ * and out of HBM).  Identical to the fp32 calls on frames v / 255.0f
+ * (reading R20; the conversion happens in the Subtraction kernels and, for
+ * the reference, in a staging kernel), so results are bit-identical to
+ * st_encode_reference / st_encode_diff on the converted frames.  Layout,
+ * strides (in elements), state rules and errors as the fp32 calls. */
+st_status st_encode_reference_u8(st_encoder *enc, const uint8_t *ref_dev, int32_t n_chunks,
+                                 int64_t chunk_stride, void *stream);
+st_status st_encode_diff_u8(st_encoder *enc, const uint8_t *frames_dev, int32_t n_diff,
+                            int64_t chunk_stride, const float *thresholds, void *stream);
+
 /* Per-site sparsity statistics of the last encode (synchronizes).
  * active: host [n_chunks][n_sites][n_diff] emitted-pixel counts (or NULL);
  * site_active / site_pixels: host [n_sites] step sums (or NULL).

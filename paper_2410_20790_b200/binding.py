@@ -51,6 +51,8 @@ SIGNATURES = {
     "st_layer_shape": (I32, [P, I32, P]),
     "st_encode_reference": (I32, [P, P, I32, I64, P]),
     "st_encode_diff": (I32, [P, P, I32, I64, P, P]),
+    "st_encode_reference_u8": (I32, [P, P, I32, I64, P]),
+    "st_encode_diff_u8": (I32, [P, P, I32, I64, P, P]),
     "st_get_sparsity": (I32, [P, P, P, P]),
     "st_copy_site_counts": (I32, [P, P, P]),
     "st_get_layer_counts": (I32, [P, P, P, P]),
@@ -172,26 +174,34 @@ class Encoder:
 
     # -- the hot path
     def encode_reference(self, ref, stream=None):
-        """ref: torch float32 cuda [B][H][W][C] (chunk dim may be strided)."""
-        assert ref.dtype.is_floating_point and ref.is_cuda
+        """ref: torch float32 or uint8 cuda [B][H][W][C] (chunk dim may be
+        strided); uint8 frames mean v / 255 (reading R20)."""
+        import torch
+        u8 = ref.dtype == torch.uint8
+        assert (u8 or ref.dtype == torch.float32) and ref.is_cuda
         per = self.net.in_h * self.net.in_w * self.net.in_c
         assert ref[0].is_contiguous(), "frame must be contiguous NHWC"
         stride = ref.stride(0) if ref.shape[0] > 1 else per
-        self._check("st_encode_reference", lib().st_encode_reference(
+        fn = "st_encode_reference_u8" if u8 else "st_encode_reference"
+        self._check(fn, getattr(lib(), fn)(
             self.h, C.c_void_p(ref.data_ptr()), ref.shape[0], stride, _stream_handle(stream)))
         self.n_chunks = ref.shape[0]
 
     def encode_diff(self, frames, thresholds, stream=None):
-        """frames: torch float32 cuda [B][n_diff][H][W][C] (chunk dim may be strided)."""
+        """frames: torch float32 or uint8 cuda [B][n_diff][H][W][C] (chunk dim
+        may be strided), or None for n_diff = 0."""
+        import torch
         th = np.ascontiguousarray(np.broadcast_to(np.asarray(thresholds, np.float32), (self.n_sites,)))
         n_diff = 0 if frames is None else frames.shape[1]
-        ptr, stride = None, 0
+        ptr, stride, u8 = None, 0, False
         if n_diff:
-            assert frames.is_cuda and frames.dtype.is_floating_point
+            u8 = frames.dtype == torch.uint8
+            assert frames.is_cuda and (u8 or frames.dtype == torch.float32)
             assert frames[0].is_contiguous(), "frames of a chunk must be contiguous"
             ptr = frames.data_ptr()
             stride = frames.stride(0) if frames.shape[0] > 1 else 0
-        self._check("st_encode_diff", lib().st_encode_diff(
+        fn = "st_encode_diff_u8" if u8 else "st_encode_diff"
+        self._check(fn, getattr(lib(), fn)(
             self.h, C.c_void_p(ptr), n_diff, stride, _np_ptr(th), _stream_handle(stream)))
         self.n_diff = n_diff
 

@@ -77,13 +77,14 @@ struct LaunchRec {
 };
 
 struct GraphKey {
-    const float *frames;
+    const void *frames;
     int64_t stride;
     int n_diff, chunks;
     int smode;   // streaming: 0 off / first call after a reference, 1 + ping-pong parity on continuations
+    bool u8;     // uint8 frames
     bool operator==(const GraphKey &o) const {
         return frames == o.frames && stride == o.stride && n_diff == o.n_diff && chunks == o.chunks &&
-               smode == o.smode;
+               smode == o.smode && u8 == o.u8;
     }
 };
 struct GraphEnt {
@@ -685,6 +686,23 @@ extern "C" st_status st_encode_reference(st_encoder *e, const float *ref_dev, in
     return ST_OK;
 }
 
+extern "C" st_status st_encode_reference_u8(st_encoder *e, const uint8_t *ref_dev, int32_t n_chunks,
+                                            int64_t chunk_stride, void *stream) {
+    if (!e) return ST_ERR_ARG;
+    if (!ref_dev) return fail(e, ST_ERR_ARG, "ref_dev is null");
+    if (n_chunks < 1 || n_chunks > e->B) return fail(e, ST_ERR_SHAPE, "n_chunks %d outside [1, %d]", n_chunks, e->B);
+    const int64_t per = (int64_t)e->in_H * e->in_W * e->in_C;
+    const int64_t stride = chunk_stride ? chunk_stride : per;
+    if (stride < per) return fail(e, ST_ERR_ARG, "chunk_stride smaller than a frame");
+    CUDA_OK(e, cudaSetDevice(e->cfg.device));
+    launch_u8_to_f32(ref_dev, stride, per, n_chunks, e->ref, (cudaStream_t)stream);
+    CUDA_OK(e, cudaGetLastError());
+    e->staged_chunks = n_chunks;
+    e->cont = false;
+    e->par = 0;
+    return ST_OK;
+}
+
 static DView view_of(const st_encoder *e, int t) {
     DView v;
     if (t < 0) {
@@ -769,10 +787,10 @@ static void make_edges_programmatic(cudaGraph_t g) {
 // the device).  Thresholds are read by the kernels from e->thr_dev, which the
 // first node refreshes from the pinned host staging buffer, so the same
 // captured graph serves every step.
-static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64_t fstride, cudaStream_t s);
+static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int F, int64_t fstride, cudaStream_t s);
 
-extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int32_t n_diff, int64_t chunk_stride,
-                                    const float *thresholds, void *stream) {
+static st_status encode_diff(st_encoder *e, const void *frames_dev, bool u8, int32_t n_diff, int64_t chunk_stride,
+                             const float *thresholds, void *stream) {
     if (!e) return ST_ERR_ARG;
     if (!thresholds) return fail(e, ST_ERR_ARG, "thresholds is null");
     if (n_diff < 0 || n_diff > e->F) return fail(e, ST_ERR_SHAPE, "n_diff %d outside [0, %d]", n_diff, e->F);
@@ -792,16 +810,16 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
     e->last_stream = s;
     const bool graphs = e->use_graphs && !e->prof && !e->cfg.debug_retain;
     if (!graphs) {
-        st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
+        st_status r = issue_step(e, frames_dev, u8, n_diff, fstride, s);
         if (r) return r;
     } else {
-        GraphKey key{frames_dev, fstride, n_diff, e->staged_chunks, e->cont ? 1 + e->par : 0};
+        GraphKey key{frames_dev, fstride, n_diff, e->staged_chunks, e->cont ? 1 + e->par : 0, u8};
         GraphEnt *ent = nullptr;
         for (auto &g : e->graphs)
             if (g.key == key) ent = &g;
         if (!ent) {   // first sight: run eagerly (lazy kernel attributes get set), capture next time
             e->graphs.push_back(GraphEnt{key, nullptr, 0});
-            st_status r = issue_step(e, frames_dev, n_diff, fstride, s);
+            st_status r = issue_step(e, frames_dev, u8, n_diff, fstride, s);
             if (r) return r;
         } else {
             // capture and replay on the encoder's own stream, forked from / joined
@@ -810,7 +828,7 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
             if (!ent->exec) {
                 cudaGraph_t g = nullptr;
                 CUDA_OK(e, cudaStreamBeginCapture(g_s, cudaStreamCaptureModeThreadLocal));
-                st_status r = issue_step(e, frames_dev, n_diff, fstride, g_s);
+                st_status r = issue_step(e, frames_dev, u8, n_diff, fstride, g_s);
                 cudaError_t ce = cudaStreamEndCapture(g_s, &g);
                 if (r) return r;
                 if (ce != cudaSuccess) return fail(e, ST_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
@@ -837,7 +855,17 @@ extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int3
     return ST_OK;
 }
 
-static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64_t fstride, cudaStream_t s) {
+extern "C" st_status st_encode_diff(st_encoder *e, const float *frames_dev, int32_t n_diff, int64_t chunk_stride,
+                                    const float *thresholds, void *stream) {
+    return encode_diff(e, frames_dev, false, n_diff, chunk_stride, thresholds, stream);
+}
+
+extern "C" st_status st_encode_diff_u8(st_encoder *e, const uint8_t *frames_dev, int32_t n_diff, int64_t chunk_stride,
+                                       const float *thresholds, void *stream) {
+    return encode_diff(e, frames_dev, true, n_diff, chunk_stride, thresholds, stream);
+}
+
+static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int F, int64_t fstride, cudaStream_t s) {
     const int B = e->staged_chunks, n = (int)e->L.size();
     const int64_t Nin = (int64_t)e->in_H * e->in_W;
     const int64_t per = Nin * e->in_C;
@@ -868,15 +896,15 @@ static st_status issue_step(st_encoder *e, const float *frames_dev, int F, int64
         uint32_t *act = e->p<uint32_t>(e->in_act);
         int32_t *pb = e->p<int32_t>(e->in_pbase);
         void *rows = e->ptr(e->in_rows);
-        const float *fr = frames_dev;
+        const void *fr = frames_dev;
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_mask(S0, per, fr, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act,
+               launch_subtract_mask(S0, per, fr, u8, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act,
                                     e->in_dd >= 0 ? e->ptr(e->in_dd) : nullptr, s));
         LAUNCH(e, KC_SCAN, -1, s,
                launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
         zero_row(e->in_rows, e->in_C);
         LAUNCH(e, KC_SUBTRACT, -1, s,
-               launch_subtract_rows(S0, per, fr, fstride, B, (int)Nin, e->in_C, act, pb, rows, bf,
+               launch_subtract_rows(S0, per, fr, u8, fstride, B, (int)Nin, e->in_C, act, pb, rows, bf,
                                     strm ? e->p<float>(e->in_S) : nullptr, s));
         LAUNCH(e, KC_COUNTS, -1, s,
                launch_frame_counts(act, B, (int)Nin, e->counts, cstride, e->site_sum, nullptr, s));

@@ -33,16 +33,19 @@ struct Geo {   // conv / pool geometry
 // Subtraction pass 1 (site 0): act bits per pixel, sequential over frames;
 // optionally also the dense per-frame emitted delta ddelta [B][n_diff][N][C]
 // (zeros where truncated; row type) for convs reading the input directly.
-void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
+// frames: fp32, or uint8 (u8: value v / 255.0f, reading R20); fr_stride in elements
+void launch_subtract_mask(const float *ref, int64_t ref_stride, const void *frames, bool u8, int64_t fr_stride,
                           int B, int N, int C, int n_diff, const float *theta, bool bf, uint32_t *act, void *ddelta,
                           cudaStream_t s);
 // Subtraction pass 2: write emitted rows at the slots of `act`; s_save
 // (streaming, nullable): final S of every pixel with an emission, [B][N][C]
 // (may alias ref when ref_stride == N*C: each pixel is read, then written, by
 // its own thread).
-void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride,
+void launch_subtract_rows(const float *ref, int64_t ref_stride, const void *frames, bool u8, int64_t fr_stride,
                           int B, int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
                           float *s_save, cudaStream_t s);
+// n uint8 frames of `per` elements (frame c at src + c*src_stride) -> fp32 v / 255.0f, packed
+void launch_u8_to_f32(const uint8_t *src, int64_t src_stride, int64_t per, int n, float *dst, cudaStream_t s);
 // out[b][q] = OR of in[b][p] over the receptive field (dense amplification)
 void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaStream_t s);
 // pbase = exclusive prefix of popc(words) over n words; *total = sum; also

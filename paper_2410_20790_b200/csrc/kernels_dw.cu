@@ -11,6 +11,7 @@
 // 16-byte bf16 vector (two float4 in FP32 mode) -- and a batch of tap loads
 // is issued before its FMAs.  FP32-mode results are bit-identical to the
 // oracle (fmaf chain in tap order from +0).
+#include <cstdlib>
 #include <type_traits>
 
 #include "rowio.cuh"
@@ -476,6 +477,12 @@ static void launch_dw_pm_t(const ConvCall &c, const uint32_t *out_act, const int
 }
 
 void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, cudaStream_t s) {
+    static const int tile_mode = [] { const char *v = getenv("ST_DW_SPARSE_TILE"); return v ? atoi(v) : 0; }();
+    if (tile_mode == 1 || (tile_mode == 2 && c.g.kh * c.g.kw <= 9)) {
+        if (c.bf ? launch_dw_tile_t<bf16, false>(c, out_act, out_pbase, s)
+                 : launch_dw_tile_t<float, false>(c, out_act, out_pbase, s))
+            return;
+    }
     if (!c.bf) launch_dw_pm_t<float>(c, out_act, out_pbase, s);
     else launch_dw_pm_t<bf16>(c, out_act, out_pbase, s);
 }

@@ -14,9 +14,14 @@
 namespace st {
 
 // ------------------------------------------------------------ subtraction
-template <int C, class T>
+// Frame element -> fp32: float frames as they are; uint8 frames v / 255.0f
+// (reading R20; IEEE division, the same value the fp32 input path receives).
+__device__ __forceinline__ float frame_val(const float *p) { return __ldg(p); }
+__device__ __forceinline__ float frame_val(const uint8_t *p) { return __fdiv_rn((float)__ldg(p), 255.0f); }
+
+template <int C, class T, class FT>
 __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__ ref, int64_t ref_stride,
-                                                       const float *__restrict__ fr, int64_t fr_stride, int B,
+                                                       const FT *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, int n_diff, const float *__restrict__ theta_p,
                                                        uint32_t *__restrict__ act, T *__restrict__ ddelta) {
     st_pdl_enter();
@@ -28,7 +33,7 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
     float S[C];
 #pragma unroll
     for (int c = 0; c < C; c++) S[c] = __ldg(r + c);
-    const float *f = fr + b * fr_stride + (int64_t)p * C;
+    const FT *f = fr + b * fr_stride + (int64_t)p * C;
     const int64_t fs = (int64_t)N * C;
     // optional dense per-frame copy of the emitted delta [B][n_diff][N][C]
     // (zeros where truncated) for convs that read the input directly
@@ -43,7 +48,7 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
         float mx = 0.0f;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            raw[c] = __fsub_rn(__ldg(f + t1 * fs + c), S[c]);
+            raw[c] = __fsub_rn(frame_val(f + t1 * fs + c), S[c]);
             mx = fmaxf(mx, fabsf(raw[c]));
         }
         const bool on = mx > theta;             // R1: strict comparison
@@ -62,9 +67,9 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
     act[i] = w;
 }
 
-template <int C, class T>
+template <int C, class T, class FT>
 __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__ ref, int64_t ref_stride,
-                                                       const float *__restrict__ fr, int64_t fr_stride, int B,
+                                                       const FT *__restrict__ fr, int64_t fr_stride, int B,
                                                        int N, const uint32_t *__restrict__ act,
                                                        const int32_t *__restrict__ pbase, T *__restrict__ rows,
                                                        float *s_save) {
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
     float S[C];
 #pragma unroll
     for (int c = 0; c < C; c++) S[c] = __ldg(r + c);
-    const float *f = fr + b * fr_stride + (int64_t)p * C;
+    const FT *f = fr + b * fr_stride + (int64_t)p * C;
     const int64_t fs = (int64_t)N * C;
     T *o = rows + (int64_t)(1 + pbase[i]) * C;
     while (w) {
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
         w &= w - 1;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const float e = rnd<T>(__fsub_rn(__ldg(f + t1 * fs + c), S[c]));   // emitted delta
+            const float e = rnd<T>(__fsub_rn(frame_val(f + t1 * fs + c), S[c]));   // emitted delta
             S[c] = __fadd_rn(S[c], e);
             str<T>(o + c, e);
         }
@@ -97,29 +102,53 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
         for (int c = 0; c < C; c++) s_save[i * C + c] = S[c];
 }
 
-#define SUB_DISPATCH(C_, KERNEL, ...)                                                    \
-    switch (C_) {                                                                        \
-    case 1: KERNEL<1, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
-    case 2: KERNEL<2, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
-    case 3: KERNEL<3, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
-    case 4: KERNEL<4, T><<<grid, 256, 0, s>>>(__VA_ARGS__); break;                       \
-    default: break;                                                                      \
+#define SUB_DISPATCH(C_, KERNEL, FT, FR, ...)                                                               \
+    switch (C_) {                                                                                           \
+    case 1: KERNEL<1, T, FT><<<grid, 256, 0, s>>>(ref, ref_stride, static_cast<const FT *>(FR), __VA_ARGS__); break; \
+    case 2: KERNEL<2, T, FT><<<grid, 256, 0, s>>>(ref, ref_stride, static_cast<const FT *>(FR), __VA_ARGS__); break; \
+    case 3: KERNEL<3, T, FT><<<grid, 256, 0, s>>>(ref, ref_stride, static_cast<const FT *>(FR), __VA_ARGS__); break; \
+    case 4: KERNEL<4, T, FT><<<grid, 256, 0, s>>>(ref, ref_stride, static_cast<const FT *>(FR), __VA_ARGS__); break; \
+    default: break;                                                                                         \
     }
 
-void launch_subtract_mask(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
-                          int N, int C, int n_diff, const float *theta_p, bool bf, uint32_t *act, void *ddelta,
+void launch_subtract_mask(const float *ref, int64_t ref_stride, const void *frames, bool u8, int64_t fr_stride,
+                          int B, int N, int C, int n_diff, const float *theta_p, bool bf, uint32_t *act, void *ddelta,
                           cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
-    ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, ref, ref_stride, frames, fr_stride, B, N, n_diff, theta_p,
-                                     act, static_cast<T *>(ddelta)));
+    if (u8)
+        ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, uint8_t, frames, fr_stride, B, N, n_diff, theta_p, act,
+                                         static_cast<T *>(ddelta)));
+    else
+        ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_mask, float, frames, fr_stride, B, N, n_diff, theta_p, act,
+                                         static_cast<T *>(ddelta)));
 }
 
-void launch_subtract_rows(const float *ref, int64_t ref_stride, const float *frames, int64_t fr_stride, int B,
-                          int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
+void launch_subtract_rows(const float *ref, int64_t ref_stride, const void *frames, bool u8, int64_t fr_stride,
+                          int B, int N, int C, const uint32_t *act, const int32_t *pbase, void *rows, bool bf,
                           float *s_save, cudaStream_t s) {
     const int grid = cdiv((int64_t)B * N, 256);
-    ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_rows, ref, ref_stride, frames, fr_stride, B, N, act, pbase,
-                                     static_cast<T *>(rows), s_save));
+    if (u8)
+        ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_rows, uint8_t, frames, fr_stride, B, N, act, pbase,
+                                         static_cast<T *>(rows), s_save));
+    else
+        ST_ROW_DISPATCH(bf, SUB_DISPATCH(C, k_subtract_rows, float, frames, fr_stride, B, N, act, pbase,
+                                         static_cast<T *>(rows), s_save));
+}
+
+// uint8 frames -> fp32 v / 255.0f (reading R20): the staged reference frames
+__global__ void __launch_bounds__(256) k_u8_to_f32(const uint8_t *__restrict__ src, int64_t src_stride,
+                                                   int64_t per, int n, float *__restrict__ dst) {
+    st_pdl_enter();
+    const int64_t tot = per * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / per, k = i - c * per;
+        dst[i] = __fdiv_rn((float)__ldg(src + c * src_stride + k), 255.0f);
+    }
+}
+
+void launch_u8_to_f32(const uint8_t *src, int64_t src_stride, int64_t per, int n, float *dst, cudaStream_t s) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(per * n, 256), 148 * 16));
+    k_u8_to_f32<<<grid, 256, 0, s>>>(src, src_stride, per, n, dst);
 }
 
 // --------------------------------------------------------------- dilation

@@ -251,3 +251,38 @@ def test_relu_maxpool_geometries_exact(C, k, s, p, h, w):
         for b in range(2):
             compare_chunk(enc, net, fr[b], th, b)
         enc.close()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("model", ["crnn", "resnet18"])
+def test_u8_frames_match_float(precision, model):
+    """st_encode_reference_u8 / st_encode_diff_u8 on uint8 frames are
+    bit-identical to the fp32 calls on v / 255.0f (reading R20), including a
+    streaming continuation."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    if model == "crnn":
+        cfg = W.get_config(2)
+        net = cfg.build_net()
+        u8 = W.gen_video(3, 10, cfg.h, cfg.w, cfg.c, 2024, **cfg.video)
+    else:
+        net = W.models.resnet18(72, 104)
+        init_weights(net, 14)
+        u8 = W.gen_video(2, 10, 72, 104, 3, 80, n_objects=4, size=(8, 24), speed=(1, 3), noise_q=0.1, noise_amp=2)
+    xf = torch.from_numpy(W.to_float(u8)).cuda()
+    xu = torch.from_numpy(np.ascontiguousarray(u8)).cuda()
+    res = {}
+    for kind, x in (("f32", xf), ("u8", xu)):
+        enc = Encoder(net, x.shape[0], 6, precision=precision, streaming=True)
+        enc.encode_reference(x[:, 0])
+        outs = []
+        for a, b in ((1, 6), (6, 10)):
+            enc.encode_diff(x[:, a:b], 0.05)
+            torch.cuda.synchronize()
+            outs.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        res[kind] = outs
+        enc.close()
+    for (of, cf), (ou, cu) in zip(res["f32"], res["u8"]):
+        assert np.array_equal(cf, cu)
+        for a, b in zip(of, ou):
+            assert np.array_equal(a, b)
