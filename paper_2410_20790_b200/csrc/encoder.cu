@@ -29,12 +29,12 @@ namespace {
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
               KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16,
-              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_N = 20;
+              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_SE_SUMS = 20, KC_N = 21;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
                               "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
                               "conv_tc_sparse", "conv_tc_dense", "se", "conv_tc_stem_sparse",
-                              "conv_tc_stem_dense", "prof_stats"};
+                              "conv_tc_stem_dense", "prof_stats", "se_sums"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -1094,18 +1094,18 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             uint32_t *refresh = reinterpret_cast<uint32_t *>(s_tab + (int64_t)B * (F + 1) * l.C);
             float *gate_tab = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(refresh + B) + 63) & ~uintptr_t(63));
             const int H = l.spec.se_hidden;
-            LAUNCH(e, KC_SE, i, s, launch_se_colsum(x_src, B, (int)N, l.C, sum0, s));
-            if (F > 0) LAUNCH(e, KC_SE, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
-            LAUNCH(e, KC_SE, i, s,
+            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_colsum(x_src, B, (int)N, l.C, sum0, s));
+            if (F > 0) LAUNCH(e, KC_SE_SUMS, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
+            LAUNCH(e, KC_SE_SUMS, i, s,
                    launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
                                       thresholds + l.site, gate_tab, s_tab, refresh, s));
-            LAUNCH(e, KC_SE, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
+            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
             if (l.b_ybf >= 0)
                 LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
-            LAUNCH(e, KC_SE, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
+            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
             LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SE, i, s,
@@ -1351,7 +1351,7 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                     fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f M=%lld Min=%lld K=%lld C=%d GBps=%.1f\n",
                             (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, (long long)M, (long long)Min, (long long)K, l.C, t > 0 ? b / t * 1e-6 : 0.0);
             } else if (r.layer >= 0 && e->last_ndiff > 0 &&
-                       (r.cls == KC_SITE_PW || r.cls == KC_SITE_MP || r.cls == KC_ACCUM)) {
+                       (r.cls == KC_SITE_PW || r.cls == KC_SITE_MP || r.cls == KC_ACCUM || r.cls == KC_SE)) {
                 // algorithmic bytes of the HBM-bound per-pixel kernels:
                 // input delta rows once, x0 of the touched input pixels once, emitted
                 // rows once, frame words in/out; Accumulation writes the dense outputs
@@ -1374,6 +1374,15 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 if (e->prof_trace)
                     fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f GBps=%.1f\n",
                             (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, t > 0 ? b / t * 1e-6 : 0.0);
+            } else if (r.layer >= 0 && r.cls == KC_SE_SUMS) {
+                // SE sums / schedule / dense apply of one layer (5 launches with diff
+                // frames, 4 without): x0 column sums, delta-row sums, dense x -> y;
+                // the layer total is spread evenly over its launches
+                const LayerRT &l = e->L[r.layer];
+                const double eb = e->cfg.precision == ST_BF16 ? 2.0 : 4.0;
+                const double BNC = (double)e->last_chunks * l.H * l.W * l.C;
+                const double tot = 3.0 * 4.0 * BNC + (e->last_ndiff > 0 ? eb * (double)rin[r.layer] * l.C : 0.0);
+                e->prof_bytes[r.cls] += tot / (e->last_ndiff > 0 ? 5.0 : 4.0);
             } else if (e->prof_trace) {
                 fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f\n", (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t);
             }
