@@ -287,7 +287,10 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             l.geo = Geo{sh, sw, sc, l.H, l.W, l.C, s.k_h, s.k_w, s.s_h, s.s_w, s.p_h, s.p_w, s.groups};
         }
         if (is_site(l.kind)) l.site = e->n_sites++;
-        if (l.C > 1152) return ST_ERR_UNSUPPORTED;
+        // register-resident site kernels: <= 1152 channels at maxpool / SE
+        // sites; pointwise sites, joins and taps up to 2048 (wide kernels)
+        if (l.C > 2048 || ((l.kind == ST_MAXPOOL || l.kind == ST_SE) && l.C > 1152)) return ST_ERR_UNSUPPORTED;
+        if ((l.kind == ST_RELU || l.kind == ST_SILU) && l.C > 1280 && l.C % 8 != 0) return ST_ERR_UNSUPPORTED;
     }
     // consumers
     for (int i = 0; i < n; i++) {

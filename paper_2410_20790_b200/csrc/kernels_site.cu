@@ -240,6 +240,95 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
     }
 }
 
+// Wide pointwise site (C > 1280, C % 8 == 0: the 2048-channel stages of
+// ResNet-152).  One warp per pixel; the pixel's x_acc,
+// y_acc and the frame's candidate live in shared memory (3 x C fp32 per
+// warp) instead of registers, walked in 256-channel chunks (8 per lane).
+// Per frame: x += Delta, c = f(x) - y over all chunks with the running
+// max; warp max; if it exceeds theta, y += rnd(c) and the row is written.
+// Same per-channel operations in the same order as k_site_pw (FP32 mode
+// bit-exact).
+constexpr int PW_WIDE_WARPS = 4;
+template <int ACT, class T>
+__global__ void __launch_bounds__(32 * PW_WIDE_WARPS) k_site_pw_wide(DView in, const float *__restrict__ x0, int64_t BN,
+                                                                  int C, const float *__restrict__ theta_p,
+                                                                  uint32_t *__restrict__ out_act, T *out_rows,
+                                                                  SiteState sst) {
+    st_pdl_enter();
+    extern __shared__ float pw_sm[];
+    const float theta = __ldg(theta_p);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float *xs = pw_sm + (size_t)wid * 3 * C, *ys = xs + C, *cs = ys + C;
+    const T *rows = static_cast<const T *>(in.rows);
+    for (int64_t bp = (int64_t)blockIdx.x * PW_WIDE_WARPS + wid; bp < BN; bp += (int64_t)gridDim.x * PW_WIDE_WARPS) {
+        uint32_t a = __ldg(in.act + bp);
+        if (!a) {
+            if (lane == 0) out_act[bp] = 0;
+            continue;
+        }
+        const int base = 1 + __ldg(in.pbase + bp);
+        const uint32_t sl = __ldg(in.slot + bp);
+        for (int c0 = lane * 8; c0 < C; c0 += 256) {
+            float x[8], y[8];
+            RowIO<float, 8>::load(x0 + bp * C + c0, x);
+            if (sst.y_init) RowIO<float, 8>::load(sst.y_init + bp * C + c0, y);
+            else
+#pragma unroll
+                for (int i = 0; i < 8; i++) y[i] = actf<ACT>(x[i]);
+            RowIO<float, 8>::store(xs + c0, x);
+            RowIO<float, 8>::store(ys + c0, y);
+        }
+        __syncwarp();
+        uint32_t emit = 0;
+        while (a) {
+            const int t1 = __ffs(a) - 1;
+            a &= a - 1;
+            const int64_t row = base + __popc(sl & lowmask(t1));
+            float mx = 0.0f;
+            for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                float v[8], x[8], y[8], cand[8];
+                RowIO<T, 8>::load(rows + row * C + c0, v);
+                RowIO<float, 8>::load(xs + c0, x);
+                RowIO<float, 8>::load(ys + c0, y);
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    x[i] = __fadd_rn(x[i], v[i]);                     // reconstruct x (Eq.3)
+                    cand[i] = __fsub_rn(actf<ACT>(x[i]), y[i]);       // restore the delta
+                    mx = fmaxf(mx, fabsf(cand[i]));
+                }
+                RowIO<float, 8>::store(xs + c0, x);
+                RowIO<float, 8>::store(cs + c0, cand);
+            }
+            mx = gmax<32>(mx, 0xffffffffu);
+            if (mx > theta) {                                          // truncation
+                for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                    float y[8], cand[8];
+                    RowIO<float, 8>::load(cs + c0, cand);
+                    RowIO<float, 8>::load(ys + c0, y);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        cand[i] = rnd<T>(cand[i]);
+                        y[i] = __fadd_rn(y[i], cand[i]);
+                    }
+                    RowIO<float, 8>::store(ys + c0, y);
+                    RowIO<T, 8>::store(out_rows + row * C + c0, cand);
+                }
+                emit |= 1u << t1;
+            }
+        }
+        if (lane == 0) out_act[bp] = emit;
+        if (sst.x_save)
+            for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                float x[8], y[8];
+                RowIO<float, 8>::load(xs + c0, x);
+                RowIO<float, 8>::load(ys + c0, y);
+                RowIO<float, 8>::store(sst.x_save + bp * C + c0, x);
+                RowIO<float, 8>::store(sst.y_save + bp * C + c0, y);
+            }
+        __syncwarp();   // state rows reused by the next pixel
+    }
+}
+
 #define CH_DISPATCH(C_, LAUNCH)                                    \
     if ((C_) <= 1) { LAUNCH(1, 1); }                               \
     else if ((C_) <= 2) { LAUNCH(2, 1); }                          \
@@ -282,7 +371,8 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
     else if ((C_) <= 256) { LAUNCH(32, 8); }                       \
     else if ((C_) <= 512) { LAUNCH(32, 16); }                      \
     else if ((C_) <= 768) { LAUNCH(32, 24); }                      \
-    else { LAUNCH(32, 40); }
+    else if ((C_) <= 1280) { LAUNCH(32, 40); }                     \
+    else { LAUNCH(32, 64); }
 
 static int groups_grid(int64_t n_groups, int G) {
     const int64_t threads = n_groups * G;
@@ -292,6 +382,19 @@ static int groups_grid(int64_t n_groups, int G) {
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
                            uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s) {
     const int64_t BN = (int64_t)B * N;
+    if (C > 1280 && C % 8 == 0) {
+        const size_t sm = (size_t)PW_WIDE_WARPS * 3 * C * sizeof(float);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(BN, PW_WIDE_WARPS), 148 * 8));
+#define L_PWW(ACT_)                                                                                    \
+    {                                                                                                  \
+        auto kf = k_site_pw_wide<ACT_, T>;                                                             \
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                \
+        kf<<<grid, 32 * PW_WIDE_WARPS, sm, s>>>(in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st); \
+    }
+        ST_ROW_DISPATCH(bf, if (act == ACT_RELU) L_PWW(ACT_RELU) else if (sizeof(T) == 4) L_PWW(ACT_SILU) else L_PWW(ACT_SILU_FAST));
+#undef L_PWW
+        return;
+    }
 
 #define L_PW(G_, CPL_)                                                                                 \
     {                                                                                                  \

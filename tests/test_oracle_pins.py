@@ -52,15 +52,20 @@ def test_dense_matches_torch_fp64(oracle_lib, seed):
 
 
 def test_dense_models_match_torch(oracle_lib):
-    """cfg1 and a reduced-resolution CRNN / ResNet-18 / EfficientNet-B0."""
+    """cfg1 and a reduced-resolution CRNN / ResNet-18 / EfficientNet-B0 /
+    ResNet-152 (N3, 2048-channel stages)."""
     for net in (W.models.toy_encoder(16, 16), W.models.crnn_vgg7(32, 64),
-                W.models.resnet18(64, 64), W.models.efficientnet_b0(64, 64)):
+                W.models.resnet18(64, 64), W.models.efficientnet_b0(64, 64), W.models.resnet152(64, 64)):
         init_weights(net, 5)
         x = np.random.default_rng(1).random((net.in_h, net.in_w, net.in_c)).astype(np.float32)
         ours = oracle.dense_forward(net, x)
         ref = dense_forward64(net, x)
+        # fp32 (oracle) vs fp64 rounding differences accumulate with depth: the
+        # 155-conv ResNet-152 gets a 10x wider bound (still orders of magnitude
+        # below the O(1) error of a dropped term or a wrong index)
+        k = 10.0 if net.name == "resnet152" else 1.0
         for i, (a, b) in enumerate(zip(ours, ref)):
-            assert close(a, b, rel=3e-4, abs_=3e-5), (net.name, i, max_err(a, b))
+            assert close(a, b, rel=3e-4 * k, abs_=3e-5 * k), (net.name, i, max_err(a, b))
 
 
 def test_dense_spec_scalars(oracle_lib):
@@ -100,14 +105,15 @@ def test_pin1_zero_threshold_equals_dense(oracle_lib, seed, order):
 
 def test_pin1_models_zero_threshold(oracle_lib):
     for net in (W.models.toy_encoder(24, 24), W.models.crnn_vgg7(32, 48), W.models.resnet18(48, 48),
-                W.models.efficientnet_b0(64, 64)):
+                W.models.efficientnet_b0(64, 64), W.models.resnet152(40, 40)):
         init_weights(net, 3)
         fr = random_frames(7, 4, net.in_h, net.in_w, net.in_c, p_change=0.2, scale=0.2)
         r = oracle.run_chunk(net, fr, 0.0, want_masks=False)
+        k = 10.0 if net.name == "resnet152" else 1.0   # depth-accumulated fp32 rounding, as above
         for tap, O in r["taps"].items():
             for t in range(4):
                 ref = dense_forward64(net, fr[t])[tap]
-                assert close(O[t], ref, rel=5e-4, abs_=5e-5), (net.name, tap, t, max_err(O[t], ref))
+                assert close(O[t], ref, rel=5e-4 * k, abs_=5e-5 * k), (net.name, tap, t, max_err(O[t], ref))
 
 
 # ---------------------------------------------- PIN2 input-only threshold

@@ -34,7 +34,8 @@ class Config:
 
     def build_net(self, weight_seed=None):
         net = {"toy": models.toy_encoder, "crnn": models.crnn_vgg7,
-               "resnet18": models.resnet18, "effb0": models.efficientnet_b0}[self.model](self.h, self.w)
+               "resnet18": models.resnet18, "effb0": models.efficientnet_b0,
+               "resnet152": models.resnet152}[self.model](self.h, self.w)
         models.init_weights(net, SEED_BASE + 1000 * self.cid + 999 if weight_seed is None else weight_seed)
         return net
 
@@ -64,6 +65,12 @@ CONFIGS = {
               video=dict(n_objects=12, size=(32, 192), speed=(1, 3), noise_q=0.10, noise_amp=2),
               policy="ibst", T=0.9, eps=0.05, cycle=8,
               note="EfficientDet-D0 backbone @1080p, 64 chunks, chunk-sharded over GPUs"),
+    # SURVEY §8(f) N3 (not a BASELINE.json config): the paper's own CRNN
+    # backbone, ResNet-152 at 320x320, chunks of 28 frames, 3 chunks per step
+    6: Config(6, "resnet152_320", "resnet152", 320, 320, 3, L=28, chunks_per_step=3, steps=4,
+              video=dict(n_objects=6, size=(32, 96), speed=(1, 3), noise_q=0.10, noise_amp=2),
+              policy="ibst", T=0.9, eps=0.05, cycle=8,
+              note="ResNet-152 CRNN backbone @320x320, 28-frame chunks, batch 3 (N3)"),
 }
 
 

@@ -199,6 +199,34 @@ def resnet18(h=720, w=1280):
     return n
 
 
+def resnet152(h=320, w=320):
+    """ResNet-152, the paper's CRNN backbone for action
+    recognition (P:217, P:231-234: 224/320/420 inputs, chunk 28, batch 3);
+    torchvision topology (bottleneck blocks [3, 8, 36, 3], stride on the 3x3)
+    without avgpool/fc, output layer4 (2048 channels).  The last 1x1 conv of
+    each residual branch uses gain 0.25 so 50 residual additions keep the
+    synthetic activations O(1) (reading R30: data-independent weights)."""
+    n = Net(3, h, w, "resnet152")
+    x = n.relu(n.conv(-1, 64, 7, 2, 3))
+    x = n.maxpool(x, 3, 2, 1)
+    c = 64
+    for width, blocks, s in [(64, 3, 1), (128, 8, 2), (256, 36, 2), (512, 3, 2)]:
+        co = 4 * width
+        for blk in range(blocks):
+            stride = s if blk == 0 else 1
+            y = n.relu(n.conv(x, width, 1, 1, 0))
+            y = n.relu(n.conv(y, width, 3, stride, 1))
+            y = n.conv(y, co, 1, 1, 0, act_gain=0.25)
+            if stride != 1 or c != co:
+                sc = n.conv(x, co, 1, stride, 0, act_gain=1.0)
+            else:
+                sc = x
+            x = n.relu(n.add(y, sc))
+            c = co
+    n.output(x)
+    return n
+
+
 def efficientnet_b0(h=512, w=512):
     """cfg3/cfg5: EfficientNet-B0 backbone (EfficientDet-D0), taps P3/P4/P5.
 
