@@ -156,7 +156,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg{cfg.cid} {cfg.note}", "chunks_per_step": 1, "frames_per_chunk": cfg.L,
+            "config": {"workload": f"cfg{cfg.cid}: {cfg.note}", "chunks_per_step": 1, "frames_per_chunk": cfg.L,
                        "sample": "1 chunk per step"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"1 chunk x {cfg.L} frames of cfg{cfg.cid} per step"},
