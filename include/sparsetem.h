@@ -123,7 +123,9 @@ st_status st_encode_reference(st_encoder *enc, const float *ref_dev, int32_t n_c
  * frames_dev: chunk c, diff frame t (1..n_diff) at frames_dev +
  * c*chunk_stride + (t-1)*H*W*C (chunk_stride 0 = packed n_diff*H*W*C).
  * thresholds: host [n_sites] fp32 truncation thresholds, constant for the
- * call (R15).  n_diff = 0 runs the dense pass only.  Errors: ST_ERR_STATE
+ * call (R15).  n_diff = 0 runs the dense pass only.  Without streaming, a
+ * repeated call (no new st_encode_reference) recomputes the chunks from the
+ * staged reference frames.  Errors: ST_ERR_STATE
  * without a staged reference; ST_ERR_SHAPE if n_diff+1 > max_frames. */
 st_status st_encode_diff(st_encoder *enc, const float *frames_dev, int32_t n_diff,
                          int64_t chunk_stride, const float *thresholds, void *stream);

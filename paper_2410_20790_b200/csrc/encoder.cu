@@ -979,7 +979,10 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             const int act_kind = l.kind == ST_RELU ? ACT_RELU : ACT_SILU;
             // the dense reference activation uses the same SiLU form as the site (fast in BF16 mode)
             const int dense_kind = (act_kind == ACT_SILU && bf) ? ACT_SILU_FAST : act_kind;
-            if (!cont)
+            // a fused ReLU's dense output is read only by the pool's dense pass,
+            // which applies the ReLU itself (kept when streaming or debugging)
+            const bool skip_dense = l.fused_pool >= 0 && !strm && !e->cfg.debug_retain;
+            if (!cont && !skip_dense)
                 LAUNCH(e, KC_DENSE_MISC, i, s,
                        launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
             SiteState sst;
@@ -1007,8 +1010,12 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             break;
         }
         case ST_MAXPOOL: {
-            if (!cont)
-                LAUNCH(e, KC_DENSE_MISC, i, s, launch_dense_maxpool(x_src, e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), s));
+            if (!cont) {
+                const bool relu_in = l.fused_relu >= 0 && !strm && !e->cfg.debug_retain;
+                LAUNCH(e, KC_DENSE_MISC, i, s,
+                       launch_dense_maxpool(relu_in ? dense_of(e, e->L[l.fused_relu].src) : x_src,
+                                            e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), s, relu_in));
+            }
             // streaming state: x_acc of the input pixels ping-pongs (windows of
             // neighbouring tiles share pixels), y_acc of the outputs in place
             SiteState sst;

@@ -114,7 +114,8 @@ enum Act { ACT_RELU = 0, ACT_SILU = 1, ACT_SILU_FAST = 2 };   // FAST: BF16 mode
 // dense reference-frame ops; ybf (optional, may be null): bf16 (RNE) shadow
 // of y for a tensor-core conv that consumes y in dense mode
 void launch_dense_act(const float *x, float *y, int64_t n, int act, void *ybf, cudaStream_t s);
-void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s);
+void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s,
+                          bool relu_in = false);   // relu_in: x = pre-activation of a fused ReLU
 void launch_dense_add(const float *a, const float *b, float *y, int64_t n, void *ybf, cudaStream_t s);
 void launch_to_bf16(const float *x, void *ybf, int64_t n, cudaStream_t s);
 // Streaming state of a site (the per-site caches of the

@@ -73,7 +73,11 @@ void launch_dense_act(const float *x, float *y, int64_t n, int act, void *ybf, c
     else k_dense_act<ACT_SILU_FAST><<<grid, 256, 0, s>>>(x, y, n, ybf);
 }
 
-__global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g, void *ybf) {
+// relu_in: x is the pre-activation of a ReLU whose only consumer is this pool
+// (fused pair): y = relu(window max) == window max of relu(x) exactly (ReLU is
+// monotone, max is exact), so the ReLU's dense output is never materialised
+__global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__ y, int B, Geo g, void *ybf,
+                                bool relu_in) {
     st_pdl_enter();
     const int No = g.Hout * g.Wout;
     const int64_t n = (int64_t)B * No * g.Cin;
@@ -93,15 +97,16 @@ __global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__
                 m = v > m ? v : m;
             }
         }
+        if (relu_in) m = relu_f(m);
         y[i] = m;
         put_bf(ybf, i, m);
     }
 }
 
-void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s) {
+void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s, bool relu_in) {
     const int64_t n = (int64_t)B * g.Hout * g.Wout * g.Cin;
     const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
-    if (grid > 0) k_dense_maxpool<<<grid, 256, 0, s>>>(x, y, B, g, ybf);
+    if (grid > 0) k_dense_maxpool<<<grid, 256, 0, s>>>(x, y, B, g, ybf, relu_in);
 }
 
 __global__ void k_dense_add(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ y, int64_t n,
