@@ -284,9 +284,18 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
         const int ntaps = g.kh * g.kw;
         const bf16 *dd = static_cast<const bf16 *>(DENSE ? c.a_dense_bf : c.ddelta);
         const int wrow0 = warp * 32;
+        // sparse: the row code of the next work item is loaded one item ahead,
+        // so a tile boundary costs no dependent DRAM round trip (a stem tile
+        // is one or a few k-blocks)
+        auto row_code = [&](int w) -> int {
+            const int r = (2 * (w / ntn) + (int)rank) * BM + m;
+            return (!DENSE && w < nwork && r < M) ? __ldg(c.ridx + r) : 0;
+        };
+        int code_cur = row_code(cid);
         for (int w = cid; w < nwork; w += ncl) {
             const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
             const int r = mt * BM + m;
+            const int code_nxt = row_code(w + ncl);
             // this thread's row: input plane (chunk, or chunk x frame) and the
             // receptive-field origin; invalid rows get an origin no tap reaches
             int plane = 0, iy0 = -(1 << 20), ix0 = -(1 << 20);
@@ -297,7 +306,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     q = r - b * Nout;
                     plane = b;
                 } else {
-                    const int code = __ldg(c.ridx + r);
+                    const int code = code_cur;
                     b = (code >> 5) / Nout;
                     q = (code >> 5) - b * Nout;
                     plane = b * c.F + (code & 31);
@@ -305,6 +314,16 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 const int oy = q / g.Wout, ox = q - oy * g.Wout;
                 iy0 = oy * g.sh - g.ph;
                 ix0 = ox * g.sw - g.pw;
+            }
+            // the rows this lane stages are fixed for the whole tile: fetch their
+            // plane / origin from the owning lanes once, not once per k-block
+            int pl_r[16], iy_r[16], ix_r[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                const int rl = c.sr > 0 ? (4 * (i & 7) + (lane >> 3)) : (2 * i + (lane >> 4));
+                pl_r[i] = __shfl_sync(0xffffffffu, plane, rl);
+                iy_r[i] = __shfl_sync(0xffffffffu, iy0, rl);
+                ix_r[i] = __shfl_sync(0xffffffffu, ix0, rl);
             }
             for (int kb = 0; kb < nkb; kb++) {
                 mbar_wait(empty + stage, phase ^ 1);
@@ -320,9 +339,9 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
                         const int rl = 4 * i + (lane >> 3), row = wrow0 + rl;
-                        const int pl = __shfl_sync(0xffffffffu, plane, rl);
-                        const int iy = __shfl_sync(0xffffffffu, iy0, rl) + dy;
-                        const int ix = __shfl_sync(0xffffffffu, ix0, rl) + dxp;   // even
+                        const int pl = pl_r[i];
+                        const int iy = iy_r[i] + dy;
+                        const int ix = ix_r[i] + dxp;   // even
                         const bool valid = sv && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
                         const bf16 *src = dd + (valid ? ((int64_t)pl * Nin + iy * g.Win + ix) * 4 : 0);
                         cp_async16(sa + row * 128 + ((p ^ (row & 7)) << 4), src, valid ? 16u : 0u);
@@ -333,12 +352,12 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     const int tap = kb * 16 + j;
                     const bool tv = tap < ntaps;
                     const int dy = tv ? tap / g.kw : 0, dx = tv ? tap - (tap / g.kw) * g.kw : 0;
-#pragma unroll 4
+#pragma unroll
                     for (int i = 0; i < 16; i++) {
                         const int rl = 2 * i + (lane >> 4), row = wrow0 + rl;
-                        const int pl = __shfl_sync(0xffffffffu, plane, rl);
-                        const int iy = __shfl_sync(0xffffffffu, iy0, rl) + dy;
-                        const int ix = __shfl_sync(0xffffffffu, ix0, rl) + dx;
+                        const int pl = pl_r[i];
+                        const int iy = iy_r[i] + dy;
+                        const int ix = ix_r[i] + dx;
                         const bool valid = tv && iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win;
                         const int64_t pix = (int64_t)pl * Nin + iy * g.Win + ix;
                         cp_async8(sa + row * 128 + ((((j >> 1) ^ (row & 7)) << 4) | ((j & 1) << 3)),
@@ -352,6 +371,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
+            code_cur = code_nxt;
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp < 4) {
