@@ -120,14 +120,15 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def ncu_traffic(kernel_class):
+def ncu_traffic(kernel_class, cid):
     """dram bytes per launch of the dominant kernel from a committed ncu --set
-    full summary (profiles/ncu_summary.json), else None."""
+    full capture of this config's bench command (profiles/ncu_summary.json),
+    else None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get("kernels", {}).get(kernel_class, {}).get("dram_bytes_per_launch")
+            d = json.load(f).get("kernels", {}).get(kernel_class, {})
+        return d.get("dram_bytes_per_launch") if d.get("config") == cid else None
     except Exception:
         return None
 
@@ -381,7 +382,7 @@ def main():
         peak = float(peaks.get(peak_key, 1590.0))
         ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": ncu_traffic(dom), "kernel": dom,
+                "traffic": ncu_traffic(dom, cfg.cid), "kernel": dom,
                 "peak_source": f"{peak_src} {peak_key}",
                 "share_of_step": d["ms"] / args.steps / step_kernel_ms}
     elif d["flops"] > 0 and dom.startswith("conv"):
@@ -389,14 +390,14 @@ def main():
         peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": ncu_traffic(dom), "kernel": dom,
+                "traffic": ncu_traffic(dom, cfg.cid), "kernel": dom,
                 "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz",
                 "share_of_step": d["ms"] / args.steps / step_kernel_ms}
     else:
         peak = float(peaks["hbm_gbs"])
         ach = (d["bytes"] / nl) / (d["ms"] / nl / 1e3) / 1e9 if d["bytes"] else None
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": ncu_traffic(dom), "kernel": dom,
+                "frac": (ach / peak) if ach else None, "traffic": ncu_traffic(dom, cfg.cid), "kernel": dom,
                 "peak_source": peak_src, "share_of_step": d["ms"] / args.steps / step_kernel_ms}
 
     # ---- own dense path: every frame as a reference frame, same kernels

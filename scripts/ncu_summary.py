@@ -81,6 +81,7 @@ def main():
     ap.add_argument("--round", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--full", nargs="*", default=[])
+    ap.add_argument("--config", type=int, default=2, help="bench config the captures were taken on")
     a = ap.parse_args()
     os.makedirs("profiles", exist_ok=True)
     if a.launches:
@@ -113,7 +114,8 @@ def main():
         wr = sum(to_bytes(*d["dram__bytes_write.sum"]) for d in res) / len(res)
         ten = [float(d[k][0]) for d in res for k in ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",)
                if k in d and d[k][0] not in ("", "n/a")]
-        summ["kernels"][cls] = {"round": a.round, "kernel": res[0]["kernel"], "launches_averaged": len(res),
+        summ["kernels"][cls] = {"round": a.round, "config": a.config, "kernel": res[0]["kernel"],
+                                "launches_averaged": len(res),
                                 "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                                 "tensor_pipe_active_pct_mean": (sum(ten) / len(ten)) if ten else None,
                                 "source": os.path.basename(path)}
