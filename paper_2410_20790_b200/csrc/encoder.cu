@@ -953,10 +953,11 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             uint32_t *act = e->p<uint32_t>(l.b_act);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, act, s));
-            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(act, B * N, pb, e->totals + i, e->scan_tmp, st + 1, s));
             const bool dw_pm = l.depthwise && !e->dw_rowmajor;   // pixel-major depthwise needs no M-row list
-            if (!dw_pm)
-                LAUNCH(e, KC_ENUM, i, s, launch_enumerate(act, pb, B * N, e->p<int32_t>(l.b_ridx), s));
+            // scan of the output frame words; the M-row list is enumerated in the same pass
+            LAUNCH(e, KC_SCAN, i, s,
+                   launch_scan_popc(act, B * N, pb, e->totals + i, e->scan_tmp, st + 1, s,
+                                    dw_pm ? nullptr : e->p<int32_t>(l.b_ridx)));
             zero_row(l.b_rows, l.C);
             c.dense = false;
             c.bf = bf;

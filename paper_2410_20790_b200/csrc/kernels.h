@@ -52,8 +52,9 @@ void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaS
 // adds the total into *stat (int64) if stat != nullptr.  tmp: scan scratch
 // (scan_tmp_ints(n) int32).
 int64_t scan_tmp_ints(int64_t n);
+// ridx (optional): also enumerate the conv M-row list (replaces launch_enumerate)
 void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp,
-                      long long *stat, cudaStream_t s);
+                      long long *stat, cudaStream_t s, int32_t *ridx = nullptr);
 // ridx[pbase+j] = ((b*N+q) << 5) | t1 for every set bit of slot (conv M rows)
 void launch_enumerate(const uint32_t *slot, const int32_t *pbase, int64_t n, int32_t *ridx, cudaStream_t s);
 // per (b, t1) popcounts of act into counts[b*cstride + t1] (int64 atomics,

@@ -245,8 +245,21 @@ __global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *t
     }
 }
 
+// ridx (optional): the conv M-row list, ((b*N+q) << 5) | (t-1) for every set
+// bit in (b, p, t) order -- enumerated here from the word's own offset
+__device__ __forceinline__ void emit_codes(uint32_t w, int64_t i, int off, int32_t *ridx) {
+    int32_t *o = ridx + off;
+    const int32_t code = (int32_t)(i << 5);
+    while (w) {
+        const int t1 = __ffs(w) - 1;
+        w &= w - 1;
+        *o++ = code | t1;
+    }
+}
+
 __global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w, int64_t n,
-                                                  const int32_t *__restrict__ tmp, int32_t *__restrict__ pbase) {
+                                                  const int32_t *__restrict__ tmp, int32_t *__restrict__ pbase,
+                                                  int32_t *__restrict__ ridx) {
     st_pdl_enter();
     __shared__ int ws[32];
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_E;
@@ -261,21 +274,68 @@ __global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w
     int off = block_excl_scan(s, ws, tot) + tmp[blockIdx.x];
 #pragma unroll
     for (int e = 0; e < SCAN_E; e++) {
-        if (base + e < n) pbase[base + e] = off;
+        if (base + e < n) {
+            pbase[base + e] = off;
+            if (ridx && c[e]) emit_codes(__ldg(w + base + e), base + e, off, ridx);
+        }
         off += c[e];
     }
 }
 
+// one CTA for small word arrays: the whole scan (+ optional enumeration) in
+// one launch instead of scan1 / scan2 / scan3 / enumerate
+constexpr int SCAN_SMALL_T = 1024, SCAN_SMALL_MAX = 2048;   // larger arrays: the enumeration parallelises better over 3 passes
+__global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t *__restrict__ w, int64_t n,
+                                                             int32_t *__restrict__ pbase, int32_t *total,
+                                                             long long *stat, int32_t *__restrict__ ridx) {
+    st_pdl_enter();
+    __shared__ int ws[32];
+    int carry = 0;
+    for (int64_t b0 = 0; b0 < n; b0 += (int64_t)SCAN_SMALL_T * 4) {
+        const int64_t base = b0 + threadIdx.x * 4;
+        uint32_t v[4];
+        int c[4], sum = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            v[e] = base + e < n ? __ldg(w + base + e) : 0u;
+            c[e] = __popc(v[e]);
+            sum += c[e];
+        }
+        int tot;
+        int off = carry + block_excl_scan(sum, ws, tot);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (base + e < n) {
+                pbase[base + e] = off;
+                if (ridx && c[e]) emit_codes(v[e], base + e, off, ridx);
+            }
+            off += c[e];
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        *total = carry;
+        if (stat) atomicAdd((unsigned long long *)stat, (unsigned long long)carry);
+    }
+}
+
 void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp,
-                      long long *stat, cudaStream_t s) {
+                      long long *stat, cudaStream_t s, int32_t *ridx) {
     const int nb = cdiv(n, SCAN_TILE);
     if (nb == 0) {
         cudaMemsetAsync(total, 0, sizeof(int32_t), s);
         return;
     }
+    if (n <= SCAN_SMALL_MAX) {
+        k_scan_small<<<1, SCAN_SMALL_T, 0, s>>>(words, n, pbase, total, stat, ridx);
+        return;
+    }
     k_scan1<<<nb, SCAN_T, 0, s>>>(words, n, tmp);
     k_scan2<<<1, 1024, 0, s>>>(tmp, nb, total, stat);
-    k_scan3<<<nb, SCAN_T, 0, s>>>(words, n, tmp, pbase);
+    // enumeration in its own pass: one thread per word (up to 32 codes each)
+    // parallelises 8x better than the scan's 8-words-per-thread layout
+    k_scan3<<<nb, SCAN_T, 0, s>>>(words, n, tmp, pbase, nullptr);
+    if (ridx) launch_enumerate(words, pbase, n, ridx, s);
 }
 
 // -------------------------------------------------------------- enumerate
