@@ -7,8 +7,9 @@ For each config: st_memory_report of a SparseBatch encoder and of a
 streaming encoder (the vanilla DeltaCNN schedule's persistent per-site
 caches), the oracle accountant's element counts for both schedules, and the
 diff-frame throughput of (a) the SparseBatch step (reference + 31 diff
-frames) and (b) streaming continuation calls (no reference frame, each call
-continuing every chunk by L-1 frames).  CUDA events on the launch stream,
+frames), (b) streaming continuation calls (no reference frame, each call
+continuing every chunk by L-1 frames) and (c) the vanilla DeltaCNN schedule
+(reference + L-1 single-frame passes with the caches kept across passes).  CUDA events on the launch stream,
 L2 flushed between calls.  One JSON document on stdout.
 """
 import argparse
@@ -62,13 +63,21 @@ for cid in [int(c) for c in a.configs.split(",")]:
             ms += e0.elapsed_time(e1)
         return ms / k
 
-    for mode in ("sparsebatch", "streaming"):
-        enc = Encoder(net, B, L, precision=a.precision, streaming=(mode == "streaming"))
+    for mode in ("sparsebatch", "streaming", "vanilla"):
+        enc = Encoder(net, B, L, precision=a.precision, streaming=(mode != "sparsebatch"))
         mem = enc.memory_report()
         if mode == "sparsebatch":
             def step():
                 enc.encode_reference(x[:, 0], s)
                 enc.encode_diff(x[:, 1:L], th, s)
+            ms = timed(step, a.steps)
+        elif mode == "vanilla":
+            # the vanilla DeltaCNN schedule: one pass through
+            # all layers per frame index, every site's caches kept across passes
+            def step():
+                enc.encode_reference(x[:, 0], s)
+                for t in range(1, L):
+                    enc.encode_diff(x[:, t:t + 1], th, s)
             ms = timed(step, a.steps)
         else:
             enc.encode_reference(x[:, 0], s)
