@@ -103,8 +103,56 @@ __global__ void k_dense_maxpool(const float *__restrict__ x, float *__restrict__
     }
 }
 
+// C % 4 == 0: one thread per (output pixel, 4 channels), float4 window loads,
+// 32-bit index math (the scalar kernel above spends most of its time in 64-bit
+// divisions); the same max / relu per element
+__global__ void k_dense_maxpool4(const float *__restrict__ x, float *__restrict__ y, int B, Geo g, void *ybf,
+                                 bool relu_in) {
+    st_pdl_enter();
+    const int No = g.Hout * g.Wout, C4 = g.Cin >> 2;
+    const int n = B * No * C4;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int c4 = i % C4, bq = i / C4;
+        const int b = bq / No, q = bq - b * No;
+        const int oy = q / g.Wout, ox = q - oy * g.Wout;
+        float4 m = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+        for (int dy = 0; dy < g.kh; dy++) {
+            const int iy = oy * g.sh - g.ph + dy;
+            if (iy < 0 || iy >= g.Hin) continue;
+            for (int dx = 0; dx < g.kw; dx++) {
+                const int ix = ox * g.sw - g.pw + dx;
+                if (ix < 0 || ix >= g.Win) continue;
+                const float4 v =
+                    __ldg(reinterpret_cast<const float4 *>(x + ((int64_t)(b * g.Hin + iy) * g.Win + ix) * g.Cin) + c4);
+                m.x = v.x > m.x ? v.x : m.x;
+                m.y = v.y > m.y ? v.y : m.y;
+                m.z = v.z > m.z ? v.z : m.z;
+                m.w = v.w > m.w ? v.w : m.w;
+            }
+        }
+        if (relu_in) {
+            m.x = relu_f(m.x);
+            m.y = relu_f(m.y);
+            m.z = relu_f(m.z);
+            m.w = relu_f(m.w);
+        }
+        reinterpret_cast<float4 *>(y)[i] = m;
+        if (ybf) {
+            uint2 u;
+            u.x = RowIO<bf16, 2>::pack(m.x, m.y);
+            u.y = RowIO<bf16, 2>::pack(m.z, m.w);
+            reinterpret_cast<uint2 *>(ybf)[i] = u;
+        }
+    }
+}
+
 void launch_dense_maxpool(const float *x, float *y, int B, const Geo &g, void *ybf, cudaStream_t s, bool relu_in) {
     const int64_t n = (int64_t)B * g.Hout * g.Wout * g.Cin;
+    if (g.Cin % 4 == 0 && n < (int64_t)1 << 31) {
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n / 4, 256), 148 * 16));
+        k_dense_maxpool4<<<grid, 256, 0, s>>>(x, y, B, g, ybf, relu_in);
+        return;
+    }
     const int grid = (int)std::min<int64_t>(cdiv(n, 256), 148 * 16);
     if (grid > 0) k_dense_maxpool<<<grid, 256, 0, s>>>(x, y, B, g, ybf, relu_in);
 }
