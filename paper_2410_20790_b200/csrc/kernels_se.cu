@@ -402,7 +402,11 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
     if (C % 8 == 0 && F >= 1 && F <= 32) {
         // channel slice: as many 8-channel groups as fit 256 threads at F frames
         const int CS = std::max(8, std::min((C + 7) / 8 * 8, (256 / F) * 8));
-        const int ppb = 2048;
+        // pixels per block: enough blocks for two waves of the 148 SMs (small
+        // late-stage maps otherwise ran 32 blocks), 256-pixel granules, <= 2048
+        const int nsl = cdiv(C, CS);
+        const int want = std::max(1, 296 / std::max(1, nsl * B));
+        const int ppb = std::min(2048, std::max(256, (cdiv(N, want) + 255) / 256 * 256));
         dim3 grid(cdiv(N, ppb), cdiv(C, CS), B);
         if (bf) k_se_delta_sums_v<bf16><<<grid, 256, 0, s>>>(in, N, C, F, ppb, CS, dsum);
         else k_se_delta_sums_v<float><<<grid, 256, 0, s>>>(in, N, C, F, ppb, CS, dsum);
