@@ -221,8 +221,8 @@ constexpr int DWT_STG = 96 * 1024;         // staging bytes per CTA (two CTAs pe
 template <class TI>
 struct DwTile {
     static constexpr int EPL = 16 / (int)sizeof(TI);   // elements per 16-byte piece
-    static size_t smem(int FP, int TO, int kk) {
-        return (size_t)kk * DWT_CS * 4 + (size_t)FP * 12 + (size_t)TO * 8 + DWT_STG + 64;
+    static size_t smem(int FP, int TO, int kk, size_t stg) {
+        return (size_t)kk * DWT_CS * 4 + (size_t)FP * 12 + (size_t)TO * 8 + stg + 64;
     }
 };
 
@@ -396,11 +396,19 @@ static bool launch_dw_tile_t(const ConvCall &c, const uint32_t *out_act, const i
     if (g.Cin % 8 != 0) return false;
     // footprint small enough that a group holds >= 4 frames (sparse) / 1 frame (dense)
     const int csw = std::min(DWT_CS, g.Cin);
-    const int fp_max = std::min<int>(512, (int)(DWT_STG / ((DENSE ? 1 : 4) * csw * sizeof(TI))));
+    // dense: a smaller staging budget -> more resident CTAs overlap their
+    // staging round trips (the sparse frame-group path keeps DWT_STG)
+    static const int dense_stg = [] {
+        const char *v = getenv("ST_DW_DENSE_STG_KB");
+        return (v ? atoi(v) : 48) * 1024;   // measured: 48 KB best of 96 / 48 / 32 on cfg5
+    }();
+    const int stg_budget = DENSE ? std::min(dense_stg, DWT_STG) : DWT_STG;
+    const int fp_max = std::min<int>(512, (int)(stg_budget / ((DENSE ? 1 : 4) * csw * sizeof(TI))));
     int TOH, TOW;
     if (!dw_tile_dims(g, fp_max, TOH, TOW)) return false;
     const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
-    const size_t sm = DwTile<TI>::smem(FP, TOH * TOW, g.kh * g.kw);
+    const size_t sm = DwTile<TI>::smem(FP, TOH * TOW, g.kh * g.kw,
+                                       DENSE ? (size_t)FP * csw * sizeof(TI) + 16 : (size_t)DWT_STG);
     const int64_t grid = (int64_t)c.B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW) *
                          ((g.Cin + DWT_CS - 1) / DWT_CS);
     static bool attr = false;
