@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t
                                                       const int32_t *__restrict__ out_pbase) {
     st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 4 : 3;   // active taps loaded per batch
+    constexpr bool PAIR = sizeof(T) == 2 && CPL == 8;   // two frames per pass (see below)
     extern __shared__ int4 dw_meta[];   // [256/G groups][KMAX] {act, slot, 1 + pbase, 0}
     const Geo g = c.g;
     const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
@@ -157,6 +158,91 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t
         }
         __syncwarp(gmask);
         int64_t orow = 1 + __ldg(out_pbase + bq);
+        if constexpr (PAIR) {
+            // bf16, 8 channels per lane: two frames per pass over the live taps,
+            // rows kept as raw 16-byte vectors until their FMA (the register cost
+            // of one frame's float rows), so each round trip serves up to TB
+            // taps x 2 frames; every frame's chain stays in ascending tap order
+            while (w) {
+                const int tA = __ffs(w) - 1;
+                w &= w - 1;
+                const int tB = w ? __ffs(w) - 1 : -1;
+                if (w) w &= w - 1;
+                const uint32_t lmA = lowmask(tA), lmB = tB >= 0 ? lowmask(tB) : 0u;
+                const uint32_t fm = (1u << tA) | (tB >= 0 ? 1u << tB : 0u);
+                for (int cb = 0; cb < C; cb += G * CPL) {
+                    const int c0 = cb + lane * CPL;
+                    const bool full = c0 + CPL <= C;
+                    auto load_raw = [&](int64_t row) -> uint4 {
+                        if (full) return *reinterpret_cast<const uint4 *>(A + row * C + c0);
+                        const uint16_t *r16 = reinterpret_cast<const uint16_t *>(A + row * C);
+                        uint32_t h[8];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) h[i] = c0 + i < C ? r16[c0 + i] : 0u;
+                        return make_uint4(h[0] | h[1] << 16, h[2] | h[3] << 16, h[4] | h[5] << 16, h[6] | h[7] << 16);
+                    };
+                    float accA[8], accB[8];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) accA[i] = accB[i] = 0.0f;
+                    int k = 0;
+                    while (k < nlive) {
+                        int tp[TB];
+                        uint4 vA[TB], vB[TB];
+                        uint32_t on = 0;   // bit 2j: tap j active in frame A, bit 2j+1: in frame B
+#pragma unroll
+                        for (int j = 0; j < TB; j++) {
+                            tp[j] = -1;
+                            while (k < nlive) {
+                                const int tap = meta[k].w;
+                                k++;
+                                const int4 m = meta[tap];
+                                const uint32_t hit = (uint32_t)m.x & fm;
+                                if (hit) {
+                                    tp[j] = tap;
+                                    if ((hit >> tA) & 1u) {
+                                        vA[j] = load_raw(m.z + __popc((uint32_t)m.y & lmA));
+                                        on |= 1u << (2 * j);
+                                    }
+                                    if (tB >= 0 && ((hit >> tB) & 1u)) {
+                                        vB[j] = load_raw(m.z + __popc((uint32_t)m.y & lmB));
+                                        on |= 2u << (2 * j);
+                                    }
+                                    break;
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < TB; j++) {
+                            if (tp[j] < 0) continue;
+                            float wv[8];
+                            row_load<float, 8>(c.wk + (int64_t)tp[j] * C, c0, C, full, wv);
+                            if ((on >> (2 * j)) & 1u) {
+                                const uint32_t u[4] = {vA[j].x, vA[j].y, vA[j].z, vA[j].w};
+#pragma unroll
+                                for (int q = 0; q < 4; q++) {
+                                    accA[2 * q] = fmaf(wv[2 * q], __uint_as_float(u[q] << 16), accA[2 * q]);
+                                    accA[2 * q + 1] = fmaf(wv[2 * q + 1], __uint_as_float(u[q] & 0xFFFF0000u), accA[2 * q + 1]);
+                                }
+                            }
+                            if ((on >> (2 * j + 1)) & 1u) {
+                                const uint32_t u[4] = {vB[j].x, vB[j].y, vB[j].z, vB[j].w};
+#pragma unroll
+                                for (int q = 0; q < 4; q++) {
+                                    accB[2 * q] = fmaf(wv[2 * q], __uint_as_float(u[q] << 16), accB[2 * q]);
+                                    accB[2 * q + 1] = fmaf(wv[2 * q + 1], __uint_as_float(u[q] & 0xFFFF0000u), accB[2 * q + 1]);
+                                }
+                            }
+                        }
+                    }
+                    if (c0 < C) {
+                        row_store<T, 8>(O + orow * C, c0, C, full, accA);
+                        if (tB >= 0) row_store<T, 8>(O + (orow + 1) * C, c0, C, full, accB);
+                    }
+                }
+                orow += tB >= 0 ? 2 : 1;
+            }
+            continue;
+        }
         while (w) {
             const int t1 = __ffs(w) - 1;
             w &= w - 1;
