@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
 // then read back as one 16-byte broadcast per tap, so 5x5 kernels keep the
 // register budget of two CTAs per SM.
 template <int G, int CPL, int KMAX, class T>
-__global__ void __launch_bounds__(256, 2) k_dwconv_pm(ConvCall c, const uint32_t *__restrict__ out_act,
+__global__ void __launch_bounds__(256, 3) k_dwconv_pm(ConvCall c, const uint32_t *__restrict__ out_act,
                                                       const int32_t *__restrict__ out_pbase) {
     st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 4 : 3;   // active taps loaded per batch
