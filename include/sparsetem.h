@@ -179,6 +179,20 @@ st_status st_debug_get_rows(st_encoder *enc, int32_t layer, int32_t chunk, int32
  * (requires debug_retain), host [H*W*C]. */
 st_status st_debug_get_dense0(st_encoder *enc, int32_t layer, int32_t chunk, float *host);
 
+/* Debug: mask export for parity checks in the production launch
+ * configuration (no debug_retain, arena reuse, CUDA-graph replay).  After
+ * st_debug_export_chunk(enc, chunk), every following st_encode_diff also
+ * copies, for that chunk only, the frame words of every layer boundary --
+ * uint32 per pixel, bit t-1 set <=> pixel active in diff frame t (the
+ * emitted mask at a site, the dilated structural mask at a conv) -- into a
+ * buffer the encoder owns (sum over layers of H*W words); chunk = -1 turns it
+ * off.  The copies are stream-ordered nodes of the step.  ST_ERR_ARG for a
+ * chunk >= max_chunks, ST_ERR_OOM if the buffer cannot be allocated.
+ * st_debug_get_words: host copy of layer `layer`'s words (-1 = input site)
+ * [H_l*W_l]; syncs the stream; ST_ERR_STATE before an exporting diff call. */
+st_status st_debug_export_chunk(st_encoder *enc, int32_t chunk);
+st_status st_debug_get_words(st_encoder *enc, int32_t layer, uint32_t *words_host);
+
 /* Memory report of the SparseBatch plan (bytes): persistent (staged
  * reference + outputs), peak transient (max live set), arena total. */
 st_status st_memory_report(const st_encoder *enc, int64_t *persistent, int64_t *peak_transient,

@@ -20,6 +20,16 @@ class _Layer(C.Structure):
                [(n, C.POINTER(C.c_float)) for n in ("w", "b", "w2", "b2")]
 
 
+class _Follow(C.Structure):
+    _fields_ = [("masks", C.c_void_p), ("a_theta", C.c_float), ("a_rms", C.c_float), ("a_abs", C.c_float),
+                ("stats", C.c_void_p)]
+
+
+# Ambiguity bands of reading R23 (tau = a_theta*theta + a_rms*rms + a_abs)
+TAU_FP32 = (1e-4, 0.0, 1e-5)
+TAU_BF16 = (2e-2, 2e-2, 0.0)
+
+
 def lib_path():
     return _LIB
 
@@ -45,6 +55,7 @@ def _load():
         lib.orc_dense_forward.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P]
         lib.orc_run_chunk.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
                                       C.c_int, P, P, P, P, P, P, P]
+        lib.orc_run_chunk_follow.argtypes = lib.orc_run_chunk.argtypes + [P]
         lib.orc_dilate.argtypes = [P] + [C.c_int] * 10 + [P]
         lib.orc_set_precision.argtypes = [C.c_int]
         _lib = lib
@@ -111,7 +122,8 @@ def dense_forward(net, frame, precision="fp32"):
 
 
 def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_deltas=False,
-              want_dense0=False, mask_layers=None, delta_layers=None, precision="fp32"):
+              want_dense0=False, mask_layers=None, delta_layers=None, precision="fp32",
+              follow=None, tau=None):
     """Run one chunk (frames float32 [L][H][W][C]) through dense + diff.
 
     Returns dict with
@@ -121,6 +133,12 @@ def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_
       taps[l]   float32 [L][H_l][W_l][C_l] for OUTPUT layers
       counts    int64 [n_sites][L-1]
       in_mask   uint8 [L-1][H][W]   input-site mask; in_delta float32 [L-1][H][W][C]
+
+    follow: band-follow mode (O12, reading R23) -- {site layer: GPU emitted
+    mask uint8 [L-1][H_l][W_l]}; inside the ambiguity band (tau, default the
+    precision's R23 band) the oracle adopts the GPU's decision, elsewhere it
+    keeps its own.  Adds follow_stats int64 [n_layers][4] = (decisions, in
+    band, adopted, violations).
     """
     lib = _load()
     lib.orc_set_precision(1 if precision == "bf16" else 0)
@@ -150,13 +168,29 @@ def run_chunk(net, frames, thresholds, layer_outer=False, want_masks=True, want_
     counts = np.zeros((ns, max(F, 1)), np.int64)
     in_mask = np.zeros((max(F, 1), net.in_h, net.in_w), np.uint8)
     in_delta = np.zeros((max(F, 1), net.in_h, net.in_w, net.in_c), np.float32) if want_deltas else None
-    r = lib.orc_run_chunk(sp.ptr, n, net.in_h, net.in_w, net.in_c, Lf, fr.ctypes.data,
-                          th.ctypes.data, int(bool(layer_outer)), mp, dp, zp, tp, counts.ctypes.data,
-                          in_mask.ctypes.data, None if in_delta is None else in_delta.ctypes.data)
+    fl, fstats, keep = None, None, []
+    if follow is not None:
+        fp = (C.c_void_p * n)()
+        for li, m in follow.items():
+            m = np.ascontiguousarray(m, np.uint8).reshape(F, -1)
+            assert m.shape[1] == shp[li][0] * shp[li][1], f"follow mask of layer {li} has the wrong size"
+            keep.append(m)
+            fp[li] = m.ctypes.data
+        keep.append(fp)
+        fstats = np.zeros((n, 4), np.int64)
+        a = tau if tau is not None else (TAU_BF16 if precision == "bf16" else TAU_FP32)
+        fl = _Follow(C.cast(fp, C.c_void_p), float(a[0]), float(a[1]), float(a[2]), fstats.ctypes.data)
+    r = lib.orc_run_chunk_follow(sp.ptr, n, net.in_h, net.in_w, net.in_c, Lf, fr.ctypes.data,
+                                 th.ctypes.data, int(bool(layer_outer)), mp, dp, zp, tp, counts.ctypes.data,
+                                 in_mask.ctypes.data, None if in_delta is None else in_delta.ctypes.data,
+                                 None if fl is None else C.addressof(fl))
     if r:
         raise ValueError(f"oracle run_chunk failed ({r})")
-    return dict(masks=masks, deltas=deltas, dense0=dense0, taps=taps, counts=counts[:, :F],
-                in_mask=in_mask[:F], in_delta=None if in_delta is None else in_delta[:F])
+    out = dict(masks=masks, deltas=deltas, dense0=dense0, taps=taps, counts=counts[:, :F],
+               in_mask=in_mask[:F], in_delta=None if in_delta is None else in_delta[:F])
+    if fstats is not None:
+        out["follow_stats"] = fstats
+    return out
 
 
 def dilate(mask, k, s, p, out_hw):

@@ -112,16 +112,15 @@ static float relu_f(float x) { return x > 0.0f ? x : 0.0f; }
 static float silu_f(float x) { return x / (1.0f + exp_r(-x)); }          /* R10 */
 static float sigm_f(float x) { return 1.0f / (1.0f + exp_r(-x)); }       /* R10 */
 
-/* Precision mode (R22-BF16).  0 = FP32 mode.  1 = BF16 mode:
+/* Precision mode (R22-BF16).  0 = FP32 mode.  1 = BF16 mode, a
+ * contract stated without reference to how the GPU dispatches its kernels:
  *  - every emitted delta (input Subtraction, conv output, residual add, every
  *    non-linear site) is stored rounded to bf16 (round-to-nearest-even); the
  *    truncation decision is taken on the fp32 value, and the Subtraction
  *    buffer S and each site's y_acc advance by the rounded (emitted) value;
- *  - a convolution with groups == 1 and either c_in % 8 == 0, c_out % 8 == 0
- *    and at most 9 taps, or reading the network input with c_in <= 4,
- *    c_out % 16 == 0 and at most 64 taps, multiplies bf16-rounded operands
- *    (weight and input value) and accumulates in fp32;
- *  - dense reference activations, site states and outputs stay fp32. */
+ *  - EVERY convolution (dense or delta, any groups / kernel size) multiplies
+ *    bf16-rounded operands (weight and input value) and accumulates in fp32;
+ *  - dense reference activations, site states, SE gates and outputs stay fp32. */
 static int g_bf16 = 0;
 void orc_set_precision(int bf16) { g_bf16 = bf16 ? 1 : 0; }
 
@@ -145,13 +144,7 @@ static void conv_apply(const orc_layer *l, shp si, shp so, const float *x, const
                        int with_bias, float *out) {
     const int cin_g = si.c / l->groups, cout_g = l->c_out / l->groups;
     const int No = so.h * so.w;
-    /* BF16 mode: tensor-core convs (R22-BF16) -- c_in, c_out % 8 == 0 with at
-     * most 9 taps, or a stem on the network input with c_in <= 4, c_out % 16
-     * == 0 and <= 64 taps */
-    const int taps = l->k_h * l->k_w;
-    const int rb = g_bf16 && l->groups == 1 &&
-                   ((si.c % 8 == 0 && l->c_out % 8 == 0 && taps <= 9) ||
-                    (l->src == -1 && si.c <= 4 && l->c_out % 16 == 0 && taps <= 64));
+    const int rb = g_bf16;   /* R22-BF16: every conv multiplies bf16-rounded operands */
 #pragma omp parallel for schedule(static)
     for (int q = 0; q < No; q++) {
         float *o = out + (size_t)q * so.c;
@@ -299,6 +292,23 @@ void orc_dilate(const uint8_t *m, int H, int W, int kh, int kw, int sh, int sw, 
 
 /* ------------------------------------------------------ diff computation */
 
+/* O12 band-follow (reading R23).  A truncation decision
+ * compares max_c |c| with theta; where the two sides' values of c are not
+ * bit-matched (BF16 mode, SiLU / SE), every decision whose value lies inside
+ * the ambiguity band |max_c|c| - theta| <= tau is a correct one.  With follow
+ * masks given (the GPU's emitted masks of one chunk, per site layer [F][N_l]),
+ * the oracle adopts the GPU's decision ONLY inside the band; every other
+ * decision stays its own, and a disagreement there is counted as a violation.
+ * tau = a_theta * theta + a_rms * rms + a_abs, rms = root mean square of the
+ * oracle's candidate values over the touched pixels of that site and frame.
+ * stats per layer: [0] decisions, [1] inside the band, [2] adopted (the GPU's
+ * decision differed from the oracle's own), [3] violations. */
+typedef struct {
+    const uint8_t *const *masks;   /* [n] per layer ([F][N_l]) or NULL entries */
+    float a_theta, a_rms, a_abs;
+    int64_t *stats;                /* [n][4] */
+} follow_t;
+
 typedef struct {
     const orc_layer *L;
     int n, L_frames;
@@ -311,6 +321,10 @@ typedef struct {
     float **otap;          /* running output at OUTPUT layers */
     float *S;              /* Subtraction buffer */
     int64_t *counts;       /* [n_sites][L-1] */
+    const follow_t *fl;    /* band-follow (NULL = off) */
+    /* scratch of one site step: candidate rows [N][C], max_c |cand| [N], touched [N] */
+    float *cand, *mx;
+    uint8_t *T;
 } ctx_t;
 
 static shp src_shape(const ctx_t *c, int i) { return i < 0 ? c->in : c->s[i]; }
@@ -344,23 +358,72 @@ static void step_input(ctx_t *c, int t, const float *X, float *d, uint8_t *m) {
     if (c->counts) c->counts[(size_t)0 * (c->L_frames - 1) + (t - 1)] = cnt;
 }
 
-/* truncate candidate row cand[C] at one pixel; returns 1 if emitted. */
-static int trunc_emit(const float *cand, int C, float th, float *ya, float *dout) {
+static float row_absmax(const float *v, int C) {
     float mx = 0.0f;
     for (int ch = 0; ch < C; ch++) {
-        const float a = fabsf(cand[ch]);
+        const float a = fabsf(v[ch]);
         mx = a > mx ? a : mx;
     }
-    if (mx > th) {
-        for (int ch = 0; ch < C; ch++) {
-            const float e = emit_r(cand[ch]);   /* stored delta; y_acc advances by it */
-            ya[ch] = ya[ch] + e;
-            dout[ch] = e;
-        }
-        return 1;
+    return mx;
+}
+
+/* Truncation of one non-linear site for one frame (R1/R2/R7): the
+ * candidate rows c->cand of the touched pixels c->T are already computed,
+ * c->mx[p] = max_c |cand|.  Keep iff max_c |cand| > theta (strict); a kept
+ * row is emitted (stored rounded in BF16 mode) and y_acc advances by the
+ * emitted value; everything else is exactly 0.  Returns the emitted count. */
+static int64_t truncate_site(ctx_t *c, int i, int t, int No, int C, float *ya, float *d, uint8_t *m) {
+    const float th = c->theta[c->site[i]];
+    const uint8_t *fm = (c->fl && c->fl->masks && c->fl->masks[i]) ? c->fl->masks[i] + (size_t)(t - 1) * No : NULL;
+    double tau = 0.0;
+    int64_t *fs = fm ? c->fl->stats + (size_t)4 * i : NULL;
+    if (fm) {
+        double ss = 0.0;
+        int64_t n = 0;
+        for (int p = 0; p < No; p++)
+            if (c->T[p]) {
+                for (int ch = 0; ch < C; ch++) {
+                    const double v = c->cand[(size_t)p * C + ch];
+                    ss += v * v;
+                }
+                n += C;
+            }
+        const double rms = n ? sqrt(ss / (double)n) : 0.0;
+        tau = (double)c->fl->a_theta * th + (double)c->fl->a_rms * rms + (double)c->fl->a_abs;
     }
-    for (int ch = 0; ch < C; ch++) dout[ch] = 0.0f;
-    return 0;
+    int64_t cnt = 0;
+    for (int p = 0; p < No; p++) {
+        float *dp = d + (size_t)p * C;
+        int keep = 0;
+        if (c->T[p]) {
+            keep = c->mx[p] > th;                                   /* R1: strict */
+            if (fm) {
+                fs[0]++;
+                if (fabs((double)c->mx[p] - (double)th) <= tau) {
+                    fs[1]++;
+                    if ((int)fm[p] != keep) { fs[2]++; keep = fm[p]; }
+                } else if ((int)fm[p] != keep) {
+                    fs[3]++;
+                }
+            }
+        } else if (fm && fm[p]) {
+            fs[3]++;                                                /* GPU emitted an untouched pixel */
+        }
+        m[p] = (uint8_t)keep;
+        if (keep) {
+            const float *cp = c->cand + (size_t)p * C;
+            float *yp = ya + (size_t)p * C;
+            for (int ch = 0; ch < C; ch++) {
+                const float e = emit_r(cp[ch]);    /* stored delta; y_acc advances by it */
+                yp[ch] = yp[ch] + e;
+                dp[ch] = e;
+            }
+            cnt++;
+        } else {
+            for (int ch = 0; ch < C; ch++) dp[ch] = 0.0f;
+        }
+    }
+    return cnt;
 }
 
 /* one layer, one diff frame t.  d_a/m_a: src delta; d_b/m_b: src2 delta (ADD). */
@@ -398,74 +461,64 @@ static void step_layer(ctx_t *c, int i, int t, const float *d_a, const uint8_t *
     }
     case ORC_RELU: case ORC_SILU: {
         float *xa = c->xacc[i], *ya = c->yacc[i];
-        const float th = c->theta[c->site[i]];
-        float cand[4096];
+        const int relu = l->kind == ORC_RELU;
+#pragma omp parallel for schedule(static)
         for (int p = 0; p < No; p++) {
-            if (!m_a[p]) {                                          /* untouched */
-                m[p] = 0;
-                for (int ch = 0; ch < C; ch++) d[(size_t)p * C + ch] = 0.0f;
-                continue;
-            }
+            c->T[p] = m_a[p];                                       /* touched = input mask (R7) */
+            if (!m_a[p]) continue;
+            float *cp = c->cand + (size_t)p * C;
             for (int ch = 0; ch < C; ch++) {
                 const size_t k = (size_t)p * C + ch;
                 xa[k] = xa[k] + d_a[k];                             /* reconstruct input */
-                const float f = l->kind == ORC_RELU ? relu_f(xa[k]) : silu_f(xa[k]);
-                cand[ch] = f - ya[k];                               /* restore delta */
+                const float f = relu ? relu_f(xa[k]) : silu_f(xa[k]);
+                cp[ch] = f - ya[k];                                 /* restore delta (Eq.3) */
             }
-            m[p] = (uint8_t)trunc_emit(cand, C, th, ya + (size_t)p * C, d + (size_t)p * C);
-            cnt += m[p];
+            c->mx[p] = row_absmax(cp, C);
         }
+        cnt = truncate_site(c, i, t, No, C, ya, d, m);
         break;
     }
     case ORC_MAXPOOL: {
         float *xa = c->xacc[i], *ya = c->yacc[i];
-        const float th = c->theta[c->site[i]];
         for (int p = 0; p < Ni; p++)
             if (m_a[p])
                 for (int ch = 0; ch < C; ch++) xa[(size_t)p * C + ch] = xa[(size_t)p * C + ch] + d_a[(size_t)p * C + ch];
-        uint8_t *T = (uint8_t *)malloc(No);
-        dilate(m_a, si.h, si.w, l->k_h, l->k_w, l->s_h, l->s_w, l->p_h, l->p_w, so.h, so.w, T);
-        float cand[4096], mw[4096];
+        /* touched = pool-footprint dilation of the input mask (R7) */
+        dilate(m_a, si.h, si.w, l->k_h, l->k_w, l->s_h, l->s_w, l->p_h, l->p_w, so.h, so.w, c->T);
+#pragma omp parallel for schedule(static)
         for (int q = 0; q < No; q++) {
-            if (!T[q]) {
-                m[q] = 0;
-                for (int ch = 0; ch < C; ch++) d[(size_t)q * C + ch] = 0.0f;
-                continue;
-            }
-            maxwin(l, si, so, xa, q, mw);
-            for (int ch = 0; ch < C; ch++) cand[ch] = mw[ch] - ya[(size_t)q * C + ch];
-            m[q] = (uint8_t)trunc_emit(cand, C, th, ya + (size_t)q * C, d + (size_t)q * C);
-            cnt += m[q];
+            if (!c->T[q]) continue;
+            float *cp = c->cand + (size_t)q * C;
+            maxwin(l, si, so, xa, q, cp);
+            for (int ch = 0; ch < C; ch++) cp[ch] = cp[ch] - ya[(size_t)q * C + ch];
+            c->mx[q] = row_absmax(cp, C);
         }
-        free(T);
+        cnt = truncate_site(c, i, t, No, C, ya, d, m);
         break;
     }
     case ORC_SE: {
         float *xa = c->xacc[i], *ya = c->yacc[i], *se = c->semit[i];
-        const float th = c->theta[c->site[i]];
         for (int p = 0; p < Ni; p++)
             if (m_a[p])
                 for (int ch = 0; ch < C; ch++) xa[(size_t)p * C + ch] = xa[(size_t)p * C + ch] + d_a[(size_t)p * C + ch];
         float *st = (float *)malloc(sizeof(float) * C);
-        se_gate(l, si, xa, st);
+        se_gate(l, si, xa, st);                                     /* s_t = gate(x_acc) */
         float ds = 0.0f;
         for (int ch = 0; ch < C; ch++) {
             const float a = fabsf(st[ch] - se[ch]);
             ds = a > ds ? a : ds;
         }
-        const int refresh = ds > th;                                /* R8, theta_gate = theta_site */
+        const int refresh = ds > c->theta[c->site[i]];              /* R8, theta_gate = theta_site */
         if (refresh) memcpy(se, st, sizeof(float) * C);
-        float cand[4096];
+#pragma omp parallel for schedule(static)
         for (int p = 0; p < No; p++) {
-            if (!refresh && !m_a[p]) {
-                m[p] = 0;
-                for (int ch = 0; ch < C; ch++) d[(size_t)p * C + ch] = 0.0f;
-                continue;
-            }
-            for (int ch = 0; ch < C; ch++) cand[ch] = xa[(size_t)p * C + ch] * se[ch] - ya[(size_t)p * C + ch];
-            m[p] = (uint8_t)trunc_emit(cand, C, th, ya + (size_t)p * C, d + (size_t)p * C);
-            cnt += m[p];
+            c->T[p] = (uint8_t)(refresh || m_a[p]);                  /* refresh touches every pixel */
+            if (!c->T[p]) continue;
+            float *cp = c->cand + (size_t)p * C;
+            for (int ch = 0; ch < C; ch++) cp[ch] = xa[(size_t)p * C + ch] * se[ch] - ya[(size_t)p * C + ch];
+            c->mx[p] = row_absmax(cp, C);
         }
+        cnt = truncate_site(c, i, t, No, C, ya, d, m);
         free(st);
         break;
     }
@@ -487,19 +540,30 @@ static void step_layer(ctx_t *c, int i, int t, const float *d_a, const uint8_t *
  *   in_delta   float [(L-1)][N_in][C]    input-site emitted delta
  * thresholds: float [n_sites]; site 0 = input, then nonlinear layers in order.
  */
-int orc_run_chunk(const orc_layer *L, int n, int in_h, int in_w, int in_c, int Lf,
-                  const float *frames, const float *thresholds, int layer_outer,
-                  uint8_t **masks, float **deltas, float **dense0, float **taps, int64_t *counts,
-                  uint8_t *in_mask, float *in_delta) {
+/* follow (nullable): band-follow mode, see follow_t above */
+int orc_run_chunk_follow(const orc_layer *L, int n, int in_h, int in_w, int in_c, int Lf,
+                         const float *frames, const float *thresholds, int layer_outer,
+                         uint8_t **masks, float **deltas, float **dense0, float **taps, int64_t *counts,
+                         uint8_t *in_mask, float *in_delta, const follow_t *follow) {
     if (Lf < 1 || in_c > 64) return -10;
     ctx_t c;
     memset(&c, 0, sizeof c);
     c.L = L; c.n = n; c.L_frames = Lf; c.theta = thresholds; c.counts = counts;
     c.in.h = in_h; c.in.w = in_w; c.in.c = in_c;
+    c.fl = follow;
     c.s = (shp *)malloc(sizeof(shp) * n);
     int r = infer(L, n, c.in, c.s);
     if (r) { free(c.s); return r; }
-    for (int i = 0; i < n; i++) if (c.s[i].c > 4096) { free(c.s); return -11; }
+    size_t max_nc = 1, max_n = 1;
+    for (int i = 0; i < n; i++)
+        if (is_nonlinear(L[i].kind)) {
+            const size_t No = (size_t)c.s[i].h * c.s[i].w;
+            if (No * c.s[i].c > max_nc) max_nc = No * c.s[i].c;
+            if (No > max_n) max_n = No;
+        }
+    c.cand = (float *)malloc(max_nc * sizeof(float));
+    c.mx = (float *)malloc(max_n * sizeof(float));
+    c.T = (uint8_t *)malloc(max_n);
     c.site = (int *)calloc(n, sizeof(int));
     for (int i = 0, s = 1; i < n; i++) if (is_nonlinear(L[i].kind)) c.site[i] = s++;
     c.xacc = (float **)calloc(n, sizeof(float *));
@@ -618,5 +682,14 @@ int orc_run_chunk(const orc_layer *L, int n, int in_h, int in_w, int in_c, int L
     }
     free(y0); free(c.xacc); free(c.yacc); free(c.semit); free(c.otap);
     free(c.S); free(c.site); free(c.s);
+    free(c.cand); free(c.mx); free(c.T);
     return 0;
+}
+
+int orc_run_chunk(const orc_layer *L, int n, int in_h, int in_w, int in_c, int Lf,
+                  const float *frames, const float *thresholds, int layer_outer,
+                  uint8_t **masks, float **deltas, float **dense0, float **taps, int64_t *counts,
+                  uint8_t *in_mask, float *in_delta) {
+    return orc_run_chunk_follow(L, n, in_h, in_w, in_c, Lf, frames, thresholds, layer_outer, masks, deltas,
+                                dense0, taps, counts, in_mask, in_delta, NULL);
 }

@@ -60,6 +60,8 @@ SIGNATURES = {
     "st_debug_get_mask": (I32, [P, I32, I32, I32, P]),
     "st_debug_get_rows": (I32, [P, I32, I32, I32, P, P, P]),
     "st_debug_get_dense0": (I32, [P, I32, I32, P]),
+    "st_debug_export_chunk": (I32, [P, I32]),
+    "st_debug_get_words": (I32, [P, I32, P]),
     "st_memory_report": (I32, [P, P, P, P]),
     "st_set_profiling": (I32, [P, I32]),
     "st_num_kernel_classes": (I32, []),
@@ -266,6 +268,19 @@ class Encoder:
         out = np.zeros((h, w, c), np.float32)
         self._check("st_debug_get_dense0", lib().st_debug_get_dense0(self.h, layer, chunk, _np_ptr(out)))
         return out
+
+    def export_chunk(self, chunk):
+        """Mask export of one chunk from the production step (st_debug_export_chunk)."""
+        self._check("st_debug_export_chunk", lib().st_debug_export_chunk(self.h, int(chunk)))
+
+    def exported_masks(self, layer):
+        """uint8 [n_diff][H][W] masks of `layer` for the exported chunk."""
+        h, w, _ = self.layer_shape(layer)
+        words = np.zeros(h * w, np.uint32)
+        self._check("st_debug_get_words", lib().st_debug_get_words(self.h, layer, _np_ptr(words)))
+        F = self.n_diff
+        bits = (words[None, :] >> np.arange(F, dtype=np.uint32)[:, None]) & 1
+        return bits.reshape(F, h, w).astype(np.uint8)
 
     def memory_report(self):
         v = np.zeros(3, np.int64)

@@ -42,6 +42,8 @@ template <> __device__ __forceinline__ void str<bf16>(bf16 *p, float v) { *p = _
 template <class T> __device__ __forceinline__ float rnd(float v);
 template <> __device__ __forceinline__ float rnd<float>(float v) { return v; }
 template <> __device__ __forceinline__ float rnd<bf16>(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+// RNE bf16 rounding of an fp32 value, kept as fp32 (BF16-mode conv operands)
+__device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 // 4 consecutive elements -> float4 (p 4-element aligned)
 template <class T> __device__ __forceinline__ float4 ld4(const T *p);
 template <> __device__ __forceinline__ float4 ld4<float>(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }

@@ -144,6 +144,11 @@ struct st_encoder {
     int last_chunks = 0, last_ndiff = -1;
     cudaStream_t last_stream = nullptr;
     std::string err;
+    // mask export of one chunk (st_debug_export_chunk): words per layer boundary
+    int exp_chunk = -1;
+    uint32_t *exp_words = nullptr;
+    std::vector<int64_t> exp_off;   // [n_layers + 1]: input site, then layer l at l + 1 (-1 = none)
+    bool exp_valid = false;
     // profiling
     bool prof = false;
     std::vector<LaunchRec> recs;
@@ -251,6 +256,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             l.W = out_dim(sw, s.k_w, s.s_w, s.p_w);
             l.C = s.c_out;
             if (s.k_h * s.k_w > 49) return ST_ERR_UNSUPPORTED;
+            if (l.depthwise && s.k_h * s.k_w > 25) return ST_ERR_UNSUPPORTED;   // depthwise kernels: <= 5x5 taps
             break;
         }
         case ST_MAXPOOL: {
@@ -352,12 +358,22 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             if (l.kind != ST_CONV) continue;
             const int kh = l.spec.k_h, kw = l.spec.k_w, cin_g = l.geo.Cin / l.spec.groups, co = l.C;
             l.wk = e->weights_mem + o;
+            // BF16 mode (R22-BF16): every conv multiplies bf16-rounded weights,
+            // so the CUDA-core convs (depthwise, small c_in) get RNE-rounded values too
+            const bool rw = cfg->precision == ST_BF16;
             for (int dy = 0; dy < kh; dy++)
                 for (int dx = 0; dx < kw; dx++)
                     for (int ci = 0; ci < cin_g; ci++)
-                        for (int c = 0; c < co; c++)
-                            host[o + ((int64_t)(dy * kw + dx) * cin_g + ci) * co + c] =
-                                l.spec.w[(((int64_t)c * cin_g + ci) * kh + dy) * kw + dx];
+                        for (int c = 0; c < co; c++) {
+                            float v = l.spec.w[(((int64_t)c * cin_g + ci) * kh + dy) * kw + dx];
+                            if (rw) {
+                                uint32_t u;
+                                std::memcpy(&u, &v, 4);
+                                u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+                                std::memcpy(&v, &u, 4);
+                            }
+                            host[o + ((int64_t)(dy * kw + dx) * cin_g + ci) * co + c] = v;
+                        }
             o += ((int64_t)kh * kw * cin_g * co + 63) / 64 * 64;   // 256-byte aligned (float4 loads)
             l.bias = e->weights_mem + o;
             for (int c = 0; c < co; c++) host[o + c] = l.spec.b[c];
@@ -646,6 +662,7 @@ static st_status plan(st_encoder *e) {
 
 extern "C" void st_encoder_destroy(st_encoder *e) {
     if (!e) return;
+    cudaFree(e->exp_words);
     cudaFree(e->arena);
     cudaFree(e->smallmem);
     cudaFree(e->ref);
@@ -850,6 +867,7 @@ static st_status encode_diff(st_encoder *e, const void *frames_dev, bool u8, int
     }
     CUDA_OK(e, cudaEventRecord(e->thr_ev, s));
     e->thr_pending = true;
+    e->exp_valid = e->exp_chunk >= 0 && e->exp_chunk < e->staged_chunks && n_diff > 0;
     if (e->cfg.streaming) {   // the chunks continue from the saved state next call
         e->cont = true;
         e->par ^= 1;
@@ -912,6 +930,16 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
         LAUNCH(e, KC_COUNTS, -1, s,
                launch_frame_counts(act, B, (int)Nin, e->counts, cstride, e->site_sum, nullptr, s));
     }
+    // mask export (st_debug_export_chunk): the chunk's words of a layer boundary
+    const bool exporting = e->exp_chunk >= 0 && e->exp_chunk < B && F > 0;
+    auto export_words = [&](int layer) {
+        if (!exporting) return;
+        const int64_t Nl = layer < 0 ? Nin : (int64_t)e->L[layer].H * e->L[layer].W;
+        const uint32_t *src = layer < 0 ? e->p<uint32_t>(e->in_act) : e->p<uint32_t>(e->L[layer].b_act);
+        cudaMemcpyAsync(e->exp_words + e->exp_off[layer + 1], src + (int64_t)e->exp_chunk * Nl, Nl * 4,
+                        cudaMemcpyDeviceToDevice, s);
+    };
+    export_words(-1);
 
     if (e->in_refbf >= 0 && !cont)
         LAUNCH(e, KC_DENSE_MISC, -1, s, launch_pad4_bf16(e->ref, (int64_t)B * Nin, e->in_C, e->ptr(e->in_refbf), s));
@@ -940,6 +968,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             if (l.tc_small) conv_tc_small_layout(l.geo, c.sr, c.shift);
             c.wk = l.wk;
             c.bias = l.bias;
+            c.rnd_a = bf;   // BF16 mode: the dense A operand is bf16-rounded (R22-BF16)
             c.out = e->p<float>(l.b_y0);
             if (!cont)
                 LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
@@ -960,6 +989,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                                     dw_pm ? nullptr : e->p<int32_t>(l.b_ridx)));
             zero_row(l.b_rows, l.C);
             c.dense = false;
+            c.rnd_a = false;   // delta rows are already bf16 values in BF16 mode
             c.bf = bf;
             c.a = in;
             c.ridx = e->p<int32_t>(l.b_ridx);
@@ -1138,6 +1168,9 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
         default:
             return fail(e, ST_ERR_INTERNAL, "layer kind %d not executable", l.kind);
         }
+        // a fused ReLU's words are written by its pool's pass
+        if (l.kind != ST_OUTPUT && l.fused_pool < 0) export_words(i);
+        if (l.fused_relu >= 0) export_words(l.fused_relu);
         (void)Cs;
     }
     CUDA_OK(e, cudaGetLastError());
@@ -1305,6 +1338,50 @@ extern "C" st_status st_debug_get_dense0(st_encoder *e, int32_t layer, int32_t c
     const LayerRT &l = e->L[layer];
     const int64_t ne = (int64_t)l.H * l.W * l.C;
     CUDA_OK(e, cudaMemcpy(host, dense_of(e, layer) + chunk * ne, ne * 4, cudaMemcpyDeviceToHost));
+    return ST_OK;
+}
+
+extern "C" st_status st_debug_export_chunk(st_encoder *e, int32_t chunk) {
+    if (!e) return ST_ERR_ARG;
+    if (chunk < -1 || chunk >= e->B) return fail(e, ST_ERR_ARG, "export chunk %d outside [-1, %d)", chunk, e->B);
+    CUDA_OK(e, cudaSetDevice(e->cfg.device));
+    if (chunk >= 0 && !e->exp_words) {
+        const int n = (int)e->L.size();
+        e->exp_off.assign(n + 1, -1);
+        int64_t o = 0;
+        e->exp_off[0] = o;
+        o += (int64_t)e->in_H * e->in_W;
+        for (int i = 0; i < n; i++)
+            if (e->L[i].kind != ST_OUTPUT) {
+                e->exp_off[i + 1] = o;
+                o += (int64_t)e->L[i].H * e->L[i].W;
+            }
+        if (cudaMalloc(&e->exp_words, o * 4) != cudaSuccess) {
+            cudaGetLastError();
+            e->exp_words = nullptr;
+            return fail(e, ST_ERR_OOM, "mask export buffer of %lld bytes", (long long)o * 4);
+        }
+    }
+    if (chunk != e->exp_chunk) {   // the issued step changes: drop captured graphs
+        CUDA_OK(e, cudaDeviceSynchronize());
+        for (auto &g : e->graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        e->graphs.clear();
+    }
+    e->exp_chunk = chunk;
+    e->exp_valid = false;
+    return ST_OK;
+}
+
+extern "C" st_status st_debug_get_words(st_encoder *e, int32_t layer, uint32_t *words) {
+    if (!e || !words) return ST_ERR_ARG;
+    if (layer < -1 || layer >= (int)e->L.size()) return fail(e, ST_ERR_ARG, "bad layer %d", layer);
+    if (!e->exp_valid || e->exp_chunk < 0) return fail(e, ST_ERR_STATE, "no exporting st_encode_diff yet");
+    int t = layer;
+    while (t >= 0 && e->L[t].kind == ST_OUTPUT) t = e->L[t].src;
+    CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    const int64_t N = t < 0 ? (int64_t)e->in_H * e->in_W : (int64_t)e->L[t].H * e->L[t].W;
+    CUDA_OK(e, cudaMemcpy(words, e->exp_words + e->exp_off[t + 1], N * 4, cudaMemcpyDeviceToHost));
     return ST_OK;
 }
 

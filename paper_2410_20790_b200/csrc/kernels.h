@@ -70,6 +70,7 @@ struct ConvCall {
     int B;
     bool dense;             // reference-frame mode (fp32 activations in and out)
     bool bf;                // sparse mode: rows are bf16 (BF16 mode)
+    bool rnd_a;             // dense mode, BF16 mode: round the fp32 A operand to bf16 (RNE, R22-BF16)
     // A operand
     const float *a_dense;   // dense: [B][Nin][Cin]
     const float *zeros;     // >= 1 KiB of device zeros (source of absent taps / padding)

@@ -111,6 +111,9 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                 } else {
                     ra[0] = ra[1] = ra[2] = ra[3] = 0.0f;
                 }
+                if (c.rnd_a)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) ra[j] = bf16_round(ra[j]);
             } else {
                 const int kk = tid & 7;
                 const int k = k0 + kk;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
                         const int idx = tab[m * ntaps + tap];
                         if (idx >= 0) v = ldr<T>(A + (int64_t)idx * astride + ci);
                     }
-                    ra[j] = v;
+                    ra[j] = c.rnd_a ? bf16_round(v) : v;
                 }
             }
             // B: [K][Cout]

@@ -73,8 +73,12 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
                 float v[TB][CPL];
 #pragma unroll
                 for (int j = 0; j < TB; j++)
-                    if (t0 + j < KMAX && idx[t0 + j] >= 0)
+                    if (t0 + j < KMAX && idx[t0 + j] >= 0) {
                         row_load<T, CPL>(A + (int64_t)idx[t0 + j] * C, c0, C, full, v[j]);
+                        if (c.rnd_a)
+#pragma unroll
+                            for (int i = 0; i < CPL; i++) v[j][i] = bf16_round(v[j][i]);
+                    }
 #pragma unroll
                 for (int j = 0; j < TB; j++) {
                     if (t0 + j >= KMAX || idx[t0 + j] < 0) continue;
@@ -437,6 +441,9 @@ __global__ void __launch_bounds__(256) k_dw_tile(ConvCall c, const uint32_t *__r
                         float v[8], w[8];
                         if (f_row[p] >= 0 && ((f_act[p] >> t1) & 1u)) {
                             RowIO<TI, 8>::load(stg + ((size_t)p * FG + j) * csw + cg * 8, v);
+                            if (DENSE && c.rnd_a)
+#pragma unroll
+                                for (int i = 0; i < 8; i++) v[i] = bf16_round(v[i]);
                         } else {
 #pragma unroll
                             for (int i = 0; i < 8; i++) v[i] = 0.0f;

@@ -87,6 +87,82 @@ def compare_chunk(enc, net, frames_chunk, thresholds, chunk, exact=True, check_r
     return report
 
 
+def bf16_within(a, b, rel=2e-2, rms_frac=2e-2):
+    """North_star bf16 bound (reading R29): |a-b| <= 2e-2 |b| + 2e-2 rms(b)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    rms = float(np.sqrt(np.mean(b * b))) if b.size else 0.0
+    err = np.abs(a - b)
+    bound = rel * np.abs(b) + rms_frac * rms
+    return bool(np.all(err <= bound)), float(np.max(err / np.maximum(bound, 1e-30))) if b.size else 0.0
+
+
+def site_layers(net):
+    return [i for i, l in enumerate(net.layers) if l["kind"] in W.NONLINEAR]
+
+
+def follow_compare(enc, net, frames_chunk, thresholds, chunk, precision, exported=False, check_rows=None):
+    """Band-follow parity (reading R23) of one chunk.
+
+    The GPU's emitted masks of every site -- from the debug retention or, in
+    the production launch configuration, from st_debug_export_chunk -- are
+    handed to the oracle, which adopts them ONLY inside the ambiguity band
+    |max_c|c| - theta| <= tau (tau of R23 for the precision); every decision
+    outside the band must agree (zero violations).  Then, elementwise:
+    every layer's mask (= its ascending active-index list) per frame, per-site
+    per-frame counts and (debug runs) every layer's delta rows; tap outputs
+    within R29 (bit-exact in FP32 mode when nothing was adopted).  Returns a
+    report with the number of decisions, in-band and adopted ones."""
+    L = frames_chunk.shape[0]
+    F = L - 1
+    get = enc.exported_masks if exported else (lambda i: np.stack([enc.debug_mask(i, chunk, t) for t in range(1, L)]))
+    gmasks = {i: get(i) for i in range(len(net.layers))}
+    gin = get(-1)
+    follow = {i: gmasks[i] for i in site_layers(net)}
+    if check_rows is None:
+        check_rows = not exported
+    r = oracle.run_chunk(net, frames_chunk, thresholds, want_deltas=check_rows, precision=precision,
+                         follow=follow)
+    fs = r["follow_stats"]
+    bad = {i: int(fs[i, 3]) for i in range(len(net.layers)) if fs[i, 3]}
+    assert not bad, f"decisions outside the R23 band disagree (layer: count): {bad}"
+    assert np.array_equal(gin, r["in_mask"]), "input-site (Subtraction) mask"
+    for i in range(len(net.layers)):
+        if net.layers[i]["kind"] == W.OUTPUT:
+            continue
+        assert np.array_equal(gmasks[i], r["masks"][i]), \
+            f"layer {i} ({W.KIND_NAMES[net.layers[i]['kind']]}) mask differs in {int((gmasks[i] != r['masks'][i]).sum())}"
+    act, _, _ = enc.get_sparsity()
+    assert np.array_equal(act[chunk], r["counts"]), "per-site per-frame counts"
+    if check_rows:
+        for i in range(len(net.layers)):
+            if net.layers[i]["kind"] == W.OUTPUT:
+                continue
+            for t in range(1, L):
+                idx, rows = enc.debug_rows(i, chunk, t)
+                C = rows.shape[1]
+                exp = r["deltas"][i][t - 1].reshape(-1, C)[idx]
+                if precision == "bf16":
+                    ok, e = bf16_within(rows, exp)
+                    assert ok, f"layer {i} frame {t} rows beyond the bf16 bound ({e:.2f} x bound)"
+                else:
+                    assert within(rows, exp), f"layer {i} frame {t} rows beyond tolerance"
+    adopted = int(fs[:, 2].sum())
+    worst = 0.0
+    for tap, O in r["taps"].items():
+        got = enc.outputs(tap)[chunk].cpu().numpy()
+        if precision == "bf16":
+            ok, e = bf16_within(got, O)
+            worst = max(worst, e)
+            assert ok, f"tap {tap} beyond the bf16 bound ({e:.2f} x bound)"
+        elif adopted == 0 and all(net.layers[i]["kind"] in (W.RELU, W.MAXPOOL) for i in site_layers(net)):
+            assert np.array_equal(got, O), f"tap {tap} outputs differ"
+        else:
+            assert within(got, O), f"tap {tap} outputs beyond tolerance"
+    return dict(decisions=int(fs[:, 0].sum()), in_band=int(fs[:, 1].sum()), adopted=adopted,
+                worst_tap_err_over_bound=worst, frames=F)
+
+
 def make_frames(cfg, n_chunks, L=None, h=None, w=None):
     L = L or cfg.L
     h = h or cfg.h

@@ -412,24 +412,190 @@ def test_pin16_se_zero_threshold(oracle_lib):
 
 
 # ------------------------------------------------ BF16-mode conv contract
-@pytest.mark.parametrize("cin,cout", [(64, 16), (128, 32), (32, 16), (24, 40), (12, 16), (16, 12)])
-def test_bf16_mode_conv_matches_rounded_fp64(oracle_lib, cin, cout):
-    """BF16 mode (R22-BF16): eligible convs (c_in % 8 == 0, c_out % 8 == 0)
-    equal the fp64 convolution of bf16-rounded weights and inputs (torch
-    bfloat16 casts); ineligible ones (c_in = 12, c_out = 12) are unchanged
-    from FP32 mode."""
-    n = Net(cin, 7, 9)
-    c = n.conv(-1, cout, 3)
+def _rb(a):
+    """bf16 round-to-nearest-even of fp32 values (torch's cast: a library routine)."""
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).to(torch.float64)
+
+
+@pytest.mark.parametrize("cin,cout,k,s,groups", [
+    (64, 16, 3, 1, 1), (128, 32, 3, 2, 1), (24, 40, 1, 1, 1), (12, 16, 3, 1, 1), (16, 12, 3, 1, 1),
+    (3, 32, 3, 2, 1), (3, 64, 7, 2, 1), (1, 64, 3, 1, 1), (6, 5, 2, 1, 1),
+    (32, 32, 3, 1, 32), (40, 40, 5, 2, 40), (8, 8, 7, 1, 8)])
+def test_bf16_mode_conv_matches_rounded_fp64(oracle_lib, cin, cout, k, s, groups):
+    """BF16 mode (R22-BF16) is one contract for EVERY convolution -- any
+    channel count, kernel size, stride or groups (stems, depthwise, 1x1):
+    the dense conv equals the fp64 convolution of bf16-rounded weights and
+    inputs (torch bfloat16 casts, F.conv2d); it differs from FP32 mode."""
+    n = Net(cin, 11, 9)
+    c = n.conv(-1, cout, k, s, k // 2, groups=groups)
     n.output(c)
-    init_weights(n, cin)
-    x = np.random.default_rng(cin).standard_normal((7, 9, cin)).astype(np.float32)
+    init_weights(n, cin + k)
+    x = np.random.default_rng(cin).standard_normal((11, 9, cin)).astype(np.float32)
     got = oracle.dense_forward(n, x, precision="bf16")[c]
-    rb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64)
-    if cin % 8 == 0 and cout % 8 == 0:
-        xw = rb(x).permute(2, 0, 1).unsqueeze(0)
-        ww = rb(n.layers[c]["w"])
-        ref = F.conv2d(xw, ww, torch.from_numpy(n.layers[c]["b"].astype(np.float64)), padding=1)[0].permute(1, 2, 0).numpy()
-        assert close(got, ref, rel=1e-4, abs_=1e-5), max_err(got, ref)
-        assert not np.array_equal(got, oracle.dense_forward(n, x)[c])
-    else:
-        assert np.array_equal(got, oracle.dense_forward(n, x)[c])
+    xw = _rb(x).permute(2, 0, 1).unsqueeze(0)
+    ref = F.conv2d(xw, _rb(n.layers[c]["w"]), torch.from_numpy(n.layers[c]["b"].astype(np.float64)),
+                   stride=s, padding=k // 2, groups=groups)[0].permute(1, 2, 0).numpy()
+    assert close(got, ref, rel=1e-4, abs_=1e-5), max_err(got, ref)
+    assert not np.array_equal(got, oracle.dense_forward(n, x)[c])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_bf16_mode_stored_deltas_are_bf16(oracle_lib, seed):
+    """R22-BF16: every stored delta (Subtraction, conv, add, every site) is a
+    bf16 value: its fp32 bit pattern has zero low 16 bits."""
+    net = random_net(900 + seed)
+    fr = random_frames(seed, 6, net.in_h, net.in_w, net.in_c)
+    r = oracle.run_chunk(net, fr, 0.03, want_deltas=True, precision="bf16")
+    for i, d in list(r["deltas"].items()) + [(-1, r["in_delta"])]:
+        assert np.all((d.view(np.uint32) & 0xFFFF) == 0), (seed, i)
+    assert np.any(r["in_delta"] != 0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_bf16_mode_subtraction_rounding(oracle_lib, seed):
+    """BF16 Subtraction: the decision is taken on the fp32 raw difference
+    (R1/R2), the emitted delta is RNE-bf16(raw) (torch cast) and S
+    advances by the emitted value (R3), so S_t = X_0 + sum of emitted."""
+    net = _single(lambda n: n.relu(-1), 3, 7, 8, seed)
+    fr = random_frames(seed, 8, 7, 8, 3, p_change=0.5, scale=0.05)
+    th = 0.02
+    r = oracle.run_chunk(net, fr, [th, 0.0], want_deltas=True, precision="bf16")
+    S = fr[0].copy()
+    for t in range(1, 8):
+        raw = (fr[t] - S).astype(np.float32)
+        act = np.abs(raw).max(axis=2) > np.float32(th)
+        assert np.array_equal(r["in_mask"][t - 1].astype(bool), act)
+        e = np.where(act[..., None], _rb(raw).numpy(), 0.0).astype(np.float32)
+        assert np.array_equal(r["in_delta"][t - 1], e)
+        S = (S + e).astype(np.float32)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_bf16_mode_site_rounding(oracle_lib, seed):
+    """BF16 ReLU site: c = relu(x_acc) - y_acc on the touched pixels, emit iff
+    max_c |c| > theta on the fp32 value, the stored delta is RNE-bf16(c) and
+    y_acc advances by it -- rebuilt from the oracle's own outputs (x_acc =
+    x0 + sum conv deltas, y_acc = y0 + sum emitted, fp32 adds) and torch's
+    bf16 cast."""
+    net = Net(2, 8, 8)
+    c = net.conv(-1, 8, 3)
+    a = net.relu(c)
+    net.output(a)
+    init_weights(net, seed)
+    fr = random_frames(seed, 7, 8, 8, 2, p_change=0.5, scale=0.3)
+    th = 0.05
+    r = oracle.run_chunk(net, fr, [0.0, th], want_deltas=True, want_dense0=True, precision="bf16")
+    xa, ya = r["dense0"][c].copy(), r["dense0"][a].copy()
+    n_emit = 0
+    for t in range(6):
+        tm = r["masks"][c][t].astype(bool)
+        xa = (xa + r["deltas"][c][t]).astype(np.float32)
+        cand = (np.maximum(xa, 0) - ya).astype(np.float32)
+        keep = tm & (np.abs(cand).max(axis=2) > np.float32(th))
+        assert np.array_equal(r["masks"][a][t].astype(bool), keep), (seed, t)
+        e = np.where(keep[..., None], _rb(cand).numpy(), 0.0).astype(np.float32)
+        assert np.array_equal(r["deltas"][a][t], e), (seed, t)
+        ya = (ya + e).astype(np.float32)
+        n_emit += int(keep.sum())
+    assert n_emit > 0
+
+
+# ------------------------------------------------- SE site at theta > 0 (R8)
+def test_se_refresh_worked_example(oracle_lib):
+    """Hand-worked 1-pixel / 2-channel SE example (tests/golden/se_refresh.json,
+    reading R8): gate refresh on frame 2 only; the candidate uses the EMITTED
+    gate s_emit, not the current s_t (frames 1, 5 and 6 tell them apart)."""
+    g = _gold("se_refresh.json")
+    n = Net(2, 1, 1)
+    x = n.se(-1, 1)
+    n.output(x)
+    n.layers[x]["w"] = np.array(g["w1"], np.float32)
+    n.layers[x]["b"] = np.array(g["b1"], np.float32)
+    n.layers[x]["w2"] = np.array(g["w2"], np.float32)
+    n.layers[x]["b2"] = np.array(g["b2"], np.float32)
+    fr = np.array(g["frames"], np.float32).reshape(-1, 1, 1, 2)
+    r = oracle.run_chunk(n, fr, [g["theta_input"], g["theta_se"]], want_deltas=True)
+    assert list(r["counts"][1]) == g["expect_emitted"]
+    np.testing.assert_allclose(r["deltas"][x].reshape(-1, 2), np.array(g["expect_delta"]), atol=g["tol"], rtol=0)
+    np.testing.assert_allclose(r["taps"][1].reshape(-1, 2), np.array(g["expect_output"]), atol=g["tol"], rtol=0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_se_drift_bound_r21(oracle_lib, seed):
+    """R21 drift bound at theta > 0: with x_acc = x0 + sum of the SE input's
+    deltas, y_acc = y0 + sum of the SE's emitted deltas and s_t = gate(x_acc)
+    (torch fp64), every pixel and channel obeys |x_acc*s_t - y_acc| <= theta +
+    |x_acc|*theta_gate after every frame (theta_gate = theta_site): the
+    residual of the last touch is <= theta and the gate moved by <= theta_gate
+    since the last refresh."""
+    net = Net(3, 6, 7)
+    c = net.conv(-1, 6, 3)
+    x = net.se(c, 2)
+    net.output(x)
+    init_weights(net, 40 + seed)
+    L, th = 9, 0.04
+    fr = random_frames(seed, L, 6, 7, 3, p_change=0.35, scale=0.25)
+    r = oracle.run_chunk(net, fr, [0.01, th], want_deltas=True, want_dense0=True)
+    xa = r["dense0"][c].astype(np.float64)
+    ya = r["dense0"][x].astype(np.float64)
+    l = net.layers[x]
+    w1, b1, w2, b2 = (torch.from_numpy(l[k].astype(np.float64)) for k in ("w", "b", "w2", "b2"))
+    for t in range(L - 1):
+        xa = xa + r["deltas"][c][t]
+        ya = ya + r["deltas"][x][t]
+        m = torch.from_numpy(xa).mean(dim=(0, 1))
+        h = w1 @ m + b1
+        s_t = torch.sigmoid(w2 @ (h * torch.sigmoid(h)) + b2).numpy()
+        bound = th + np.abs(xa) * th + 1e-5
+        assert np.all(np.abs(xa * s_t - ya) <= bound), (seed, t)
+    assert r["counts"][1].sum() > 0
+
+
+# ------------------------------------------------ O12 band-follow mode
+def _follow_net(seed):
+    net = Net(2, 8, 9)
+    c = net.conv(-1, 6, 3)
+    a = net.silu(c)
+    c2 = net.conv(a, 4, 3)
+    m = net.maxpool(net.relu(c2), 2, 2)
+    net.output(m)
+    init_weights(net, seed)
+    return net, [a, m - 1, m]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_follow_own_masks_is_identity(oracle_lib, precision):
+    """Following the oracle's own decisions changes nothing: bit-identical
+    outputs, zero adoptions, zero violations."""
+    net, sites = _follow_net(3)
+    fr = random_frames(3, 7, 8, 9, 2, p_change=0.4, scale=0.3)
+    a = oracle.run_chunk(net, fr, 0.05, want_deltas=True, precision=precision)
+    b = oracle.run_chunk(net, fr, 0.05, want_deltas=True, precision=precision,
+                         follow={i: a["masks"][i] for i in sites})
+    for i in a["masks"]:
+        assert np.array_equal(a["masks"][i], b["masks"][i]) and np.array_equal(a["deltas"][i], b["deltas"][i])
+    fs = b["follow_stats"]
+    assert fs[:, 2].sum() == 0 and fs[:, 3].sum() == 0 and fs[sites, 0].sum() > 0
+
+
+def test_follow_adopts_only_inside_band(oracle_lib):
+    """A flipped decision far from theta is a violation and is NOT adopted; a
+    flipped decision inside the band (tau widened to cover it) is adopted,
+    and the run continues from the GPU's decision (reading R23)."""
+    net, sites = _follow_net(5)
+    fr = random_frames(5, 6, 8, 9, 2, p_change=0.4, scale=0.3)
+    th = 0.05
+    a = oracle.run_chunk(net, fr, th, want_deltas=True, precision="fp32")
+    site = sites[0]
+    m = a["masks"][site].copy()
+    t, y, x = map(int, np.argwhere(m == 1)[0])
+    m[t, y, x] = 0                                   # the "GPU" truncated an emitted pixel
+    # tight band: the flip is outside it -> violation, own decision kept
+    b = oracle.run_chunk(net, fr, th, want_deltas=True, follow={site: m}, tau=(1e-4, 0.0, 1e-5))
+    assert b["follow_stats"][site, 3] >= 1 and b["follow_stats"][site, 2] == 0
+    assert np.array_equal(b["masks"][site], a["masks"][site])
+    # band wide enough to contain that pixel's value -> adopted
+    c = oracle.run_chunk(net, fr, th, want_deltas=True, follow={site: m}, tau=(0.0, 0.0, 10.0))
+    assert c["follow_stats"][site, 2] == 1 and c["follow_stats"][site, 3] == 0
+    assert c["masks"][site][t, y, x] == 0 and np.all(c["deltas"][site][t, y, x] == 0)
+    assert c["counts"][sites.index(site) + 1][t] == a["counts"][sites.index(site) + 1][t] - 1

@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 
-def _value_noise(rng, h, w, c, cell):
+def _value_noise(rng, h, w, c, cell):  # float32 map
     gh, gw = h // cell + 2, w // cell + 2
     g = rng.uniform(40, 215, (gh, gw, c))
     ys = np.arange(h) / cell
@@ -35,7 +35,7 @@ def _value_noise(rng, h, w, c, cell):
     b = g[y0][:, x0 + 1]
     cc = g[y0 + 1][:, x0]
     d = g[y0 + 1][:, x0 + 1]
-    return a * (1 - fy) * (1 - fx) + b * (1 - fy) * fx + cc * fy * (1 - fx) + d * fy * fx
+    return (a * (1 - fy) * (1 - fx) + b * (1 - fy) * fx + cc * fy * (1 - fx) + d * fy * fx).astype(np.float32)
 
 
 def _background(rng, h, w, c, n_blocks):
@@ -76,7 +76,6 @@ def gen_chunk(seed, L, h, w, c, n_objects=3, size=(8, 16), speed=(1, 1), frames_
             vy=int(rng.integers(-speed[1], speed[1] + 1)),
             vx=int(rng.choice([-1, 1]) * rng.integers(speed[0], speed[1] + 1)),
             disc=bool(rng.integers(0, 2)), col=rng.uniform(0, 255, c)))
-    yy, xx = np.mgrid[0:h, 0:w]
     frames = np.empty((L, h, w, c), np.uint8)
     for t in range(L):
         steps = t // frames_per_px
@@ -91,18 +90,25 @@ def gen_chunk(seed, L, h, w, c, n_objects=3, size=(8, 16), speed=(1, 1), frames_
         for o in objs:
             py = _reflect(o["y"] + o["vy"] * steps, 0, h - o["hy"])
             px = _reflect(o["x"] + o["vx"] * steps, 0, w - o["hx"])
-            if o["disc"]:
-                cy, cx = py + o["hy"] / 2.0, px + o["hx"] / 2.0
-                m = ((yy + 0.5 - cy) / (o["hy"] / 2.0)) ** 2 + ((xx + 0.5 - cx) / (o["hx"] / 2.0)) ** 2 <= 1.0
-                img[m] = o["col"]
+            box = img[py:py + o["hy"], px:px + o["hx"]]
+            if o["disc"]:   # ellipse inscribed in the object's box
+                yy = (np.arange(box.shape[0])[:, None] + 0.5 - o["hy"] / 2.0) / (o["hy"] / 2.0)
+                xx = (np.arange(box.shape[1])[None, :] + 0.5 - o["hx"] / 2.0) / (o["hx"] / 2.0)
+                box[yy * yy + xx * xx <= 1.0] = o["col"]
             else:
-                img[py:py + o["hy"], px:px + o["hx"]] = o["col"]
+                box[...] = o["col"]
         if flicker:
             img = img + flicker * (1 if t % 2 else -1)
         if noise_q > 0:
-            hit = rng.random((h, w, c)) < noise_q
-            mag = rng.integers(1, noise_amp + 1, (h, w, c)) * rng.choice([-1, 1], (h, w, c))
-            img = img + hit * mag
+            # one uniform draw per pixel-channel: u < q is a hit; u / q picks
+            # the offset uniformly from {-amp..-1, 1..amp}
+            u = rng.random((h, w, c), dtype=np.float32).ravel()
+            hit = np.flatnonzero(u < np.float32(noise_q))
+            k = np.minimum((u[hit] * np.float32(2 * noise_amp / noise_q)).astype(np.int32), 2 * noise_amp - 1)
+            tab = np.array([(1 + j // 2) * (1 if j % 2 == 0 else -1) for j in range(2 * noise_amp)], np.float32)
+            img = img.reshape(-1)
+            img[hit] += tab[k]
+            img = img.reshape(h, w, c)
         frames[t] = np.clip(np.rint(img), 0, 255).astype(np.uint8)
     return frames
 
