@@ -1,30 +1,44 @@
 #!/usr/bin/env python
 """Benchmark of the SparseTem Diff Computation hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
+Workload (default): cfg5 = BASELINE.json configs[4], the largest config that
+fits one GPU -- the EfficientDet-D0 (EfficientNet-B0) backbone on a job of 64
+chunks x 16 frames of synthetic 1080p video, with online threshold
+adjustment.  The metric names no config, so the N=1 line is the largest one.
 One step = one SparseBatch pass (all §8(a) rows: reference-frame dense pass,
 Subtraction, masks, compaction, sparse conv, non-linear correction,
-truncation, Accumulation, per-site statistics) over one batch of synthetic
-chunks: BASELINE.json configs[1] = cfg2, the CRNN VGG-7 conv encoder on
-64 chunks x 32 frames of 32x128 grayscale synthetic text video.
+truncation, Accumulation, per-site statistics, the controller's all-gather
+and update) over one fixed group of 8 chunks; the job is 8 such groups and
+step s processes group s mod 8 (reading R15).
+
+Thresholds: the controller (BST) is run UNTIMED on the job's
+steps until every site is frozen (in band or at resolution); the timed steps
+then run with those thresholds (the controller still observes every step --
+the counts copy, the all-gather, the host update are inside the timed region
+-- but a frozen BST does not move).  Per-site thresholds and sparsity are
+printed.
 
 value  = diff frames / s of the whole job (all ranks), inputs resident in
-         HBM, L2 flushed between timed steps (untimed 256 MiB write), CUDA
-         events on the launch stream, max over ranks.
+         HBM (uint8 frames, v/255 in-kernel, R20), L2 flushed between timed
+         steps (untimed 256 MiB write), CUDA events on the launch stream, max
+         over ranks.
 e2e    = the same metric through the C ABI with pinned HOST buffers: H2D of
-         every step's frames and D2H of every step's dense tap outputs inside
-         one timed region, the copies pipelined against compute on two copy
-         streams (a serving loop: step k+1's input upload and step k's result
-         download overlap step k+1's kernels).
-roofline = dominant kernel class (per-launch CUDA events inside the library,
-         a separate profiled pass), algorithmic flops or bytes per launch /
-         mean launch time vs the measured / derived peak.
+         every step's frames and D2H of every step's dense tap outputs (all
+         taps) inside one timed region, copies pipelined on two copy streams.
+roofline = the dominant kernel class (per-launch CUDA events on the library's
+         launch stream, a separate profiled pass), algorithmic bytes or flops
+         per launch / mean launch time vs MEASURED_PEAKS.json (the burst
+         tensor peak when the sampled SM clock sat at max, else the sustained
+         one; HBM: the measured copy bandwidth); traffic = ncu dram bytes per
+         launch from profiles/ncu_summary.json when it was captured on this
+         same command, else null.
 cpu_baseline = the oracle (test infrastructure) on a bounded sample.
-Multi-GPU (torchrun): rank r processes its own 64 chunks per step (weak
-scaling, chunks are independent); no data-path collective for the
-fixed-threshold config; with --policy bst/ibst the per-site counts are
-all-gathered over NCCL every step for the controller.
+Multi-GPU (torchrun): rank r of G processes chunks r, r+G, ... of each group
+(reading R15), so the job and every output are the same for every G: strong
+scaling of a fixed job.  The only collective is the all-gather of the per-site
+int64 counts.
 """
 from __future__ import annotations
 
@@ -53,21 +67,25 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--policy", default=None, choices=[None, "fixed", "bst", "ibst"])
+    ap.add_argument("--policy", default=None, choices=[None, "fixed", "bst", "ibst"],
+                    help="threshold policy (default: the config's; bst/ibst are calibrated untimed, then frozen)")
+    ap.add_argument("--live", action="store_true", help="keep IBST live in the timed region (no freeze)")
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"],
                     help="fp32: exact CUDA-core path; bf16: tcgen05 tensor-core convs (R22-BF16)")
+    ap.add_argument("--groups", type=int, default=None, help="distinct chunk groups resident (default: the job's)")
     ap.add_argument("--no-dense", action="store_true", help="skip the own-dense-path reference timing")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32-mode context timing")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and clock-event reasons sampled DURING the timed region
-    (B200_PROFILING.md).  NVML polled from a thread every ~2 ms (a cfg2
-    timed region is only tens of ms); nvidia-smi -lms as the fallback."""
+    (B200_PROFILING.md): NVML polled from a thread every ~2 ms, nvidia-smi
+    -lms as the fallback."""
 
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
@@ -148,34 +166,63 @@ def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f), "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+            return json.load(f), "MEASURED_PEAKS.json"
+    # B200_PROFILING.md fallback figures
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel_class, cid):
-    """dram bytes per launch of the dominant kernel from a committed ncu --set
-    full capture of this config's bench command (profiles/ncu_summary.json),
-    else None."""
+def ncu_traffic(kernel_class, cid, precision):
+    """dram bytes per launch of a kernel class from a committed ncu --set full
+    capture of THIS bench command (profiles/ncu_summary.json records the
+    config and precision it was captured on), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f).get("kernels", {}).get(kernel_class, {})
-        return d.get("dram_bytes_per_launch") if d.get("config") == cid else None
+            d = json.load(f)
+        if d.get("config") != cid or d.get("precision", "bf16") != precision:
+            return None
+        return d.get("kernels", {}).get(kernel_class, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
 
+def gen_chunks(cfg, ids, L):
+    """uint8 [len(ids)][L][H][W][C] of the config's chunks (seed per chunk),
+    generated in worker processes (the generator is numpy, ~0.1 s per 1080p
+    frame)."""
+    import concurrent.futures as cf
+    import multiprocessing as mpc
+    args = [(cfg.video_seed(c), L, cfg.h, cfg.w, cfg.c) for c in ids]
+    if len(ids) <= 2:
+        return np.stack([W.gen_chunk(*a, **cfg.video) for a in args])
+    nw = max(1, min(len(ids), (os.cpu_count() or 2) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))))
+    with cf.ProcessPoolExecutor(nw, mp_context=mpc.get_context("spawn")) as ex:
+        out = list(ex.map(_gen_one, [(a, cfg.video) for a in args]))
+    return np.stack(out)
+
+
+def _gen_one(a):
+    (seed, L, h, w, c), video = a
+    return W.gen_chunk(seed, L, h, w, c, **video)
+
+
 # -------------------------------------------------------------- reference
+def ref_sample_frames(cfg):
+    """Frames per chunk of the oracle's bounded sample: small configs run
+    whole chunks; 1080p / 720p chunks run the reference frame + 3 diff frames."""
+    return cfg.L if cfg.h * cfg.w <= 512 * 512 else min(cfg.L, 4)
+
+
 def run_reference(args, cfg):
-    """--impl reference: the oracle (as it stands) on the host cores, each
-    step a bounded sample (1 chunk x L frames) of the same workload."""
+    """--impl reference: the oracle (as it stands) on the host cores; each
+    step a bounded sample of the same workload (1 chunk)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
     net = cfg.build_net()
-    u8 = W.gen_video(1, cfg.L, cfg.h, cfg.w, cfg.c, cfg.video_seed(0), **cfg.video)
-    fr = W.to_float(u8)[0]
+    Ls = ref_sample_frames(cfg)
+    fr = W.to_float(W.gen_chunk(cfg.video_seed(0), Ls, cfg.h, cfg.w, cfg.c, **cfg.video))
     th = cfg.theta_fixed
     oracle.build()
     for _ in range(max(args.warmup, 0)):
@@ -184,15 +231,16 @@ def run_reference(args, cfg):
     for _ in range(args.steps):
         oracle.run_chunk(net, fr, th, want_masks=False)
     dt = time.perf_counter() - t0
-    v = args.steps * (cfg.L - 1) / dt
+    v = args.steps * (Ls - 1) / dt
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = f"1 chunk x {Ls} frames (reference + {Ls - 1} diff) of cfg{cfg.cid} per step, theta {th} at every site"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg{cfg.cid}: {cfg.note}", "chunks_per_step": 1, "frames_per_chunk": cfg.L,
-                       "sample": "1 chunk per step"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"1 chunk x {cfg.L} frames of cfg{cfg.cid} per step"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"cfg{cfg.cid}: {cfg.note}", "chunks_per_step": 1, "frames_per_chunk": Ls,
+                       "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -202,9 +250,8 @@ def cpu_baseline(cfg):
     import oracle
     oracle.build()
     net = cfg.build_net()
-    u8 = W.gen_video(1, cfg.L, cfg.h, cfg.w, cfg.c, cfg.video_seed(0), **cfg.video)
-    fr = W.to_float(u8)[0]
-    oracle.run_chunk(net, fr[:2], cfg.theta_fixed, want_masks=False)   # warm
+    Ls = ref_sample_frames(cfg)
+    fr = W.to_float(W.gen_chunk(cfg.video_seed(0), Ls, cfg.h, cfg.w, cfg.c, **cfg.video))
     reps, t0 = 0, time.perf_counter()
     while True:
         oracle.run_chunk(net, fr, cfg.theta_fixed, want_masks=False)
@@ -213,8 +260,8 @@ def cpu_baseline(cfg):
             break
     dt = time.perf_counter() - t0
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": reps * (cfg.L - 1) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{reps} x (1 chunk x {cfg.L} frames) of cfg{cfg.cid}, {dt:.1f} s"}
+    return {"value": reps * (Ls - 1) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{reps} x (1 chunk x {Ls} frames) of cfg{cfg.cid}, theta {cfg.theta_fixed}, {dt:.1f} s"}
 
 
 # -------------------------------------------------------------------- ours
@@ -224,59 +271,73 @@ def main():
     if args.impl == "reference":
         return run_reference(args, cfg)
 
-    import torch
-    import torch.distributed as dist
-    from paper_2410_20790_b200 import Encoder, ThresholdController
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    B, L = cfg.chunks_per_step, cfg.L
+    if B % world:
+        raise SystemExit(f"cfg{cfg.cid}: {B} chunks per step do not divide over {world} GPUs")
+    n_groups = max(1, cfg.steps)
+    res_groups = min(n_groups, args.groups or n_groups)
+    from paper_2410_20790_b200.sharding import shard
+    # the rank's chunks of every resident group, generated before CUDA starts
+    host = [gen_chunks(cfg, shard(g, B, rank, world), L) for g in range(res_groups)]
+
+    import torch
+    import torch.distributed as dist
+    from paper_2410_20790_b200 import Encoder, ThresholdController
+    from paper_2410_20790_b200.sharding import StatsExchange, StepLoop
+
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     policy = args.policy or cfg.policy
-    B, L = cfg.chunks_per_step, cfg.L
+    Br = B // world
     net = cfg.build_net()
-    enc = Encoder(net, max_chunks=B, max_frames=L, device=local, precision=args.precision)
+    enc = Encoder(net, max_chunks=Br, max_frames=L, device=local, precision=args.precision)
     ns = enc.n_sites
-    ctl = ThresholdController(ns, policy=policy, T=cfg.T, eps=cfg.eps, theta_fixed=cfg.theta_fixed,
-                              cycle=cfg.cycle)
-
-    # inputs: distinct synthetic batches per step (rank r owns global chunks r + world*j)
-    from paper_2410_20790_b200.sharding import shard
-    n_batches = max(1, min(cfg.steps, 4 if cfg.h * cfg.w <= 512 * 512 else 2))
-    batches = []
-    for s in range(n_batches):
-        u8 = np.stack([W.gen_chunk(cfg.video_seed(cid), L, cfg.h, cfg.w, cfg.c, **cfg.video)
-                       for cid in shard(s, B * world, rank, world)])
-        # uint8 frames, the camera / decoder format (v / 255 inside the
-        # Subtraction kernels, reading R20; bit-identical to fp32 frames)
-        batches.append(torch.from_numpy(np.ascontiguousarray(u8)).to(dev))
-    frame_bytes = batches[0].numel() * batches[0].element_size()
+    frozen_run = policy != "fixed" and not args.live
+    ctl = ThresholdController(ns, policy="bst" if frozen_run else policy, T=cfg.T, eps=cfg.eps,
+                              theta_fixed=cfg.theta_fixed, cycle=cfg.cycle)
+    ex = StatsExchange(ns, device=dev)
+    loop = StepLoop(B, n_groups, rank, world, ctl, ex)
+    inputs = [torch.from_numpy(np.ascontiguousarray(h)).to(dev) for h in host]
+    frame_bytes = inputs[0].numel() * inputs[0].element_size()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    from paper_2410_20790_b200.sharding import StatsExchange
-    ex = StatsExchange(ns, device=dev)
 
-    def step(x):
-        th = ctl.thresholds()
-        enc.encode_reference(x[:, 0], stream)
-        enc.encode_diff(x[:, 1:], th, stream)
-        if policy != "fixed":
-            # the only collective: NCCL all-gather of int64 per-site counts
-            enc.copy_site_counts(ex.local, stream)
-            ctl.observe(*ex.exchange())
+    def encode_on(x):
+        def encode(group, ids, th):
+            enc.encode_reference(x(group)[:, 0], stream)
+            enc.encode_diff(x(group)[:, 1:], th, stream)
+            if policy != "fixed":
+                enc.copy_site_counts(ex.local, stream)   # -> the NCCL all-gather
+            return None
+        return encode
 
-    for w in range(args.warmup):
-        step(batches[w % n_batches])
-    # every input batch seen twice before timing: the library captures a CUDA
-    # graph of the step on the second sight of a (frames, shape) key
-    for w in range(2 * n_batches):
-        step(batches[w % n_batches])
+    resident = encode_on(lambda g: inputs[g % res_groups])
+    observe = policy != "fixed"
+    step_no = 0
+
+    # ---- untimed calibration: BST until every site is frozen
+    calib_steps = 0
+    if frozen_run:
+        while calib_steps < 40:
+            loop.run_step(step_no, resident, observe=True)
+            step_no += 1
+            calib_steps += 1
+            if bool(np.all(ctl.state()[3])):
+                break
+    # ---- warm-up; every resident group twice (the library captures a CUDA
+    # graph of the step on the second sight of an input buffer)
+    for _ in range(args.warmup + 2 * res_groups):
+        loop.run_step(step_no, resident, observe=observe)
+        step_no += 1
     torch.cuda.synchronize(dev)
     launches_per_step = enc.last_launch_count()
+    theta = [float(v) for v in ctl.thresholds()]
 
     # ---- timed region: K steps, L2 flushed between steps (untimed)
     clk = ClockSampler(local)
@@ -289,7 +350,8 @@ def main():
         flush.fill_(float(k))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step(batches[k % n_batches])
+        loop.run_step(step_no, resident, observe=observe)
+        step_no += 1
         e1.record(stream)
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
@@ -301,31 +363,35 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    diff_frames = B * (L - 1) * world
+    diff_frames = B * (L - 1)          # the whole group, all ranks
     value = diff_frames / (ms_step / 1e3)
+    theta_timed = [float(v) for v in ctl.thresholds()]
 
     # ---- statistics of the last step
     act, sa, sp = enc.get_sparsity()
-    site_sparsity = [round(1 - a / p, 4) if p else None for a, p in zip(sa, sp)]
+    sa_all, sp_all = ex.exchange(np.concatenate([sa, sp])) if world > 1 else (sa, sp)
+    site_sparsity = [round(1 - a / p, 4) if p else None for a, p in zip(sa_all, sp_all)]
     lc = enc.layer_counts()
 
-    # ---- e2e: pinned host buffers through the C ABI.  Every step copies its
-    # frames H2D and its dense tap outputs D2H; the copies run on two copy
-    # streams, pipelined against the compute stream (H2D of step k+1 and D2H
-    # of step k overlap step k+1's kernels; double-buffered device inputs, the
-    # outputs staged D2D so the next step may overwrite the Accumulation
-    # buffer).  One timed region over all e2e steps, end = last D2H landed.
-    host_in = [b.cpu().pin_memory() for b in batches]
-    tap = enc.taps[0]
-    out_shape = tuple(enc.outputs(tap).shape)
-    host_out = [torch.empty(out_shape, dtype=torch.float32).pin_memory() for _ in range(2)]
-    dev_in = [torch.empty_like(batches[0]) for _ in range(2)]
-    stage = [torch.empty(out_shape, dtype=torch.float32, device=dev) for _ in range(2)]
+    # ---- e2e: pinned host buffers through the C ABI; every step copies its
+    # frames H2D and ALL its dense tap outputs D2H, pipelined on two copy
+    # streams (H2D of step k+1 and D2H of step k overlap step k+1's kernels)
+    n_pin = min(2, res_groups)
+    host_in = [torch.from_numpy(host[g]).pin_memory() for g in range(n_pin)]
+    taps = enc.taps
+    out_shapes = [tuple(enc.outputs(tp).shape) for tp in taps]
+    host_out = [[torch.empty(s, dtype=torch.float32).pin_memory() for s in out_shapes] for _ in range(2)]
+    dev_in = [torch.empty_like(inputs[0]) for _ in range(2)]
+    stage = [[torch.empty(s, dtype=torch.float32, device=dev) for s in out_shapes] for _ in range(2)]
+    d2h_bytes = sum(int(np.prod(s)) * 4 for s in out_shapes)
     h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    for j in range(2):   # graph capture of both input buffers' keys (untimed)
+    buffered = encode_on(lambda g: dev_in[cur_buf[0]])
+    cur_buf = [0]
+    for j in range(2):   # graph capture of both device input buffers (untimed)
+        cur_buf[0] = j
         for _ in range(2):
             dev_in[j].copy_(host_in[0], non_blocking=True)
-            step(dev_in[j])
+            loop.run_step(step_no, buffered, observe=observe)
     torch.cuda.synchronize(dev)
     e2e_steps = max(3, min(args.steps, 10))
     ev = lambda: torch.cuda.Event()  # noqa: E731
@@ -336,9 +402,11 @@ def main():
         if k >= 2:
             h2d_s.wait_event(used_ev[k - 2])   # step k-2 has consumed dev_in[k % 2]
         with torch.cuda.stream(h2d_s):
-            dev_in[k % 2].copy_(host_in[k % n_batches], non_blocking=True)
+            dev_in[k % 2].copy_(host_in[k % n_pin], non_blocking=True)
         h2d_ev[k].record(h2d_s)
 
+    if world > 1:
+        dist.barrier()
     e0.record(stream)
     h2d_s.wait_stream(stream)
     d2h_s.wait_stream(stream)
@@ -348,98 +416,99 @@ def main():
             issue_h2d(k + 1)
         stream.wait_event(h2d_ev[k])
         flush.fill_(float(k))
-        step(dev_in[k % 2])
+        cur_buf[0] = k % 2
+        loop.run_step(step_no, buffered, observe=observe)
+        step_no += 1
         used_ev[k].record(stream)
         if k >= 2:
             stream.wait_event(d2h_ev[k - 2])   # stage[k % 2] drained to the host
-        stage[k % 2].copy_(enc.outputs(tap), non_blocking=True)
+        for j, tp in enumerate(taps):
+            stage[k % 2][j].copy_(enc.outputs(tp), non_blocking=True)
         staged_ev[k].record(stream)
         d2h_s.wait_event(staged_ev[k])
         with torch.cuda.stream(d2h_s):
-            host_out[k % 2].copy_(stage[k % 2], non_blocking=True)
+            for j in range(len(taps)):
+                host_out[k % 2][j].copy_(stage[k % 2][j], non_blocking=True)
         d2h_ev[k].record(d2h_s)
     stream.wait_stream(d2h_s)
     e1.record(stream)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
-    assert torch.equal(host_out[(e2e_steps - 1) % 2], enc.outputs(tap).cpu()), "e2e output landed on the host"
+    for j, tp in enumerate(taps):
+        assert torch.equal(host_out[(e2e_steps - 1) % 2][j], enc.outputs(tp).cpu()), "e2e output landed on the host"
     te = torch.tensor([e2e_ms / e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = diff_frames / (float(te.item()) / 1e3)
+    del host_in, host_out, stage, dev_in
 
-    # ---- roofline of the dominant kernel (separate profiled pass)
+    # ---- roofline of the dominant kernel (separate profiled pass, same steps)
     enc.set_profiling(True)
     enc.kernel_times(reset=True)
     for k in range(args.steps):
         flush.fill_(float(k))
-        step(batches[k % n_batches])
+        loop.run_step(step_no, resident, observe=observe)
+        step_no += 1
         enc.kernel_times(reset=False)
     kt = enc.kernel_times(reset=True)
     enc.set_profiling(False)
     kt.pop("prof_stats", None)   # roofline-only statistics launched by the profiled pass, not part of a step
     step_kernel_ms = sum(v["ms"] for v in kt.values()) / args.steps
-    dom = max(kt, key=lambda k: kt[k]["ms"])
     peaks, peak_src = measured_peaks()
-    # per-class achieved rate vs its roofline (algorithmic bytes / flops)
+    at_max = bool(clocks and clocks.get("sm_mhz") and clocks.get("sm_max_mhz")
+                  and clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
+    tc_key = "bf16_tflops" if (at_max or "bf16_tflops_sustained" not in peaks) else "bf16_tflops_sustained"
+    p_tc = float(peaks.get(tc_key, 1590.0))                      # TF/s, one denominator everywhere
+    p_hbm = float(peaks["hbm_gbs"])                                # GB/s
+    p_f32 = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TF/s, derived
     kroof = {}
     for k, v in kt.items():
         if not v["launches"] or v["ms"] <= 0:
             continue
+        s = v["ms"] / 1e3
         if v["flops"] > 0 and k.startswith("conv_tc"):
-            tf = v["flops"] / (v["ms"] / 1e3) / 1e12
-            kroof[k] = {"TFLOP/s": round(tf, 1), "frac": round(tf / float(peaks.get("bf16_tflops", 1590.0)), 3),
-                        "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)}
+            tf = v["flops"] / s / 1e12
+            kroof[k] = {"TFLOP/s": round(tf, 1), "frac": round(tf / p_tc, 3), "GB/s": round(v["bytes"] / s / 1e9, 1),
+                        "hbm_frac": round(v["bytes"] / s / 1e9 / p_hbm, 3)}
         elif v["bytes"] > 0:
-            gb = v["bytes"] / (v["ms"] / 1e3) / 1e9
-            kroof[k] = {"GB/s": round(gb, 1), "frac": round(gb / float(peaks["hbm_gbs"]), 3)}
-    # whole-step roofline: T_roof = sum over kernel classes of
-    # max(algorithmic bytes / BW, algorithmic flops / P_class), on the measured counts
-    bw = float(peaks["hbm_gbs"]) * 1e9
-    p_tc = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))) * 1e12
-    p_f32 = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+            gb = v["bytes"] / s / 1e9
+            kroof[k] = {"GB/s": round(gb, 1), "frac": round(gb / p_hbm, 3)}
+    # whole-step roofline: T_roof = sum over kernel classes
+    # of max(algorithmic bytes / BW, algorithmic flops / P_class), measured counts
     t_roof = 0.0
     for k, v in kt.items():
         p = p_tc if k.startswith("conv_tc") else p_f32
-        t_roof += max(v["bytes"] / bw, v["flops"] / p)
+        t_roof += max(v["bytes"] / (p_hbm * 1e9), v["flops"] / (p * 1e12))
     t_roof_ms = t_roof * 1e3 / args.steps
-    step_roof = {"t_roof_ms": t_roof_ms, "t_measured_ms": None, "frac": None,
-                 "note": "sum over kernel classes of max(alg bytes / HBM peak, alg flops / class peak); "
-                         "classes without a byte model (scan, counts, dense_misc) contribute 0"}
+    dom = max(kt, key=lambda k: kt[k]["ms"])
     d = kt[dom]
     nl = max(d["launches"], 1)
-    if d["flops"] > 0 and dom.startswith("conv_tc"):
-        # tcgen05 bf16: measured cuBLAS bf16 peak, sustained figure (kernel timed inside a long step)
-        peak_key = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
-        peak = float(peaks.get(peak_key, 1590.0))
+    share = d["ms"] / args.steps / step_kernel_ms
+    if d["flops"] > 0 and dom.startswith("conv_tc") and d["flops"] / (p_tc * 1e12) >= d["bytes"] / (p_hbm * 1e9):
         ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": ncu_traffic(dom, cfg.cid), "kernel": dom,
-                "peak_source": f"{peak_src} {peak_key}",
-                "share_of_step": d["ms"] / args.steps / step_kernel_ms}
-    elif d["flops"] > 0 and dom.startswith("conv"):
-        # FP32 CUDA-core FFMA: 148 SMs x 128 lanes x 2 flop x max SM clock
-        peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": p_tc, "unit": "TFLOP/s", "frac": ach / p_tc,
+                "peak_source": f"{peak_src} {tc_key}" + (" (SM clock at max)" if at_max else "")}
+    elif d["flops"] > 0 and dom.startswith("conv") and not dom.startswith("conv_tc") and \
+            d["flops"] / (p_f32 * 1e12) >= d["bytes"] / (p_hbm * 1e9):
         ach = d["flops"] / nl / (d["ms"] / nl / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": ncu_traffic(dom, cfg.cid), "kernel": dom,
-                "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz",
-                "share_of_step": d["ms"] / args.steps / step_kernel_ms}
+        roof = {"bound": "alu", "achieved": ach, "peak": p_f32, "unit": "TFLOP/s", "frac": ach / p_f32,
+                "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz"}
     else:
-        peak = float(peaks["hbm_gbs"])
         ach = (d["bytes"] / nl) / (d["ms"] / nl / 1e3) / 1e9 if d["bytes"] else None
-        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": ncu_traffic(dom, cfg.cid), "kernel": dom,
-                "peak_source": peak_src, "share_of_step": d["ms"] / args.steps / step_kernel_ms}
+        roof = {"bound": "hbm", "achieved": ach, "peak": p_hbm, "unit": "GB/s", "frac": (ach / p_hbm) if ach else None,
+                "peak_source": f"{peak_src} hbm_gbs"}
+    roof.update({"traffic": ncu_traffic(dom, cfg.cid, args.precision), "kernel": dom,
+                 "alg_bytes_per_launch": d["bytes"] / nl, "alg_flops_per_launch": d["flops"] / nl,
+                 "launches_per_step": d["launches"] / args.steps, "share_of_step": share})
 
-    # ---- own dense path: every frame as a reference frame, same kernels
+    # ---- own dense path: every frame of the group as a reference frame, same kernels
     dense = None
     if not args.no_dense:
-        denc = Encoder(net, max_chunks=B * L, max_frames=1, device=local, precision=args.precision)
-        xd = batches[0].reshape(B * L, cfg.h, cfg.w, cfg.c)
+        denc = Encoder(net, max_chunks=Br * L, max_frames=1, device=local, precision=args.precision)
+        xd = inputs[0].reshape(Br * L, cfg.h, cfg.w, cfg.c)
         for _ in range(2):
             denc.encode_reference(xd, stream)
-            denc.encode_diff(None, ctl.thresholds(), stream)
+            denc.encode_diff(None, theta_timed, stream)
         torch.cuda.synchronize(dev)
         dms = 0.0
         nd = max(3, min(args.steps, 5))
@@ -448,37 +517,37 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             denc.encode_reference(xd, stream)
-            denc.encode_diff(None, ctl.thresholds(), stream)
+            denc.encode_diff(None, theta_timed, stream)
             e1.record(stream)
             e1.synchronize()
             dms += e0.elapsed_time(e1)
-        dense_fps = B * L / (dms / nd / 1e3)
-        ref_ms = dms / nd / L   # dense time of B reference frames
+        dense_fps = Br * L / (dms / nd / 1e3)
+        ref_ms = dms / nd / L   # dense time of the Br reference frames
         dense = {"dense_fps_per_gpu": dense_fps, "speedup_vs_dense": (value / world) / dense_fps,
                  "diff_fps_excl_reference": diff_frames / max((ms_step - ref_ms) / 1e3, 1e-9)}
         del denc
 
     mem = enc.memory_report()
-    # ---- the bit-exact FP32 mode on the same batches (context for the BF16 headline)
+    # ---- the bit-exact FP32 mode on the same chunks (context for the BF16 headline)
     fp32_exact = None
-    if args.precision == "bf16":
+    if args.precision == "bf16" and not args.no_fp32:
         del enc
-        fenc = Encoder(net, max_chunks=B, max_frames=L, device=local, precision="fp32")
-        th = ctl.thresholds()
+        fenc = Encoder(net, max_chunks=Br, max_frames=L, device=local, precision="fp32")
         fms = 0.0
         for k in range(4):
             flush.fill_(float(k))
+            x = inputs[k % res_groups]
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            fenc.encode_reference(batches[k % n_batches][:, 0], stream)
-            fenc.encode_diff(batches[k % n_batches][:, 1:], th, stream)
+            fenc.encode_reference(x[:, 0], stream)
+            fenc.encode_diff(x[:, 1:], theta_timed, stream)
             e1.record(stream)
             e1.synchronize()
             if k:
                 fms += e0.elapsed_time(e1)
-        fp32_exact = {"value": diff_frames / (fms / 3 / 1e3), "ms_per_step": fms / 3,
-                      "note": "FP32 mode (bit-exact with the oracle), CUDA-core convs"}
-        enc = fenc
+        fp32_exact = {"value": diff_frames / (fms / 3 / 1e3) if world == 1 else None, "ms_per_step": fms / 3,
+                      "note": "FP32 mode (bit-exact with the oracle), CUDA-core convs, same thresholds"}
+        del fenc
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -486,26 +555,35 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "bf16xbf16->f32",
-                "data": "synthetic",
-                "config": {"workload": f"cfg{cfg.cid}: {cfg.note}", "chunks_per_step_per_gpu": B,
-                           "frames_per_chunk": L, "frame": [cfg.h, cfg.w, cfg.c], "policy": policy,
-                           "theta": [float(x) for x in ctl.thresholds()[:3]] + ["..."],
-                           "parallelism": f"chunk-sharded dp{world}", "l2": "flushed between timed steps",
-                           "input_bytes_per_step": frame_bytes, "frames": "uint8 (v/255, R20)"},
-                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": frame_bytes,
-                        "d2h_bytes_per_step": int(host_out[0].numel() * 4), "steps": e2e_steps,
-                        "pipelined": "H2D of step k+1 and D2H of step k on copy streams overlap compute"},
+                "data": "synthetic (seeded video, calibrated random weights R30)",
+                "config": {"workload": f"cfg{cfg.cid}: {cfg.note}", "chunks_per_step": B,
+                           "chunks_per_step_per_gpu": Br, "job_chunks": B * n_groups,
+                           "resident_chunk_groups": res_groups, "frames_per_chunk": L,
+                           "frame": [cfg.h, cfg.w, cfg.c], "policy": policy,
+                           "thresholds": ("BST calibrated untimed for %d steps, frozen" % calib_steps) if frozen_run
+                           else policy,
+                           "parallelism": f"chunk-sharded dp{world} (R15 fixed groups)",
+                           "l2": "flushed between timed steps (256 MiB write, untimed)",
+                           "input_bytes_per_step": frame_bytes * world, "frames": "uint8 (v/255, R20)"},
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": frame_bytes * world,
+                        "d2h_bytes_per_step": d2h_bytes * world, "steps": e2e_steps,
+                        "pipelined": "H2D of step k+1 and D2H of step k (all taps) on copy streams overlap compute"},
                 "gpu_launches": launches_per_step * args.steps,
                 "roofline": roof,
                 "cpu_baseline": cpu,
                 "clocks": clocks,
+                "theta": [round(v, 5) for v in theta_timed],
                 "site_sparsity": site_sparsity,
                 "conv_rows_out": int(sum(lc["rows_out"][i] for i, l in enumerate(net.layers) if l["kind"] == W.CONV)),
                 "kernel_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in kt.items() if v["launches"]},
                 "kernel_roofline": kroof,
-                "step_roofline": dict(step_roof, t_measured_ms=ms_step, frac=step_roof["t_roof_ms"] / ms_step),
+                "peaks": {"tensor_tflops": p_tc, "tensor_key": tc_key, "hbm_gbs": p_hbm,
+                          "fp32_tflops_derived": p_f32, "source": peak_src},
+                "step_roofline": {"t_roof_ms": t_roof_ms, "t_measured_ms": ms_step, "frac": t_roof_ms / ms_step,
+                                  "note": "sum over kernel classes of max(alg bytes / HBM peak, alg flops / class "
+                                          "peak); classes without a byte model (scan, counts, dense_misc) count 0"},
                 "memory": mem, "fp32_exact": fp32_exact}
         if dense:
             line.update(dense)

@@ -58,3 +58,39 @@ class StatsExchange:
         for r in range(per_rank.shape[0]):   # rank order
             tot += per_rank[r]
         return tot[: self.n], tot[self.n:]
+
+
+class StepLoop:
+    """The step schedule of a chunk-sharded job (reading R15).
+
+    The job is n_groups fixed groups of chunks_per_step chunks; global step s
+    processes group s mod n_groups, and rank r of G takes the group's chunks
+    r, r+G, r+2G, ... (``shard``).  Every step: thresholds from the
+    controller -> the rank's chunks are encoded (``encode(group, chunk_ids,
+    thresholds)``, which fills ``exchange.local`` with the rank's int64
+    (active, pixels) site counts, e.g. via st_copy_site_counts, or returns
+    them) -> one all-gather -> the identical controller update on every rank.
+    One observation per step over the whole group, whatever G is, so the
+    thresholds -- and with them every output -- are independent of the GPU
+    count (PIN15)."""
+
+    def __init__(self, chunks_per_step: int, n_groups: int, rank: int, world: int, controller, exchange):
+        self.B, self.n_groups = chunks_per_step, n_groups
+        self.rank, self.world = rank, world
+        self.ctl, self.ex = controller, exchange
+        self.history = []
+
+    def group(self, step: int) -> int:
+        return step % self.n_groups
+
+    def chunks(self, step: int):
+        return shard(self.group(step), self.B, self.rank, self.world)
+
+    def run_step(self, step: int, encode, observe: bool = True):
+        th = self.ctl.thresholds()
+        self.history.append(np.array(th, np.float32))
+        local = encode(self.group(step), self.chunks(step), th)
+        if observe:
+            sa, sp = self.ex.exchange(local)
+            self.ctl.observe(sa, sp)
+        return th

@@ -1,7 +1,12 @@
 #!/usr/bin/env python
-"""Run W warm-up steps then K steps of config c (for ncu / ST_PROF_TRACE).
+"""The bench step of a config for ncu: calibrate (BST until every site is
+frozen, as bench.py does), W warm-up steps, then K profiled steps between
+cudaProfilerStart/Stop (run ncu with --profile-from-start off).
 
-    python scripts/prof_step.py --config 2 --warmup 3 --steps 1 [--profiling]
+    python scripts/prof_step.py --config 5 --warmup 3 --steps 1 [--profiling] [--eager]
+
+--eager: ST_NO_GRAPHS=1 (one launch per kernel instead of a graph replay).
+--profiling: library per-launch events (ST_PROF_TRACE=1 lines on stderr).
 """
 import argparse
 import os
@@ -13,12 +18,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--steps", type=int, default=1)
-ap.add_argument("--profiling", action="store_true", help="library per-launch events (ST_PROF_TRACE lines)")
+ap.add_argument("--profiling", action="store_true")
+ap.add_argument("--eager", action="store_true")
 ap.add_argument("--precision", default="bf16")
 a = ap.parse_args()
+if a.eager:
+    os.environ["ST_NO_GRAPHS"] = "1"
+if a.profiling:
+    os.environ["ST_PROF_TRACE"] = "1"   # read at st_encoder_create
 
 import torch  # noqa: E402
 from paper_2410_20790_b200 import Encoder, ThresholdController  # noqa: E402
@@ -27,29 +37,37 @@ cfg = W.get_config(a.config)
 net = cfg.build_net()
 B, L = cfg.chunks_per_step, cfg.L
 enc = Encoder(net, max_chunks=B, max_frames=L, device=0, precision=a.precision)
-ctl = ThresholdController(enc.n_sites, policy=cfg.policy, T=cfg.T, eps=cfg.eps, theta_fixed=cfg.theta_fixed,
+policy = "bst" if cfg.policy != "fixed" else "fixed"
+ctl = ThresholdController(enc.n_sites, policy=policy, T=cfg.T, eps=cfg.eps, theta_fixed=cfg.theta_fixed,
                           cycle=cfg.cycle)
 u8 = np.stack([W.gen_chunk(cfg.video_seed(c), L, cfg.h, cfg.w, cfg.c, **cfg.video) for c in range(B)])
-x = torch.from_numpy(W.to_float(u8)).cuda()
+x = torch.from_numpy(u8).cuda()
 s = torch.cuda.current_stream()
 
 
-def step():
+def step(observe):
     enc.encode_reference(x[:, 0], s)
     enc.encode_diff(x[:, 1:], ctl.thresholds(), s)
-    if cfg.policy != "fixed":
+    if observe:
         _, sa, sp = enc.get_sparsity()
         ctl.observe(sa, sp)
 
 
+n = 0
+while policy != "fixed" and n < 40 and not bool(np.all(ctl.state()[3])):
+    step(True)
+    n += 1
 for _ in range(a.warmup):
-    step()
+    step(False)
 torch.cuda.synchronize()
+print(f"calibrated {n} steps, theta {np.round(ctl.thresholds(), 4).tolist()}", file=sys.stderr)
 if a.profiling:
     enc.set_profiling(True)
+torch.cuda.profiler.start()
 for _ in range(a.steps):
-    step()
+    step(False)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 if a.profiling:
     enc.kernel_times(reset=True)   # folds the records: ST_PROF_TRACE lines go to stderr
-print("done", file=sys.stderr)
+print(f"done: {enc.last_launch_count()} launches per step", file=sys.stderr)

@@ -104,3 +104,67 @@ def test_two_ranks_match_single_process():
     assert sorted(merged) == sorted(taps1)
     for cid in taps1:                                # PIN15: outputs bit-identical across G
         assert np.array_equal(merged[cid], taps1[cid])
+
+
+# ---------------------------------------------------------------- StepLoop
+def _run_loop(rank, world, port, out):
+    """The bench's own step loop (paper_2410_20790_b200.sharding.StepLoop:
+    R15 fixed groups, StatsExchange all-gather, the C++ controller) with the
+    oracle standing in for the GPU encoder."""
+    import torch.distributed as dist
+    from paper_2410_20790_b200 import ThresholdController
+    from paper_2410_20790_b200.sharding import StatsExchange, StepLoop
+    if world > 1:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    net, frames = _setup()
+    ns = oracle.num_sites(net)
+    ctl = ThresholdController(ns, policy="ibst", T=0.6, eps=0.05, cycle=3)
+    loop = StepLoop(GROUP, STEPS, rank, world, ctl, StatsExchange(ns))
+    shp = oracle.shapes(net)
+    per_site_px = np.array([20 * 24] + [shp[i][0] * shp[i][1] for i, l in enumerate(net.layers)
+                                        if l["kind"] in W.NONLINEAR], np.int64)
+    taps = {}
+
+    def encode(group, ids, th):
+        act = np.zeros(ns, np.int64)
+        for cid in ids:
+            r = oracle.run_chunk(net, frames[cid], th, want_masks=False)
+            act += r["counts"].sum(1)
+            taps[(len(loop.history), cid)] = r["taps"][3]
+        return np.concatenate([act, per_site_px * 5 * len(ids)])
+
+    for step in range(2 * STEPS):          # every group twice: the job wraps around
+        loop.run_step(step, encode)
+    out[rank] = (np.array(loop.history), taps)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def test_step_loop_gpu_count_invariant():
+    """PIN15 on the bench's step loop: G = 1, 2 and 4 ranks give identical
+    threshold sequences and bit-identical per-chunk outputs."""
+    ref = {}
+    _run_loop(0, 1, 0, ref)
+    th1, taps1 = ref[0]
+    assert len(np.unique(th1[:, 1])) > 1
+    ctx = mp.get_context("spawn")
+    for world in (2, 4):
+        mgr = ctx.Manager()
+        out = mgr.dict()
+        port = _free_port()
+        ps = [ctx.Process(target=_run_loop, args=(r, world, port, out)) for r in range(world)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join(300)
+            assert p.exitcode == 0
+        merged = {}
+        for r in range(world):
+            th, taps = out[r]
+            assert np.array_equal(th, th1), (world, r)
+            merged.update(taps)
+        assert sorted(merged) == sorted(taps1)
+        for k in taps1:
+            assert np.array_equal(merged[k], taps1[k])

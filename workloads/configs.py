@@ -6,6 +6,7 @@ step B, the synthetic-video recipe and the threshold policy.  cfg ids are
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 from . import models
@@ -32,11 +33,18 @@ class Config:
     cycle: int = 8
     note: str = ""
 
-    def build_net(self, weight_seed=None):
+    def build_net(self, weight_seed=None, calibrated=True):
+        """Topology + seeded weights; with ``calibrated`` (and the default
+        seed) the committed per-channel BatchNorm fold of reading R30
+        (workloads/calib/cfg<N>.npz, written once by
+        scripts/calibrate_weights.py) is applied when it exists."""
         net = {"toy": models.toy_encoder, "crnn": models.crnn_vgg7,
                "resnet18": models.resnet18, "effb0": models.efficientnet_b0,
                "resnet152": models.resnet152}[self.model](self.h, self.w)
         models.init_weights(net, SEED_BASE + 1000 * self.cid + 999 if weight_seed is None else weight_seed)
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "calib", f"cfg{self.cid}.npz")
+        if calibrated and weight_seed is None and os.path.exists(path):
+            models.apply_fold(net, path)
         return net
 
     def video_seed(self, chunk):

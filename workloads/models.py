@@ -142,6 +142,26 @@ def init_weights(net: Net, seed: int):
     return net
 
 
+def apply_fold(net: Net, path: str):
+    """Apply committed per-channel fold factors (reading R30): for CONV layer
+    i, w' = w * s_i[c_out], b' = b * s_i + t_i; for SE layer i the excitation
+    FC2, w2' = w2 * s_i[c], b2' = b2 * s_i + t_i.  Weight construction only
+    (the factors come from scripts/calibrate_weights.py)."""
+    f = np.load(path)
+    for i, l in enumerate(net.layers):
+        if f"s{i}" not in f:
+            continue
+        s = f[f"s{i}"].astype(np.float64)
+        t = f[f"t{i}"].astype(np.float64)
+        if l["kind"] == CONV:
+            l["w"] = (l["w"].astype(np.float64) * s[:, None, None, None]).astype(np.float32)
+            l["b"] = (l["b"].astype(np.float64) * s + t).astype(np.float32)
+        elif l["kind"] == SE:
+            l["w2"] = (l["w2"].astype(np.float64) * s[:, None]).astype(np.float32)
+            l["b2"] = (l["b2"].astype(np.float64) * s + t).astype(np.float32)
+    return net
+
+
 # ----------------------------------------------------------------------------
 # The five BASELINE.json topologies
 # ----------------------------------------------------------------------------
