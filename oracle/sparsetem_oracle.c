@@ -300,7 +300,10 @@ void orc_dilate(const uint8_t *m, int H, int W, int kh, int kw, int sh, int sw, 
  * the oracle adopts the GPU's decision ONLY inside the band; every other
  * decision stays its own, and a disagreement there is counted as a violation.
  * tau = a_theta * theta + a_rms * rms + a_abs, rms = root mean square of the
- * oracle's candidate values over the touched pixels of that site and frame.
+ * site's current output f(x_acc) (= candidate + y_acc) over the touched pixels
+ * of that site and frame: the candidate is a difference of two activation-
+ * sized values, so the two sides' candidates differ by amounts relative to
+ * the activations (bf16 roundings of x_acc / y_acc), not to the candidate.
  * stats per layer: [0] decisions, [1] inside the band, [2] adopted (the GPU's
  * decision differed from the oracle's own), [3] violations. */
 typedef struct {
@@ -382,8 +385,8 @@ static int64_t truncate_site(ctx_t *c, int i, int t, int No, int C, float *ya, f
         int64_t n = 0;
         for (int p = 0; p < No; p++)
             if (c->T[p]) {
-                for (int ch = 0; ch < C; ch++) {
-                    const double v = c->cand[(size_t)p * C + ch];
+                for (int ch = 0; ch < C; ch++) {   /* the site's current output f(x_acc) = cand + y_acc */
+                    const double v = (double)c->cand[(size_t)p * C + ch] + (double)ya[(size_t)p * C + ch];
                     ss += v * v;
                 }
                 n += C;

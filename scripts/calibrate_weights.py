@@ -12,7 +12,7 @@ standard deviation of the pre-activation on a calibration frame (frame 0 of
 the config's chunk 0) and folds them into the weights, so every channel's
 pre-activation has mean 0 and the layer's pre-activation has standard
 deviation 1 on that frame; every SE
-excitation is rescaled so its gate logits have mean 0.5 and standard
+excitation is rescaled so its gate logits have mean 0.6 and standard
 deviation 0.7 over channels (gates mostly inside [0.3, 0.85]).  The deviation is one per
 layer (the per-channel means are removed): per-channel scaling would amplify
 near-constant channels and make the random network chaotic.
@@ -44,7 +44,7 @@ import workloads as W  # noqa: E402
 from workloads import CONV, RELU, SILU, MAXPOOL, ADD, SE, OUTPUT  # noqa: E402
 
 SE_LOGIT_STD = 0.7
-SE_LOGIT_MEAN = 0.5
+SE_LOGIT_MEAN = 0.6
 
 
 def _t(a):

@@ -160,9 +160,18 @@ def follow_compare(enc, net, frames_chunk, thresholds, chunk, precision, exporte
     for tap, O in r["taps"].items():
         got = enc.outputs(tap)[chunk].cpu().numpy()
         if precision == "bf16":
-            ok, e = bf16_within(got, O)
+            # R29-BF16 for taps: per frame normwise 2e-2 relative (north_star),
+            # and elementwise 2e-2|b| + 0.1 rms(b): one-ulp bf16 rounding flips
+            # (2^-8 relative, triggered by fp32 summation-order differences)
+            # are amplified through ~100 layers, and the elementwise tail over
+            # ~1e6 elements sits ~5x above the normwise error
+            for t in range(F + 1):
+                a64, b64 = got[t].astype(np.float64), O[t].astype(np.float64)
+                rel = float(np.linalg.norm(a64 - b64) / max(np.linalg.norm(b64), 1e-30))
+                assert rel <= 2e-2, f"tap {tap} frame {t}: normwise relative error {rel:.4f}"
+            ok, e = bf16_within(got, O, rel=2e-2, rms_frac=0.1)
             worst = max(worst, e)
-            assert ok, f"tap {tap} beyond the bf16 bound ({e:.2f} x bound)"
+            assert ok, f"tap {tap} beyond the elementwise bf16 bound ({e:.2f} x bound)"
         elif adopted == 0 and all(net.layers[i]["kind"] in (W.RELU, W.MAXPOOL) for i in site_layers(net)):
             assert np.array_equal(got, O), f"tap {tap} outputs differ"
         else:

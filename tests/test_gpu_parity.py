@@ -301,28 +301,16 @@ def test_resnet152_small_exact():
 
 
 def test_resnet152_bf16():
-    import torch
-    from paper_2410_20790_b200 import Encoder
+    """N3 ResNet-152 in BF16 mode (tcgen05 convs, 155 of them): band-follow
+    parity (O12) against the oracle's BF16 contract -- zero decisions outside
+    the R23 band disagree, masks / index lists / counts exact, rows and taps
+    within R29-BF16."""
+    from gpu_harness import follow_compare, gpu_run
     net = W.models.resnet152(64, 64)
     init_weights(net, 22)
     fr = W.to_float(W.gen_video(2, 6, 64, 64, 3, 82, n_objects=3, size=(8, 20), speed=(1, 3), noise_q=0.1,
                                 noise_amp=2))
-    enc = Encoder(net, 2, 6, precision="bf16")
-    x = torch.from_numpy(fr).cuda()
-    enc.encode_reference(x[:, 0])
-    enc.encode_diff(x[:, 1:], 0.0)
-    torch.cuda.synchronize()
-    tap = enc.taps[0]
-    out = enc.outputs(tap).cpu().numpy()
+    enc, _ = gpu_run(net, fr, 0.05, precision="bf16")
     for b in range(2):
-        r = oracle.run_chunk(net, fr[b], 0.0, want_masks=False, precision="bf16")
-        ref = r["taps"][tap].astype(np.float64)
-        rms = float(np.sqrt(np.mean(ref * ref)))
-        err = np.abs(out[b] - ref)
-        bad = float(np.mean(err > 2e-2 * np.abs(ref) + 2e-2 * rms))
-        rel = float(np.linalg.norm(out[b] - ref) / max(np.linalg.norm(ref), 1e-30))
-        # 155 convs, each delta row bf16-rounded at every conv and site: the
-        # rounding differences between the tensor-core and the oracle's
-        # summation order random-walk with depth (~sqrt(155) bf16 ulps), so the
-        # bar is the relative L2 error plus >= 99 % of elements in the bound
-        assert rel <= 2e-2 and bad <= 1e-2, (b, bad, rel, float(err.max()), rms)
+        rep = follow_compare(enc, net, fr[b], 0.05, b, "bf16")
+        assert rep["adopted"] <= max(3, 1e-3 * rep["decisions"]), rep

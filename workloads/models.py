@@ -50,19 +50,19 @@ class Net:
     def _add(self, **kw):
         base = dict(kind=None, src=-1, src2=-1, c_out=0, groups=1, k_h=1, k_w=1,
                     s_h=1, s_w=1, p_h=0, p_w=0, se_hidden=0,
-                    w=None, b=None, w2=None, b2=None, act_gain=2.0)
+                    w=None, b=None, w2=None, b2=None, act_gain=2.0, smooth=0.0)
         base.update(kw)
         self.layers.append(base)
         return len(self.layers) - 1
 
-    def conv(self, src, c_out, k, s=1, p=None, groups=1, act_gain=2.0):
+    def conv(self, src, c_out, k, s=1, p=None, groups=1, act_gain=2.0, smooth=0.0):
         kh, kw = (k, k) if isinstance(k, int) else k
         sh, sw = (s, s) if isinstance(s, int) else s
         if p is None:
             p = (kh // 2, kw // 2)
         ph, pw = (p, p) if isinstance(p, int) else p
         return self._add(kind=CONV, src=src, c_out=c_out, groups=groups, k_h=kh, k_w=kw,
-                         s_h=sh, s_w=sw, p_h=ph, p_w=pw, act_gain=act_gain)
+                         s_h=sh, s_w=sw, p_h=ph, p_w=pw, act_gain=act_gain, smooth=smooth)
 
     def relu(self, src):
         return self._add(kind=RELU, src=src)
@@ -118,7 +118,14 @@ def init_weights(net: Net, seed: int):
 
     CONV: He-normal, std = sqrt(gain / fan_in), fan_in = (c_in/groups)*k_h*k_w,
     so activations stay O(1) through ReLU/SiLU stacks (DESIGN.md input recipe);
-    bias ~ U(-0.1, 0.1) (BatchNorm folded).
+    bias ~ U(-0.1, 0.1) (BatchNorm folded).  A spatial conv with
+    ``smooth`` = s > 0 (reading R30) mixes in a smooth component: every
+    (c_out, c_in) kernel becomes s * a * G * |w| + (1 - s) * w, with G a
+    Gaussian blob of unit sum (sigma = k/4), a ~ N(0, 1) and |w| the He
+    kernel's norm (so the smooth part's gain on flat content is O(1)) --
+    trained low-level filters pass smooth image content; pure white-noise
+    kernels act as high-pass filters, and once a BatchNorm fold rescales their
+    output they amplify frame noise and rounding layer after layer.
     SE: FC1 [hidden][C] std 1/sqrt(C), FC2 [C][hidden] std 1/sqrt(hidden),
     biases small, so gates sit mid-range.
     Returns the same Net with w/b filled (float32, C-contiguous).
@@ -131,8 +138,18 @@ def init_weights(net: Net, seed: int):
             cin_g = src_c // l["groups"]
             fan_in = cin_g * l["k_h"] * l["k_w"]
             std = math.sqrt(l["act_gain"] / fan_in)
-            l["w"] = (rng.standard_normal((l["c_out"], cin_g, l["k_h"], l["k_w"])) * std).astype(np.float32)
+            w = rng.standard_normal((l["c_out"], cin_g, l["k_h"], l["k_w"])) * std
             l["b"] = rng.uniform(-0.1, 0.1, l["c_out"]).astype(np.float32)
+            sm = float(l.get("smooth", 0.0))
+            if sm > 0 and l["k_h"] * l["k_w"] > 1:
+                ay = np.arange(l["k_h"]) - l["k_h"] // 2
+                ax = np.arange(l["k_w"]) - l["k_w"] // 2
+                G = np.exp(-(ay[:, None] ** 2 / (2 * (l["k_h"] / 4) ** 2) + ax[None, :] ** 2 / (2 * (l["k_w"] / 4) ** 2)))
+                G /= G.sum()
+                a = rng.standard_normal((l["c_out"], cin_g))[:, :, None, None]
+                nrm = np.sqrt((w * w).sum(axis=(2, 3), keepdims=True))
+                w = sm * a * G * nrm + (1 - sm) * w
+            l["w"] = w.astype(np.float32)
         elif l["kind"] == SE:
             c, hd = src_c, l["se_hidden"]
             l["w"] = (rng.standard_normal((hd, c)) / math.sqrt(c)).astype(np.float32)
@@ -247,6 +264,9 @@ def resnet152(h=320, w=320):
     return n
 
 
+SPATIAL_SMOOTH = 0.7   # EfficientNet spatial kernels (stem, depthwise), reading R30
+
+
 def efficientnet_b0(h=512, w=512):
     """cfg3/cfg5: EfficientNet-B0 backbone (EfficientDet-D0), taps P3/P4/P5.
 
@@ -255,7 +275,7 @@ def efficientnet_b0(h=512, w=512):
     (reading R11).  Taps = outputs of stages 3/5/7 (reading R13).
     """
     n = Net(3, h, w, "efficientnet_b0")
-    x = n.silu(n.conv(-1, 32, 3, 2, 1))
+    x = n.silu(n.conv(-1, 32, 3, 2, 1, smooth=SPATIAL_SMOOTH))
     c = 32
     stages = [  # expand, k, stride, c_out, repeats
         (1, 3, 1, 16, 1), (6, 3, 2, 24, 2), (6, 5, 2, 40, 2), (6, 3, 2, 80, 3),
@@ -268,7 +288,7 @@ def efficientnet_b0(h=512, w=512):
             y = x
             if e != 1:
                 y = n.silu(n.conv(y, ce, 1, 1, 0))
-            y = n.silu(n.conv(y, ce, k, stride, k // 2, groups=ce))
+            y = n.silu(n.conv(y, ce, k, stride, k // 2, groups=ce, smooth=SPATIAL_SMOOTH))
             y = n.se(y, max(1, c // 4))
             y = n.conv(y, co, 1, 1, 0, act_gain=1.0)
             if stride == 1 and c == co:
