@@ -78,6 +78,9 @@ def parse():
     ap.add_argument("--no-dense", action="store_true", help="skip the own-dense-path reference timing")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32-mode context timing")
+    ap.add_argument("--headroom", type=float, default=1.25,
+                    help="row capacity = headroom x the largest row count seen in the untimed steps (a9); 0 = keep "
+                         "the all-active bound")
     return ap.parse_args()
 
 
@@ -330,10 +333,32 @@ def main():
             calib_steps += 1
             if bool(np.all(ctl.state()[3])):
                 break
+    # ---- row capacity from measured occupancy: every
+    # resident group once at the all-active bound, then the arena is re-planned
+    # at headroom x the largest row count of each delta tensor
+    mem_bound = dict(enc.memory_report(), device_bytes=enc.device_bytes())
+    if args.headroom >= 1.0:
+        for _ in range(res_groups):
+            loop.run_step(step_no, resident, observe=observe)
+            step_no += 1
+        enc.fit_capacity(args.headroom)
+    reissued = 0
+
+    def checked_step(fn):
+        # a step whose rows exceed a fitted capacity is clamped on the device and
+        # flagged: re-plan from the counts it saw and run it again
+        nonlocal reissued
+        while True:
+            fn()
+            if enc.step_ok():
+                return
+            reissued += 1
+            enc.fit_capacity(args.headroom)
+
     # ---- warm-up; every resident group twice (the library captures a CUDA
     # graph of the step on the second sight of an input buffer)
     for _ in range(args.warmup + 2 * res_groups):
-        loop.run_step(step_no, resident, observe=observe)
+        checked_step(lambda: loop.run_step(step_no, resident, observe=observe))
         step_no += 1
     torch.cuda.synchronize(dev)
     launches_per_step = enc.last_launch_count()
@@ -346,15 +371,23 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     total_ms = 0.0
-    for k in range(args.steps):
+    k = 0
+    while k < args.steps:
         flush.fill_(float(k))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         loop.run_step(step_no, resident, observe=observe)
-        step_no += 1
         e1.record(stream)
         e1.synchronize()
+        if not enc.step_ok():   # untimed check: a clamped step is re-planned and timed again
+            reissued += 1
+            enc.fit_capacity(args.headroom)
+            for _ in range(2):   # graph capture on the new arena
+                checked_step(lambda: loop.run_step(step_no, resident, observe=False))
+            continue
         total_ms += e0.elapsed_time(e1)
+        step_no += 1
+        k += 1
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -527,7 +560,8 @@ def main():
                  "diff_fps_excl_reference": diff_frames / max((ms_step - ref_ms) / 1e3, 1e-9)}
         del denc
 
-    mem = enc.memory_report()
+    mem = dict(enc.memory_report(), device_bytes=enc.device_bytes(), headroom=args.headroom,
+               reissued_steps=reissued, at_all_active_bound=mem_bound)
     # ---- the bit-exact FP32 mode on the same chunks (context for the BF16 headline)
     fp32_exact = None
     if args.precision == "bf16" and not args.no_fp32:

@@ -50,7 +50,11 @@ typedef enum {
     ST_ERR_UNSUPPORTED = 4,  /* valid but not implemented (e.g. L-1 > 32)     */
     ST_ERR_OOM = 5,          /* arena allocation failed                       */
     ST_ERR_CUDA = 6,         /* CUDA runtime error (message has the detail)   */
-    ST_ERR_INTERNAL = 7,     /* invariant violated (e.g. row capacity overflow) */
+    ST_ERR_INTERNAL = 7,     /* invariant violated                                  */
+    ST_ERR_CAPACITY = 8,     /* a delta tensor of the last step needed more rows than
+                                its capacity (row_frac / st_encoder_fit_capacity): the
+                                step's outputs and statistics are invalid; re-plan
+                                with st_encoder_fit_capacity and re-issue the step */
 } st_status;
 
 /* Layer kinds.  CONV is Eq.(1) (zero padding, groups; groups == c_in is
@@ -95,6 +99,14 @@ typedef struct {
                                   * (chunks longer than max_frames, live video).  *
                                   * Memory: those caches (st_memory_report).      *
                                   * ST_ERR_UNSUPPORTED with SE layers.            */
+    float row_frac;              /* row capacity of every delta tensor (SURVEY    *
+                                  * §8(a) a9; P:139, P:152 -- memory, not time,   *
+                                  * is the claim): 0 or >= 1 = the all-active     *
+                                  * bound B*(L-1)*N rows; in (0,1) = that         *
+                                  * fraction of it (>= 4096 rows).  A step that   *
+                                  * needs more rows is clamped on the device and  *
+                                  * reported as ST_ERR_CAPACITY; see              *
+                                  * st_encoder_fit_capacity.                      */
 } st_encoder_config;
 
 /* Validate specs, infer shapes, number the sites, repack weights, plan the
@@ -197,6 +209,32 @@ st_status st_debug_get_words(st_encoder *enc, int32_t layer, uint32_t *words_hos
  * reference + outputs), peak transient (max live set), arena total. */
 st_status st_memory_report(const st_encoder *enc, int64_t *persistent, int64_t *peak_transient,
                            int64_t *arena_total);
+/* Total device bytes the encoder holds: the arena plus the fixed areas
+ * (staged reference, counts, scan scratch) and the device weights. */
+st_status st_device_bytes(const st_encoder *enc, int64_t *total);
+
+/* Row capacity.  Every scan of a delta tensor checks its
+ * row capacity on the device; words whose rows would not fit are cleared
+ * (nothing is written past a buffer) and the step is flagged.
+ * st_step_status: synchronizes the last encode's stream; ST_ERR_CAPACITY if
+ *   that step was clamped, else ST_OK.
+ * st_get_capacity: per delta tensor (layer i at [i], the input site at
+ *   [n_layers]; -1 for layers without their own rows) the current capacity
+ *   and the largest row count any step needed since create (host arrays of
+ *   n_layers + 1, either may be NULL; synchronizes).
+ * st_encoder_fit_capacity: re-plan the arena with every capacity = ceil(
+ *   headroom * largest row count seen) (>= 4096, <= the all-active bound;
+ *   headroom >= 1), i.e. from measured occupancy instead of the all-active
+ *   bound.  Frees and reallocates the arena: borrowed output pointers and
+ *   the last step's results become invalid, captured graphs are dropped.
+ *   The staged reference frames survive, so the same step can be re-issued
+ *   with st_encode_diff.  ST_ERR_UNSUPPORTED for streaming encoders (their
+ *   caches live in the arena), ST_ERR_ARG for headroom < 1, ST_ERR_OOM if
+ *   the new arena cannot be allocated (the encoder then has none: destroy
+ *   it). */
+st_status st_step_status(st_encoder *enc);
+st_status st_get_capacity(st_encoder *enc, int64_t *rows_cap, int64_t *rows_peak);
+st_status st_encoder_fit_capacity(st_encoder *enc, double headroom);
 
 /* Optional per-kernel timing with CUDA events on the launch stream (adds an
  * event pair per launch; off by default).  Kernel classes are named by

@@ -7,5 +7,5 @@ with the same names (argument marshalling only).  There is no CPU fallback:
 loading fails loudly when the library is missing.
 """
 from .binding import (  # noqa: F401
-    lib, load_library, StError, Encoder, ThresholdController, KIND, PRECISION,
+    lib, load_library, StError, CapacityError, Encoder, ThresholdController, KIND, PRECISION,
 )

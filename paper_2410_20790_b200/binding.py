@@ -17,13 +17,19 @@ LIB_PATH = os.path.join(HERE, "libsparsetem.so")
 KIND = dict(conv=0, relu=1, silu=2, maxpool=3, add=4, se=5, output=6)
 PRECISION = dict(fp32=0, bf16=1)
 STATUS = {0: "ST_OK", 1: "ST_ERR_ARG", 2: "ST_ERR_SHAPE", 3: "ST_ERR_STATE", 4: "ST_ERR_UNSUPPORTED",
-          5: "ST_ERR_OOM", 6: "ST_ERR_CUDA", 7: "ST_ERR_INTERNAL"}
+          5: "ST_ERR_OOM", 6: "ST_ERR_CUDA", 7: "ST_ERR_INTERNAL", 8: "ST_ERR_CAPACITY"}
+ST_ERR_CAPACITY = 8
 
 
 class StError(RuntimeError):
     def __init__(self, fn, status, msg=""):
         self.status = status
         super().__init__(f"{fn} failed: {STATUS.get(status, status)} {msg}".strip())
+
+
+class CapacityError(StError):
+    """The last step needed more delta rows than a tensor's capacity
+    (ST_ERR_CAPACITY): its results are invalid; fit_capacity() and re-issue."""
 
 
 class st_layer_spec(C.Structure):
@@ -34,7 +40,7 @@ class st_layer_spec(C.Structure):
 
 class st_encoder_config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("in_c", "in_h", "in_w", "max_chunks", "max_frames", "precision",
-                                         "device", "debug_retain", "streaming")]
+                                         "device", "debug_retain", "streaming")] + [("row_frac", C.c_float)]
 
 
 class st_ctl_config(C.Structure):
@@ -63,6 +69,10 @@ SIGNATURES = {
     "st_debug_export_chunk": (I32, [P, I32]),
     "st_debug_get_words": (I32, [P, I32, P]),
     "st_memory_report": (I32, [P, P, P, P]),
+    "st_device_bytes": (I32, [P, P]),
+    "st_step_status": (I32, [P]),
+    "st_get_capacity": (I32, [P, P, P]),
+    "st_encoder_fit_capacity": (I32, [P, C.c_double]),
     "st_set_profiling": (I32, [P, I32]),
     "st_num_kernel_classes": (I32, []),
     "st_kernel_class_name": (C.c_char_p, [I32]),
@@ -123,7 +133,7 @@ class Encoder:
     """One encoder = one network on one device (st_encoder_create)."""
 
     def __init__(self, net, max_chunks, max_frames, precision="fp32", device=0, debug_retain=False,
-                 streaming=False):
+                 streaming=False, row_frac=0.0):
         L = lib()
         self.net = net
         self.n_layers = len(net.layers)
@@ -140,7 +150,7 @@ class Encoder:
                     keep.append(a)
                     setattr(s, f, a.ctypes.data_as(C.POINTER(C.c_float)))
         cfg = st_encoder_config(net.in_c, net.in_h, net.in_w, max_chunks, max_frames, PRECISION[precision],
-                                device, int(bool(debug_retain)), int(bool(streaming)))
+                                device, int(bool(debug_retain)), int(bool(streaming)), float(row_frac))
         h = C.c_void_p()
         r = L.st_encoder_create(C.byref(cfg), C.cast(arr, C.c_void_p), self.n_layers, C.byref(h))
         if r != 0:
@@ -156,7 +166,8 @@ class Encoder:
     # -- helpers
     def _check(self, fn, r):
         if r != 0:
-            raise StError(fn, r, lib().st_last_error(self.h).decode(errors="replace"))
+            cls = CapacityError if r == ST_ERR_CAPACITY else StError
+            raise cls(fn, r, lib().st_last_error(self.h).decode(errors="replace"))
 
     def close(self):
         if getattr(self, "h", None):
@@ -287,6 +298,32 @@ class Encoder:
         self._check("st_memory_report", lib().st_memory_report(self.h, _np_ptr(v[0:]), _np_ptr(v[1:]),
                                                                _np_ptr(v[2:])))
         return dict(persistent_bytes=int(v[0]), peak_transient_bytes=int(v[1]), arena_bytes=int(v[2]))
+
+    def device_bytes(self):
+        v = np.zeros(1, np.int64)
+        self._check("st_device_bytes", lib().st_device_bytes(self.h, _np_ptr(v)))
+        return int(v[0])
+
+    # -- row capacity (a9)
+    def step_ok(self):
+        """False if the last step exceeded a row capacity (synchronizes)."""
+        r = lib().st_step_status(self.h)
+        if r == ST_ERR_CAPACITY:
+            return False
+        self._check("st_step_status", r)
+        return True
+
+    def capacity(self):
+        """(rows_cap, rows_peak) per delta tensor: layers, then the input site (-1: no own rows)."""
+        cap = np.zeros(self.n_layers + 1, np.int64)
+        pk = np.zeros(self.n_layers + 1, np.int64)
+        self._check("st_get_capacity", lib().st_get_capacity(self.h, _np_ptr(cap), _np_ptr(pk)))
+        return cap, pk
+
+    def fit_capacity(self, headroom=1.25):
+        """Re-plan the arena from the measured row counts (x headroom)."""
+        self._check("st_encoder_fit_capacity", lib().st_encoder_fit_capacity(self.h, C.c_double(headroom)))
+        self.n_diff = -1
 
     # -- profiling
     def set_profiling(self, on):

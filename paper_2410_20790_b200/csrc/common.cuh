@@ -74,6 +74,33 @@ __device__ __forceinline__ float sigm_f(float x) { return __fdiv_rn(1.0f, __fadd
 // the bf16 rounding of every emitted delta.
 __device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
+// pointwise non-linearity f of a site (kind fixed at compile time / at run time)
+template <int ACT>
+__device__ __forceinline__ float actf(float x) {
+    return ACT == ACT_RELU ? relu_f(x) : ACT == ACT_SILU ? silu_f(x) : silu_fast(x);
+}
+__device__ __forceinline__ float act_rt(int kind, float x) {
+    return kind == ACT_RELU ? relu_f(x) : kind == ACT_SILU ? silu_f(x) : silu_fast(x);
+}
+
+// lanes of this thread's pixel group (G lanes, G a power of two <= 32)
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+    if constexpr (G == 32) {
+        return 0xffffffffu;
+    } else {
+        const int lane = threadIdx.x & 31;
+        return ((1u << G) - 1u) << (lane & ~(G - 1));
+    }
+}
+
+template <int G>
+__device__ __forceinline__ float gmax(float v, unsigned mask) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+}
+
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // host-side dispatch on the row type

@@ -12,6 +12,7 @@
 // reference frames ("one buffer for Subtraction") and the output taps ("one
 // for Accumulation") persist across the step.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -29,12 +30,12 @@ namespace {
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
               KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16,
-              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_SE_SUMS = 20, KC_N = 21;
+              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_SE_SUMS = 20, KC_DW_SITE = 21, KC_N = 22;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
                               "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
                               "conv_tc_sparse", "conv_tc_dense", "se", "conv_tc_stem_sparse",
-                              "conv_tc_stem_dense", "prof_stats", "se_sums"};
+                              "conv_tc_stem_dense", "prof_stats", "se_sums", "dwconv_site"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -54,6 +55,8 @@ struct LayerRT {
     int n_consumers = 0, last_consumer = 0;
     int fused_pool = -1;      // ReLU: the maxpool that runs this site in its own pass
     int fused_relu = -1;      // MAXPOOL: the ReLU site folded into this layer's pass
+    int fused_dw = -1;        // ReLU/SiLU: the depthwise conv whose pass runs this site (N2)
+    int dw_site = -1;         // depthwise CONV: the pointwise site its sparse pass runs
     // streaming state (N1, persistent): pointwise site sx[0]/sy[0] in place;
     // maxpool sx[0..1] ping-pong x_acc + spy y_acc; fused pool (on the pool
     // layer) sx[0..1] ReLU x_acc, sy[0..1] ReLU y_acc, spy pool y_acc; OUTPUT sx[0]
@@ -106,6 +109,12 @@ struct st_encoder {
     int in_dd = -1;              // dense per-frame input delta for CUDA-core convs on the input
     int in_refbf = -1;           // reference frames as 4-channel-padded bf16 (tensor-core stems)
     int64_t in_rows_cap = 0;
+    // row capacity (a9): per delta tensor (layer i at i, the input at n) the
+    // fitted capacity (-1: none; then cfg.row_frac of the all-active bound)
+    std::vector<int64_t> cap_fit;
+    int32_t *ovf = nullptr;      // device: a scan clamped a tensor this step
+    long long *rows_peak = nullptr;   // device [n + 1]: max unclamped rows per tensor since create
+    int64_t fixed_bytes = 0;     // device bytes outside the arena (fixed areas, staged reference, weights)
     bool bf = false;             // BF16 mode: delta rows stored as bf16 (R22-BF16)
     int esz = 4;                 // delta-row element size in bytes
     std::vector<Buf> bufs;
@@ -209,6 +218,7 @@ static void prof_end(st_encoder *e, cudaStream_t s) {
 
 // ------------------------------------------------------------------- create
 static st_status plan(st_encoder *e);
+static st_status alloc_fixed(st_encoder *e);
 
 extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_layer_spec *layers, int32_t n,
                                        st_encoder **out) {
@@ -326,6 +336,21 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 r.fused_pool = i;
             }
     }
+    // depthwise conv -> pointwise site (ReLU / SiLU, the conv's only consumer):
+    // the site's state machine runs in the conv's pixel loop
+    {
+        const char *nf = getenv("ST_NO_FUSE_DW");   // A/B switch
+        const char *dr = getenv("ST_DW_ROWMAJOR");
+        if (!(nf && nf[0] == '1') && !(dr && dr[0] == '1') && !cfg->streaming)
+            for (int i = 0; i < n; i++) {
+                LayerRT &r = e->L[i];
+                if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0) continue;
+                LayerRT &cv = e->L[r.src];
+                if (cv.kind != ST_CONV || !cv.depthwise || cv.n_consumers != 1 || !dwconv_site_fusable(cv.geo)) continue;
+                r.fused_dw = r.src;
+                cv.dw_site = i;
+            }
+    }
     // ---- weights (K-major repack: wk[(dy*kw+dx)*cin_g + ci][co], reading R18)
     int64_t wfloats = 0;
     for (auto &l : e->L)
@@ -337,6 +362,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             wfloats += 2 * ((hc + 63) / 64 * 64) + (l.spec.se_hidden + 63) / 64 * 64 + (l.C + 63) / 64 * 64;
         }
     CUDA_OK(e.get(), cudaMalloc(&e->weights_mem, std::max<int64_t>(wfloats, 1) * sizeof(float)));
+    e->fixed_bytes += std::max<int64_t>(wfloats, 1) * (int64_t)sizeof(float);
     {
         std::vector<float> host(std::max<int64_t>(wfloats, 1));
         int64_t o = 0;
@@ -398,6 +424,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
         }
         if (nbf) {
             CUDA_OK(e.get(), cudaMalloc(&e->wbf_mem, nbf * 2));
+            e->fixed_bytes += nbf * 2;
             std::vector<uint16_t> hb(nbf, 0);
             int64_t o = 0;
             for (auto &l : e->L) {
@@ -428,7 +455,9 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
         }
     }
     for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
+    e->cap_fit.assign(n + 1, -1);
     st_status r = plan(e.get());
+    if (r == ST_OK) r = alloc_fixed(e.get());
     if (r != ST_OK) {
         cudaFree(e->weights_mem);
         return r;
@@ -438,10 +467,27 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
 }
 
 // ------------------------------------------------------------------- planner
+// row capacity of delta tensor `idx` (layer i, or n = the input site) whose
+// all-active bound is `full` rows (B * (L-1) * N): the fitted capacity, else
+// cfg.row_frac of the bound (at least 4096 rows), else the bound
+static int64_t cap_for(const st_encoder *e, int idx, int64_t full) {
+    if (e->cap_fit[idx] >= 0) return std::min(full, e->cap_fit[idx]);
+    const double f = e->cfg.row_frac;
+    if (f > 0.0 && f < 1.0) return std::min(full, std::max<int64_t>((int64_t)std::ceil(f * (double)full), 4096));
+    return full;
+}
+
 static st_status plan(st_encoder *e) {
     const int n = (int)e->L.size();
     const int64_t B = e->B, F = e->F;
     const int END = n + 1;   // step end
+    e->bufs.clear();
+    e->in_act = e->in_pbase = e->in_rows = e->in_dd = e->in_refbf = e->in_S = -1;
+    for (auto &l : e->L) {
+        l.b_y0 = l.b_act = l.b_slot = l.b_pbase = l.b_rows = l.b_ridx = l.b_out = l.b_ybf = l.b_se = -1;
+        l.alias_rows_of = -1;
+        l.sx[0] = l.sx[1] = l.sy[0] = l.sy[1] = l.spy = -1;
+    }
     auto add = [&](int64_t bytes, int first, int last) {
         Buf b;
         b.bytes = (bytes + 255) / 256 * 256;
@@ -457,7 +503,7 @@ static st_status plan(st_encoder *e) {
     for (int i = 0; i < n; i++)
         if (e->L[i].src == -1 || (e->L[i].kind == ST_ADD && e->L[i].src2 == -1)) in_last = std::max(in_last, t_of(i));
     const int64_t Nin = (int64_t)e->in_H * e->in_W;
-    e->in_rows_cap = B * F * Nin;
+    e->in_rows_cap = cap_for(e, n, B * F * Nin);
     e->in_act = add(B * Nin * 4, 0, in_last);
     e->in_pbase = add(B * Nin * 4, 0, in_last);
     const int64_t ES = e->esz;   // delta-row element size: 4 (FP32 mode) or 2 (BF16 mode)
@@ -486,7 +532,7 @@ static st_status plan(st_encoder *e) {
         }
         l.b_y0 = add(B * N * l.C * 4, tdef, tlast);
         l.b_act = add(B * N * 4, tdef, tlast);
-        l.rows_cap = B * F * N;
+        l.rows_cap = cap_for(e, i, B * F * N);
         switch (l.kind) {
         case ST_CONV:
             l.b_pbase = add(B * N * 4, tdef, tlast);
@@ -619,15 +665,24 @@ static st_status plan(st_encoder *e) {
         peak = std::max(peak, live);
     }
     e->peak_transient = peak;
-    // ---- allocations
     if (cudaMalloc(&e->arena, std::max<int64_t>(total, 256)) != cudaSuccess) {
         cudaGetLastError();
+        e->arena = nullptr;
         return fail(e, ST_ERR_OOM, "arena of %lld bytes failed", (long long)total);
     }
+    return ST_OK;
+}
+
+// fixed device areas (counts, scan scratch, thresholds, staged reference ...),
+// streams and events: allocated once at create
+static st_status alloc_fixed(st_encoder *e) {
+    const int n = (int)e->L.size();
+    const int64_t B = e->B;
+    const int64_t Nin = (int64_t)e->in_H * e->in_W;
     int64_t max_words = B * Nin;
     for (auto &l : e->L) max_words = std::max<int64_t>(max_words, B * l.H * l.W);
     const int64_t small = (n + 1) * 4 + B * e->n_sites * 32 * 8 + (n + 1) * 3 * 8 + e->n_sites * 8 +
-                          scan_tmp_ints(max_words) * 4 + e->n_sites * 4 + 1024 + 8 * 256;
+                          scan_tmp_ints(max_words) * 4 + e->n_sites * 4 + 1024 + (n + 1) * 8 + 256 + 10 * 256;
     CUDA_OK(e, cudaMalloc(&e->smallmem, small));
     char *p = e->smallmem;
     auto take = [&](int64_t bytes) { char *r = p; p += (bytes + 255) / 256 * 256; return r; };
@@ -639,6 +694,10 @@ static st_status plan(st_encoder *e) {
     e->thr_dev = (float *)take(e->n_sites * 4);
     e->zeros = (float *)take(1024);
     CUDA_OK(e, cudaMemset(e->zeros, 0, 1024));
+    e->rows_peak = (long long *)take((n + 1) * 8);
+    e->ovf = (int32_t *)take(256);
+    CUDA_OK(e, cudaMemset(e->rows_peak, 0, (n + 1) * 8));
+    CUDA_OK(e, cudaMemset(e->ovf, 0, 4));
     CUDA_OK(e, cudaMallocHost(&e->thr_host, e->n_sites * 4));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->thr_ev, cudaEventDisableTiming));
     const char *ng = getenv("ST_NO_GRAPHS");
@@ -657,6 +716,7 @@ static st_status plan(st_encoder *e) {
     (void)take(0);
     CUDA_OK(e, cudaMalloc(&e->ref, B * Nin * e->in_C * 4));
     // zero rows (row 0 of every rows buffer) are written per step (arena reuse)
+    e->fixed_bytes += small + B * Nin * e->in_C * 4;
     return ST_OK;
 }
 
@@ -897,6 +957,14 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
     CUDA_OK(e, cudaMemsetAsync(e->counts, 0, (size_t)e->B * e->n_sites * 32 * 8, s));
     CUDA_OK(e, cudaMemsetAsync(e->stats, 0, (size_t)(n + 1) * 3 * 8, s));
     CUDA_OK(e, cudaMemsetAsync(e->site_sum, 0, (size_t)e->n_sites * 8, s));
+    CUDA_OK(e, cudaMemsetAsync(e->ovf, 0, 4, s));
+    auto capv = [&](int idx, int64_t cap) {   // row capacity check of one scanned tensor (a9)
+        ScanCap c;
+        c.cap = cap;
+        c.ovf = e->ovf;
+        c.peak = e->rows_peak + idx;
+        return c;
+    };
     const int64_t cstride = (int64_t)e->n_sites * 32;
     auto zero_row = [&](int buf, int C) {
         if (buf >= 0) cudaMemsetAsync(e->ptr(buf), 0, (size_t)C * e->esz, s);
@@ -922,7 +990,8 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                launch_subtract_mask(S0, per, fr, u8, fstride, B, (int)Nin, e->in_C, F, thresholds, bf, act,
                                     e->in_dd >= 0 ? e->ptr(e->in_dd) : nullptr, s));
         LAUNCH(e, KC_SCAN, -1, s,
-               launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s));
+               launch_scan_popc(act, B * Nin, pb, e->totals + n, e->scan_tmp, e->stats + 3 * n + 1, s, nullptr,
+                                capv(n, e->in_rows_cap)));
         zero_row(e->in_rows, e->in_C);
         LAUNCH(e, KC_SUBTRACT, -1, s,
                launch_subtract_rows(S0, per, fr, u8, fstride, B, (int)Nin, e->in_C, act, pb, rows, bf,
@@ -970,6 +1039,11 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             c.bias = l.bias;
             c.rnd_a = bf;   // BF16 mode: the dense A operand is bf16-rounded (R22-BF16)
             c.out = e->p<float>(l.b_y0);
+            if (l.dw_site >= 0) {   // the site's dense output from the same epilogue
+                const LayerRT &r = e->L[l.dw_site];
+                c.act_out = e->p<float>(r.b_y0);
+                c.act_kind = r.kind == ST_RELU ? ACT_RELU : bf ? ACT_SILU_FAST : ACT_SILU;
+            }
             if (!cont)
                 LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
                        l.depthwise  ? launch_dwconv_f32(c, s)
@@ -986,7 +1060,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             // scan of the output frame words; the M-row list is enumerated in the same pass
             LAUNCH(e, KC_SCAN, i, s,
                    launch_scan_popc(act, B * N, pb, e->totals + i, e->scan_tmp, st + 1, s,
-                                    dw_pm ? nullptr : e->p<int32_t>(l.b_ridx)));
+                                    dw_pm ? nullptr : e->p<int32_t>(l.b_ridx), capv(i, l.rows_cap)));
             zero_row(l.b_rows, l.C);
             c.dense = false;
             c.rnd_a = false;   // delta rows are already bf16 values in BF16 mode
@@ -996,8 +1070,23 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             c.F = F;
             c.ddelta = (l.src == -1 && !l.depthwise && !l.tc && e->in_dd >= 0) ? e->ptr(e->in_dd) : nullptr;
             c.m_dev = e->totals + i;
-            c.m_cap = (int64_t)B * F * N;
+            c.m_cap = l.rows_cap;
             c.out = e->ptr(l.b_rows);
+            c.act_out = nullptr;
+            if (l.dw_site >= 0) {   // depthwise conv + its site in one pass (N2)
+                const LayerRT &r = e->L[l.dw_site];
+                DwSite d;
+                d.out_act = act;
+                d.out_pbase = pb;
+                d.x0 = e->p<float>(l.b_y0);
+                d.theta = thresholds + r.site;
+                d.act = r.kind == ST_RELU ? ACT_RELU : ACT_SILU;
+                d.site_act = e->p<uint32_t>(r.b_act);
+                d.site_rows = const_cast<void *>(view_of(e, l.dw_site).rows);
+                d.conv_rows = r.b_rows >= 0 ? e->ptr(l.b_rows) : nullptr;   // own site rows: keep the conv's too
+                LAUNCH(e, KC_DW_SITE, i, s, launch_dwconv_site(c, d, s));
+                break;
+            }
             LAUNCH(e, l.depthwise ? KC_DW_SPARSE : l.tc ? KC_TC_SPARSE : l.tc_small ? KC_STEM_SPARSE : KC_CONV_SPARSE, i, s,
                    dw_pm        ? launch_dwconv_pm(c, act, pb, s)
                    : l.depthwise ? launch_dwconv_f32(c, s)
@@ -1012,7 +1101,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             const int dense_kind = (act_kind == ACT_SILU && bf) ? ACT_SILU_FAST : act_kind;
             // a fused ReLU's dense output is read only by the pool's dense pass,
             // which applies the ReLU itself (kept when streaming or debugging)
-            const bool skip_dense = l.fused_pool >= 0 && !strm && !e->cfg.debug_retain;
+            const bool skip_dense = (l.fused_pool >= 0 && !strm && !e->cfg.debug_retain) || l.fused_dw >= 0;
             if (!cont && !skip_dense)
                 LAUNCH(e, KC_DENSE_MISC, i, s,
                        launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
@@ -1032,7 +1121,8 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             DView me = view_of(e, i);
             if (l.b_rows >= 0) zero_row(l.b_rows, l.C);   // own buffer (not in place)
             if (l.fused_pool >= 0) break;                 // runs inside the pool's pass
-            LAUNCH(e, KC_SITE_PW, i, s,
+            if (l.fused_dw < 0)                           // else: ran inside the conv's pass
+                LAUNCH(e, KC_SITE_PW, i, s,
                    launch_site_pointwise(in, x_init, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
                                          e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), sst, s));
             LAUNCH(e, KC_COUNTS, i, s,
@@ -1081,7 +1171,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 const LayerRT &r = e->L[l.fused_relu];
                 const DView cv = view_of(e, r.src);
                 LAUNCH(e, KC_DILATE, i, s, launch_dilate(cv.act, B, l.geo, slot, s));
-                LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+                LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s, nullptr, capv(i, l.rows_cap)));
                 zero_row(l.b_rows, l.C);
                 LAUNCH(e, KC_SITE_MP, i, s,
                        launch_site_relu_maxpool(cv, strm ? x_init : dense_of(e, r.src), B, l.geo, thresholds + r.site,
@@ -1099,7 +1189,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 break;
             }
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, slot, s));
-            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s, nullptr, capv(i, l.rows_cap)));
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SITE_MP, i, s,
                    launch_site_maxpool(in, x_init, B, l.geo, thresholds + l.site, bf, slot, pb,
@@ -1119,7 +1209,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_ADD, i, s, launch_or_words(in.act, in2.act, B * N, slot, s));
-            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s, nullptr, capv(i, l.rows_cap)));
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_ADD, i, s, launch_add_rows(in, in2, slot, pb, B, (int)N, l.C, bf, e->ptr(l.b_rows), s));
             CUDA_OK(e, cudaMemcpyAsync(e->p<uint32_t>(l.b_act), slot, (size_t)B * N * 4, cudaMemcpyDeviceToDevice, s));
@@ -1147,7 +1237,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_SE_SUMS, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
-            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s));
+            LAUNCH(e, KC_SCAN, i, s, launch_scan_popc(slot, B * N, pb, e->totals + i, e->scan_tmp, nullptr, s, nullptr, capv(i, l.rows_cap)));
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SE, i, s,
                    launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds + l.site, bf, slot, pb,
@@ -1183,6 +1273,9 @@ extern "C" st_status st_get_sparsity(st_encoder *e, int64_t *active, int64_t *si
     if (e->last_ndiff < 0) return fail(e, ST_ERR_STATE, "no encode_diff yet");
     CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
     const int B = e->last_chunks, F = e->last_ndiff, S = e->n_sites;
+    int32_t ov = 0;
+    CUDA_OK(e, cudaMemcpy(&ov, e->ovf, 4, cudaMemcpyDeviceToHost));
+    if (ov) return fail(e, ST_ERR_CAPACITY, "the last step exceeded a row capacity; its statistics are invalid");
     if (active) {
         std::vector<long long> h((size_t)e->B * S * 32);
         CUDA_OK(e, cudaMemcpy(h.data(), e->counts, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -1385,6 +1478,56 @@ extern "C" st_status st_debug_get_words(st_encoder *e, int32_t layer, uint32_t *
     return ST_OK;
 }
 
+extern "C" st_status st_device_bytes(const st_encoder *e, int64_t *total) {
+    if (!e || !total) return ST_ERR_ARG;
+    *total = e->arena_bytes + e->fixed_bytes;
+    return ST_OK;
+}
+
+extern "C" st_status st_step_status(st_encoder *e) {
+    if (!e) return ST_ERR_ARG;
+    if (e->last_ndiff < 0) return ST_OK;
+    CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    int32_t ov = 0;
+    CUDA_OK(e, cudaMemcpy(&ov, e->ovf, 4, cudaMemcpyDeviceToHost));
+    return ov ? fail(e, ST_ERR_CAPACITY, "the last step exceeded a row capacity") : ST_OK;
+}
+
+extern "C" st_status st_get_capacity(st_encoder *e, int64_t *rows_cap, int64_t *rows_peak) {
+    if (!e) return ST_ERR_ARG;
+    const int n = (int)e->L.size();
+    if (e->last_stream) CUDA_OK(e, cudaStreamSynchronize(e->last_stream));
+    std::vector<long long> pk(n + 1);
+    CUDA_OK(e, cudaMemcpy(pk.data(), e->rows_peak, (n + 1) * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i <= n; i++) {
+        const bool own = i == n || e->L[i].b_rows >= 0 || e->L[i].kind == ST_CONV || e->L[i].kind == ST_MAXPOOL ||
+                         e->L[i].kind == ST_ADD || e->L[i].kind == ST_SE;
+        if (rows_cap) rows_cap[i] = !own ? -1 : i == n ? e->in_rows_cap : e->L[i].rows_cap;
+        if (rows_peak) rows_peak[i] = own ? pk[i] : -1;
+    }
+    return ST_OK;
+}
+
+extern "C" st_status st_encoder_fit_capacity(st_encoder *e, double headroom) {
+    if (!e) return ST_ERR_ARG;
+    if (!(headroom >= 1.0)) return fail(e, ST_ERR_ARG, "headroom %g < 1", headroom);
+    if (e->cfg.streaming) return fail(e, ST_ERR_UNSUPPORTED, "streaming caches live in the arena");
+    CUDA_OK(e, cudaSetDevice(e->cfg.device));
+    CUDA_OK(e, cudaDeviceSynchronize());
+    const int n = (int)e->L.size();
+    std::vector<long long> pk(n + 1);
+    CUDA_OK(e, cudaMemcpy(pk.data(), e->rows_peak, (n + 1) * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i <= n; i++) e->cap_fit[i] = std::max<int64_t>((int64_t)std::ceil(headroom * (double)pk[i]), 4096);
+    for (auto &g : e->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    e->graphs.clear();
+    cudaFree(e->arena);
+    e->arena = nullptr;
+    e->arena_bytes = 0;
+    e->last_ndiff = -1;   // the last step's results are gone
+    return plan(e);
+}
+
 extern "C" st_status st_memory_report(const st_encoder *e, int64_t *persistent, int64_t *peak, int64_t *arena) {
     if (!e) return ST_ERR_ARG;
     if (persistent) *persistent = e->persistent_bytes;
@@ -1438,6 +1581,24 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 if (e->prof_trace)
                     fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f M=%lld Min=%lld K=%lld C=%d GBps=%.1f\n",
                             (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, (long long)M, (long long)Min, (long long)K, l.C, t > 0 ? b / t * 1e-6 : 0.0);
+            } else if (r.layer >= 0 && r.cls == KC_DW_SITE && e->last_ndiff > 0) {
+                // depthwise conv + its site: active input rows once, x0 of the touched
+                // output pixels once, the site's emitted rows once, frame words; the
+                // conv's own delta rows never leave the chip
+                const LayerRT &l = e->L[r.layer];
+                const int si = l.dw_site;
+                const double eb = e->cfg.precision == ST_BF16 ? 2.0 : 4.0;
+                const double C = l.C, Bc = e->last_chunks;
+                const int64_t K = (int64_t)l.geo.kh * l.geo.kw;
+                e->prof_flops[r.cls] += 2.0 * K * l.C * (double)rout[r.layer];
+                const double b = eb * ((double)rin[r.layer] + (double)rout[si]) * C + 4.0 * tch[si] * C +
+                                 12.0 * tch[si] + 4.0 * Bc * ((double)l.geo.Hin * l.geo.Win + 2.0 * l.H * l.W) +
+                                 4.0 * K * C;
+                e->prof_bytes[r.cls] += b;
+                if (e->prof_trace)
+                    fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f M=%lld Min=%lld GBps=%.1f\n",
+                            (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t, (long long)rout[r.layer],
+                            (long long)rin[r.layer], t > 0 ? b / t * 1e-6 : 0.0);
             } else if (r.layer >= 0 && e->last_ndiff > 0 &&
                        (r.cls == KC_SITE_PW || r.cls == KC_SITE_MP || r.cls == KC_ACCUM || r.cls == KC_SE)) {
                 // algorithmic bytes of the HBM-bound per-pixel kernels:
@@ -1471,6 +1632,9 @@ extern "C" st_status st_get_kernel_times(st_encoder *e, double *ms, int64_t *lau
                 const double BNC = (double)e->last_chunks * l.H * l.W * l.C;
                 const double tot = 3.0 * 4.0 * BNC + (e->last_ndiff > 0 ? eb * (double)rin[r.layer] * l.C : 0.0);
                 e->prof_bytes[r.cls] += tot / (e->last_ndiff > 0 ? 5.0 : 4.0);
+                if (e->prof_trace)
+                    fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f\n", (int)(e->cfg.precision == ST_BF16),
+                            r.cls, r.layer, t);
             } else if (e->prof_trace) {
                 fprintf(stderr, "[st-prof] bf=%d cls=%d layer=%d ms=%.4f\n", (int)(e->cfg.precision == ST_BF16), r.cls, r.layer, t);
             }
@@ -1501,6 +1665,7 @@ extern "C" const char *st_status_string(st_status s) {
     case ST_ERR_OOM: return "out of device memory";
     case ST_ERR_CUDA: return "CUDA error";
     case ST_ERR_INTERNAL: return "internal error";
+    case ST_ERR_CAPACITY: return "row capacity exceeded (re-plan with st_encoder_fit_capacity and re-issue)";
     }
     return "unknown status";
 }

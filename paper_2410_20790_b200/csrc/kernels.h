@@ -53,8 +53,16 @@ void launch_dilate(const uint32_t *in, int B, const Geo &g, uint32_t *out, cudaS
 // (scan_tmp_ints(n) int32).
 int64_t scan_tmp_ints(int64_t n);
 // ridx (optional): also enumerate the conv M-row list (replaces launch_enumerate)
-void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp,
-                      long long *stat, cudaStream_t s, int32_t *ridx = nullptr);
+// cap (optional): row capacity of the tensor -- words whose rows would end
+// past cap are cleared, *total becomes the rows that fit and *ovf is set;
+// peak (optional): running max of the unclamped totals (int64 atomicMax)
+struct ScanCap {
+    int64_t cap = 0;
+    int32_t *ovf = nullptr;   // null: no capacity check
+    long long *peak = nullptr;
+};
+void launch_scan_popc(uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp, long long *stat,
+                      cudaStream_t s, int32_t *ridx = nullptr, const ScanCap &cap = ScanCap());
 // ridx[pbase+j] = ((b*N+q) << 5) | t1 for every set bit of slot (conv M rows)
 void launch_enumerate(const uint32_t *slot, const int32_t *pbase, int64_t n, int32_t *ridx, cudaStream_t s);
 // per (b, t1) popcounts of act into counts[b*cstride + t1] (int64 atomics,
@@ -86,11 +94,32 @@ struct ConvCall {
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only
     void *out;              // dense: float [B*Nout][Cout]; sparse: rows_out (row 1+r)
+    // dense depthwise only, optional: the consuming pointwise site's dense
+    // output f(out) (act_kind: Act) written by the same epilogue
+    float *act_out = nullptr;
+    int act_kind = 0;
 };
 void launch_conv_f32(const ConvCall &c, cudaStream_t s);
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s);
 // sparse depthwise, pixel-major over the output frame words (no M-row list)
 void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t *out_pbase, cudaStream_t s);
+// Sparse depthwise conv + the pointwise site (ReLU / SiLU) that is its only
+// consumer, in one pass (conv-epilogue non-linear correction, SURVEY §8(f)
+// N2): the group that computes an output pixel's delta rows (frames in
+// order) steps the site's x_acc / y_acc on them at once, so the conv's delta
+// rows never reach HBM.  Requires C % 8 == 0.
+struct DwSite {
+    const uint32_t *out_act = nullptr;   // conv output frame words (the site's touched set and row layout)
+    const int32_t *out_pbase = nullptr;  // their row bases
+    const float *x0 = nullptr;           // conv dense output of the reference frame = the site's x_acc start
+    const float *theta = nullptr;        // the site's threshold (device)
+    int act = 0;                         // Act
+    uint32_t *site_act = nullptr;        // site emitted frame words [B][N]
+    void *site_rows = nullptr;           // site emitted rows, in the conv's row layout
+    void *conv_rows = nullptr;           // optional (debug_retain): the conv's own delta rows
+};
+bool dwconv_site_fusable(const Geo &g);
+void launch_dwconv_site(const ConvCall &c, const DwSite &d, cudaStream_t s);
 // BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu).  Weights bf16
 // [Cout][K] are read through a TMA descriptor (CUtensorMap, 128 bytes)
 // built once at create by make_weight_tmap.

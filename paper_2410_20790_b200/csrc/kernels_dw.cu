@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
 #pragma unroll
                 for (int i = 0; i < CPL; i++) acc[i] = __fadd_rn(acc[i], bb[i]);
                 row_store<float, CPL>(static_cast<float *>(c.out) + r * C, c0, C, full, acc);
+                if (c.act_out) {   // the consuming site's dense output f(x0)
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) acc[i] = act_rt(c.act_kind, acc[i]);
+                    row_store<float, CPL>(c.act_out + r * C, c0, C, full, acc);
+                }
             } else {
                 row_store<T, CPL>(static_cast<T *>(c.out) + (r + 1) * C, c0, C, full, acc);
             }
@@ -111,23 +116,172 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
 // group's lanes in parallel (lane j: taps j, j+G, ...) into shared memory,
 // then read back as one 16-byte broadcast per tap, so 5x5 kernels keep the
 // register budget of two CTAs per SM.
+
+// tap metadata of output pixel (b, oy, ox) into meta[tap] = {act, slot, 1 +
+// pbase, -}, then the live taps (active in some frame of the step) in
+// ascending order into meta[k].w; returns their number
+template <int G, int KMAX>
+__device__ __forceinline__ int dw_gather_meta(const ConvCall &c, int b, int oy, int ox, int lane, uint32_t gmask,
+                                              int4 *meta) {
+    const Geo &g = c.g;
+    const int Nin = g.Hin * g.Win, ntaps = g.kh * g.kw;
+    __syncwarp(gmask);   // previous pixel's metadata fully consumed
+    for (int tap = lane; tap < KMAX; tap += G) {
+        int4 m = make_int4(0, 0, 0, 0);
+        if (tap < ntaps) {
+            const int dy = tap / g.kw, dx = tap - dy * g.kw;
+            const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+            if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
+                m.x = (int)__ldg(c.a.act + bp);
+                m.y = (int)__ldg(c.a.slot + bp);
+                m.z = 1 + __ldg(c.a.pbase + bp);
+            }
+        }
+        meta[tap] = m;
+    }
+    __syncwarp(gmask);
+    int nlive = 0;
+    for (int r = 0; r < KMAX; r += G) {
+        const int tap = r + lane;
+        const bool live = tap < KMAX && meta[tap].x != 0;
+        const uint32_t bal = __ballot_sync(gmask, live) >> ((threadIdx.x & 31) & ~(G - 1));
+        if (live) meta[nlive + __popc(bal & ((1u << lane) - 1u))].w = tap;
+        nlive += __popc(bal);
+    }
+    __syncwarp(gmask);
+    return nlive;
+}
+
+// 8 bf16 channels [c0, c0+8) of a row as one raw 16-byte vector (zeros past C)
+__device__ __forceinline__ uint4 dw_load_raw(const bf16 *A, int64_t row, int C, int c0, bool full) {
+    if (full) return *reinterpret_cast<const uint4 *>(A + row * C + c0);
+    const uint16_t *r16 = reinterpret_cast<const uint16_t *>(A + row * C);
+    uint32_t h[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) h[i] = c0 + i < C ? r16[c0 + i] : 0u;
+    return make_uint4(h[0] | h[1] << 16, h[2] | h[3] << 16, h[4] | h[5] << 16, h[6] | h[7] << 16);
+}
+
+// bf16 rows, 8 channels at c0: the depthwise deltas of frames tA and tB (tB <
+// 0: none) in one pass over the live taps -- each batch loads the rows of TB
+// taps for both frames, kept as raw 16-byte vectors until their FMA (the
+// register cost of one frame's float rows), so one round trip serves up to
+// 2*TB rows; every frame's chain stays in ascending tap order
+template <int TB>
+__device__ __forceinline__ void dw_acc_pair(const bf16 *A, const float *wk, int C, int c0, bool full,
+                                            const int4 *meta, int nlive, int tA, int tB, float (&accA)[8],
+                                            float (&accB)[8]) {
+    const uint32_t lmA = lowmask(tA), lmB = tB >= 0 ? lowmask(tB) : 0u;
+    const uint32_t fm = (1u << tA) | (tB >= 0 ? 1u << tB : 0u);
+#pragma unroll
+    for (int i = 0; i < 8; i++) accA[i] = accB[i] = 0.0f;
+    int k = 0;
+    while (k < nlive) {
+        int tp[TB];
+        uint4 vA[TB], vB[TB];
+        uint32_t on = 0;   // bit 2j: tap j active in frame A, bit 2j+1: in frame B
+#pragma unroll
+        for (int j = 0; j < TB; j++) {
+            tp[j] = -1;
+            while (k < nlive) {
+                const int tap = meta[k].w;
+                k++;
+                const int4 m = meta[tap];
+                const uint32_t hit = (uint32_t)m.x & fm;
+                if (hit) {
+                    tp[j] = tap;
+                    if ((hit >> tA) & 1u) {
+                        vA[j] = dw_load_raw(A, m.z + __popc((uint32_t)m.y & lmA), C, c0, full);
+                        on |= 1u << (2 * j);
+                    }
+                    if (tB >= 0 && ((hit >> tB) & 1u)) {
+                        vB[j] = dw_load_raw(A, m.z + __popc((uint32_t)m.y & lmB), C, c0, full);
+                        on |= 2u << (2 * j);
+                    }
+                    break;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < TB; j++) {
+            if (tp[j] < 0) continue;
+            float wv[8];
+            row_load<float, 8>(wk + (int64_t)tp[j] * C, c0, C, full, wv);
+            if ((on >> (2 * j)) & 1u) {
+                const uint32_t u[4] = {vA[j].x, vA[j].y, vA[j].z, vA[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    accA[2 * q] = fmaf(wv[2 * q], __uint_as_float(u[q] << 16), accA[2 * q]);
+                    accA[2 * q + 1] = fmaf(wv[2 * q + 1], __uint_as_float(u[q] & 0xFFFF0000u), accA[2 * q + 1]);
+                }
+            }
+            if ((on >> (2 * j + 1)) & 1u) {
+                const uint32_t u[4] = {vB[j].x, vB[j].y, vB[j].z, vB[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    accB[2 * q] = fmaf(wv[2 * q], __uint_as_float(u[q] << 16), accB[2 * q]);
+                    accB[2 * q + 1] = fmaf(wv[2 * q + 1], __uint_as_float(u[q] & 0xFFFF0000u), accB[2 * q + 1]);
+                }
+            }
+        }
+    }
+}
+
+// one frame t1, CPL channels at c0: batches of TB taps ACTIVE in t1 (found by
+// walking the live list), loaded together; fmaf chain in ascending tap order
+template <int TB, int CPL, class T>
+__device__ __forceinline__ void dw_acc_one(const T *A, const float *wk, int C, int c0, bool full, const int4 *meta,
+                                           int nlive, int t1, float (&acc)[CPL]) {
+    const uint32_t lm = lowmask(t1);
+#pragma unroll
+    for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
+    int k = 0;
+    while (k < nlive) {
+        int tp[TB];
+        float v[TB][CPL];
+#pragma unroll
+        for (int j = 0; j < TB; j++) {
+            tp[j] = -1;
+            while (k < nlive) {
+                const int tap = meta[k].w;
+                k++;
+                const int4 m = meta[tap];
+                if (((uint32_t)m.x >> t1) & 1u) {
+                    tp[j] = tap;
+                    const int64_t row = m.z + __popc((uint32_t)m.y & lm);
+                    row_load<T, CPL>(A + row * C, c0, C, full, v[j]);
+                    break;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < TB; j++) {
+            if (tp[j] < 0) continue;
+            float wv[CPL];
+            row_load<float, CPL>(wk + (int64_t)tp[j] * C, c0, C, full, wv);
+#pragma unroll
+            for (int i = 0; i < CPL; i++) acc[i] = fmaf(wv[i], v[j][i], acc[i]);
+        }
+    }
+}
+
 template <int G, int CPL, int KMAX, class T>
 __global__ void __launch_bounds__(256, 3) k_dwconv_pm(ConvCall c, const uint32_t *__restrict__ out_act,
                                                       const int32_t *__restrict__ out_pbase) {
     st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 4 : 3;   // active taps loaded per batch
-    constexpr bool PAIR = sizeof(T) == 2 && CPL == 8;   // two frames per pass (see below)
-    extern __shared__ int4 dw_meta[];   // [256/G groups][KMAX] {act, slot, 1 + pbase, 0}
+    constexpr bool PAIR = sizeof(T) == 2 && CPL == 8;   // two frames per pass (dw_acc_pair)
+    extern __shared__ int4 dw_meta[];   // [256/G groups][KMAX] {act, slot, 1 + pbase, live tap}
     const Geo g = c.g;
-    const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
+    const int Nout = g.Wout * g.Hout;
     const int C = g.Cin;
     const int lane = threadIdx.x & (G - 1);
-    const uint32_t gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    const uint32_t gmask = group_mask<G>();
     int4 *meta = dw_meta + (threadIdx.x / G) * KMAX;
     const int64_t BNo = (int64_t)c.B * Nout;
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
-    const int ntaps = g.kh * g.kw;
     const T *A = static_cast<const T *>(c.a.rows);
     T *O = static_cast<T *>(c.out);
     for (int64_t bq = grp; bq < BNo; bq += ngrp) {
@@ -135,109 +289,19 @@ __global__ void __launch_bounds__(256, 3) k_dwconv_pm(ConvCall c, const uint32_t
         if (!w) continue;
         const int b = (int)(bq / Nout), q = (int)(bq - (int64_t)b * Nout);
         const int oy = q / g.Wout, ox = q - oy * g.Wout;
-        __syncwarp(gmask);   // previous pixel's metadata fully consumed
-        for (int tap = lane; tap < KMAX; tap += G) {
-            int4 m = make_int4(0, 0, 0, 0);
-            if (tap < ntaps) {
-                const int dy = tap / g.kw, dx = tap - dy * g.kw;
-                const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
-                if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
-                    const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
-                    m.x = (int)__ldg(c.a.act + bp);
-                    m.y = (int)__ldg(c.a.slot + bp);
-                    m.z = 1 + __ldg(c.a.pbase + bp);
-                }
-            }
-            meta[tap] = m;
-        }
-        __syncwarp(gmask);
-        // live taps (active in some frame of this step), ascending, into meta[k].w
-        int nlive = 0;
-        for (int r = 0; r < KMAX; r += G) {
-            const int tap = r + lane;
-            const bool live = tap < KMAX && meta[tap].x != 0;
-            const uint32_t bal = __ballot_sync(gmask, live) >> ((threadIdx.x & 31) & ~(G - 1));
-            if (live) meta[nlive + __popc(bal & ((1u << lane) - 1u))].w = tap;
-            nlive += __popc(bal);
-        }
-        __syncwarp(gmask);
+        const int nlive = dw_gather_meta<G, KMAX>(c, b, oy, ox, lane, gmask, meta);
         int64_t orow = 1 + __ldg(out_pbase + bq);
         if constexpr (PAIR) {
-            // bf16, 8 channels per lane: two frames per pass over the live taps,
-            // rows kept as raw 16-byte vectors until their FMA (the register cost
-            // of one frame's float rows), so each round trip serves up to TB
-            // taps x 2 frames; every frame's chain stays in ascending tap order
             while (w) {
                 const int tA = __ffs(w) - 1;
                 w &= w - 1;
                 const int tB = w ? __ffs(w) - 1 : -1;
                 if (w) w &= w - 1;
-                const uint32_t lmA = lowmask(tA), lmB = tB >= 0 ? lowmask(tB) : 0u;
-                const uint32_t fm = (1u << tA) | (tB >= 0 ? 1u << tB : 0u);
                 for (int cb = 0; cb < C; cb += G * CPL) {
                     const int c0 = cb + lane * CPL;
                     const bool full = c0 + CPL <= C;
-                    auto load_raw = [&](int64_t row) -> uint4 {
-                        if (full) return *reinterpret_cast<const uint4 *>(A + row * C + c0);
-                        const uint16_t *r16 = reinterpret_cast<const uint16_t *>(A + row * C);
-                        uint32_t h[8];
-#pragma unroll
-                        for (int i = 0; i < 8; i++) h[i] = c0 + i < C ? r16[c0 + i] : 0u;
-                        return make_uint4(h[0] | h[1] << 16, h[2] | h[3] << 16, h[4] | h[5] << 16, h[6] | h[7] << 16);
-                    };
                     float accA[8], accB[8];
-#pragma unroll
-                    for (int i = 0; i < 8; i++) accA[i] = accB[i] = 0.0f;
-                    int k = 0;
-                    while (k < nlive) {
-                        int tp[TB];
-                        uint4 vA[TB], vB[TB];
-                        uint32_t on = 0;   // bit 2j: tap j active in frame A, bit 2j+1: in frame B
-#pragma unroll
-                        for (int j = 0; j < TB; j++) {
-                            tp[j] = -1;
-                            while (k < nlive) {
-                                const int tap = meta[k].w;
-                                k++;
-                                const int4 m = meta[tap];
-                                const uint32_t hit = (uint32_t)m.x & fm;
-                                if (hit) {
-                                    tp[j] = tap;
-                                    if ((hit >> tA) & 1u) {
-                                        vA[j] = load_raw(m.z + __popc((uint32_t)m.y & lmA));
-                                        on |= 1u << (2 * j);
-                                    }
-                                    if (tB >= 0 && ((hit >> tB) & 1u)) {
-                                        vB[j] = load_raw(m.z + __popc((uint32_t)m.y & lmB));
-                                        on |= 2u << (2 * j);
-                                    }
-                                    break;
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int j = 0; j < TB; j++) {
-                            if (tp[j] < 0) continue;
-                            float wv[8];
-                            row_load<float, 8>(c.wk + (int64_t)tp[j] * C, c0, C, full, wv);
-                            if ((on >> (2 * j)) & 1u) {
-                                const uint32_t u[4] = {vA[j].x, vA[j].y, vA[j].z, vA[j].w};
-#pragma unroll
-                                for (int q = 0; q < 4; q++) {
-                                    accA[2 * q] = fmaf(wv[2 * q], __uint_as_float(u[q] << 16), accA[2 * q]);
-                                    accA[2 * q + 1] = fmaf(wv[2 * q + 1], __uint_as_float(u[q] & 0xFFFF0000u), accA[2 * q + 1]);
-                                }
-                            }
-                            if ((on >> (2 * j + 1)) & 1u) {
-                                const uint32_t u[4] = {vB[j].x, vB[j].y, vB[j].z, vB[j].w};
-#pragma unroll
-                                for (int q = 0; q < 4; q++) {
-                                    accB[2 * q] = fmaf(wv[2 * q], __uint_as_float(u[q] << 16), accB[2 * q]);
-                                    accB[2 * q + 1] = fmaf(wv[2 * q + 1], __uint_as_float(u[q] & 0xFFFF0000u), accB[2 * q + 1]);
-                                }
-                            }
-                        }
-                    }
+                    dw_acc_pair<TB>(A, c.wk, C, c0, full, meta, nlive, tA, tB, accA, accB);
                     if (c0 < C) {
                         row_store<T, 8>(O + orow * C, c0, C, full, accA);
                         if (tB >= 0) row_store<T, 8>(O + (orow + 1) * C, c0, C, full, accB);
@@ -245,52 +309,237 @@ __global__ void __launch_bounds__(256, 3) k_dwconv_pm(ConvCall c, const uint32_t
                 }
                 orow += tB >= 0 ? 2 : 1;
             }
+        } else {
+            while (w) {
+                const int t1 = __ffs(w) - 1;
+                w &= w - 1;
+                for (int cb = 0; cb < C; cb += G * CPL) {
+                    const int c0 = cb + lane * CPL;
+                    const bool full = (C % 8 == 0) && (c0 + CPL <= C);
+                    float acc[CPL];
+                    dw_acc_one<TB, CPL, T>(A, c.wk, C, c0, full, meta, nlive, t1, acc);
+                    if (c0 < C) row_store<T, CPL>(O + orow * C, c0, C, full, acc);
+                }
+                orow++;
+            }
+        }
+    }
+}
+
+// ---- sparse depthwise + pointwise site in one pass (SURVEY §8(f) N2 for
+// depthwise convs; Eq.2 then Eq.3).  The group that owns an
+// output pixel computes its delta rows frame by frame in ascending order (as
+// k_dwconv_pm), rounds each to the stored row type (the value the separate
+// conv kernel would write, R22-BF16) and steps the site right away:
+//     x_acc += Delta; c = f(x_acc) - y_acc; emit iff max_c |c| > theta;
+//     y_acc += rnd(c)   (the operations of k_site_pw, in its order)
+// x_acc starts from the conv's dense reference output x0, y_acc = f(x0).
+// The site's emitted rows go to the conv's row layout (the in-place layout of
+// the separate site kernel), so the conv's delta rows never reach HBM
+// (written only when d.conv_rows is set: debug_retain).  Narrow form: C <=
+// G*8, one 8-channel chunk per lane, state in registers.
+template <int G, int KMAX, class T, int ACT>
+__global__ void __launch_bounds__(256, 2) k_dwconv_site(ConvCall c, DwSite d) {
+    st_pdl_enter();
+    constexpr int TB = KMAX > 9 ? 4 : 3;
+    constexpr bool PAIR = sizeof(T) == 2;
+    extern __shared__ int4 dw_meta[];
+    const float theta = __ldg(d.theta);
+    const Geo g = c.g;
+    const int Nout = g.Wout * g.Hout;
+    const int C = g.Cin;
+    const int lane = threadIdx.x & (G - 1);
+    const uint32_t gmask = group_mask<G>();
+    int4 *meta = dw_meta + (threadIdx.x / G) * KMAX;
+    const int64_t BNo = (int64_t)c.B * Nout;
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    const T *A = static_cast<const T *>(c.a.rows);
+    T *SR = static_cast<T *>(d.site_rows);
+    T *CR = static_cast<T *>(d.conv_rows);
+    const int c0 = lane * 8;
+    const bool full = c0 + 8 <= C;   // C % 8 == 0: a lane's chunk is whole or past C
+    for (int64_t bq = grp; bq < BNo; bq += ngrp) {
+        uint32_t w = __ldg(d.out_act + bq);
+        if (!w) {
+            if (lane == 0) d.site_act[bq] = 0u;
             continue;
         }
-        while (w) {
-            const int t1 = __ffs(w) - 1;
-            w &= w - 1;
-            const uint32_t lm = lowmask(t1);
-            for (int cb = 0; cb < C; cb += G * CPL) {
-                const int c0 = cb + lane * CPL;
-                const bool full = (C % 8 == 0) && (c0 + CPL <= C);
-                float acc[CPL];
+        const int b = (int)(bq / Nout), q = (int)(bq - (int64_t)b * Nout);
+        const int oy = q / g.Wout, ox = q - oy * g.Wout;
+        const int nlive = dw_gather_meta<G, KMAX>(c, b, oy, ox, lane, gmask, meta);
+        float xa[8], ya[8];
+        row_load<float, 8>(d.x0 + bq * C, c0, C, full, xa);
 #pragma unroll
-                for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
-                // batches of TB taps ACTIVE in frame t1 (found by walking the live
-                // list), loaded together; fmaf chain in ascending tap order
-                int k = 0;
-                while (k < nlive) {
-                    int tp[TB];
-                    float v[TB][CPL];
+        for (int i = 0; i < 8; i++) ya[i] = actf<ACT>(xa[i]);
+        uint32_t emit = 0;
+        int64_t orow = 1 + __ldg(d.out_pbase + bq);
+        auto step = [&](const float (&acc)[8], int64_t row, int t1) {
+            float cand[8];
+            float mx = 0.0f;
 #pragma unroll
-                    for (int j = 0; j < TB; j++) {
-                        tp[j] = -1;
-                        while (k < nlive) {
-                            const int tap = meta[k].w;
-                            k++;
-                            const int4 m = meta[tap];
-                            if (((uint32_t)m.x >> t1) & 1u) {
-                                tp[j] = tap;
-                                const int64_t row = m.z + __popc((uint32_t)m.y & lm);
-                                row_load<T, CPL>(A + row * C, c0, C, full, v[j]);
-                                break;
-                            }
-                        }
-                    }
+            for (int i = 0; i < 8; i++) {
+                const float v = rnd<T>(acc[i]);                        // the conv's stored delta
+                xa[i] = __fadd_rn(xa[i], v);                           // reconstruct x (Eq.3)
+                cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);          // restore the delta
+                mx = fmaxf(mx, fabsf(cand[i]));
+            }
+            if (CR && c0 < C) row_store<T, 8>(CR + row * C, c0, C, full, acc);
+            mx = gmax<G>(mx, gmask);
+            if (mx > theta) {                                          // truncation
 #pragma unroll
-                    for (int j = 0; j < TB; j++) {
-                        if (tp[j] < 0) continue;
-                        float wv[CPL];
-                        row_load<float, CPL>(c.wk + (int64_t)tp[j] * C, c0, C, full, wv);
-#pragma unroll
-                        for (int i = 0; i < CPL; i++) acc[i] = fmaf(wv[i], v[j][i], acc[i]);
-                    }
+                for (int i = 0; i < 8; i++) {
+                    cand[i] = rnd<T>(cand[i]);
+                    ya[i] = __fadd_rn(ya[i], cand[i]);
                 }
-                if (c0 < C) row_store<T, CPL>(O + orow * C, c0, C, full, acc);
+                if (c0 < C) row_store<T, 8>(SR + row * C, c0, C, full, cand);
+                emit |= 1u << t1;
+            }
+        };
+        if constexpr (PAIR) {
+            while (w) {
+                const int tA = __ffs(w) - 1;
+                w &= w - 1;
+                const int tB = w ? __ffs(w) - 1 : -1;
+                if (w) w &= w - 1;
+                float accA[8], accB[8];
+                dw_acc_pair<TB>(reinterpret_cast<const bf16 *>(A), c.wk, C, c0, full, meta, nlive, tA, tB, accA, accB);
+                step(accA, orow, tA);
+                if (tB >= 0) step(accB, orow + 1, tB);
+                orow += tB >= 0 ? 2 : 1;
+            }
+        } else {
+            while (w) {
+                const int t1 = __ffs(w) - 1;
+                w &= w - 1;
+                float acc[8];
+                dw_acc_one<TB, 8, T>(A, c.wk, C, c0, full, meta, nlive, t1, acc);
+                step(acc, orow, t1);
+                orow++;
+            }
+        }
+        if (lane == 0) d.site_act[bq] = emit;
+    }
+}
+
+// Wide form (C > 256): one warp per output pixel, the pixel's x_acc / y_acc
+// (and, for the second frame of a bf16 pair, its stored delta) in shared
+// memory, walked in 256-channel chunks.  Per frame: pass 1 adds the delta to
+// x_acc and takes the running max of |f(x_acc) - y_acc|; on emission pass 2
+// recomputes the candidate from the stored state (the same operations, so
+// the same bits), rounds it, advances y_acc and writes the row.
+constexpr int DWS_WARPS = 8;
+template <int KMAX, class T, int ACT>
+__global__ void __launch_bounds__(32 * DWS_WARPS, 1) k_dwconv_site_wide(ConvCall c, DwSite d) {
+    st_pdl_enter();
+    constexpr int TB = KMAX > 9 ? 4 : 3;
+    constexpr bool PAIR = sizeof(T) == 2;
+    extern __shared__ int4 dw_meta[];   // [warps][KMAX] metadata, then [warps][3][C] fp32 state
+    const float theta = __ldg(d.theta);
+    const Geo g = c.g;
+    const int Nout = g.Wout * g.Hout;
+    const int C = g.Cin;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int4 *meta = dw_meta + wid * KMAX;
+    float *xs = reinterpret_cast<float *>(dw_meta + DWS_WARPS * KMAX) + (size_t)wid * 3 * C;
+    float *ys = xs + C, *bs = ys + C;
+    const int64_t BNo = (int64_t)c.B * Nout;
+    const T *A = static_cast<const T *>(c.a.rows);
+    T *SR = static_cast<T *>(d.site_rows);
+    T *CR = static_cast<T *>(d.conv_rows);
+    // pass 2 of one frame: the emitted row from the stored state
+    auto emit_row = [&](int64_t row) {
+        for (int c0 = lane * 8; c0 < C; c0 += 256) {
+            float x[8], y[8], cand[8];
+            RowIO<float, 8>::load(xs + c0, x);
+            RowIO<float, 8>::load(ys + c0, y);
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                cand[i] = rnd<T>(__fsub_rn(actf<ACT>(x[i]), y[i]));
+                y[i] = __fadd_rn(y[i], cand[i]);
+            }
+            RowIO<float, 8>::store(ys + c0, y);
+            RowIO<T, 8>::store(SR + row * C + c0, cand);
+        }
+    };
+    for (int64_t bq = (int64_t)blockIdx.x * DWS_WARPS + wid; bq < BNo; bq += (int64_t)gridDim.x * DWS_WARPS) {
+        uint32_t w = __ldg(d.out_act + bq);
+        if (!w) {
+            if (lane == 0) d.site_act[bq] = 0u;
+            continue;
+        }
+        const int b = (int)(bq / Nout), q = (int)(bq - (int64_t)b * Nout);
+        const int oy = q / g.Wout, ox = q - oy * g.Wout;
+        const int nlive = dw_gather_meta<32, KMAX>(c, b, oy, ox, lane, 0xffffffffu, meta);
+        for (int c0 = lane * 8; c0 < C; c0 += 256) {
+            float x[8], y[8];
+            RowIO<float, 8>::load(d.x0 + bq * C + c0, x);
+#pragma unroll
+            for (int i = 0; i < 8; i++) y[i] = actf<ACT>(x[i]);
+            RowIO<float, 8>::store(xs + c0, x);
+            RowIO<float, 8>::store(ys + c0, y);
+        }
+        uint32_t emit = 0;
+        int64_t orow = 1 + __ldg(d.out_pbase + bq);
+        while (w) {
+            const int tA = __ffs(w) - 1;
+            w &= w - 1;
+            int tB = -1;
+            if (PAIR && w) {
+                tB = __ffs(w) - 1;
+                w &= w - 1;
+            }
+            // pass 1 of frame A (+ the delta of frame B into bs)
+            float mx = 0.0f;
+            for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                float accA[8], accB[8], x[8], y[8];
+                if constexpr (PAIR)
+                    dw_acc_pair<TB>(reinterpret_cast<const bf16 *>(A), c.wk, C, c0, true, meta, nlive, tA, tB, accA,
+                                    accB);
+                else
+                    dw_acc_one<TB, 8, T>(A, c.wk, C, c0, true, meta, nlive, tA, accA);
+                RowIO<float, 8>::load(xs + c0, x);
+                RowIO<float, 8>::load(ys + c0, y);
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    x[i] = __fadd_rn(x[i], rnd<T>(accA[i]));
+                    mx = fmaxf(mx, fabsf(__fsub_rn(actf<ACT>(x[i]), y[i])));
+                }
+                RowIO<float, 8>::store(xs + c0, x);
+                if (CR) RowIO<T, 8>::store(CR + orow * C + c0, accA);
+                if (PAIR && tB >= 0) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) accB[i] = rnd<T>(accB[i]);
+                    RowIO<float, 8>::store(bs + c0, accB);
+                    if (CR) RowIO<T, 8>::store(CR + (orow + 1) * C + c0, accB);
+                }
+            }
+            if (gmax<32>(mx, 0xffffffffu) > theta) {   // truncation
+                emit_row(orow);
+                emit |= 1u << tA;
+            }
+            orow++;
+            if (tB < 0) continue;
+            mx = 0.0f;
+            for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                float x[8], y[8], v[8];
+                RowIO<float, 8>::load(xs + c0, x);
+                RowIO<float, 8>::load(ys + c0, y);
+                RowIO<float, 8>::load(bs + c0, v);
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    x[i] = __fadd_rn(x[i], v[i]);
+                    mx = fmaxf(mx, fabsf(__fsub_rn(actf<ACT>(x[i]), y[i])));
+                }
+                RowIO<float, 8>::store(xs + c0, x);
+            }
+            if (gmax<32>(mx, 0xffffffffu) > theta) {
+                emit_row(orow);
+                emit |= 1u << tB;
             }
             orow++;
         }
+        if (lane == 0) d.site_act[bq] = emit;
     }
 }
 
@@ -458,6 +707,11 @@ __global__ void __launch_bounds__(256) k_dw_tile(ConvCall c, const uint32_t *__r
 #pragma unroll
                     for (int i = 0; i < 8; i++) acc[i] = __fadd_rn(acc[i], bb[i]);
                     RowIO<float, 8>::store(static_cast<float *>(c.out) + (int64_t)o_row[o] * C + cs0 + cg * 8, acc);
+                    if (c.act_out) {   // the consuming site's dense output f(x0)
+#pragma unroll
+                        for (int i = 0; i < 8; i++) acc[i] = act_rt(c.act_kind, acc[i]);
+                        RowIO<float, 8>::store(c.act_out + (int64_t)o_row[o] * C + cs0 + cg * 8, acc);
+                    }
                 } else {
                     const int64_t orow = (int64_t)o_row[o] + __popc(oa & lowmask(t1));
                     RowIO<TO, 8>::store(static_cast<TO *>(c.out) + orow * C + cs0 + cg * 8, acc);
@@ -586,6 +840,63 @@ void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t 
     }
     if (!c.bf) launch_dw_pm_t<float>(c, out_act, out_pbase, s);
     else launch_dw_pm_t<bf16>(c, out_act, out_pbase, s);
+}
+
+bool dwconv_site_fusable(const Geo &g) { return g.Cin % 8 == 0 && g.kh * g.kw <= 25; }
+
+template <int G, int KMAX, class T, int ACT>
+static void launch_dws_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaStream_t s) {
+    constexpr int smem = (256 / G) * KMAX * 16;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dwconv_site<G, KMAX, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo * G + 255) / 256, 148 * 16));
+    k_dwconv_site<G, KMAX, T, ACT><<<grid, 256, smem, s>>>(c, d);
+}
+
+template <int KMAX, class T, int ACT>
+static void launch_dws_wide_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaStream_t s) {
+    const int smem = DWS_WARPS * KMAX * 16 + DWS_WARPS * 3 * c.g.Cin * 4;
+    static int attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_dwconv_site_wide<KMAX, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = smem;
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo + DWS_WARPS - 1) / DWS_WARPS, 148 * 4));
+    k_dwconv_site_wide<KMAX, T, ACT><<<grid, 32 * DWS_WARPS, smem, s>>>(c, d);
+}
+
+template <class T, int ACT>
+static void launch_dws_t(const ConvCall &c, const DwSite &d, cudaStream_t s) {
+    const int64_t BNo = (int64_t)c.B * c.g.Hout * c.g.Wout;
+    const int C = c.g.Cin;
+    const bool k9 = c.g.kh * c.g.kw <= 9;
+#define L_DWS(G_)                                                               \
+    {                                                                           \
+        if (k9) launch_dws_k<G_, 9, T, ACT>(c, d, BNo, s);                      \
+        else launch_dws_k<G_, 25, T, ACT>(c, d, BNo, s);                        \
+    }
+    if (C <= 8) L_DWS(1)
+    else if (C <= 16) L_DWS(2)
+    else if (C <= 32) L_DWS(4)
+    else if (C <= 64) L_DWS(8)
+    else if (C <= 128) L_DWS(16)
+    else if (C <= 256) L_DWS(32)
+    else if (k9) launch_dws_wide_k<9, T, ACT>(c, d, BNo, s);
+    else launch_dws_wide_k<25, T, ACT>(c, d, BNo, s);
+#undef L_DWS
+}
+
+void launch_dwconv_site(const ConvCall &c, const DwSite &d, cudaStream_t s) {
+    if (c.bf) {
+        if (d.act == ACT_RELU) launch_dws_t<bf16, ACT_RELU>(c, d, s);
+        else launch_dws_t<bf16, ACT_SILU_FAST>(c, d, s);   // BF16 mode: the fast SiLU of the site kernels
+    } else {
+        if (d.act == ACT_RELU) launch_dws_t<float, ACT_RELU>(c, d, s);
+        else launch_dws_t<float, ACT_SILU>(c, d, s);
+    }
 }
 
 }  // namespace st

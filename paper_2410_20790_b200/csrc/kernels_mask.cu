@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan1(const uint32_t *__restrict__ w
     if (threadIdx.x == 0) tmp[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *total, long long *stat) {
+__global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *total, long long *stat,
+                                                long long *peak) {
     st_pdl_enter();
     __shared__ int ws[32];
     __shared__ int carry;
@@ -242,7 +243,27 @@ __global__ void __launch_bounds__(1024) k_scan2(int32_t *tmp, int nb, int32_t *t
     if (threadIdx.x == 0) {
         *total = carry;
         if (stat) atomicAdd((unsigned long long *)stat, (unsigned long long)carry);
+        if (peak) atomicMax(peak, (long long)carry);
     }
+}
+
+// Row capacity (reading of SURVEY §8(a) a9: buffers sized from measured
+// occupancy): a word whose rows would end past `cap` is cleared -- with the
+// ordered prefix, exactly the words from the first one that does not fit on
+// -- so no kernel of the step writes past the buffer; the first cleared
+// word's offset becomes the tensor's total and *ovf is raised (the step's
+// results are invalid; the host re-plans and re-issues it).
+__device__ __forceinline__ bool fits_cap(uint32_t *w, int64_t i, int off, int c, int64_t cap, int32_t *total,
+                                         int32_t *ovf) {
+    if ((int64_t)off + c <= cap) return true;
+    if (c) {
+        w[i] = 0u;
+        if ((int64_t)off <= cap) {   // the first word that does not fit (unique)
+            *total = off;
+            *ovf = 1;
+        }
+    }
+    return false;
 }
 
 // ridx (optional): the conv M-row list, ((b*N+q) << 5) | (t-1) for every set
@@ -257,9 +278,9 @@ __device__ __forceinline__ void emit_codes(uint32_t w, int64_t i, int off, int32
     }
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w, int64_t n,
-                                                  const int32_t *__restrict__ tmp, int32_t *__restrict__ pbase,
-                                                  int32_t *__restrict__ ridx) {
+__global__ void __launch_bounds__(SCAN_T) k_scan3(uint32_t *w, int64_t n, const int32_t *__restrict__ tmp,
+                                                  int32_t *__restrict__ pbase, int32_t *__restrict__ ridx,
+                                                  int64_t cap, int32_t *total, int32_t *ovf) {
     st_pdl_enter();
     __shared__ int ws[32];
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + threadIdx.x * SCAN_E;
@@ -267,7 +288,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w
     int s = 0;
 #pragma unroll
     for (int e = 0; e < SCAN_E; e++) {
-        c[e] = base + e < n ? __popc(__ldg(w + base + e)) : 0;
+        c[e] = base + e < n ? __popc(w[base + e]) : 0;
         s += c[e];
     }
     int tot;
@@ -276,7 +297,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w
     for (int e = 0; e < SCAN_E; e++) {
         if (base + e < n) {
             pbase[base + e] = off;
-            if (ridx && c[e]) emit_codes(__ldg(w + base + e), base + e, off, ridx);
+            if (fits_cap(w, base + e, off, c[e], cap, total, ovf) && ridx && c[e])
+                emit_codes(w[base + e], base + e, off, ridx);
         }
         off += c[e];
     }
@@ -285,9 +307,10 @@ __global__ void __launch_bounds__(SCAN_T) k_scan3(const uint32_t *__restrict__ w
 // one CTA for small word arrays: the whole scan (+ optional enumeration) in
 // one launch instead of scan1 / scan2 / scan3 / enumerate
 constexpr int SCAN_SMALL_T = 1024, SCAN_SMALL_MAX = 2048;   // larger arrays: the enumeration parallelises better over 3 passes
-__global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t *__restrict__ w, int64_t n,
-                                                             int32_t *__restrict__ pbase, int32_t *total,
-                                                             long long *stat, int32_t *__restrict__ ridx) {
+__global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(uint32_t *w, int64_t n, int32_t *__restrict__ pbase,
+                                                             int32_t *total, long long *stat,
+                                                             int32_t *__restrict__ ridx, int64_t cap, int32_t *ovf,
+                                                             long long *peak) {
     st_pdl_enter();
     __shared__ int ws[32];
     int carry = 0;
@@ -297,7 +320,7 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t *__r
         int c[4], sum = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            v[e] = base + e < n ? __ldg(w + base + e) : 0u;
+            v[e] = base + e < n ? w[base + e] : 0u;
             c[e] = __popc(v[e]);
             sum += c[e];
         }
@@ -307,34 +330,36 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t *__r
         for (int e = 0; e < 4; e++) {
             if (base + e < n) {
                 pbase[base + e] = off;
-                if (ridx && c[e]) emit_codes(v[e], base + e, off, ridx);
+                if (fits_cap(w, base + e, off, c[e], cap, total, ovf) && ridx && c[e]) emit_codes(v[e], base + e, off, ridx);
             }
             off += c[e];
         }
         carry += tot;
     }
     if (threadIdx.x == 0) {
-        *total = carry;
         if (stat) atomicAdd((unsigned long long *)stat, (unsigned long long)carry);
+        if (peak) atomicMax(peak, (long long)carry);
+        if ((int64_t)carry <= cap) *total = carry;   // else: set by the first word that did not fit
     }
 }
 
-void launch_scan_popc(const uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp,
-                      long long *stat, cudaStream_t s, int32_t *ridx) {
+void launch_scan_popc(uint32_t *words, int64_t n, int32_t *pbase, int32_t *total, int32_t *tmp, long long *stat,
+                      cudaStream_t s, int32_t *ridx, const ScanCap &cap) {
     const int nb = cdiv(n, SCAN_TILE);
     if (nb == 0) {
         cudaMemsetAsync(total, 0, sizeof(int32_t), s);
         return;
     }
+    const int64_t cp = cap.ovf ? cap.cap : INT64_MAX;
     if (n <= SCAN_SMALL_MAX) {
-        k_scan_small<<<1, SCAN_SMALL_T, 0, s>>>(words, n, pbase, total, stat, ridx);
+        k_scan_small<<<1, SCAN_SMALL_T, 0, s>>>(words, n, pbase, total, stat, ridx, cp, cap.ovf, cap.peak);
         return;
     }
     k_scan1<<<nb, SCAN_T, 0, s>>>(words, n, tmp);
-    k_scan2<<<1, 1024, 0, s>>>(tmp, nb, total, stat);
+    k_scan2<<<1, 1024, 0, s>>>(tmp, nb, total, stat, cap.peak);
     // enumeration in its own pass: one thread per word (up to 32 codes each)
     // parallelises 8x better than the scan's 8-words-per-thread layout
-    k_scan3<<<nb, SCAN_T, 0, s>>>(words, n, tmp, pbase, nullptr);
+    k_scan3<<<nb, SCAN_T, 0, s>>>(words, n, tmp, pbase, nullptr, cp, total, cap.ovf);
     if (ridx) launch_enumerate(words, pbase, n, ridx, s);
 }
 

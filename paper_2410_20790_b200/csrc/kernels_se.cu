@@ -353,6 +353,108 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
     }
 }
 
+// ---- (iii') SE site pixel loop, C % 8 == 0: lane l of a pixel's group owns
+// the CPL consecutive channels [l*CPL, (l+1)*CPL) and moves x0, the delta
+// rows and the frame's gate as 16-byte vectors (rowio.cuh); the rows of the
+// next P touched frames are fetched together; while pixel k runs, the touched
+// word of pixel k+2 and the metadata + x0 of pixel k+1 are in flight.  Same
+// per-channel operations in the same order as k_se_site (FP32 bit-exact).
+template <int G, int CPL, class T>
+__global__ void __launch_bounds__(256) k_se_site_v(DView in, const float *__restrict__ x0,
+                                                   const float *__restrict__ s_tab, int N, int C, int F, int64_t BN,
+                                                   const float *__restrict__ theta_p, const uint32_t *__restrict__ slot,
+                                                   const int32_t *__restrict__ pbase, uint32_t *__restrict__ out_act,
+                                                   T *__restrict__ out_rows) {
+    st_pdl_enter();
+    constexpr int P = CPL <= 8 ? 2 : 1;   // frames prefetched per batch (~16 values per lane)
+    const float theta = __ldg(theta_p);
+    const T *rows = static_cast<const T *>(in.rows);
+    const int lane = threadIdx.x & (G - 1);
+    const int c0 = lane * CPL;
+    const bool full = c0 + CPL <= C;   // C % 8 == 0: whole or past C
+    const unsigned mask = group_mask<G>();
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    int64_t bp = grp;
+    uint32_t T_nx = bp < BN ? __ldg(slot + bp) : 0u;
+    uint32_t a_nx = 0, isl_nx = 0;
+    int ib_nx = 0, ob_nx = 0;
+    float x_nx[CPL];
+    auto meta = [&](int64_t q, uint32_t Tw) {
+        if (!Tw) return;
+        a_nx = __ldg(in.act + q);
+        ib_nx = a_nx ? 1 + __ldg(in.pbase + q) : 0;
+        isl_nx = a_nx ? __ldg(in.slot + q) : 0u;
+        ob_nx = 1 + __ldg(pbase + q);
+        row_load<float, CPL>(x0 + q * C, c0, C, full, x_nx);
+    };
+    meta(bp, T_nx);
+    uint32_t T_nn = bp + ngrp < BN ? __ldg(slot + bp + ngrp) : 0u;
+    for (; bp < BN; bp += ngrp) {
+        const uint32_t Tw = T_nx, a = a_nx, isl = isl_nx;
+        const int ibase = ib_nx, obase = ob_nx;
+        float xa[CPL], ya[CPL];
+#pragma unroll
+        for (int i = 0; i < CPL; i++) xa[i] = x_nx[i];
+        const int64_t b1 = bp + ngrp;
+        T_nx = T_nn;
+        meta(b1, T_nx);
+        T_nn = b1 + ngrp < BN ? __ldg(slot + b1 + ngrp) : 0u;
+        if (!Tw) {
+            if (lane == 0) out_act[bp] = 0;
+            continue;
+        }
+        const int b = (int)(bp / N);
+        const float *st = s_tab + (int64_t)b * (F + 1) * C;
+        {
+            float s0[CPL];
+            row_load<float, CPL>(st, c0, C, full, s0);
+#pragma unroll
+            for (int i = 0; i < CPL; i++) ya[i] = __fmul_rn(xa[i], s0[i]);   // y0 = x0 * s_emit(0)
+        }
+        uint32_t bits = Tw, emit = 0;
+        while (bits) {
+            int t1s[P];
+            float v[P][CPL], sn[P][CPL];
+#pragma unroll
+            for (int j = 0; j < P; j++) {   // the next P touched frames (absent: row 0 = zeros)
+                const int t1 = __ffs(bits) - 1;
+                t1s[j] = t1;
+                bits &= bits - 1;
+                const int64_t irow = (t1 >= 0 && ((a >> t1) & 1u)) ? ibase + __popc(isl & lowmask(t1)) : 0;
+                row_load<T, CPL>(rows + irow * C, c0, C, full, v[j]);
+                row_load<float, CPL>(st + (int64_t)(t1 >= 0 ? t1 + 1 : 0) * C, c0, C, full, sn[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < P; j++) {
+                const int t1 = t1s[j];
+                if (t1 < 0) continue;
+                const bool act = (a >> t1) & 1u;
+                float cand[CPL];
+                float mx = 0.0f;
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    if (act) xa[i] = __fadd_rn(xa[i], v[j][i]);
+                    cand[i] = __fsub_rn(__fmul_rn(xa[i], sn[j][i]), ya[i]);
+                    mx = fmaxf(mx, fabsf(cand[i]));
+                }
+                mx = gmax<G>(mx, mask);
+                if (mx > theta) {
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        cand[i] = rnd<T>(cand[i]);
+                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                    }
+                    if (c0 < C) row_store<T, CPL>(out_rows + (obase + __popc(Tw & lowmask(t1))) * (int64_t)C, c0, C,
+                                                  full, cand);
+                    emit |= 1u << t1;
+                }
+            }
+        }
+        if (lane == 0) out_act[bp] = emit;
+    }
+}
+
 void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s) {
     cudaMemsetAsync(sum0, 0, (size_t)B * C * 8, s);
     const int ppb = 1024;
@@ -427,6 +529,25 @@ void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N,
     auto grid_for = [&](int G) {
         return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(BN * G, 256), 148 * 8));
     };
+    if (C % 8 == 0 && C <= 1280) {   // vectorised blocked form
+#define L_SEV(G_, CPL_)                                                                                          \
+    k_se_site_v<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \
+                                                          static_cast<T *>(out_rows))
+#define SEV_CH                            \
+    if (C <= 8) L_SEV(1, 8);              \
+    else if (C <= 16) L_SEV(2, 8);        \
+    else if (C <= 32) L_SEV(4, 8);        \
+    else if (C <= 64) L_SEV(8, 8);        \
+    else if (C <= 128) L_SEV(16, 8);      \
+    else if (C <= 256) L_SEV(32, 8);      \
+    else if (C <= 512) L_SEV(32, 16);     \
+    else if (C <= 768) L_SEV(32, 24);     \
+    else L_SEV(32, 40);
+        ST_ROW_DISPATCH(bf, SEV_CH);
+#undef SEV_CH
+#undef L_SEV
+        return;
+    }
 #define L_SE(G_, CPL_)                                                                                      \
     k_se_site<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \
                                                         static_cast<T *>(out_rows))

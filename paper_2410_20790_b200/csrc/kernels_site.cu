@@ -24,28 +24,6 @@
 
 namespace st {
 
-template <int G>
-__device__ __forceinline__ unsigned group_mask() {
-    if constexpr (G == 32) {
-        return 0xffffffffu;
-    } else {
-        const int lane = threadIdx.x & 31;
-        return ((1u << G) - 1u) << (lane & ~(G - 1));
-    }
-}
-
-template <int G>
-__device__ __forceinline__ float gmax(float v, unsigned mask) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(mask, v, o, G));
-    return v;
-}
-
-template <int ACT>
-__device__ __forceinline__ float actf(float x) {
-    return ACT == ACT_RELU ? relu_f(x) : ACT == ACT_SILU ? silu_f(x) : silu_fast(x);
-}
-
 // frames whose rows are fetched per batch (~16 prefetched values per lane:
 // deeper batches cost more registers than they save in latency -- measured)
 constexpr int prefetch_depth(int cpl) { return cpl <= 2 ? 8 : cpl <= 4 ? 4 : cpl <= 8 ? 2 : 1; }

@@ -1,0 +1,89 @@
+"""Depthwise conv + pointwise site in one pass (SURVEY §8(f) N2 for depthwise
+convs; Eq.2 then Eq.3), -m gpu.
+
+The fused kernel computes an output pixel's depthwise delta rows frame by
+frame and steps the ReLU / SiLU site on them at once, so the conv's delta
+rows never reach HBM.  It must give bit-identical results to the separate
+conv and site kernels (ST_NO_FUSE_DW=1) in both modes, and in FP32 mode
+match the oracle (masks exact; ReLU values exact, SiLU within R29) -- also
+with debug_retain, where the fused pass writes the conv's own rows too."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+from workloads import Net, init_weights
+from gpu_harness import gpu_run, compare_chunk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2410_20790_b200 import load_library
+    load_library()
+
+
+def dw_net(C, k, s, act, h, w, seed):
+    """stem 3x3 3->C + act, depthwise kxk/s + act, 1x1 C->8 (+ an SE-free tail)."""
+    n = Net(3, h, w, f"dw{C}k{k}s{s}{act}")
+    x = n.conv(-1, C, 3, 1, 1)
+    x = n.relu(x) if act == "relu" else n.silu(x)
+    x = n.conv(x, C, k, s, k // 2, groups=C)
+    x = n.relu(x) if act == "relu" else n.silu(x)
+    x = n.conv(x, 8, 1, 1, 0)
+    n.output(x)
+    init_weights(n, seed)
+    return n
+
+
+CASES = [(8, 3, 1, "relu", 19, 23), (24, 3, 2, "silu", 21, 26), (64, 5, 1, "relu", 14, 17),
+         (136, 3, 1, "silu", 12, 13), (264, 5, 2, "relu", 11, 14), (520, 3, 1, "silu", 9, 10)]
+
+
+def frames_for(h, w, seed, B=2, L=9):
+    return W.to_float(W.gen_video(B, L, h, w, 3, seed, n_objects=3, size=(3, 7), speed=(1, 2),
+                                  noise_q=0.08, noise_amp=2))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("C,k,s,act,h,w", CASES)
+def test_fused_dw_site_matches_separate(C, k, s, act, h, w, precision, monkeypatch):
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    net = dw_net(C, k, s, act, h, w, 5 + C)
+    fr = torch.from_numpy(frames_for(h, w, 900 + C)).cuda()
+    outs = {}
+    for mode in ("fused", "separate"):
+        if mode == "separate":
+            monkeypatch.setenv("ST_NO_FUSE_DW", "1")
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.02, 0.0, 0.08):
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs[mode] = res
+        enc.close()
+    for (og, cg), (oe, ce) in zip(outs["fused"], outs["separate"]):
+        assert np.array_equal(cg, ce), "per-site per-frame counts"
+        for a, b in zip(og, oe):
+            assert np.array_equal(a, b), f"tap outputs differ (max {np.abs(a - b).max():.3e})"
+
+
+@pytest.mark.parametrize("C,k,s,act,h,w", CASES)
+def test_fused_dw_site_vs_oracle_fp32(C, k, s, act, h, w):
+    """debug_retain run (the fused pass also writes the conv's rows): every
+    layer's mask / index list and rows against the oracle."""
+    net = dw_net(C, k, s, act, h, w, 5 + C)
+    fr = frames_for(h, w, 900 + C)
+    th = [0.02] * (1 + sum(l["kind"] in W.NONLINEAR for l in net.layers))
+    enc, _ = gpu_run(net, fr, th)
+    for b in range(fr.shape[0]):
+        compare_chunk(enc, net, fr[b], th, b, exact=(act == "relu"))
+    enc.close()
