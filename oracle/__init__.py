@@ -19,4 +19,4 @@ from .core import (  # noqa: F401
     build, lib_path, shapes, num_sites, dense_forward, run_chunk, dilate,
 )
 from .controller import Controller, ControllerConfig  # noqa: F401
-from .memory import account_memory  # noqa: F401
+from .memory import account_memory, rows_from_run  # noqa: F401

@@ -305,7 +305,9 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
         if (is_site(l.kind)) l.site = e->n_sites++;
         // register-resident site kernels: <= 1152 channels at maxpool / SE
         // sites; pointwise sites, joins and taps up to 2048 (wide kernels)
-        if (l.C > 2048 || ((l.kind == ST_MAXPOOL || l.kind == ST_SE) && l.C > 1152)) return ST_ERR_UNSUPPORTED;
+        if (l.C > 4096 || (l.kind == ST_MAXPOOL && l.C > 1152) || (l.kind == ST_SE && l.C > 1152 && l.C % 8 != 0))
+            return ST_ERR_UNSUPPORTED;
+        if ((l.kind == ST_ADD || l.kind == ST_OUTPUT) && l.C > 2048) return ST_ERR_UNSUPPORTED;
         if ((l.kind == ST_RELU || l.kind == ST_SILU) && l.C > 1280 && l.C % 8 != 0) return ST_ERR_UNSUPPORTED;
     }
     // consumers
@@ -614,6 +616,14 @@ static st_status plan(st_encoder *e) {
             }
         }
     }
+    // a depthwise conv's pass writes its fused site's dense output (dense
+    // epilogue) and frame words (sparse pass) at the conv's step time
+    for (int i = 0; i < n; i++)
+        if (e->L[i].fused_dw >= 0) {
+            const int tc = t_of(e->L[i].fused_dw);
+            for (int id : {e->L[i].b_y0, e->L[i].b_ybf, e->L[i].b_act, e->L[i].b_rows})
+                if (id >= 0) e->bufs[id].first = std::min(e->bufs[id].first, tc);
+        }
     // a fused ReLU -> maxpool pass reads the conv's dense pre-activation (the
     // ReLU's x0) at the pool's step time
     for (int i = 0; i < n; i++)
@@ -1042,6 +1052,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             if (l.dw_site >= 0) {   // the site's dense output from the same epilogue
                 const LayerRT &r = e->L[l.dw_site];
                 c.act_out = e->p<float>(r.b_y0);
+                c.act_bf = ybf_of(e, l.dw_site);
                 c.act_kind = r.kind == ST_RELU ? ACT_RELU : bf ? ACT_SILU_FAST : ACT_SILU;
             }
             if (!cont)
@@ -1073,6 +1084,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             c.m_cap = l.rows_cap;
             c.out = e->ptr(l.b_rows);
             c.act_out = nullptr;
+            c.act_bf = nullptr;
             if (l.dw_site >= 0) {   // depthwise conv + its site in one pass (N2)
                 const LayerRT &r = e->L[l.dw_site];
                 DwSite d;

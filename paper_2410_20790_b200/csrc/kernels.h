@@ -97,6 +97,7 @@ struct ConvCall {
     // dense depthwise only, optional: the consuming pointwise site's dense
     // output f(out) (act_kind: Act) written by the same epilogue
     float *act_out = nullptr;
+    void *act_bf = nullptr;   // optional bf16 (RNE) shadow of act_out (a tensor-core conv reads it densely)
     int act_kind = 0;
 };
 void launch_conv_f32(const ConvCall &c, cudaStream_t s);

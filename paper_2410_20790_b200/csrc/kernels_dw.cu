@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(256, 2) k_dwconv(ConvCall c) {
 #pragma unroll
                     for (int i = 0; i < CPL; i++) acc[i] = act_rt(c.act_kind, acc[i]);
                     row_store<float, CPL>(c.act_out + r * C, c0, C, full, acc);
+                    if (c.act_bf) row_store<bf16, CPL>(static_cast<bf16 *>(c.act_bf) + r * C, c0, C, full, acc);
                 }
             } else {
                 row_store<T, CPL>(static_cast<T *>(c.out) + (r + 1) * C, c0, C, full, acc);
@@ -711,6 +712,9 @@ __global__ void __launch_bounds__(256) k_dw_tile(ConvCall c, const uint32_t *__r
 #pragma unroll
                         for (int i = 0; i < 8; i++) acc[i] = act_rt(c.act_kind, acc[i]);
                         RowIO<float, 8>::store(c.act_out + (int64_t)o_row[o] * C + cs0 + cg * 8, acc);
+                        if (c.act_bf)
+                            RowIO<bf16, 8>::store(static_cast<bf16 *>(c.act_bf) + (int64_t)o_row[o] * C + cs0 + cg * 8,
+                                                  acc);
                     }
                 } else {
                     const int64_t orow = (int64_t)o_row[o] + __popc(oa & lowmask(t1));
@@ -842,7 +846,9 @@ void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t 
     else launch_dw_pm_t<bf16>(c, out_act, out_pbase, s);
 }
 
-bool dwconv_site_fusable(const Geo &g) { return g.Cin % 8 == 0 && g.kh * g.kw <= 25; }
+bool dwconv_site_fusable(const Geo &g) {
+    return g.Cin % 8 == 0 && g.kh * g.kw <= 25 && DWS_WARPS * (25 * 16 + 3 * g.Cin * 4) <= 200 * 1024;
+}
 
 template <int G, int KMAX, class T, int ACT>
 static void launch_dws_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaStream_t s) {
@@ -858,7 +864,7 @@ static void launch_dws_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaSt
 
 template <int KMAX, class T, int ACT>
 static void launch_dws_wide_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaStream_t s) {
-    const int smem = DWS_WARPS * KMAX * 16 + DWS_WARPS * 3 * c.g.Cin * 4;
+    const int smem = DWS_WARPS * KMAX * 16 + DWS_WARPS * 3 * c.g.Cin * 4;   // <= 200 KB (dwconv_site_fusable)
     static int attr = 0;
     if (smem > attr) {
         cudaFuncSetAttribute(k_dwconv_site_wide<KMAX, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

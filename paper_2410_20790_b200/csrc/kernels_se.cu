@@ -455,6 +455,93 @@ __global__ void __launch_bounds__(256) k_se_site_v(DView in, const float *__rest
     }
 }
 
+// ---- (iii'') SE site for wide layers (C > 1280, C % 8 == 0: the expanded
+// stages of EfficientNet-B4..B6): one warp per pixel, x_acc /
+// y_acc in shared memory, 256-channel chunks (8 per lane).  Per touched frame
+// pass 1 adds the delta and takes the running max of |x_acc * s - y_acc|; on
+// emission pass 2 recomputes the candidate from the stored state (same
+// operations, same bits), rounds it, advances y_acc and writes the row.
+constexpr int SE_WIDE_WARPS = 4;
+template <class T>
+__global__ void __launch_bounds__(32 * SE_WIDE_WARPS) k_se_site_wide(DView in, const float *__restrict__ x0,
+                                                                     const float *__restrict__ s_tab, int N, int C,
+                                                                     int F, int64_t BN, const float *__restrict__ theta_p,
+                                                                     const uint32_t *__restrict__ slot,
+                                                                     const int32_t *__restrict__ pbase,
+                                                                     uint32_t *__restrict__ out_act,
+                                                                     T *__restrict__ out_rows) {
+    st_pdl_enter();
+    extern __shared__ float sew_sm[];
+    const float theta = __ldg(theta_p);
+    const T *rows = static_cast<const T *>(in.rows);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float *xs = sew_sm + (size_t)wid * 2 * C, *ys = xs + C;
+    for (int64_t bp = (int64_t)blockIdx.x * SE_WIDE_WARPS + wid; bp < BN; bp += (int64_t)gridDim.x * SE_WIDE_WARPS) {
+        const uint32_t Tw = __ldg(slot + bp);
+        if (!Tw) {
+            if (lane == 0) out_act[bp] = 0;
+            continue;
+        }
+        const int b = (int)(bp / N);
+        const float *st = s_tab + (int64_t)b * (F + 1) * C;
+        const uint32_t a = __ldg(in.act + bp);
+        const int ibase = a ? 1 + __ldg(in.pbase + bp) : 0;
+        const uint32_t isl = a ? __ldg(in.slot + bp) : 0u;
+        const int obase = 1 + __ldg(pbase + bp);
+        for (int c0 = lane * 8; c0 < C; c0 += 256) {
+            float x[8], s0[8], y[8];
+            RowIO<float, 8>::load(x0 + bp * C + c0, x);
+            RowIO<float, 8>::load(st + c0, s0);
+#pragma unroll
+            for (int i = 0; i < 8; i++) y[i] = __fmul_rn(x[i], s0[i]);   // y0 = x0 * s_emit(0)
+            RowIO<float, 8>::store(xs + c0, x);
+            RowIO<float, 8>::store(ys + c0, y);
+        }
+        uint32_t bits = Tw, emit = 0;
+        while (bits) {
+            const int t1 = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const bool act = (a >> t1) & 1u;
+            const int64_t irow = act ? ibase + __popc(isl & lowmask(t1)) : 0;
+            const float *s_now = st + (int64_t)(t1 + 1) * C;
+            float mx = 0.0f;
+            for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                float x[8], y[8], v[8], sn[8];
+                RowIO<float, 8>::load(xs + c0, x);
+                RowIO<float, 8>::load(ys + c0, y);
+                RowIO<float, 8>::load(s_now + c0, sn);
+                if (act) {
+                    RowIO<T, 8>::load(rows + irow * C + c0, v);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) x[i] = __fadd_rn(x[i], v[i]);
+                    RowIO<float, 8>::store(xs + c0, x);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++) mx = fmaxf(mx, fabsf(__fsub_rn(__fmul_rn(x[i], sn[i]), y[i])));
+            }
+            mx = gmax<32>(mx, 0xffffffffu);
+            if (mx > theta) {
+                const int64_t orow = obase + __popc(Tw & lowmask(t1));
+                for (int c0 = lane * 8; c0 < C; c0 += 256) {
+                    float x[8], y[8], sn[8], e[8];
+                    RowIO<float, 8>::load(xs + c0, x);
+                    RowIO<float, 8>::load(ys + c0, y);
+                    RowIO<float, 8>::load(s_now + c0, sn);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        e[i] = rnd<T>(__fsub_rn(__fmul_rn(x[i], sn[i]), y[i]));
+                        y[i] = __fadd_rn(y[i], e[i]);
+                    }
+                    RowIO<float, 8>::store(ys + c0, y);
+                    RowIO<T, 8>::store(out_rows + orow * C + c0, e);
+                }
+                emit |= 1u << t1;
+            }
+        }
+        if (lane == 0) out_act[bp] = emit;
+    }
+}
+
 void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStream_t s) {
     cudaMemsetAsync(sum0, 0, (size_t)B * C * 8, s);
     const int ppb = 1024;
@@ -529,6 +616,19 @@ void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N,
     auto grid_for = [&](int G) {
         return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(BN * G, 256), 148 * 8));
     };
+    if (C % 8 == 0 && C > 1280) {   // wide layers: state in shared memory
+        const size_t sm = (size_t)SE_WIDE_WARPS * 2 * C * sizeof(float);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(BN, SE_WIDE_WARPS), 148 * 8));
+#define L_SEW                                                                                               \
+    {                                                                                                       \
+        cudaFuncSetAttribute(k_se_site_wide<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
+        k_se_site_wide<T><<<grid, 32 * SE_WIDE_WARPS, sm, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, \
+                                                              out_act, static_cast<T *>(out_rows));         \
+    }
+        ST_ROW_DISPATCH(bf, L_SEW);
+#undef L_SEW
+        return;
+    }
     if (C % 8 == 0 && C <= 1280) {   // vectorised blocked form
 #define L_SEV(G_, CPL_)                                                                                          \
     k_se_site_v<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \

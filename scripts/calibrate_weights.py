@@ -76,15 +76,36 @@ def _se_logits(l, a):
     return _t(l["w2"]) @ h + _t(l["b2"])
 
 
+def _last_use(net):
+    """Index of the last layer reading each layer's output (OUTPUT taps and
+    sites are kept: the report reads them)."""
+    last = {}
+    for i, l in enumerate(net.layers):
+        for s in (l["src"], l["src2"] if l["kind"] == ADD else -1):
+            if s >= 0:
+                last[s] = i
+    return last
+
+
+def _drop(net, outs, i, last, keep_sites):
+    # free tensors whose last reader has run (B4-B6 at 1024-1280 px in fp64
+    # would otherwise hold tens of GB); sites and taps are kept for the report
+    for s in (net.layers[i]["src"], net.layers[i]["src2"] if net.layers[i]["kind"] == ADD else -1):
+        if s >= 0 and last.get(s) == i and not (keep_sites and net.layers[s]["kind"] in W.NONLINEAR + (OUTPUT,)):
+            outs[s] = None
+
+
 def forward(net, frame):
     x = _t(frame).permute(2, 0, 1).unsqueeze(0)
     outs = []
-    for l in net.layers:
+    last = _last_use(net)
+    for i, l in enumerate(net.layers):
         a = x if l["src"] < 0 else outs[l["src"]]
         b2 = None
         if l["kind"] == ADD:
             b2 = x if l["src2"] < 0 else outs[l["src2"]]
         outs.append(_layer(l, a, b2))
+        _drop(net, outs, i, last, True)
     return outs
 
 
@@ -93,6 +114,7 @@ def calibrate(net, frame):
     x = _t(frame).permute(2, 0, 1).unsqueeze(0)
     outs = []
     fold = {}
+    last = _last_use(net)
     for i, l in enumerate(net.layers):
         a = x if l["src"] < 0 else outs[l["src"]]
         if l["kind"] == CONV:
@@ -123,6 +145,7 @@ def calibrate(net, frame):
         if l["kind"] == ADD:
             b2 = x if l["src2"] < 0 else outs[l["src2"]]
         outs.append(_layer(l, a, b2))
+        _drop(net, outs, i, last, False)
     return fold
 
 

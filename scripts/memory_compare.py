@@ -1,16 +1,21 @@
 #!/usr/bin/env python
-"""SparseBatch vs vanilla (streaming caches) memory and throughput per config
-(PAPER.md P:139 vs P:152, the Fig. memory_comparison /
-Table 1 memory analogue on synthetic inputs).
+"""SparseBatch vs vanilla vs own dense: device memory and throughput per
+config (PAPER.md P:139 vs P:152, the Fig.
+memory_comparison / Table 1 memory analogue on synthetic inputs).
 
-For each config: st_memory_report of a SparseBatch encoder and of a
-streaming encoder (the vanilla DeltaCNN schedule's persistent per-site
-caches), the oracle accountant's element counts for both schedules, and the
-diff-frame throughput of (a) the SparseBatch step (reference + 31 diff
-frames), (b) streaming continuation calls (no reference frame, each call
-continuing every chunk by L-1 frames) and (c) the vanilla DeltaCNN schedule
-(reference + L-1 single-frame passes with the caches kept across passes).  CUDA events on the launch stream,
-L2 flushed between calls.  One JSON document on stdout.
+Encoders (total device bytes = arena + fixed areas + weights, st_device_bytes):
+(a) SparseBatch: one step over L-1 diff frames; row capacity first at the
+    all-active bound, then re-planned from the measured occupancy
+    (st_encoder_fit_capacity, --headroom);
+(b) streaming continuation: the SparseBatch step with the vanilla caches
+    kept, each call continuing every chunk by L-1 frames;
+(c) vanilla DeltaCNN schedule: a per-frame encoder (max_frames 2, arena for
+    one frame) driven reference + L-1 single-frame passes, every site's
+    x_acc / y_acc cached across passes;
+(d) own dense path: every frame a reference frame, one frame per call.
+Plus the oracle accountant's element counts (SparseBatch evaluated on the
+measured rows).  CUDA events on the launch stream, L2 flushed between
+calls.  One JSON document on stdout.
 """
 import argparse
 import json
@@ -26,6 +31,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="2,4")
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--precision", default="bf16")
+ap.add_argument("--headroom", type=float, default=1.25)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -63,21 +69,41 @@ for cid in [int(c) for c in a.configs.split(",")]:
             ms += e0.elapsed_time(e1)
         return ms / k
 
-    for mode in ("sparsebatch", "streaming", "vanilla"):
-        enc = Encoder(net, B, L, precision=a.precision, streaming=(mode != "sparsebatch"))
-        mem = enc.memory_report()
+    rows = None
+    for mode in ("sparsebatch", "streaming", "vanilla", "dense"):
+        # vanilla: a genuinely per-frame encoder (max_frames = 2: one diff frame
+        # per call, its arena sized for one frame) whose streaming caches carry
+        # every site's x_acc / y_acc from frame to frame;
+        # dense: the own dense path, one frame of each chunk per call
+        Lm = {"vanilla": 2, "dense": 1}.get(mode, L)
+        enc = Encoder(net, B, Lm, precision=a.precision, streaming=mode in ("streaming", "vanilla"))
+        mem = dict(enc.memory_report(), device_bytes=enc.device_bytes())
         if mode == "sparsebatch":
             def step():
                 enc.encode_reference(x[:, 0], s)
                 enc.encode_diff(x[:, 1:L], th, s)
+            step()
+            torch.cuda.synchronize()
+            cap, pk = enc.capacity()
+            rows = {i: int(v) // B for i, v in enumerate(pk[:-1]) if v >= 0}
+            rows[-1] = int(pk[-1]) // B
+            mem["all_active_bound"] = dict(mem)
+            enc.fit_capacity(a.headroom)   # row capacity from the measured occupancy (a9)
+            mem.update(enc.memory_report(), device_bytes=enc.device_bytes(), headroom=a.headroom)
             ms = timed(step, a.steps)
         elif mode == "vanilla":
-            # the vanilla DeltaCNN schedule: one pass through
-            # all layers per frame index, every site's caches kept across passes
             def step():
                 enc.encode_reference(x[:, 0], s)
                 for t in range(1, L):
                     enc.encode_diff(x[:, t:t + 1], th, s)
+            ms = timed(step, a.steps)
+        elif mode == "dense":
+            xd = x[:, :L].reshape(B, L, *x.shape[2:])
+
+            def step():
+                for t in range(L):
+                    enc.encode_reference(xd[:, t], s)
+                    enc.encode_diff(None, th, s)
             ms = timed(step, a.steps)
         else:
             enc.encode_reference(x[:, 0], s)
@@ -90,12 +116,16 @@ for cid in [int(c) for c in a.configs.split(",")]:
                 enc.encode_diff(x[:, 1 + k * (L - 1):1 + (k + 1) * (L - 1)], th, s)
                 state["k"] += 1
             ms = timed(step, a.steps)
-        res[mode] = {"memory": mem, "ms_per_call": ms, "diff_fps": B * (L - 1) / (ms / 1e3)}
+        nfr = B * L if mode == "dense" else B * (L - 1)
+        res[mode] = {"memory": mem, "ms_per_call": ms, "fps": nfr / (ms / 1e3)}
         del enc
         torch.cuda.empty_cache()
+    eb = 2 if a.precision == "bf16" else 4
     for sched in ("sparsebatch", "vanilla"):
-        m = oracle.account_memory(net, sched, n_videos=B, L=L)
-        res[f"accountant_{sched}_MB_fp32"] = {k: v * 4 / 1e6 for k, v in m.items() if k.endswith("values")}
+        m = oracle.account_memory(net, sched, n_videos=B, L=L, rows=rows if sched == "sparsebatch" else None)
+        res[f"accountant_{sched}_MB"] = {k: v * 4 / 1e6 for k, v in m.items() if k.endswith("values")}
+    res["accountant_note"] = ("oracle/memory.py element counts x 4 bytes (fp32 states); SparseBatch evaluated on "
+                              "the measured rows per tensor (rows x %d-byte deltas counted as 4)" % eb)
     doc[f"cfg{cid}"] = res
     print(json.dumps({f"cfg{cid}": res}), file=sys.stderr)
 print(json.dumps(doc))

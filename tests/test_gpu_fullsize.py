@@ -96,3 +96,26 @@ def test_cfg4_resnet18_720p_fp32():
 def test_cfg5_effdet_d0_1080p_fp32():
     """cfg5 EfficientDet-D0 backbone @1080p, FP32, 2 chunks x 6 frames."""
     _check(W.get_config(5), "fp32", (1,), L=6, B=2)
+
+
+# ---- SURVEY §8(f) N3: the paper's own backbones at their sizes
+@pytest.mark.parametrize("cid", [7, 8, 9])
+def test_effdet_d4_d6_backbones(cid):
+    """EfficientNet-B4 @1024 / B5 @1280 / B6 @1280 (the Table 1 detectors'
+    backbones), full frame size, 2 chunks x 4 frames: FP32 and
+    BF16 (band-follow) on the last chunk, in the bench launch configuration."""
+    cfg = W.get_config(cid)
+    theta = 0.05
+    _check(cfg, "fp32", (1,), L=4, B=2, theta=theta)
+    _check(cfg, "bf16", (1,), L=4, B=2, theta=theta)
+
+
+@pytest.mark.parametrize("cid", [10, 6, 11])
+def test_resnet152_crnn_resolutions(cid):
+    """ResNet-152 (the CRNN backbone) at the paper's three resolutions 224 /
+    320 / 420, batch 3, 28-frame chunks cut to 6 frames: FP32
+    bit-exact (ReLU/maxpool), BF16 band-follow, on the last chunk."""
+    cfg = W.get_config(cid)
+    reps = _check(cfg, "fp32", (2,), L=6, theta=0.05)
+    assert reps[0]["adopted"] == 0
+    _check(cfg, "bf16", (2,), L=6, theta=0.05)

@@ -402,6 +402,53 @@ def test_pin13_memory_separation(oracle_lib):
     assert n16[2] >= 10 * n16[1]
 
 
+def test_pin13b_memory_rows_worked_example(oracle_lib):
+    """The accountant's SparseBatch transient = the live set of (dense x0 +
+    delta rows) tensors per layer step ("N" order).  Hand-worked on
+    a 2-ch 6x7 input (N = 42), conv3x3 2->3, ReLU, conv1x1 3->4, tap, L = 5:
+      input rows 4*42*2 = 336        live steps 0-1
+      conv0  126 + 4*42*3 = 630      live 1-2
+      relu   126 + 504    = 630      live 2-3
+      conv1  168 + 4*42*4 = 840      live 3-4 (the tap)
+    peak = step 3: 630 + 840 = 1470; persistent = 84 + 5*168 = 924.
+    Vanilla: persistent 84 + 168 + (126 + 126) = 504, one frame's tensors
+    peak at step 3: 252 + 336 = 588."""
+    n = Net(2, 6, 7)
+    x = n.relu(n.conv(-1, 3, 3))
+    n.output(n.conv(x, 4, 1, 1, 0))
+    sb = oracle.account_memory(n, "sparsebatch", L=5)
+    va = oracle.account_memory(n, "vanilla", L=5)
+    assert (sb["persistent_values"], sb["peak_transient_values"]) == (924, 1470)
+    assert (va["persistent_values"], va["peak_transient_values"]) == (504, 588)
+    # measured rows replace the all-active bound: 10 active input pixel-frames,
+    # 30 conv0 rows, 12 emitted ReLU rows, 12 conv1 rows
+    r = {-1: 10, 0: 30, 1: 12, 2: 12}
+    sbr = oracle.account_memory(n, "sparsebatch", L=5, rows=r)
+    # steps: 1: 20 + (126 + 90) = 236; 2: 216 + (126 + 36) = 378; 3: 162 + (168 + 48) = 378
+    assert sbr["peak_transient_values"] == 378
+
+
+def test_pin13c_memory_rows_from_oracle_run(oracle_lib):
+    """rows_from_run counts the oracle's masks; identical frames give no
+    rows (PIN3), so the transient falls to the dense reference activations,
+    and more active rows never lower the peak."""
+    n = Net(2, 9, 9)
+    x = n.relu(n.conv(-1, 4, 3))
+    n.output(n.conv(x, 4, 3))
+    init_weights(n, 3)
+    still = np.repeat(random_frames(1, 1, 9, 9, 2), 5, axis=0)
+    r0 = oracle.rows_from_run(oracle.run_chunk(n, still, 0.0), n)
+    assert all(v == 0 for v in r0.values())
+    dense_only = oracle.account_memory(n, "sparsebatch", L=5, rows=r0)["peak_transient_values"]
+    assert dense_only == 2 * 9 * 9 * 4   # conv0 x0 + relu y0 (step 2), or relu + conv1 (step 3)
+    moving = random_frames(2, 5, 9, 9, 2, p_change=0.3)
+    rm = oracle.rows_from_run(oracle.run_chunk(n, moving, 0.0), n)
+    assert rm[-1] > 0 and rm[0] >= rm[-1]   # dilation: a 3x3 conv never has fewer rows
+    assert oracle.account_memory(n, "sparsebatch", L=5, rows=rm)["peak_transient_values"] > dense_only
+    assert oracle.account_memory(n, "sparsebatch", L=5)["peak_transient_values"] >= \
+        oracle.account_memory(n, "sparsebatch", L=5, rows=rm)["peak_transient_values"]
+
+
 # -------------------------------------------------------- PIN16 SE exact
 def test_pin16_se_zero_threshold(oracle_lib):
     net = _single(lambda n: n.se(-1, 3), 6, 5, 5, 2)

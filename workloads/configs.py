@@ -38,9 +38,12 @@ class Config:
         seed) the committed per-channel BatchNorm fold of reading R30
         (workloads/calib/cfg<N>.npz, written once by
         scripts/calibrate_weights.py) is applied when it exists."""
-        net = {"toy": models.toy_encoder, "crnn": models.crnn_vgg7,
-               "resnet18": models.resnet18, "effb0": models.efficientnet_b0,
-               "resnet152": models.resnet152}[self.model](self.h, self.w)
+        builders = {"toy": models.toy_encoder, "crnn": models.crnn_vgg7,
+                    "resnet18": models.resnet18, "effb0": models.efficientnet_b0,
+                    "resnet152": models.resnet152}
+        for v in ("b4", "b5", "b6"):
+            builders["eff" + v] = (lambda vv: lambda h, w: models.efficientnet(h, w, vv))(v)
+        net = builders[self.model](self.h, self.w)
         models.init_weights(net, SEED_BASE + 1000 * self.cid + 999 if weight_seed is None else weight_seed)
         path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "calib", f"cfg{self.cid}.npz")
         if calibrated and weight_seed is None and os.path.exists(path):
@@ -79,6 +82,30 @@ CONFIGS = {
               video=dict(n_objects=6, size=(32, 96), speed=(1, 3), noise_q=0.10, noise_amp=2),
               policy="ibst", T=0.9, eps=0.05, cycle=8,
               note="ResNet-152 CRNN backbone @320x320, 28-frame chunks, batch 3 (N3)"),
+    # the Table 1 detectors' backbones,
+    # EfficientDet-d4 / d5 / d6 = EfficientNet-B4 @1024 / B5 @1280 / B6 @1280,
+    # on static-camera street video like cfg5 (MOT16), 16-frame chunks
+    7: Config(7, "effdet_d4_1024", "effb4", 1024, 1024, 3, L=16, chunks_per_step=2, steps=4,
+              video=dict(n_objects=10, size=(32, 160), speed=(1, 3), noise_q=0.10, noise_amp=2),
+              policy="ibst", T=0.9, eps=0.05, cycle=8,
+              note="EfficientDet-d4 backbone (EfficientNet-B4) @1024x1024, 16-frame chunks (N3)"),
+    8: Config(8, "effdet_d5_1280", "effb5", 1280, 1280, 3, L=16, chunks_per_step=2, steps=4,
+              video=dict(n_objects=12, size=(32, 192), speed=(1, 3), noise_q=0.10, noise_amp=2),
+              policy="ibst", T=0.9, eps=0.05, cycle=8,
+              note="EfficientDet-d5 backbone (EfficientNet-B5) @1280x1280, 16-frame chunks (N3)"),
+    9: Config(9, "effdet_d6_1280", "effb6", 1280, 1280, 3, L=16, chunks_per_step=2, steps=4,
+              video=dict(n_objects=12, size=(32, 192), speed=(1, 3), noise_q=0.10, noise_amp=2),
+              policy="ibst", T=0.9, eps=0.05, cycle=8,
+              note="EfficientDet-d6 backbone (EfficientNet-B6) @1280x1280, 16-frame chunks (N3)"),
+    # the paper's CRNN experiments at its other two resolutions
+    10: Config(10, "resnet152_224", "resnet152", 224, 224, 3, L=28, chunks_per_step=3, steps=4,
+               video=dict(n_objects=5, size=(24, 72), speed=(1, 3), noise_q=0.10, noise_amp=2),
+               policy="ibst", T=0.9, eps=0.05, cycle=8,
+               note="ResNet-152 CRNN backbone @224x224, 28-frame chunks, batch 3 (N3)"),
+    11: Config(11, "resnet152_420", "resnet152", 420, 420, 3, L=28, chunks_per_step=3, steps=4,
+               video=dict(n_objects=8, size=(40, 128), speed=(1, 3), noise_q=0.10, noise_amp=2),
+               policy="ibst", T=0.9, eps=0.05, cycle=8,
+               note="ResNet-152 CRNN backbone @420x420, 28-frame chunks, batch 3 (N3)"),
 }
 
 

@@ -267,20 +267,46 @@ def resnet152(h=320, w=320):
 SPATIAL_SMOOTH = 0.7   # EfficientNet spatial kernels (stem, depthwise), reading R30
 
 
+# EfficientNet compound scaling (width, depth) of the backbones of
+# EfficientDet-D0 (B0) and of the paper's Table 1 detectors d4 / d5 / d6
+# (B4 / B5 / B6)
+EFFNET_SCALE = {"b0": (1.0, 1.0), "b4": (1.4, 1.8), "b5": (1.6, 2.2), "b6": (1.8, 2.6)}
+
+
+def _round_filters(c, width):
+    """Channels scaled by width, rounded to a multiple of 8 (never below 90%)."""
+    if width == 1.0:
+        return c
+    v = c * width
+    r = max(8, int(v + 4) // 8 * 8)
+    return r + 8 if r < 0.9 * v else r
+
+
 def efficientnet_b0(h=512, w=512):
-    """cfg3/cfg5: EfficientNet-B0 backbone (EfficientDet-D0), taps P3/P4/P5.
+    """cfg3/cfg5: EfficientNet-B0 backbone (EfficientDet-D0), taps P3/P4/P5."""
+    return efficientnet(h, w, "b0")
+
+
+def efficientnet(h=512, w=512, variant="b0"):
+    """EfficientNet-B<v> backbone, taps P3/P4/P5.
 
     MBConv: [1x1 expand -> SiLU] -> kxk depthwise -> SiLU -> SE -> 1x1 project
     (+ residual when stride 1 and c_in == c_out).  Symmetric k//2 padding
-    (reading R11).  Taps = outputs of stages 3/5/7 (reading R13).
+    (reading R11).  Taps = outputs of stages 3/5/7 (reading R13).  B4-B6 scale
+    every stage's channels by the width factor (multiples of 8) and its
+    repeats by ceil(depth * repeats); the SE width is a quarter of the block's
+    input channels, as in B0.
     """
-    n = Net(3, h, w, "efficientnet_b0")
-    x = n.silu(n.conv(-1, 32, 3, 2, 1, smooth=SPATIAL_SMOOTH))
-    c = 32
+    width, depth = EFFNET_SCALE[variant]
+    n = Net(3, h, w, f"efficientnet_{variant}")
+    c = _round_filters(32, width)
+    x = n.silu(n.conv(-1, c, 3, 2, 1, smooth=SPATIAL_SMOOTH))
     stages = [  # expand, k, stride, c_out, repeats
         (1, 3, 1, 16, 1), (6, 3, 2, 24, 2), (6, 5, 2, 40, 2), (6, 3, 2, 80, 3),
         (6, 5, 1, 112, 3), (6, 5, 2, 192, 4), (6, 3, 1, 320, 1)]
     for si, (e, k, s, co, rep) in enumerate(stages):
+        co = _round_filters(co, width)
+        rep = int(math.ceil(depth * rep))
         for r in range(rep):
             stride = s if r == 0 else 1
             inp = x
