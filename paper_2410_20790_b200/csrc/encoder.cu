@@ -72,6 +72,12 @@ struct LayerRT {
     int b_ybf = -1;           // bf16 shadow of y0 (BF16 mode: feeds a tcgen05 conv in dense mode)
     int alias_rows_of = -1;   // rows / slot / pbase borrowed from another tensor
     int64_t rows_cap = 0;     // rows excluding the zero row
+    bool rowmap = false;      // CONV 1x1/s1/p0: output rows in the input's row layout, A row r = input row r
+                              // (no dilation / scan / gather; reading R26 tiles of the input layout)
+    bool zero_gaps = false;   // site: also writes zero rows at touched-but-not-emitted slots (a rowmap
+                              // conv reads its layout's rows as a plain matrix)
+    bool bf_only = false;     // BF16 mode: the dense output is kept only as its bf16 shadow (every
+                              // consumer is a tensor-core conv reading the shadow; SE layers)
 };
 
 struct LaunchRec {
@@ -353,6 +359,47 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 cv.dw_site = i;
             }
     }
+    // 1x1/s1 convs in the input's row layout (rowmap): the layout must have no
+    // stale rows at touched-but-not-emitted slots -- input site, convs, adds
+    // have none; ReLU / SiLU / SE sites are asked to zero theirs (zero_gaps);
+    // maxpool layouts are not used
+    {
+        const char *nr = getenv("ST_NO_ROWMAP");   // A/B switch
+        if (!(nr && nr[0] == '1'))
+            for (int i = 0; i < n; i++) {
+                LayerRT &l = e->L[i];
+                if (l.kind != ST_CONV || l.depthwise || l.spec.groups != 1 || l.spec.k_h != 1 || l.spec.k_w != 1 ||
+                    l.spec.s_h != 1 || l.spec.s_w != 1 || l.spec.p_h != 0 || l.spec.p_w != 0 || l.src < 0)
+                    continue;
+                int o = l.src;
+                while (o >= 0 && e->L[o].kind == ST_OUTPUT) o = e->L[o].src;
+                if (o < 0) continue;
+                // the layout's owner chain: sites / rowmap convs borrow their source's layout
+                bool ok = true;
+                for (int t = o; t >= 0;) {
+                    const LayerRT &q = e->L[t];
+                    if (q.kind == ST_MAXPOOL || q.fused_pool >= 0) { ok = false; break; }
+                    if (q.kind == ST_RELU || q.kind == ST_SILU || (q.kind == ST_CONV && q.rowmap)) {
+                        t = q.src;
+                        while (t >= 0 && e->L[t].kind == ST_OUTPUT) t = e->L[t].src;
+                        continue;
+                    }
+                    break;
+                }
+                if (!ok) continue;
+                l.rowmap = true;
+                for (int t = o; t >= 0;) {   // every site on the chain zero-fills its gaps
+                    LayerRT &q = e->L[t];
+                    if (q.kind == ST_RELU || q.kind == ST_SILU || q.kind == ST_SE) q.zero_gaps = true;
+                    if (q.kind == ST_RELU || q.kind == ST_SILU || (q.kind == ST_CONV && q.rowmap)) {
+                        t = q.src;
+                        while (t >= 0 && e->L[t].kind == ST_OUTPUT) t = e->L[t].src;
+                        continue;
+                    }
+                    break;
+                }
+            }
+    }
     // ---- weights (K-major repack: wk[(dy*kw+dx)*cin_g + ci][co], reading R18)
     int64_t wfloats = 0;
     for (auto &l : e->L)
@@ -479,6 +526,17 @@ static int64_t cap_for(const st_encoder *e, int idx, int64_t full) {
     return full;
 }
 
+// the tensor whose slot / pbase (row layout) a layer's delta tensor uses:
+// sites and rowmap convs borrow their source's layout; n = the input site
+static int layout_owner(const st_encoder *e, int t) {
+    while (t >= 0) {
+        const LayerRT &l = e->L[t];
+        if (l.kind == ST_OUTPUT || l.kind == ST_RELU || l.kind == ST_SILU || (l.kind == ST_CONV && l.rowmap)) t = l.src;
+        else return t;
+    }
+    return (int)e->L.size();
+}
+
 static st_status plan(st_encoder *e) {
     const int n = (int)e->L.size();
     const int64_t B = e->B, F = e->F;
@@ -489,6 +547,19 @@ static st_status plan(st_encoder *e) {
         l.b_y0 = l.b_act = l.b_slot = l.b_pbase = l.b_rows = l.b_ridx = l.b_out = l.b_ybf = l.b_se = -1;
         l.alias_rows_of = -1;
         l.sx[0] = l.sx[1] = l.sy[0] = l.sy[1] = l.spy = -1;
+    }
+    // SE outputs whose every consumer is a tensor-core conv (the 1x1 project
+    // conv of an MBConv block) keep only the bf16 shadow of their dense output
+    for (int i = 0; i < n; i++) {
+        LayerRT &l = e->L[i];
+        l.bf_only = false;
+        if (l.kind != ST_SE || !e->bf || e->cfg.debug_retain || e->cfg.streaming || l.n_consumers == 0) continue;
+        bool ok = true;
+        for (int j = i + 1; j < n; j++) {
+            const LayerRT &c = e->L[j];
+            if (c.src == i || (c.kind == ST_ADD && c.src2 == i)) ok = ok && c.kind == ST_CONV && c.tc;
+        }
+        l.bf_only = ok;
     }
     auto add = [&](int64_t bytes, int first, int last) {
         Buf b;
@@ -532,7 +603,15 @@ static st_status plan(st_encoder *e) {
             l.b_out = add(B * (F + 1) * N * l.C * 4, 0, END);
             continue;
         }
-        l.b_y0 = add(B * N * l.C * 4, tdef, tlast);
+        l.b_y0 = l.bf_only ? -1 : add(B * N * l.C * 4, tdef, tlast);
+        if (l.bf_only) l.b_ybf = add(B * N * l.C * 2, tdef, tlast);
+        if (l.kind == ST_CONV && l.rowmap) {
+            // rows in the input's layout (same capacity); frame words borrowed
+            const int o = layout_owner(e, l.src);
+            l.rows_cap = o == n ? e->in_rows_cap : e->L[o].rows_cap;
+            l.b_rows = add((l.rows_cap + 1) * l.C * ES, tdef, tlast);
+            continue;
+        }
         l.b_act = add(B * N * 4, tdef, tlast);
         l.rows_cap = cap_for(e, i, B * F * N);
         switch (l.kind) {
@@ -573,7 +652,7 @@ static st_status plan(st_encoder *e) {
         if (c.kind != ST_CONV || !c.tc || c.src < 0) continue;
         int o = c.src;
         while (o >= 0 && e->L[o].kind == ST_OUTPUT) o = e->L[o].src;
-        if (o < 0 || e->L[o].b_y0 < 0 || e->L[o].b_ybf >= 0) continue;
+        if (o < 0 || e->L[o].b_y0 < 0 || e->L[o].b_ybf >= 0) continue;   // (bf_only: shadow already planned)
         const LayerRT &ol = e->L[o];
         const Buf &yb = e->bufs[ol.b_y0];
         e->L[o].b_ybf = add(B * (int64_t)ol.H * ol.W * ol.C * 2, yb.first, yb.last);
@@ -581,18 +660,24 @@ static st_status plan(st_encoder *e) {
     // aliases extend the lifetime of the borrowed buffers
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
-        if (l.alias_rows_of < 0 && !(l.kind == ST_RELU || l.kind == ST_SILU)) continue;
+        const bool rm = l.kind == ST_CONV && l.rowmap;
+        if (l.alias_rows_of < 0 && !(l.kind == ST_RELU || l.kind == ST_SILU) && !rm) continue;
         const int tlast = std::max(t_of(i), l.n_consumers ? t_of(l.last_consumer) : t_of(i));
         int s = l.src;
+        bool rows_too = !rm;   // a rowmap conv borrows frame words only
         while (true) {   // walk to the tensor that owns slot/pbase (and maybe rows)
+            while (s >= 0 && e->L[s].kind == ST_OUTPUT) s = e->L[s].src;
             if (s < 0) {
-                for (int id : {e->in_act, e->in_pbase, e->in_rows}) e->bufs[id].last = std::max(e->bufs[id].last, tlast);
+                for (int id : {e->in_act, e->in_pbase}) e->bufs[id].last = std::max(e->bufs[id].last, tlast);
+                if (rows_too) e->bufs[e->in_rows].last = std::max(e->bufs[e->in_rows].last, tlast);
                 break;
             }
             LayerRT &o = e->L[s];
-            for (int id : {o.b_act, o.b_slot, o.b_pbase, o.b_rows})
+            for (int id : {o.b_act, o.b_slot, o.b_pbase})
                 if (id >= 0) e->bufs[id].last = std::max(e->bufs[id].last, tlast);
+            if (rows_too && o.b_rows >= 0) e->bufs[o.b_rows].last = std::max(e->bufs[o.b_rows].last, tlast);
             if (o.kind == ST_RELU || o.kind == ST_SILU) { s = o.src; continue; }
+            if (o.kind == ST_CONV && o.rowmap) { s = o.src; rows_too = false; continue; }
             break;
         }
     }
@@ -804,6 +889,11 @@ static DView view_of(const st_encoder *e, int t) {
     }
     const LayerRT &l = e->L[t];
     if (l.kind == ST_OUTPUT) return view_of(e, l.src);
+    if (l.kind == ST_CONV && l.rowmap) {   // the input's frame words and row layout, own rows
+        DView s = view_of(e, l.src);
+        s.rows = e->ptr(l.b_rows);
+        return s;
+    }
     v.act = e->p<uint32_t>(l.b_act);
     if (l.kind == ST_RELU || l.kind == ST_SILU) {
         DView s = view_of(e, l.src);
@@ -1014,7 +1104,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
     auto export_words = [&](int layer) {
         if (!exporting) return;
         const int64_t Nl = layer < 0 ? Nin : (int64_t)e->L[layer].H * e->L[layer].W;
-        const uint32_t *src = layer < 0 ? e->p<uint32_t>(e->in_act) : e->p<uint32_t>(e->L[layer].b_act);
+        const uint32_t *src = view_of(e, layer).act;
         cudaMemcpyAsync(e->exp_words + e->exp_off[layer + 1], src + (int64_t)e->exp_chunk * Nl, Nl * 4,
                         cudaMemcpyDeviceToDevice, s);
     };
@@ -1064,6 +1154,25 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             if (l.b_ybf >= 0 && !cont)
                 LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
             if (F == 0) break;
+            if (l.rowmap) {   // 1x1/s1: a plain GEMM over the rows of the input's layout
+                zero_row(l.b_rows, l.C);
+                c.dense = false;
+                c.rnd_a = false;
+                c.bf = bf;
+                c.a = in;
+                c.rowmap = true;
+                c.ridx = nullptr;
+                c.F = F;
+                c.ddelta = nullptr;
+                c.m_dev = e->totals + layout_owner(e, l.src);
+                c.m_cap = l.rows_cap;
+                c.out = e->ptr(l.b_rows);
+                c.act_out = nullptr;
+                c.act_bf = nullptr;
+                LAUNCH(e, l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE, i, s,
+                       l.tc ? launch_conv_tc(c, l.tmap, s) : launch_conv_f32(c, s));
+                break;
+            }
             uint32_t *act = e->p<uint32_t>(l.b_act);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_DILATE, i, s, launch_dilate(in.act, B, l.geo, act, s));
@@ -1096,6 +1205,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 d.site_act = e->p<uint32_t>(r.b_act);
                 d.site_rows = const_cast<void *>(view_of(e, l.dw_site).rows);
                 d.conv_rows = r.b_rows >= 0 ? e->ptr(l.b_rows) : nullptr;   // own site rows: keep the conv's too
+                d.zero_gaps = r.zero_gaps;
                 LAUNCH(e, KC_DW_SITE, i, s, launch_dwconv_site(c, d, s));
                 break;
             }
@@ -1136,7 +1246,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             if (l.fused_dw < 0)                           // else: ran inside the conv's pass
                 LAUNCH(e, KC_SITE_PW, i, s,
                    launch_site_pointwise(in, x_init, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
-                                         e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), sst, s));
+                                         e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), sst, s, l.zero_gaps));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
@@ -1242,9 +1352,8 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             LAUNCH(e, KC_SE_SUMS, i, s,
                    launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
                                       thresholds + l.site, gate_tab, s_tab, refresh, s));
-            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), s));
-            if (l.b_ybf >= 0)
-                LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
+            LAUNCH(e, KC_SE_SUMS, i, s,
+                   launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), ybf_of(e, i), s));
             if (F == 0) break;
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
@@ -1253,7 +1362,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             zero_row(l.b_rows, l.C);
             LAUNCH(e, KC_SE, i, s,
                    launch_se_site(in, x_src, s_tab, B, (int)N, l.C, F, thresholds + l.site, bf, slot, pb,
-                                  e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s));
+                                  e->p<uint32_t>(l.b_act), e->ptr(l.b_rows), s, l.zero_gaps));
             LAUNCH(e, KC_COUNTS, i, s,
                    launch_frame_counts(e->p<uint32_t>(l.b_act), B, (int)N, e->counts + l.site * 32, cstride,
                                        e->site_sum + l.site, nullptr, s));
@@ -1338,7 +1447,7 @@ extern "C" st_status st_get_layer_counts(st_encoder *e, int64_t *rows_in, int64_
     for (int i = 0; i < n; i++) {
         const LayerRT &l = e->L[i];
         int64_t out = 0;
-        if (l.kind == ST_CONV) out = tot[i];
+        if (l.kind == ST_CONV) out = l.rowmap ? (int64_t)h[3 * i] : (int64_t)tot[i];   // rowmap: the input's rows
         else if (is_site(l.kind)) out = ss[l.site];
         else if (l.kind == ST_ADD) out = tot[i];
         if (rows_in) rows_in[i] = h[3 * i];

@@ -90,6 +90,7 @@ struct ConvCall {
     const void *ddelta;     // sparse, optional: dense per-frame input delta [B][F][Nin][Cin]
     int F;                  // diff frames (ddelta indexing)
     int sr, shift;          // stems: paired K layout (sr > 0), see conv_tc_small_layout
+    bool rowmap = false;    // sparse 1x1/s1: M row r = input row r + 1 -> output row r + 1 (no ridx)
     // B operand / output
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only
@@ -118,6 +119,7 @@ struct DwSite {
     uint32_t *site_act = nullptr;        // site emitted frame words [B][N]
     void *site_rows = nullptr;           // site emitted rows, in the conv's row layout
     void *conv_rows = nullptr;           // optional (debug_retain): the conv's own delta rows
+    bool zero_gaps = false;              // zero rows at touched, not emitted slots (rowmap consumer)
 };
 bool dwconv_site_fusable(const Geo &g);
 void launch_dwconv_site(const ConvCall &c, const DwSite &d, cudaStream_t s);
@@ -166,8 +168,11 @@ struct SiteState {
     float *ry_save = nullptr;        //                     ReLU y_acc at end
 };
 // pointwise site: emitted rows written into out_rows at the input slots
+// zero_gaps: also write zero rows at touched frames that were not emitted
+// (the layout is read as a plain matrix by a rowmap 1x1 conv)
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
-                           uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s);
+                           uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s,
+                           bool zero_gaps = false);
 // maxpool site: touched layout (t_slot, t_pbase) = dilation of in.act
 void launch_site_maxpool(DView in, const float *x0, int B, const Geo &g, const float *theta, bool bf,
                          const uint32_t *t_slot, const int32_t *t_pbase, uint32_t *out_act, void *out_rows,
@@ -191,10 +196,13 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                         const float *b1, const float *w2, const float *b2, const float *theta, float *gate_tab,
                         float *s_tab, uint32_t *refresh, cudaStream_t s);
-void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s);
+// y (fp32) and ybf (bf16 shadow) each nullable
+void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, void *ybf,
+                           cudaStream_t s);
 void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N, uint32_t *slot, cudaStream_t s);
 void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, const float *theta, bool bf,
-                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s);
+                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s,
+                    bool zero_gaps = false);
 // Accumulation at a tap: out[b][t][N][C], t = 0..n_diff (frame 0 = y0, the
 // start state [B][N][C]); o_save (streaming, nullable, may alias y0): the
 // last frame's output, the start of the next call

@@ -59,7 +59,9 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
             const int m = i / ntaps, tap = i - m * ntaps;
             const int r = m0 + m;
             int idx = -1;
-            if (r < M) {
+            if (r < M && c.rowmap) {   // 1x1/s1 in the input's row layout
+                idx = r + 1;
+            } else if (r < M) {
                 int b, q, t1 = 0;
                 if (c.dense) {
                     b = r / Nout;

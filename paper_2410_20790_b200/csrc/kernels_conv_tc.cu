@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             return (w < nwork && r < M) ? __ldg(c.ridx + r) : 0;
         };
         int code_nx = 0;
-        if (!DENSE) {
+        const bool rowmap = !DENSE && c.rowmap;   // 1x1/s1: tile row r reads input row r + 1
+        if (!DENSE && !rowmap) {
             fetch_taps(cid, code_of(cid));
             code_nx = code_of(cid + ncl);
         }
@@ -443,6 +444,9 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                         if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) tapidx[t] = b * Nin + iy * g.Win + ix;
                     }
                 }
+            } else if (rowmap) {
+#pragma unroll
+                for (int t = 0; t < TAPS; t++) tapidx[t] = (t == 0 && rv) ? r + 1 : -1;
             } else {
                 // this tile's lookups (issued a tile ago) -> delta-row index per tap (-1 = zero)
 #pragma unroll

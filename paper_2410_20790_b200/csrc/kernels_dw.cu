@@ -395,6 +395,9 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_site(ConvCall c, DwSite d) {
                 }
                 if (c0 < C) row_store<T, 8>(SR + row * C, c0, C, full, cand);
                 emit |= 1u << t1;
+            } else if (d.zero_gaps && c0 < C) {   // a rowmap conv reads this slot as a row
+                const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                row_store<T, 8>(SR + row * C, c0, C, full, z);
             }
         };
         if constexpr (PAIR) {
@@ -463,6 +466,10 @@ __global__ void __launch_bounds__(32 * DWS_WARPS, 1) k_dwconv_site_wide(ConvCall
             RowIO<T, 8>::store(SR + row * C + c0, cand);
         }
     };
+    auto zero_row = [&](int64_t row) {   // a rowmap conv reads non-emitted slots as rows
+        const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c0 = lane * 8; c0 < C; c0 += 256) RowIO<T, 8>::store(SR + row * C + c0, z);
+    };
     for (int64_t bq = (int64_t)blockIdx.x * DWS_WARPS + wid; bq < BNo; bq += (int64_t)gridDim.x * DWS_WARPS) {
         uint32_t w = __ldg(d.out_act + bq);
         if (!w) {
@@ -518,6 +525,8 @@ __global__ void __launch_bounds__(32 * DWS_WARPS, 1) k_dwconv_site_wide(ConvCall
             if (gmax<32>(mx, 0xffffffffu) > theta) {   // truncation
                 emit_row(orow);
                 emit |= 1u << tA;
+            } else if (d.zero_gaps) {
+                zero_row(orow);
             }
             orow++;
             if (tB < 0) continue;
@@ -537,6 +546,8 @@ __global__ void __launch_bounds__(32 * DWS_WARPS, 1) k_dwconv_site_wide(ConvCall
             if (gmax<32>(mx, 0xffffffffu) > theta) {
                 emit_row(orow);
                 emit |= 1u << tB;
+            } else if (d.zero_gaps) {
+                zero_row(orow);
             }
             orow++;
         }

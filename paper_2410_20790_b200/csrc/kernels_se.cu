@@ -12,6 +12,8 @@
 // frame's delta rows; (ii) one CTA per chunk runs the sequential gate
 // schedule (frames are sequential, channels parallel); (iii) the pixel loop
 // with x_acc / y_acc in registers, like the pointwise site.
+#include <cstdlib>
+
 #include <math_constants.h>
 
 #include "rowio.cuh"
@@ -161,6 +163,91 @@ __global__ void __launch_bounds__(256) k_se_delta_sums_v(DView in, int N, int C,
             if (acc[i] != 0.0) atomicAdd(dsum + ((int64_t)b * F + t) * C + c0 + i, acc[i]);
 }
 
+// ---- (i-b'') the same sums over ACTIVE pixels only: the CTA compacts the
+// active pixels of each 256-pixel batch of its range (frame word, slot, row
+// base) into shared memory; thread (replica, t, cg) walks every R-th entry
+// of the list and adds frame t's row (8 channels, one 16-byte load) of the
+// entries active at t into fp64 registers, several entries per batch in
+// flight; the R replica partials meet in shared memory at the end.  Threads
+// = R x F x (CS / 8) <= 256, so short chunks do not idle most of the CTA.
+template <class T>
+__global__ void __launch_bounds__(256) k_se_delta_sums_c(DView in, int N, int C, int F, int ppb, int CS, int R,
+                                                         double *__restrict__ dsum) {
+    st_pdl_enter();
+    __shared__ uint32_t m_act[256], m_sl[256];
+    __shared__ int32_t m_row[256];
+    __shared__ int n_list;
+    extern __shared__ double part[];   // [R][F][CS]
+    const T *rows = static_cast<const T *>(in.rows);
+    const int b = blockIdx.z, ncg = CS / 8;
+    const int per = F * ncg;
+    const int rep = threadIdx.x / per, rem = threadIdx.x - rep * per;
+    const int t = rem / ncg, cg = rem - t * ncg;
+    const int c0 = blockIdx.y * CS + cg * 8;
+    const bool mine = rep < R && c0 < C;   // C % 8 == 0
+    const uint32_t tbit = 1u << t;
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc[i] = 0.0;
+    const int p0 = blockIdx.x * ppb, p1 = min(N, p0 + ppb);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ int wcount[8];
+    for (int pb = p0; pb < p1; pb += 256) {
+        const int p = pb + threadIdx.x;
+        uint32_t a = 0;
+        const int64_t bp = (int64_t)b * N + p;
+        if (p < p1) a = __ldg(in.act + bp);
+        // ordered compaction of the batch's active pixels
+        const uint32_t bal = __ballot_sync(0xffffffffu, a != 0);
+        if (lane == 0) wcount[wid] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+        for (int w = 0; w < wid; w++) off += wcount[w];
+        if (a) {
+            const int k = off + __popc(bal & ((1u << lane) - 1u));
+            m_act[k] = a;
+            m_sl[k] = __ldg(in.slot + bp);
+            m_row[k] = 1 + __ldg(in.pbase + bp);
+        }
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < 8; w++) tot += wcount[w];
+            n_list = tot;
+        }
+        __syncthreads();
+        const int nl = n_list;
+        if (mine) {
+            for (int k0 = rep; k0 < nl; k0 += 4 * R) {
+                float v[4][8];
+                bool on[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int k = k0 + u * R;
+                    on[u] = k < nl && (m_act[k] & tbit);
+                    if (on[u]) RowIO<T, 8>::load(rows + (int64_t)(m_row[k] + __popc(m_sl[k] & lowmask(t))) * C + c0, v[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (on[u])
+#pragma unroll
+                        for (int i = 0; i < 8; i++) acc[i] += (double)v[u][i];
+            }
+        }
+        __syncthreads();   // list reused by the next batch
+    }
+    if (mine)
+#pragma unroll
+        for (int i = 0; i < 8; i++) part[((size_t)rep * F + t) * CS + cg * 8 + i] = acc[i];
+    __syncthreads();
+    for (int j = threadIdx.x; j < F * CS; j += blockDim.x) {
+        const int tt = j / CS, cc = blockIdx.y * CS + (j - tt * CS);
+        if (cc >= C) continue;
+        double sum = 0.0;
+        for (int r = 0; r < R; r++) sum += part[((size_t)r * F) * CS + j];
+        if (sum != 0.0) atomicAdd(dsum + ((int64_t)b * F + tt) * C + cc, sum);
+    }
+}
+
 // gate of one chunk from fp32 means m[C] (block-wide; hid/gate in smem)
 __device__ void se_gate_block(const float *m, int C, int H, const float *w1, const float *b1, const float *w2,
                               const float *b2, float *hid, float *gate) {
@@ -244,15 +331,18 @@ __global__ void __launch_bounds__(256) k_se_schedule(const float *__restrict__ g
 }
 
 // dense reference SE: y0 = x0 * s_tab[b][0]; grid (pixel blocks, chunk),
-// float4 over channels when C % 4 == 0
+// float4 over channels when C % 4 == 0.  y (fp32) and ybf (its bf16 shadow,
+// read by a tensor-core conv in dense mode) are each optional: an SE whose
+// consumers are all tensor-core convs gets only the shadow (BF16 mode)
 __global__ void k_se_dense_apply(const float *__restrict__ x, const float *__restrict__ s_tab, int N, int C, int F,
-                                 float *__restrict__ y) {
+                                 float *__restrict__ y, bf16 *__restrict__ ybf) {
     st_pdl_enter();
     const int b = blockIdx.y;
     const float *sb = s_tab + (int64_t)b * (F + 1) * C;
     const int64_t n = (int64_t)N * C;
     const float *xb = x + (int64_t)b * n;
-    float *yb = y + (int64_t)b * n;
+    float *yb = y ? y + (int64_t)b * n : nullptr;
+    bf16 *hb = ybf ? ybf + (int64_t)b * n : nullptr;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if ((C & 3) == 0) {
         const int64_t n4 = n >> 2;
@@ -260,16 +350,26 @@ __global__ void k_se_dense_apply(const float *__restrict__ x, const float *__res
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
             const int c = (int)(i % C4) * 4;
             const float4 v = __ldg(reinterpret_cast<const float4 *>(xb) + i);
+            const float4 sc = __ldg(reinterpret_cast<const float4 *>(sb + c));
             float4 o;
-            o.x = __fmul_rn(v.x, __ldg(sb + c));
-            o.y = __fmul_rn(v.y, __ldg(sb + c + 1));
-            o.z = __fmul_rn(v.z, __ldg(sb + c + 2));
-            o.w = __fmul_rn(v.w, __ldg(sb + c + 3));
-            reinterpret_cast<float4 *>(yb)[i] = o;
+            o.x = __fmul_rn(v.x, sc.x);
+            o.y = __fmul_rn(v.y, sc.y);
+            o.z = __fmul_rn(v.z, sc.z);
+            o.w = __fmul_rn(v.w, sc.w);
+            if (yb) reinterpret_cast<float4 *>(yb)[i] = o;
+            if (hb) {
+                uint2 u;
+                u.x = RowIO<bf16, 2>::pack(o.x, o.y);
+                u.y = RowIO<bf16, 2>::pack(o.z, o.w);
+                reinterpret_cast<uint2 *>(hb)[i] = u;
+            }
         }
     } else {
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-            yb[i] = __fmul_rn(xb[i], __ldg(sb + (int)(i % C)));
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+            const float o = __fmul_rn(xb[i], __ldg(sb + (int)(i % C)));
+            if (yb) yb[i] = o;
+            if (hb) hb[i] = __float2bfloat16_rn(o);
+        }
     }
 }
 
@@ -286,7 +386,8 @@ template <int G, int CPL, class T>
 __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restrict__ x0, const float *__restrict__ s_tab,
                                                  int N, int C, int F, int64_t BN, const float *__restrict__ theta_p,
                                                  const uint32_t *__restrict__ slot, const int32_t *__restrict__ pbase,
-                                                 uint32_t *__restrict__ out_act, T *__restrict__ out_rows) {
+                                                 uint32_t *__restrict__ out_act, T *__restrict__ out_rows,
+                                                 bool zero_gaps) {
     st_pdl_enter();
     const float theta = __ldg(theta_p);
     const T *rows = static_cast<const T *>(in.rows);
@@ -347,6 +448,11 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
                     }
                 }
                 emit |= 1u << t1;
+            } else if (zero_gaps) {   // a rowmap conv reads this slot as a row
+                const int64_t orow = obase + __popc(Tw & lowmask(t1));
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + G * i < C) str<T>(out_rows + orow * C + lane + G * i, 0.0f);
             }
         }
         if (lane == 0) out_act[bp] = emit;
@@ -364,7 +470,7 @@ __global__ void __launch_bounds__(256) k_se_site_v(DView in, const float *__rest
                                                    const float *__restrict__ s_tab, int N, int C, int F, int64_t BN,
                                                    const float *__restrict__ theta_p, const uint32_t *__restrict__ slot,
                                                    const int32_t *__restrict__ pbase, uint32_t *__restrict__ out_act,
-                                                   T *__restrict__ out_rows) {
+                                                   T *__restrict__ out_rows, bool zero_gaps) {
     st_pdl_enter();
     constexpr int P = CPL <= 8 ? 2 : 1;   // frames prefetched per batch (~16 values per lane)
     const float theta = __ldg(theta_p);
@@ -448,6 +554,11 @@ __global__ void __launch_bounds__(256) k_se_site_v(DView in, const float *__rest
                     if (c0 < C) row_store<T, CPL>(out_rows + (obase + __popc(Tw & lowmask(t1))) * (int64_t)C, c0, C,
                                                   full, cand);
                     emit |= 1u << t1;
+                } else if (zero_gaps && c0 < C) {   // a rowmap conv reads this slot as a row
+                    float z[CPL];
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) z[i] = 0.0f;
+                    row_store<T, CPL>(out_rows + (obase + __popc(Tw & lowmask(t1))) * (int64_t)C, c0, C, full, z);
                 }
             }
         }
@@ -469,7 +580,7 @@ __global__ void __launch_bounds__(32 * SE_WIDE_WARPS) k_se_site_wide(DView in, c
                                                                      const uint32_t *__restrict__ slot,
                                                                      const int32_t *__restrict__ pbase,
                                                                      uint32_t *__restrict__ out_act,
-                                                                     T *__restrict__ out_rows) {
+                                                                     T *__restrict__ out_rows, bool zero_gaps) {
     st_pdl_enter();
     extern __shared__ float sew_sm[];
     const float theta = __ldg(theta_p);
@@ -536,6 +647,10 @@ __global__ void __launch_bounds__(32 * SE_WIDE_WARPS) k_se_site_wide(DView in, c
                     RowIO<T, 8>::store(out_rows + orow * C + c0, e);
                 }
                 emit |= 1u << t1;
+            } else if (zero_gaps) {   // a rowmap conv reads this slot as a row
+                const int64_t orow = obase + __popc(Tw & lowmask(t1));
+                const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int c0 = lane * 8; c0 < C; c0 += 256) RowIO<T, 8>::store(out_rows + orow * C + c0, z);
             }
         }
         if (lane == 0) out_act[bp] = emit;
@@ -568,10 +683,11 @@ void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, in
     k_se_schedule<<<B, 256, smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
 }
 
-void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, cudaStream_t s) {
+void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, void *ybf,
+                           cudaStream_t s) {
     const int64_t n = (int64_t)N * C / ((C & 3) == 0 ? 4 : 1);
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16 / std::max(B, 1) + 1));
-    if (n > 0 && B > 0) k_se_dense_apply<<<dim3(gx, B), 256, 0, s>>>(x, s_tab, N, C, F, y);
+    if (n > 0 && B > 0) k_se_dense_apply<<<dim3(gx, B), 256, 0, s>>>(x, s_tab, N, C, F, y, static_cast<bf16 *>(ybf));
 }
 
 template <class T>
@@ -597,6 +713,14 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
         const int want = std::max(1, 296 / std::max(1, nsl * B));
         const int ppb = std::min(2048, std::max(256, (cdiv(N, want) + 255) / 256 * 256));
         dim3 grid(cdiv(N, ppb), cdiv(C, CS), B);
+        const int R = std::max(1, 256 / (F * (CS / 8)));   // replicas of the (t, cg) threads
+        const size_t sm = (size_t)R * F * CS * sizeof(double);
+        static const bool old = [] { const char *v = getenv("ST_SE_SUMS_DENSE"); return v && v[0] == '1'; }();
+        if (!old && sm <= 48 * 1024) {
+            if (bf) k_se_delta_sums_c<bf16><<<grid, 256, sm, s>>>(in, N, C, F, ppb, CS, R, dsum);
+            else k_se_delta_sums_c<float><<<grid, 256, sm, s>>>(in, N, C, F, ppb, CS, R, dsum);
+            return;
+        }
         if (bf) k_se_delta_sums_v<bf16><<<grid, 256, 0, s>>>(in, N, C, F, ppb, CS, dsum);
         else k_se_delta_sums_v<float><<<grid, 256, 0, s>>>(in, N, C, F, ppb, CS, dsum);
         return;
@@ -611,7 +735,8 @@ void launch_se_slots(const uint32_t *act, const uint32_t *refresh, int B, int N,
 }
 
 void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N, int C, int F, const float *theta, bool bf,
-                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s) {
+                    const uint32_t *slot, const int32_t *pbase, uint32_t *out_act, void *out_rows, cudaStream_t s,
+                    bool zero_gaps) {
     const int64_t BN = (int64_t)B * N;
     auto grid_for = [&](int G) {
         return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(BN * G, 256), 148 * 8));
@@ -623,7 +748,7 @@ void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N,
     {                                                                                                       \
         cudaFuncSetAttribute(k_se_site_wide<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
         k_se_site_wide<T><<<grid, 32 * SE_WIDE_WARPS, sm, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, \
-                                                              out_act, static_cast<T *>(out_rows));         \
+                                                              out_act, static_cast<T *>(out_rows), zero_gaps); \
     }
         ST_ROW_DISPATCH(bf, L_SEW);
 #undef L_SEW
@@ -632,7 +757,7 @@ void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N,
     if (C % 8 == 0 && C <= 1280) {   // vectorised blocked form
 #define L_SEV(G_, CPL_)                                                                                          \
     k_se_site_v<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \
-                                                          static_cast<T *>(out_rows))
+                                                          static_cast<T *>(out_rows), zero_gaps)
 #define SEV_CH                            \
     if (C <= 8) L_SEV(1, 8);              \
     else if (C <= 16) L_SEV(2, 8);        \
@@ -650,7 +775,7 @@ void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N,
     }
 #define L_SE(G_, CPL_)                                                                                      \
     k_se_site<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \
-                                                        static_cast<T *>(out_rows))
+                                                        static_cast<T *>(out_rows), zero_gaps)
 #define SE_CH                          \
     if (C <= 8) L_SE(8, 1);            \
     else if (C <= 16) L_SE(16, 1);     \

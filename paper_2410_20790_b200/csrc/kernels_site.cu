@@ -176,7 +176,7 @@ void launch_to_bf16(const float *x, void *ybf, int64_t n, cudaStream_t s) {
 template <int G, int CPL, int ACT, class T>
 __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restrict__ x0, int64_t BN, int C,
                                                  const float *__restrict__ theta_p, uint32_t *__restrict__ out_act,
-                                                 T *out_rows, SiteState sst) {
+                                                 T *out_rows, SiteState sst, bool zero_gaps) {
     st_pdl_enter();
     const float theta = __ldg(theta_p);
     constexpr int P = prefetch_depth(CPL);
@@ -260,6 +260,11 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
                     }
                     row_store<T, CPL>(out_rows + rws[j] * C, c0, C, full, cand);
                     emit |= 1u << t1s[j];
+                } else if (zero_gaps) {   // a rowmap conv reads this slot as a row
+                    float z[CPL];
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) z[i] = 0.0f;
+                    row_store<T, CPL>(out_rows + rws[j] * C, c0, C, full, z);
                 }
             }
         }
@@ -284,7 +289,7 @@ template <int ACT, class T>
 __global__ void __launch_bounds__(32 * PW_WIDE_WARPS) k_site_pw_wide(DView in, const float *__restrict__ x0, int64_t BN,
                                                                   int C, const float *__restrict__ theta_p,
                                                                   uint32_t *__restrict__ out_act, T *out_rows,
-                                                                  SiteState sst) {
+                                                                  SiteState sst, bool zero_gaps) {
     st_pdl_enter();
     extern __shared__ float pw_sm[];
     const float theta = __ldg(theta_p);
@@ -345,6 +350,9 @@ __global__ void __launch_bounds__(32 * PW_WIDE_WARPS) k_site_pw_wide(DView in, c
                     RowIO<T, 8>::store(out_rows + row * C + c0, cand);
                 }
                 emit |= 1u << t1;
+            } else if (zero_gaps) {   // a rowmap conv reads this slot as a row
+                const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int c0 = lane * 8; c0 < C; c0 += 256) RowIO<T, 8>::store(out_rows + row * C + c0, z);
             }
         }
         if (lane == 0) out_act[bp] = emit;
@@ -411,7 +419,7 @@ static int groups_grid(int64_t n_groups, int G) {
 }
 
 void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int act, const float *theta, bool bf,
-                           uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s) {
+                           uint32_t *out_act, void *out_rows, const SiteState &st, cudaStream_t s, bool zero_gaps) {
     const int64_t BN = (int64_t)B * N;
     if (C > 1280 && C % 8 == 0) {
         const size_t sm = (size_t)PW_WIDE_WARPS * 3 * C * sizeof(float);
@@ -420,7 +428,8 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
     {                                                                                                  \
         auto kf = k_site_pw_wide<ACT_, T>;                                                             \
         cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                \
-        kf<<<grid, 32 * PW_WIDE_WARPS, sm, s>>>(in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st); \
+        kf<<<grid, 32 * PW_WIDE_WARPS, sm, s>>>(in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st,   \
+                                                zero_gaps);                                                    \
     }
         ST_ROW_DISPATCH(bf, if (act == ACT_RELU) L_PWW(ACT_RELU) else if (sizeof(T) == 4) L_PWW(ACT_SILU) else L_PWW(ACT_SILU_FAST));
 #undef L_PWW
@@ -432,10 +441,11 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
         const int grid = groups_grid(BN, G_);                                                          \
         if (act == ACT_RELU)                                                                           \
             k_site_pw<G_, CPL_, ACT_RELU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
-                                                                  static_cast<T *>(out_rows), st);     \
+                                                                  static_cast<T *>(out_rows), st,      \
+                                                                  zero_gaps);                          \
         else /* SiLU: exact (double exp) in FP32 mode, fast in BF16 mode */                            \
             k_site_pw<G_, CPL_, (sizeof(T) == 4 ? ACT_SILU : ACT_SILU_FAST), T><<<grid, 256, 0, s>>>(  \
-                in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st);                        \
+                in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st, zero_gaps);             \
     }
     ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_PW));
 #undef L_PW

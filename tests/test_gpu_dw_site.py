@@ -87,3 +87,67 @@ def test_fused_dw_site_vs_oracle_fp32(C, k, s, act, h, w):
     for b in range(fr.shape[0]):
         compare_chunk(enc, net, fr[b], th, b, exact=(act == "relu"))
     enc.close()
+
+
+# ---- 1x1/s1 convs in the input's row layout ("rowmap"): no dilation, scan or
+# gather; the sites that feed them zero their touched-but-not-emitted slots
+def _bottleneck_net(seed):
+    """ResNet-style bottleneck and MBConv-style blocks: 1x1 convs reading a
+    ReLU, an SE, an ADD and another 1x1 conv."""
+    n = Net(3, 20, 28, "rowmap")
+    x = n.relu(n.conv(-1, 32, 3, 1, 1))
+    y = n.relu(n.conv(x, 16, 1, 1, 0))        # 1x1 on a ReLU (in place in the stem conv's layout)
+    y = n.relu(n.conv(y, 16, 3, 1, 1))
+    y = n.conv(y, 32, 1, 1, 0)                # 1x1 on a ReLU
+    x = n.relu(n.add(y, x))
+    z = n.conv(x, 24, 1, 1, 0)                # 1x1 on a ReLU of an ADD
+    z = n.conv(z, 24, 1, 1, 0)                # 1x1 on a 1x1 conv
+    z = n.silu(z)
+    z = n.se(z, 6)
+    z = n.conv(z, 32, 1, 1, 0)                # 1x1 on an SE (MBConv project)
+    n.output(n.add(z, x))
+    init_weights(n, seed)
+    return n
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("model", ["bottleneck", "effnet"])
+def test_rowmap_matches_gathered(model, precision, monkeypatch):
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    if model == "effnet":
+        net = W.models.efficientnet_b0(64, 96)
+        init_weights(net, 31)
+        h, w = 64, 96
+    else:
+        net = _bottleneck_net(7)
+        h, w = 20, 28
+    fr = torch.from_numpy(frames_for(h, w, 77)).cuda()
+    outs = {}
+    for mode in ("rowmap", "gathered"):
+        if mode == "gathered":
+            monkeypatch.setenv("ST_NO_ROWMAP", "1")
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.03, 0.0):
+            for _ in range(2):   # eager, then graph replay
+                enc.encode_reference(fr[:, 0])
+                enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs[mode] = res
+        enc.close()
+    for (og, cg), (oe, ce) in zip(outs["rowmap"], outs["gathered"]):
+        assert np.array_equal(cg, ce), "per-site per-frame counts"
+        for a, b in zip(og, oe):
+            assert np.array_equal(a, b), f"tap outputs differ (max {np.abs(a - b).max():.3e})"
+
+
+def test_rowmap_vs_oracle_fp32():
+    net = _bottleneck_net(9)
+    fr = frames_for(20, 28, 78)
+    th = 0.03
+    enc, _ = gpu_run(net, fr, th)
+    for b in range(fr.shape[0]):
+        compare_chunk(enc, net, fr[b], th, b, exact=False)
+    enc.close()
