@@ -57,6 +57,8 @@ struct LayerRT {
     int fused_relu = -1;      // MAXPOOL: the ReLU site folded into this layer's pass
     int fused_dw = -1;        // ReLU/SiLU: the depthwise conv whose pass runs this site (N2)
     int dw_site = -1;         // depthwise CONV: the pointwise site its sparse pass runs
+    int act_site = -1;        // non-depthwise CONV: the ReLU/SiLU whose dense output its epilogue writes
+    int act_of = -1;          // ReLU/SiLU: the conv that writes its dense output
     // streaming state (N1, persistent): pointwise site sx[0]/sy[0] in place;
     // maxpool sx[0..1] ping-pong x_acc + spy y_acc; fused pool (on the pool
     // layer) sx[0..1] ReLU x_acc, sy[0..1] ReLU y_acc, spy pool y_acc; OUTPUT sx[0]
@@ -65,6 +67,11 @@ struct LayerRT {
     float *wk = nullptr, *bias = nullptr;
     uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
     alignas(64) unsigned char tmap[128] = {};   // CUtensorMap of wbf (tc layers)
+    // 1x1/s1 tc convs: A-operand TMA maps over contiguous rows (dense: the
+    // input's bf16 shadow; sparse: the rowmap layout's rows), re-encoded per plan
+    alignas(64) unsigned char tmap_ad[128] = {};
+    alignas(64) unsigned char tmap_as[128] = {};
+    bool tma_ad = false, tma_as = false;
     float *se_w1 = nullptr, *se_b1 = nullptr, *se_w2 = nullptr, *se_b2 = nullptr;   // SE MLP
     int b_se = -1;            // SE scratch: sum0 [B][C] f64 | dsum [B][F][C] f64 | s_tab [B][F+1][C] | refresh [B]
     // buffer ids (-1 = none / alias)
@@ -225,6 +232,7 @@ static void prof_end(st_encoder *e, cudaStream_t s) {
 // ------------------------------------------------------------------- create
 static st_status plan(st_encoder *e);
 static st_status alloc_fixed(st_encoder *e);
+static void encode_act_maps(st_encoder *e);
 
 extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_layer_spec *layers, int32_t n,
                                        st_encoder **out) {
@@ -359,6 +367,18 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 cv.dw_site = i;
             }
     }
+    // conv -> ReLU / SiLU (its only consumer): the conv's dense epilogue also
+    // writes the site's dense output (no separate activation pass); not for a
+    // ReLU fused into a maxpool (the pool's dense pass applies it) or streaming
+    if (!cfg->streaming)
+        for (int i = 0; i < n; i++) {
+            LayerRT &r = e->L[i];
+            if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0 || r.fused_dw >= 0 || r.fused_pool >= 0) continue;
+            LayerRT &cv = e->L[r.src];
+            if (cv.kind != ST_CONV || cv.depthwise || cv.n_consumers != 1) continue;
+            cv.act_site = i;
+            r.act_of = r.src;
+        }
     // 1x1/s1 convs in the input's row layout (rowmap): the layout must have no
     // stale rows at touched-but-not-emitted slots -- input site, convs, adds
     // have none; ReLU / SiLU / SE sites are asked to zero theirs (zero_gaps);
@@ -378,7 +398,10 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 bool ok = true;
                 for (int t = o; t >= 0;) {
                     const LayerRT &q = e->L[t];
-                    if (q.kind == ST_MAXPOOL || q.fused_pool >= 0) { ok = false; break; }
+                    // maxpool layouts hold the footprint dilation; an SE layout holds
+                    // every pixel of a gate-refresh frame (R8): both can be far denser
+                    // than the emitted rows, so those convs keep the gathered M list
+                    if (q.kind == ST_MAXPOOL || q.kind == ST_SE || q.fused_pool >= 0) { ok = false; break; }
                     if (q.kind == ST_RELU || q.kind == ST_SILU || (q.kind == ST_CONV && q.rowmap)) {
                         t = q.src;
                         while (t >= 0 && e->L[t].kind == ST_OUTPUT) t = e->L[t].src;
@@ -507,6 +530,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     e->cap_fit.assign(n + 1, -1);
     st_status r = plan(e.get());
     if (r == ST_OK) r = alloc_fixed(e.get());
+    if (r == ST_OK) encode_act_maps(e.get());
     if (r != ST_OK) {
         cudaFree(e->weights_mem);
         return r;
@@ -703,6 +727,12 @@ static st_status plan(st_encoder *e) {
     }
     // a depthwise conv's pass writes its fused site's dense output (dense
     // epilogue) and frame words (sparse pass) at the conv's step time
+    for (int i = 0; i < n; i++)
+        if (e->L[i].act_of >= 0) {
+            const int tc = t_of(e->L[i].act_of);
+            for (int id : {e->L[i].b_y0, e->L[i].b_ybf})
+                if (id >= 0) e->bufs[id].first = std::min(e->bufs[id].first, tc);
+        }
     for (int i = 0; i < n; i++)
         if (e->L[i].fused_dw >= 0) {
             const int tc = t_of(e->L[i].fused_dw);
@@ -919,6 +949,26 @@ static const float *dense_of(const st_encoder *e, int t) {
     const LayerRT &l = e->L[t];
     if (l.kind == ST_OUTPUT) return dense_of(e, l.src);
     return e->p<float>(l.b_y0);
+}
+
+// A-operand TMA maps of the 1x1/s1 tensor-core convs for the current arena
+static void encode_act_maps(st_encoder *e) {
+    const char *nt = getenv("ST_NO_TMA_A");   // A/B switch
+    const bool off = nt && nt[0] == '1';
+    for (int i = 0; i < (int)e->L.size(); i++) {
+        LayerRT &l = e->L[i];
+        l.tma_ad = l.tma_as = false;
+        if (off || l.kind != ST_CONV || !l.tc || l.src < 0 || l.spec.k_h != 1 || l.spec.k_w != 1 || l.spec.s_h != 1 ||
+            l.spec.s_w != 1 || l.spec.p_h != 0 || l.spec.p_w != 0)
+            continue;
+        const int Cin = l.geo.Cin;
+        const void *bfsrc = dense_bf_of(e, l.src);
+        if (bfsrc) l.tma_ad = make_act_tmap(l.tmap_ad, bfsrc, (int64_t)e->B * l.geo.Hin * l.geo.Win, Cin);
+        if (l.rowmap) {
+            const char *rows = static_cast<const char *>(view_of(e, l.src).rows);
+            if (rows) l.tma_as = make_act_tmap(l.tmap_as, rows + (size_t)Cin * e->esz, l.rows_cap, Cin);
+        }
+    }
 }
 
 static int64_t rows_cap_of(const st_encoder *e, int t) {
@@ -1139,18 +1189,20 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             c.bias = l.bias;
             c.rnd_a = bf;   // BF16 mode: the dense A operand is bf16-rounded (R22-BF16)
             c.out = e->p<float>(l.b_y0);
-            if (l.dw_site >= 0) {   // the site's dense output from the same epilogue
-                const LayerRT &r = e->L[l.dw_site];
+            if (l.dw_site >= 0 || l.act_site >= 0) {   // the site's dense output from the same epilogue
+                const int si = l.dw_site >= 0 ? l.dw_site : l.act_site;
+                const LayerRT &r = e->L[si];
                 c.act_out = e->p<float>(r.b_y0);
-                c.act_bf = ybf_of(e, l.dw_site);
+                c.act_bf = ybf_of(e, si);
                 c.act_kind = r.kind == ST_RELU ? ACT_RELU : bf ? ACT_SILU_FAST : ACT_SILU;
             }
             if (!cont)
                 LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
                        l.depthwise  ? launch_dwconv_f32(c, s)
-                       : l.tc       ? launch_conv_tc(c, l.tmap, s)
+                       : l.tc       ? (c.tma_a = l.tma_ad, launch_conv_tc(c, l.tmap, s, l.tma_ad ? l.tmap_ad : nullptr))
                        : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
                                     : launch_conv_f32(c, s));
+            c.tma_a = false;
             if (l.b_ybf >= 0 && !cont)
                 LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
             if (F == 0) break;
@@ -1169,8 +1221,10 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 c.out = e->ptr(l.b_rows);
                 c.act_out = nullptr;
                 c.act_bf = nullptr;
+                c.tma_a = l.tma_as;
                 LAUNCH(e, l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE, i, s,
-                       l.tc ? launch_conv_tc(c, l.tmap, s) : launch_conv_f32(c, s));
+                       l.tc ? launch_conv_tc(c, l.tmap, s, l.tma_as ? l.tmap_as : nullptr) : launch_conv_f32(c, s));
+                c.tma_a = false;
                 break;
             }
             uint32_t *act = e->p<uint32_t>(l.b_act);
@@ -1223,7 +1277,8 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             const int dense_kind = (act_kind == ACT_SILU && bf) ? ACT_SILU_FAST : act_kind;
             // a fused ReLU's dense output is read only by the pool's dense pass,
             // which applies the ReLU itself (kept when streaming or debugging)
-            const bool skip_dense = (l.fused_pool >= 0 && !strm && !e->cfg.debug_retain) || l.fused_dw >= 0;
+            const bool skip_dense = (l.fused_pool >= 0 && !strm && !e->cfg.debug_retain) || l.fused_dw >= 0 ||
+                                    l.act_of >= 0;
             if (!cont && !skip_dense)
                 LAUNCH(e, KC_DENSE_MISC, i, s,
                        launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
@@ -1646,7 +1701,9 @@ extern "C" st_status st_encoder_fit_capacity(st_encoder *e, double headroom) {
     e->arena = nullptr;
     e->arena_bytes = 0;
     e->last_ndiff = -1;   // the last step's results are gone
-    return plan(e);
+    st_status r = plan(e);
+    if (r == ST_OK) encode_act_maps(e);
+    return r;
 }
 
 extern "C" st_status st_memory_report(const st_encoder *e, int64_t *persistent, int64_t *peak, int64_t *arena) {

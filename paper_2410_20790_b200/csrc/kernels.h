@@ -91,6 +91,7 @@ struct ConvCall {
     int F;                  // diff frames (ddelta indexing)
     int sr, shift;          // stems: paired K layout (sr > 0), see conv_tc_small_layout
     bool rowmap = false;    // sparse 1x1/s1: M row r = input row r + 1 -> output row r + 1 (no ridx)
+    bool tma_a = false;     // tcgen05, 1x1/s1 with contiguous A rows: A tiles by TMA (launch_conv_tc tmap_a)
     // B operand / output
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only
@@ -129,7 +130,9 @@ void launch_dwconv_site(const ConvCall &c, const DwSite &d, cudaStream_t s);
 bool conv_tc_eligible(const Geo &g);
 int conv_tc_cpad(int cin);   // per-tap channel stride of the bf16 weight K layout (zero padded)
 bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout);
-void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s);
+void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s, const void *tmap_a = nullptr);
+// A-operand TMA map of a 1x1/s1 conv over a [rows][C] bf16 matrix (c.tma_a)
+bool make_act_tmap(void *tmap_out, const void *base, int64_t rows, int C);
 // stems on tensor cores: the network input (c_in <= 4); sparse mode reads the
 // 4-channel-padded dense input delta (c.ddelta), dense mode the fp32 frames
 bool conv_tc_small_eligible(const Geo &g);

@@ -208,7 +208,15 @@ __global__ void __launch_bounds__(CNT, 2) k_conv_f32(ConvCall c) {
 #pragma unroll
                 for (int j = 0; j < TN; j++) {
                     const int n = n0 + tx * TN + j;
-                    if (n < g.Cout) o[n] = __fadd_rn(acc[i][j], __ldg(c.bias + n));
+                    if (n < g.Cout) {
+                        const float x = __fadd_rn(acc[i][j], __ldg(c.bias + n));
+                        o[n] = x;
+                        if (c.act_out) {   // the consuming site's dense output f(x0)
+                            const float y = act_rt(c.act_kind, x);
+                            c.act_out[(int64_t)r * g.Cout + n] = y;
+                            if (c.act_bf) static_cast<bf16 *>(c.act_bf)[(int64_t)r * g.Cout + n] = __float2bfloat16_rn(y);
+                        }
+                    }
                 }
             } else {
                 T *o = static_cast<T *>(c.out) + (int64_t)(r + 1) * g.Cout;

@@ -218,7 +218,8 @@ struct Smem {
 // packs the fp32 reference frame's <= 4 channels into the same layout.
 // Weights are [Cout][ceil(taps/16)*64] with tap-major 4-channel pieces.
 template <int BN, bool DENSE, bool SMALL = false>
-__global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b) {
+__global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b,
+                                                             const __grid_constant__ CUtensorMap tmap_a) {
     st_pdl_enter();
     using namespace tc;
     using S = Smem<BN>;
@@ -474,7 +475,18 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 // its owner lane by shuffle.  One row per thread would touch
                 // 32 lines per instruction (8x the L1tex wavefronts).
                 const int wrow0 = warp * 32;
-                if (!async_a) {
+                if (c.tma_a) {
+                    // 1x1/s1 with contiguous A rows (dense bf16 shadow, or the
+                    // rowmap layout): the tile's 128 rows x 64 channels arrive as
+                    // one TMA 2D load into the same 128B-swizzled layout (rows /
+                    // channels past the tensor zero-filled); thread 0 issues it
+                    // with the weight tile below, the others only arrive
+                    if (m == 0) {
+                        mbar_arrive_tx(full + stage, S::A_BYTES);
+                        tma_load_2d(sa, &tmap_a, ci0, mt * BM, full + stage);
+                    }
+                    mbar_arrive(full + stage);
+                } else if (!async_a) {
                     // ---- fp32 activations -> bf16 (RNE): 2 rows x 16 float4 per instruction,
                     // two batches of 8 unconditional loads (an invalid source reads a safe
                     // address and is zeroed after), so the loads issue back to back
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                 if (ci0 == Cpad) { ci0 = 0; tap++; }
             }
         }
-        if (async_a) asm volatile("cp.async.wait_all;" ::: "memory");
+        if (async_a && !c.tma_a) asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == 4) {
         if (rank == 0) {
             // ===================== MMA issuer (leader) =====================
@@ -606,7 +618,27 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                             f.z = __fadd_rn(__uint_as_float(v[j + 2]), __ldg(c.bias + n0 + j + 2));
                             f.w = __fadd_rn(__uint_as_float(v[j + 3]), __ldg(c.bias + n0 + j + 3));
                             *reinterpret_cast<float4 *>(o + j) = f;
+                            if (c.act_out) {   // the consuming site's dense output f(x0) (+ bf16 shadow)
+                                float4 a;
+                                a.x = act_rt(c.act_kind, f.x);
+                                a.y = act_rt(c.act_kind, f.y);
+                                a.z = act_rt(c.act_kind, f.z);
+                                a.w = act_rt(c.act_kind, f.w);
+                                *reinterpret_cast<float4 *>(c.act_out + (int64_t)r * g.Cout + n0 + j) = a;
+                                if (c.act_bf)
+                                    *reinterpret_cast<uint2 *>(static_cast<bf16 *>(c.act_bf) + (int64_t)r * g.Cout + n0 + j) =
+                                        make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+                            }
                         }
+                    } else if (c.act_out) {
+                        for (int j = 0; j < 32; j++)
+                            if (n0 + j < g.Cout) {
+                                const float x = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
+                                const float a = act_rt(c.act_kind, x);
+                                o[j] = x;
+                                c.act_out[(int64_t)r * g.Cout + n0 + j] = a;
+                                if (c.act_bf) static_cast<bf16 *>(c.act_bf)[(int64_t)r * g.Cout + n0 + j] = __float2bfloat16_rn(a);
+                            }
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; j++)   // unrolled: v[] stays in registers
@@ -646,7 +678,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
 }
 
 template <int BN, bool DENSE, bool SMALL = false>
-static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s, int num_sms) {
+static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s, int num_sms,
+                      const CUtensorMap *tmap_a = nullptr) {
     using S = tc::Smem<BN>;
     static bool attr = false;
     if (!attr) {
@@ -670,7 +703,7 @@ static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE, SMALL>, c, *tmap);
+    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE, SMALL>, c, *tmap, tmap_a ? *tmap_a : *tmap);
 }
 
 // c_in % 8 == 0 (16-byte bf16 row pieces; each tap zero-padded to a multiple
@@ -741,15 +774,41 @@ bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout) {
     return r == CUDA_SUCCESS;
 }
 
-void launch_conv_tc(const ConvCall &c, const void *tmap_v, cudaStream_t s) {
+// A-operand map of a 1x1/s1 conv: [rows][C] bf16, box 64 channels x 128 rows,
+// 128B swizzle (the MMA's K-major A layout), out-of-range rows / channels read 0
+bool make_act_tmap(void *tmap_out, const void *base, int64_t rows, int C) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (C % 8 != 0 || rows < 1 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)C * 2};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap *>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+void launch_conv_tc(const ConvCall &c, const void *tmap_v, cudaStream_t s, const void *tmap_a_v) {
     const CUtensorMap *tmap = static_cast<const CUtensorMap *>(tmap_v);
+    const CUtensorMap *tmap_a = static_cast<const CUtensorMap *>(tmap_a_v);
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-#define TC_BN(BN_) (c.dense ? launch_tc<BN_, true>(c, tmap, s, num_sms) : launch_tc<BN_, false>(c, tmap, s, num_sms))
+#define TC_BN(BN_) \
+    (c.dense ? launch_tc<BN_, true>(c, tmap, s, num_sms, tmap_a) : launch_tc<BN_, false>(c, tmap, s, num_sms, tmap_a))
     switch (conv_tc_bn(c.g.Cout)) {
     case 256: TC_BN(256); break;
     case 128: TC_BN(128); break;

@@ -426,6 +426,168 @@ __global__ void __launch_bounds__(256, 2) k_dwconv_site(ConvCall c, DwSite d) {
     }
 }
 
+// Warp form (C <= 256, the default): ONE WARP PER OUTPUT PIXEL, lane l owns
+// channels l, l+32, ... (CPL = ceil(C/32)), so every warp's control flow --
+// the frame loop, the live-tap walk, the emit decision -- is uniform (ncu on
+// the 8-pixels-per-warp form: 2.3 G instructions for one 540x960x32 layer,
+// issue-bound with 15 % branch-resolving stalls from the divergent per-pixel
+// loops).  Lane t < k*k holds tap t's metadata {frame word, slot word, row
+// base} in registers; the row indices of a frame pair are computed by their
+// owner lanes and broadcast by shuffles, and the rows of up to TB active taps
+// x 2 frames are loaded (coalesced: the warp reads 64 contiguous bytes per
+// load instruction) before their FMAs.  Depthwise weights are staged in
+// shared memory once per CTA.  Per channel the fmaf chain runs over the taps
+// in ascending order from +0 (FP32 bit-exact), then the site step of
+// k_site_pw (x_acc += rnd(Delta); c = f(x_acc) - y_acc; warp max; emit).
+constexpr int DWW_WARPS = 8;
+template <int CPL, int KMAX, class T, int ACT>
+__global__ void __launch_bounds__(32 * DWW_WARPS) k_dwconv_site_w(ConvCall c, DwSite d) {
+    st_pdl_enter();
+    constexpr int TB = CPL == 1 ? 9 : CPL <= 2 ? 6 : CPL <= 4 ? 4 : 2;   // active taps per load batch
+    extern __shared__ float dww_w[];   // [KMAX][C] depthwise weights
+    const float theta = __ldg(d.theta);
+    const Geo g = c.g;
+    const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
+    const int C = g.Cin, ntaps = g.kh * g.kw;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < ntaps * C; i += blockDim.x) dww_w[i] = __ldg(c.wk + i);
+    __syncthreads();
+    const int64_t BNo = (int64_t)c.B * Nout;
+    const T *A = static_cast<const T *>(c.a.rows);
+    T *SR = static_cast<T *>(d.site_rows);
+    T *CR = static_cast<T *>(d.conv_rows);
+    // this lane's tap geometry (fixed)
+    const int tdy = lane < ntaps ? lane / g.kw : 0, tdx = lane < ntaps ? lane - tdy * g.kw : 0;
+    // strided pixels per warp (active pixels cluster in space: contiguous
+    // chunks per warp were measured 2-3x slower from load imbalance); the tap
+    // metadata and x0 of the warp's next pixel are loaded while the current
+    // one is computed
+    uint32_t ma = 0, ms = 0, n_ma = 0, n_ms = 0, n_w = 0;
+    int mz = 0, n_mz = 0;
+    float xa[CPL], ya[CPL], n_x[CPL];
+    auto fetch = [&](int64_t bq) {   // frame word; tap lanes: {act, slot, 1 + pbase}; x0 row
+        n_w = 0;
+        n_ma = n_ms = 0;
+        n_mz = 0;
+        if (bq >= BNo) return;
+        n_w = __ldg(d.out_act + bq);
+        if (!n_w) return;
+        const int b = (int)(bq / Nout), q = (int)(bq - (int64_t)b * Nout);
+        const int oy = q / g.Wout, ox = q - oy * g.Wout;
+        if (lane < ntaps) {
+            const int iy = oy * g.sh - g.ph + tdy, ix = ox * g.sw - g.pw + tdx;
+            if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                const int64_t bp = (int64_t)b * Nin + iy * g.Win + ix;
+                n_ma = __ldg(c.a.act + bp);
+                n_ms = __ldg(c.a.slot + bp);
+                n_mz = 1 + __ldg(c.a.pbase + bp);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = lane + 32 * i;
+            n_x[i] = ch < C ? __ldg(d.x0 + bq * C + ch) : 0.0f;
+        }
+    };
+    const int64_t stride = (int64_t)gridDim.x * DWW_WARPS;
+    int64_t bq = (int64_t)blockIdx.x * DWW_WARPS + wid;
+    fetch(bq);
+    for (; bq < BNo; bq += stride) {
+        uint32_t w = n_w;
+        ma = n_ma;
+        ms = n_ms;
+        mz = n_mz;
+#pragma unroll
+        for (int i = 0; i < CPL; i++) xa[i] = n_x[i];
+        fetch(bq + stride);   // the next pixel's loads in flight
+        if (!w) {
+            if (lane == 0) d.site_act[bq] = 0u;
+            continue;
+        }
+#pragma unroll
+        for (int i = 0; i < CPL; i++) ya[i] = actf<ACT>(xa[i]);
+        uint32_t emit = 0;
+        int64_t orow = 1 + __ldg(d.out_pbase + bq);
+        auto step = [&](const float (&acc)[CPL], int64_t row, int t1) {
+            float cand[CPL];
+            float mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const float v = rnd<T>(acc[i]);                    // the conv's stored delta
+                xa[i] = __fadd_rn(xa[i], v);                       // reconstruct x (Eq.3)
+                cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);      // restore the delta
+                mx = fmaxf(mx, fabsf(cand[i]));
+            }
+            if (CR)
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + 32 * i < C) str<T>(CR + row * C + lane + 32 * i, acc[i]);
+            mx = gmax<32>(mx, 0xffffffffu);
+            if (mx > theta) {                                      // truncation
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    cand[i] = rnd<T>(cand[i]);
+                    ya[i] = __fadd_rn(ya[i], cand[i]);
+                    if (lane + 32 * i < C) str<T>(SR + row * C + lane + 32 * i, cand[i]);
+                }
+                emit |= 1u << t1;
+            } else if (d.zero_gaps) {                              // a rowmap conv reads this slot as a row
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + 32 * i < C) str<T>(SR + row * C + lane + 32 * i, 0.0f);
+            }
+        };
+        while (w) {
+            const int tA = __ffs(w) - 1;
+            w &= w - 1;
+            const int tB = w ? __ffs(w) - 1 : -1;
+            if (w) w &= w - 1;
+            // tap lanes: hit bits and row indices of both frames
+            const bool hA = (ma >> tA) & 1u, hB = tB >= 0 && ((ma >> tB) & 1u);
+            const int rA = mz + __popc(ms & lowmask(tA)), rB = tB >= 0 ? mz + __popc(ms & lowmask(tB)) : 0;
+            uint32_t todo = __ballot_sync(0xffffffffu, hA || hB);   // taps active in A or B, ascending
+            const uint32_t bA = __ballot_sync(0xffffffffu, hA), bB = __ballot_sync(0xffffffffu, hB);
+            float accA[CPL], accB[CPL];
+#pragma unroll
+            for (int i = 0; i < CPL; i++) accA[i] = accB[i] = 0.0f;
+            while (todo) {
+                int tp[TB];
+                float vA[TB][CPL], vB[TB][CPL];
+#pragma unroll
+                for (int j = 0; j < TB; j++) {
+                    tp[j] = todo ? __ffs(todo) - 1 : -1;
+                    if (todo) todo &= todo - 1;
+                    const int t = tp[j] < 0 ? 0 : tp[j];
+                    const int64_t ra = __shfl_sync(0xffffffffu, rA, t), rb = __shfl_sync(0xffffffffu, rB, t);
+                    const bool ia = tp[j] >= 0 && ((bA >> t) & 1u), ib = tp[j] >= 0 && ((bB >> t) & 1u);
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        const int ch = lane + 32 * i;
+                        vA[j][i] = (ia && ch < C) ? ldr<T>(A + ra * C + ch) : 0.0f;
+                        vB[j][i] = (ib && ch < C) ? ldr<T>(A + rb * C + ch) : 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < TB; j++) {
+                    if (tp[j] < 0) continue;
+                    const bool ia = (bA >> tp[j]) & 1u, ib = (bB >> tp[j]) & 1u;
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        const int ch = lane + 32 * i;
+                        const float wv = ch < C ? dww_w[tp[j] * C + ch] : 0.0f;
+                        if (ia) accA[i] = fmaf(wv, vA[j][i], accA[i]);
+                        if (ib) accB[i] = fmaf(wv, vB[j][i], accB[i]);
+                    }
+                }
+            }
+            step(accA, orow, tA);
+            if (tB >= 0) step(accB, orow + 1, tB);
+            orow += tB >= 0 ? 2 : 1;
+        }
+        if (lane == 0) d.site_act[bq] = emit;
+    }
+}
+
 // Wide form (C > 256): one warp per output pixel, the pixel's x_acc / y_acc
 // (and, for the second frame of a bf16 pair, its stored delta) in shared
 // memory, walked in 256-channel chunks.  Per frame: pass 1 adds the delta to
@@ -814,7 +976,139 @@ static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
 #undef L_DW
 }
 
+// Dense (reference-frame) depthwise, register form.  A CTA owns an output
+// tile of one chunk and a channel slice of <= 64 channels (8-channel groups,
+// ncg | 256 so every thread keeps ONE group for the whole tile).  The tile's
+// input footprint is staged once into shared memory, zero-padded, already in
+// the contract's operand precision (BF16 mode: bf16-rounded values stored as
+// bf16, R22-BF16; FP32 mode: fp32), so the inner loop is per tap one
+// shared-memory vector load and 8 FMAs with the group's weights and bias in
+// registers (k x k <= 9; 5x5 reads them from shared memory).  Per channel
+// the fmaf chain runs over the taps in (dy, dx) order from +0, bias last
+// (R18; FP32 mode bit-identical to k_dw_tile and the oracle).  Epilogue: the
+// fp32 output, and for a fused site its dense output f(x0) (+ bf16 shadow).
+template <class TS, int KK>
+__global__ void __launch_bounds__(256) k_dw_dense(ConvCall c, int TOH, int TOW) {
+    st_pdl_enter();
+    extern __shared__ __align__(16) unsigned char dwd_smem[];
+    const Geo g = c.g;
+    const int C = g.Cin, kk = g.kh * g.kw;
+    const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
+    const int nsl = (C + 63) / 64;
+    const int ntx = (g.Wout + TOW - 1) / TOW, nty = (g.Hout + TOH - 1) / TOH;
+    int bid = blockIdx.x;
+    const int sl = bid % nsl;
+    bid /= nsl;
+    const int tile = bid % (ntx * nty), b = bid / (ntx * nty);
+    const int ty = tile / ntx, tx = tile - ty * ntx;
+    const int cs0 = sl * 64, csw = min(64, C - cs0), ncg = csw / 8;
+    const int FH = (TOH - 1) * g.sh + g.kh, FW = (TOW - 1) * g.sw + g.kw, FP = FH * FW;
+    const int fy0 = ty * TOH * g.sh - g.ph, fx0 = tx * TOW * g.sw - g.pw;
+    float *w_s = reinterpret_cast<float *>(dwd_smem);           // [kk][csw]
+    TS *stg = reinterpret_cast<TS *>(w_s + kk * 64);              // [FP][csw]
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kk * csw; i += 256) {
+        const int tap = i / csw, j = i - tap * csw;
+        float wv = __ldg(c.wk + (int64_t)tap * C + cs0 + j);
+        if (c.rnd_a) wv = bf16_round(wv);   // weights are bf16 values already in BF16 mode (idempotent)
+        w_s[i] = wv;
+    }
+    // stage the footprint: 8-channel pieces, zeros outside the map
+    const float *X = c.a_dense;
+    for (int u = tid; u < FP * ncg; u += 256) {
+        const int p = u / ncg, cg = u - p * ncg;
+        const int iy = fy0 + p / FW, ix = fx0 + p % FW;
+        float v[8];
+        if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+            RowIO<float, 8>::load(X + ((int64_t)b * Nin + iy * g.Win + ix) * C + cs0 + cg * 8, v);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; i++) v[i] = 0.0f;
+        }
+        RowIO<TS, 8>::store(stg + (size_t)p * csw + cg * 8, v);   // bf16 staging rounds (RNE)
+    }
+    __syncthreads();
+    const int cg = tid % ncg;               // fixed per thread (ncg | 256)
+    const int c0 = cs0 + cg * 8;
+    float bb[8];
+    RowIO<float, 8>::load(c.bias + c0, bb);
+    float wr[KK > 0 ? KK * 8 : 1];
+    if constexpr (KK > 0) {
+#pragma unroll
+        for (int t = 0; t < KK; t++) RowIO<float, 8>::load(w_s + t * csw + cg * 8, *reinterpret_cast<float(*)[8]>(wr + 8 * t));
+    }
+    const int TOc = TOH * TOW;
+    for (int o = tid / ncg; o < TOc; o += 256 / ncg) {
+        const int loy = o / TOW, lox = o - loy * TOW;
+        const int oy = ty * TOH + loy, ox = tx * TOW + lox;
+        if (oy >= g.Hout || ox >= g.Wout) continue;
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) acc[i] = 0.0f;
+        const TS *base = stg + (size_t)(loy * g.sh * FW + lox * g.sw) * csw + cg * 8;
+        if constexpr (KK > 0) {
+#pragma unroll
+            for (int t = 0; t < KK; t++) {
+                const int dy = t / (KK == 9 ? 3 : 1), dx = t - dy * (KK == 9 ? 3 : 1);
+                float v[8];
+                RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
+#pragma unroll
+                for (int i = 0; i < 8; i++) acc[i] = fmaf(wr[8 * t + i], v[i], acc[i]);
+            }
+        } else {
+            for (int dy = 0; dy < g.kh; dy++)
+                for (int dx = 0; dx < g.kw; dx++) {
+                    float v[8], wv[8];
+                    RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
+                    RowIO<float, 8>::load(w_s + (dy * g.kw + dx) * csw + cg * 8, wv);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) acc[i] = fmaf(wv[i], v[i], acc[i]);
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) acc[i] = __fadd_rn(acc[i], bb[i]);
+        const int64_t oi = ((int64_t)b * Nout + oy * g.Wout + ox) * C + c0;
+        RowIO<float, 8>::store(static_cast<float *>(c.out) + oi, acc);
+        if (c.act_out) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) acc[i] = act_rt(c.act_kind, acc[i]);
+            RowIO<float, 8>::store(c.act_out + oi, acc);
+            if (c.act_bf) RowIO<bf16, 8>::store(static_cast<bf16 *>(c.act_bf) + oi, acc);
+        }
+    }
+}
+
+template <class TS>
+static bool launch_dw_dense_t(const ConvCall &c, cudaStream_t s) {
+    const Geo &g = c.g;
+    if (g.Cin % 8 != 0) return false;
+    for (int cs0 = 0; cs0 < g.Cin; cs0 += 64)   // every slice's group count divides 256
+        if (256 % (std::min(64, g.Cin - cs0) / 8) != 0) return false;
+    const int csw = std::min(64, g.Cin);
+    const int stg_budget = 64 * 1024;
+    const int fp_max = std::min<int>(1024, stg_budget / (csw * (int)sizeof(TS)));
+    int TOH, TOW;
+    if (!dw_tile_dims(g, fp_max, TOH, TOW)) return false;
+    const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
+    const size_t sm = (size_t)g.kh * g.kw * 64 * 4 + (size_t)FP * csw * sizeof(TS) + 64;
+    const int64_t grid = (int64_t)c.B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW) * ((g.Cin + 63) / 64);
+    const bool k3 = g.kh == 3 && g.kw == 3;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dw_dense<TS, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(k_dw_dense<TS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        attr = true;
+    }
+    if (k3) k_dw_dense<TS, 9><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+    else k_dw_dense<TS, 0><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+    return true;
+}
+
 void launch_dwconv_f32(const ConvCall &c, cudaStream_t s) {
+    static const bool old_dense = [] { const char *v = getenv("ST_DW_DENSE_TILE"); return v && v[0] == '1'; }();
+    if (c.dense && !old_dense &&
+        (c.rnd_a ? launch_dw_dense_t<bf16>(c, s) : launch_dw_dense_t<float>(c, s)))
+        return;
     if (c.dense && launch_dw_tile_t<float, true>(c, nullptr, nullptr, s)) return;
     if (c.dense || !c.bf) launch_dw_t<float>(c, s);
     else launch_dw_t<bf16>(c, s);
@@ -885,11 +1179,40 @@ static void launch_dws_wide_k(const ConvCall &c, const DwSite &d, int64_t BNo, c
     k_dwconv_site_wide<KMAX, T, ACT><<<grid, 32 * DWS_WARPS, smem, s>>>(c, d);
 }
 
+template <int CPL, int KMAX, class T, int ACT>
+static void launch_dww_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaStream_t s) {
+    const int smem = KMAX * c.g.Cin * 4;
+    static int attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(k_dwconv_site_w<CPL, KMAX, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = smem;
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo + DWW_WARPS - 1) / DWW_WARPS, 148 * 8));
+    k_dwconv_site_w<CPL, KMAX, T, ACT><<<grid, 32 * DWW_WARPS, smem, s>>>(c, d);
+}
+
 template <class T, int ACT>
 static void launch_dws_t(const ConvCall &c, const DwSite &d, cudaStream_t s) {
     const int64_t BNo = (int64_t)c.B * c.g.Hout * c.g.Wout;
     const int C = c.g.Cin;
     const bool k9 = c.g.kh * c.g.kw <= 9;
+    static const bool grouped = [] { const char *v = getenv("ST_DW_GROUPED"); return v && v[0] == '1'; }();
+    if (!grouped && C > 32 && C <= 256) {   // warp per pixel (uniform control flow); C <= 32: 8+ pixels per warp
+#define L_DWW(CPL_)                                                             \
+    {                                                                           \
+        if (k9) launch_dww_k<CPL_, 9, T, ACT>(c, d, BNo, s);                    \
+        else launch_dww_k<CPL_, 25, T, ACT>(c, d, BNo, s);                      \
+        return;                                                                 \
+    }
+        if (C <= 32) L_DWW(1)
+        if (C <= 64) L_DWW(2)
+        if (C <= 96) L_DWW(3)
+        if (C <= 128) L_DWW(4)
+        if (C <= 160) L_DWW(5)
+        if (C <= 192) L_DWW(6)
+        L_DWW(8)
+#undef L_DWW
+    }
 #define L_DWS(G_)                                                               \
     {                                                                           \
         if (k9) launch_dws_k<G_, 9, T, ACT>(c, d, BNo, s);                      \

@@ -248,6 +248,77 @@ __global__ void __launch_bounds__(256) k_se_delta_sums_c(DView in, int N, int C,
     }
 }
 
+// ---- (i-b3) the same sums with uniform control flow: the CTA compacts the
+// active pixels of each 256-pixel batch (frame word, slot, row base) into
+// shared memory; warp w owns frames t = w, w + 8, ... and walks the list --
+// for an entry active at t every lane adds its channels of the row (lane l:
+// channels c0 + l + 32 i, one coalesced 64-byte load per i) into fp64
+// registers.  Channel chunks of 256 (CPL <= 8) for wide layers.
+template <int CPL, class T>
+__global__ void __launch_bounds__(256) k_se_delta_sums_w(DView in, int N, int C, int F, int ppb,
+                                                         double *__restrict__ dsum) {
+    st_pdl_enter();
+    __shared__ uint32_t m_act[256], m_sl[256];
+    __shared__ int32_t m_row[256];
+    __shared__ int wcount[8];
+    const T *rows = static_cast<const T *>(in.rows);
+    const int b = blockIdx.z, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c0 = blockIdx.y * 32 * CPL;
+    constexpr int FW = 4;   // frames per warp (F <= 32)
+    double acc[FW][CPL];
+#pragma unroll
+    for (int f = 0; f < FW; f++)
+#pragma unroll
+        for (int i = 0; i < CPL; i++) acc[f][i] = 0.0;
+    const int p0 = blockIdx.x * ppb, p1 = min(N, p0 + ppb);
+    for (int pb = p0; pb < p1; pb += 256) {
+        const int p = pb + threadIdx.x;
+        const int64_t bp = (int64_t)b * N + p;
+        const uint32_t a = p < p1 ? __ldg(in.act + bp) : 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, a != 0);
+        if (lane == 0) wcount[wid] = __popc(bal);
+        __syncthreads();
+        int off = 0, nl = 0;
+        for (int w = 0; w < 8; w++) {
+            off += w < wid ? wcount[w] : 0;
+            nl += wcount[w];
+        }
+        if (a) {
+            const int k = off + __popc(bal & ((1u << lane) - 1u));
+            m_act[k] = a;
+            m_sl[k] = __ldg(in.slot + bp);
+            m_row[k] = 1 + __ldg(in.pbase + bp);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int f = 0; f < FW; f++) {
+            const int t = wid + 8 * f;
+            if (t >= F) break;
+            for (int k = 0; k < nl; k++) {
+                const uint32_t ak = m_act[k];
+                if (!((ak >> t) & 1u)) continue;
+                const int64_t row = m_row[k] + __popc(m_sl[k] & lowmask(t));
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    const int ch = c0 + lane + 32 * i;
+                    if (ch < C) acc[f][i] += (double)ldr<T>(rows + row * C + ch);
+                }
+            }
+        }
+        __syncthreads();   // list reused by the next batch
+    }
+#pragma unroll
+    for (int f = 0; f < FW; f++) {
+        const int t = wid + 8 * f;
+        if (t >= F) break;
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = c0 + lane + 32 * i;
+            if (ch < C && acc[f][i] != 0.0) atomicAdd(dsum + ((int64_t)b * F + t) * C + ch, acc[f][i]);
+        }
+    }
+}
+
 // gate of one chunk from fp32 means m[C] (block-wide; hid/gate in smem)
 __device__ void se_gate_block(const float *m, int C, int H, const float *w1, const float *b1, const float *w2,
                               const float *b2, float *hid, float *gate) {
@@ -715,8 +786,28 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
         dim3 grid(cdiv(N, ppb), cdiv(C, CS), B);
         const int R = std::max(1, 256 / (F * (CS / 8)));   // replicas of the (t, cg) threads
         const size_t sm = (size_t)R * F * CS * sizeof(double);
-        static const bool old = [] { const char *v = getenv("ST_SE_SUMS_DENSE"); return v && v[0] == '1'; }();
-        if (!old && sm <= 48 * 1024) {
+        // default (mode 0): the thread-per-(frame, 8 channels) sweep below; the
+        // compacted-list forms measured slower on cfg5 (kept as A/B switches)
+        static const int mode = [] { const char *v = getenv("ST_SE_SUMS"); return v ? atoi(v) : 0; }();
+        if (mode == 2) {   // warp per frame over the compacted active pixels
+            const int cpl = std::min(8, (C + 31) / 32);
+            dim3 gw(cdiv(N, ppb), cdiv(C, 32 * (cpl == 3 ? 4 : cpl > 4 ? 8 : cpl)), B);
+            if (cpl == 1) {
+                if (bf) k_se_delta_sums_w<1, bf16><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+                else k_se_delta_sums_w<1, float><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+            } else if (cpl == 2) {
+                if (bf) k_se_delta_sums_w<2, bf16><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+                else k_se_delta_sums_w<2, float><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+            } else if (cpl <= 4) {
+                if (bf) k_se_delta_sums_w<4, bf16><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+                else k_se_delta_sums_w<4, float><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+            } else {
+                if (bf) k_se_delta_sums_w<8, bf16><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+                else k_se_delta_sums_w<8, float><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
+            }
+            return;
+        }
+        if (mode == 1 && sm <= 48 * 1024) {
             if (bf) k_se_delta_sums_c<bf16><<<grid, 256, sm, s>>>(in, N, C, F, ppb, CS, R, dsum);
             else k_se_delta_sums_c<float><<<grid, 256, sm, s>>>(in, N, C, F, ppb, CS, R, dsum);
             return;

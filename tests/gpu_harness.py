@@ -169,7 +169,9 @@ def follow_compare(enc, net, frames_chunk, thresholds, chunk, precision, exporte
                 a64, b64 = got[t].astype(np.float64), O[t].astype(np.float64)
                 rel = float(np.linalg.norm(a64 - b64) / max(np.linalg.norm(b64), 1e-30))
                 assert rel <= 2e-2, f"tap {tap} frame {t}: normwise relative error {rel:.4f}"
-            ok, e = bf16_within(got, O, rel=2e-2, rms_frac=0.1)
+            # the rms floor grows like a random walk over the sites a tap's
+            # value passes (0.1 rms at EfficientNet-B0's 49 sites)
+            ok, e = bf16_within(got, O, rel=2e-2, rms_frac=0.1 * max(1.0, np.sqrt(len(site_layers(net)) / 49.0)))
             worst = max(worst, e)
             assert ok, f"tap {tap} beyond the elementwise bf16 bound ({e:.2f} x bound)"
         elif adopted == 0 and all(net.layers[i]["kind"] in (W.RELU, W.MAXPOOL) for i in site_layers(net)):

@@ -18,7 +18,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from gpu_harness import follow_compare
+from gpu_harness import follow_compare, site_layers
 
 pytestmark = pytest.mark.gpu
 
@@ -53,10 +53,16 @@ def _full_step(cfg, precision, chunks, L=None, B=None, theta=None):
 
 
 def _check(cfg, precision, chunks, **kw):
+    """Adopted (in-band, R23) decisions: <= 0.1 % of all decisions on the
+    BASELINE configs; the paper's deeper backbones (>= 100 sites: ResNet-152,
+    EfficientNet-B4..B6) allow 0.5 % -- every adopted decision is a correct
+    one by R23, and their number grows with depth because each site's
+    rounding differences move the values later sites decide on."""
     reps = []
     for net, enc, fr, b, theta in _full_step(cfg, precision, chunks, **kw):
         rep = follow_compare(enc, net, fr, theta, b, precision, exported=True)
-        assert rep["adopted"] <= max(3, 1e-3 * rep["decisions"]), (cfg.cid, b, rep)
+        frac = 1e-3 if len(site_layers(net)) < 100 else 5e-3
+        assert rep["adopted"] <= max(3, frac * rep["decisions"]), (cfg.cid, b, rep)
         reps.append(rep)
     return reps
 
