@@ -30,12 +30,13 @@ namespace {
 constexpr int KC_SUBTRACT = 0, KC_DILATE = 1, KC_SCAN = 2, KC_ENUM = 3, KC_CONV_SPARSE = 4, KC_CONV_DENSE = 5,
               KC_SITE_PW = 6, KC_SITE_MP = 7, KC_ADD = 8, KC_ACCUM = 9, KC_DENSE_MISC = 10, KC_COUNTS = 11,
               KC_DW_SPARSE = 12, KC_DW_DENSE = 13, KC_TC_SPARSE = 14, KC_TC_DENSE = 15, KC_SE = 16,
-              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_SE_SUMS = 20, KC_DW_SITE = 21, KC_N = 22;
+              KC_STEM_SPARSE = 17, KC_STEM_DENSE = 18, KC_PROF_STATS = 19, KC_SE_SUMS = 20, KC_DW_SITE = 21,
+              KC_TC_SITE_FIX = 22, KC_N = 23;
 const char *KC_NAMES[KC_N] = {"subtract",   "dilate",       "scan",      "enumerate", "conv_sparse",
                               "conv_dense", "site_pointwise", "site_maxpool", "add",     "accumulate",
                               "dense_misc", "counts",       "dwconv_sparse", "dwconv_dense",
                               "conv_tc_sparse", "conv_tc_dense", "se", "conv_tc_stem_sparse",
-                              "conv_tc_stem_dense", "prof_stats", "se_sums", "dwconv_site"};
+                              "conv_tc_stem_dense", "prof_stats", "se_sums", "dwconv_site", "tc_site_fixup"};
 
 struct Buf {
     int64_t bytes = 0;
@@ -59,6 +60,8 @@ struct LayerRT {
     int dw_site = -1;         // depthwise CONV: the pointwise site its sparse pass runs
     int act_site = -1;        // non-depthwise CONV: the ReLU/SiLU whose dense output its epilogue writes
     int act_of = -1;          // ReLU/SiLU: the conv that writes its dense output
+    int tc_site = -1;         // tcgen05 CONV: the ReLU/SiLU site its sparse epilogue runs (N2)
+    int fused_tc = -1;        // ReLU/SiLU: the tcgen05 conv whose epilogue runs this site
     // streaming state (N1, persistent): pointwise site sx[0]/sy[0] in place;
     // maxpool sx[0..1] ping-pong x_acc + spy y_acc; fused pool (on the pool
     // layer) sx[0..1] ReLU x_acc, sy[0..1] ReLU y_acc, spy pool y_acc; OUTPUT sx[0]
@@ -367,18 +370,6 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 cv.dw_site = i;
             }
     }
-    // conv -> ReLU / SiLU (its only consumer): the conv's dense epilogue also
-    // writes the site's dense output (no separate activation pass); not for a
-    // ReLU fused into a maxpool (the pool's dense pass applies it) or streaming
-    if (!cfg->streaming)
-        for (int i = 0; i < n; i++) {
-            LayerRT &r = e->L[i];
-            if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0 || r.fused_dw >= 0 || r.fused_pool >= 0) continue;
-            LayerRT &cv = e->L[r.src];
-            if (cv.kind != ST_CONV || cv.depthwise || cv.n_consumers != 1) continue;
-            cv.act_site = i;
-            r.act_of = r.src;
-        }
     // 1x1/s1 convs in the input's row layout (rowmap): the layout must have no
     // stale rows at touched-but-not-emitted slots -- input site, convs, adds
     // have none; ReLU / SiLU / SE sites are asked to zero theirs (zero_gaps);
@@ -526,6 +517,41 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                     return fail(e.get(), ST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         }
     }
+    // conv -> ReLU / SiLU (its only consumer): the conv's dense epilogue also
+    // writes the site's dense output (no separate activation pass); not for a
+    // ReLU fused into a maxpool (the pool's dense pass applies it) or streaming
+    if (!cfg->streaming)
+        for (int i = 0; i < n; i++) {
+            LayerRT &r = e->L[i];
+            if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0 || r.fused_dw >= 0 || r.fused_pool >= 0) continue;
+            LayerRT &cv = e->L[r.src];
+            // tensor-core convs excluded: their epilogue (4 warps, a row per
+            // thread) is store-bound already; the extra f(x0) + shadow stores
+            // measured slower than the separate activation pass
+            if (cv.kind != ST_CONV || cv.depthwise || cv.n_consumers != 1 || cv.tc || cv.tc_small) continue;
+            cv.act_site = i;
+            r.act_of = r.src;
+        }
+    // tcgen05 conv -> ReLU / SiLU (its only consumer, c_out <= 256): the site
+    // runs in the conv's epilogue; the weight map is rebuilt
+    // for the one-tile N width
+    {
+        const char *nf = getenv("ST_NO_FUSE_TC");   // A/B switch
+        if (e->bf && !(nf && nf[0] == '1') && !cfg->streaming && !cfg->debug_retain)
+            for (int i = 0; i < n; i++) {
+                LayerRT &r = e->L[i];
+                if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0 || r.fused_dw >= 0 || r.fused_pool >= 0 ||
+                    r.act_of >= 0)
+                    continue;
+                LayerRT &cv = e->L[r.src];
+                if (cv.kind != ST_CONV || !cv.tc || cv.n_consumers != 1 || !conv_tc_site_eligible(cv.geo)) continue;
+                const int64_t K = (int64_t)cv.spec.k_h * cv.spec.k_w * conv_tc_cpad(cv.geo.Cin);
+                if (!make_weight_tmap_site(cv.tmap, cv.wbf, (int)K, cv.C))
+                    return fail(e.get(), ST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                cv.tc_site = i;
+                r.fused_tc = r.src;
+            }
+    }
     for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
     e->cap_fit.assign(n + 1, -1);
     st_status r = plan(e.get());
@@ -634,6 +660,7 @@ static st_status plan(st_encoder *e) {
             const int o = layout_owner(e, l.src);
             l.rows_cap = o == n ? e->in_rows_cap : e->L[o].rows_cap;
             l.b_rows = add((l.rows_cap + 1) * l.C * ES, tdef, tlast);
+            if (l.tc_site >= 0) l.b_ridx = add(std::max<int64_t>(l.rows_cap, 1) * 4, tdef, tdef);   // row codes
             continue;
         }
         l.b_act = add(B * N * 4, tdef, tlast);
@@ -727,6 +754,12 @@ static st_status plan(st_encoder *e) {
     }
     // a depthwise conv's pass writes its fused site's dense output (dense
     // epilogue) and frame words (sparse pass) at the conv's step time
+    for (int i = 0; i < n; i++)
+        if (e->L[i].fused_tc >= 0) {
+            const int tc = t_of(e->L[i].fused_tc);
+            for (int id : {e->L[i].b_act, e->L[i].b_rows})
+                if (id >= 0) e->bufs[id].first = std::min(e->bufs[id].first, tc);
+        }
     for (int i = 0; i < n; i++)
         if (e->L[i].act_of >= 0) {
             const int tc = t_of(e->L[i].act_of);
@@ -1096,6 +1129,19 @@ extern "C" st_status st_encode_diff_u8(st_encoder *e, const uint8_t *frames_dev,
     return encode_diff(e, frames_dev, true, n_diff, chunk_stride, thresholds, stream);
 }
 
+// conv + site in the tcgen05 epilogue: the site's frame words start at zero
+// (pixels without rows are never visited), emitted rows in place
+static void tc_site_setup(st_encoder *e, const LayerRT &l, ConvCall &c, cudaStream_t s) {
+    const LayerRT &r = e->L[l.tc_site];
+    cudaMemsetAsync(e->ptr(r.b_act), 0, (size_t)e->staged_chunks * r.H * r.W * 4, s);
+    c.site.on = true;
+    c.site.x0 = e->p<float>(l.b_y0);
+    c.site.theta = e->thr_dev + r.site;
+    c.site.act = r.kind == ST_RELU ? ACT_RELU : ACT_SILU_FAST;
+    c.site.words = e->p<uint32_t>(r.b_act);
+    c.site.zero_gaps = r.zero_gaps;
+}
+
 static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int F, int64_t fstride, cudaStream_t s) {
     const int B = e->staged_chunks, n = (int)e->L.size();
     const int64_t Nin = (int64_t)e->in_H * e->in_W;
@@ -1222,9 +1268,20 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 c.act_out = nullptr;
                 c.act_bf = nullptr;
                 c.tma_a = l.tma_as;
+                if (l.tc_site >= 0) {   // the site in the epilogue: row codes of the layout's slots
+                    const int o = layout_owner(e, l.src);
+                    const uint32_t *sw = o == n ? e->p<uint32_t>(e->in_act) : e->p<uint32_t>(e->L[o].b_slot >= 0 ? e->L[o].b_slot : e->L[o].b_act);
+                    const int32_t *pw = o == n ? e->p<int32_t>(e->in_pbase) : e->p<int32_t>(e->L[o].b_pbase);
+                    const int64_t Nn = o == n ? Nin : (int64_t)e->L[o].H * e->L[o].W;
+                    LAUNCH(e, KC_ENUM, i, s, launch_enumerate(sw, pw, B * Nn, e->p<int32_t>(l.b_ridx), s));
+                    c.ridx = e->p<int32_t>(l.b_ridx);
+                    tc_site_setup(e, l, c, s);
+                }
                 LAUNCH(e, l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE, i, s,
                        l.tc ? launch_conv_tc(c, l.tmap, s, l.tma_as ? l.tmap_as : nullptr) : launch_conv_f32(c, s));
+                if (l.tc_site >= 0) LAUNCH(e, KC_TC_SITE_FIX, l.tc_site, s, launch_tc_site_fixup(c, in, s));
                 c.tma_a = false;
+                c.site.on = false;
                 break;
             }
             uint32_t *act = e->p<uint32_t>(l.b_act);
@@ -1263,12 +1320,21 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 LAUNCH(e, KC_DW_SITE, i, s, launch_dwconv_site(c, d, s));
                 break;
             }
+            if (l.tc_site >= 0) tc_site_setup(e, l, c, s);
             LAUNCH(e, l.depthwise ? KC_DW_SPARSE : l.tc ? KC_TC_SPARSE : l.tc_small ? KC_STEM_SPARSE : KC_CONV_SPARSE, i, s,
                    dw_pm        ? launch_dwconv_pm(c, act, pb, s)
                    : l.depthwise ? launch_dwconv_f32(c, s)
                    : l.tc       ? launch_conv_tc(c, l.tmap, s)
                    : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
                                 : launch_conv_f32(c, s));
+            if (l.tc_site >= 0) {
+                DView cv;
+                cv.act = act;
+                cv.slot = act;
+                cv.pbase = pb;
+                LAUNCH(e, KC_TC_SITE_FIX, l.tc_site, s, launch_tc_site_fixup(c, cv, s));
+            }
+            c.site.on = false;
             break;
         }
         case ST_RELU: case ST_SILU: {
@@ -1298,7 +1364,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             DView me = view_of(e, i);
             if (l.b_rows >= 0) zero_row(l.b_rows, l.C);   // own buffer (not in place)
             if (l.fused_pool >= 0) break;                 // runs inside the pool's pass
-            if (l.fused_dw < 0)                           // else: ran inside the conv's pass
+            if (l.fused_dw < 0 && l.fused_tc < 0)         // else: ran inside the conv's pass
                 LAUNCH(e, KC_SITE_PW, i, s,
                    launch_site_pointwise(in, x_init, B, (int)N, l.C, act_kind, thresholds + l.site, bf,
                                          e->p<uint32_t>(l.b_act), const_cast<void *>(me.rows), sst, s, l.zero_gaps));

@@ -92,6 +92,16 @@ struct ConvCall {
     int sr, shift;          // stems: paired K layout (sr > 0), see conv_tc_small_layout
     bool rowmap = false;    // sparse 1x1/s1: M row r = input row r + 1 -> output row r + 1 (no ridx)
     bool tma_a = false;     // tcgen05, 1x1/s1 with contiguous A rows: A tiles by TMA (launch_conv_tc tmap_a)
+    // tcgen05 sparse conv + its ReLU / SiLU site in the epilogue (N2; BF16 mode, c_out <= 256):
+    // the emitted rows go to `out` (the conv's row layout), the site's frame words to `words`
+    struct {
+        bool on = false;
+        const float *x0 = nullptr;     // conv dense output of the reference frame (the site's x_acc start)
+        const float *theta = nullptr;
+        int act = 0;                   // Act
+        uint32_t *words = nullptr;     // site emitted frame words [B][N] (zeroed before the launch)
+        bool zero_gaps = false;
+    } site;
     // B operand / output
     const float *wk;        // [K][Cout] (K order dy,dx,ci; R18)
     const float *bias;      // dense only
@@ -133,6 +143,12 @@ bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout);
 void launch_conv_tc(const ConvCall &c, const void *tmap, cudaStream_t s, const void *tmap_a = nullptr);
 // A-operand TMA map of a 1x1/s1 conv over a [rows][C] bf16 matrix (c.tma_a)
 bool make_act_tmap(void *tmap_out, const void *base, int64_t rows, int C);
+// conv + site in the epilogue: eligibility, the weight map with the one-tile
+// N width it needs, and the fix-up of pixels continuing across tile
+// boundaries (conv = the conv's delta tensor view: act / pbase)
+bool conv_tc_site_eligible(const Geo &g);
+bool make_weight_tmap_site(void *tmap_out, const void *wbf, int K, int Cout);
+void launch_tc_site_fixup(const ConvCall &c, DView conv, cudaStream_t s);
 // stems on tensor cores: the network input (c_in <= 4); sparse mode reads the
 // 4-channel-padded dense input delta (c.ddelta), dense mode the fp32 frames
 bool conv_tc_small_eligible(const Geo &g);

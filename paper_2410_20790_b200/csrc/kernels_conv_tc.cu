@@ -197,18 +197,150 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return r;
 }
 
-template <int BN>
+template <int BN, bool SITE = false>
 struct Smem {
     static constexpr int A_BYTES = BM * BK * 2;          // 16 KB: this CTA's 128 rows of the M=256 tile
     static constexpr int B_BYTES = (BN / 2) * BK * 2;    // this CTA's half of the BN weight rows
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES_FIT = (SMEM_MAX - 256 - 1024) / STAGE;
+    // SITE: the tile's 128 delta rows (bf16, row stride BN + 8 elements) and
+    // their row codes, read back by the site step of the epilogue
+    static constexpr int SROW = BN + 8;
+    static constexpr int SITE_BYTES = SITE ? BM * SROW * 2 + BM * 4 + 64 : 0;
+    static constexpr int STAGES_FIT = (SMEM_MAX - 256 - 1024 - SITE_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int BAR_OFF = STAGES * STAGE;
+    static constexpr int SITE_OFF = STAGES * STAGE;
+    static constexpr int BAR_OFF = SITE_OFF + SITE_BYTES;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers, + alignment slack
 };
 
 }  // namespace tc
+
+// ---- conv-epilogue non-linear correction (Eq.2 then Eq.3,
+// PAPER.md P:124-139).  A sparse conv whose only consumer is a ReLU /
+// SiLU site and whose c_out fits one N tile (BN >= c_out) runs the site in
+// its epilogue: the tile's 128 delta rows (rounded to the stored bf16 value,
+// R22-BF16) go from TMEM to shared memory, the accumulator is released, and
+// each epilogue warp takes the pixels that START in its 32-row slice: the
+// M rows are in (b, q, t) order, so a pixel's frames are consecutive rows.
+// Per pixel (lanes own channels l + 32 i): x_acc from the conv's dense x0,
+// y_acc = f(x0); per frame x_acc += Delta; c = f(x_acc) - y_acc; warp max;
+// emit iff > theta; y_acc += rnd(c); the emitted row goes to the conv's row
+// layout (in place, as the separate site kernel writes it).  The conv's own
+// delta rows never reach HBM -- except those of the <= 2 pixels per tile that
+// continue into a neighbouring tile, whose rows are written and finished by
+// k_tc_site_fixup (one warp per tile boundary).
+template <int BN>
+__device__ __forceinline__ void site_epilogue(const ConvCall &c, uint32_t taddr, unsigned char *sbuf, int M, int mt,
+                                              int quarter, int lane, bool releaser, uint64_t *tempty_bar) {
+    using namespace tc;
+    using S = Smem<BN, true>;
+    constexpr int SR = S::SROW;
+    constexpr int CPL = BN / 32;
+    bf16 *stg = reinterpret_cast<bf16 *>(sbuf);
+    int32_t *codes = reinterpret_cast<int32_t *>(sbuf + BM * SR * 2);
+    const int C = c.g.Cout;
+    const int rt = quarter * 32 + lane;
+    const int r = mt * BM + rt;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint4 *dst = reinterpret_cast<uint4 *>(stg + rt * SR + c0);
+#pragma unroll
+        for (int j = 0; j < 32; j += 8)
+            dst[j / 8] = make_uint4(pack_bf16x2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
+                                    pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])),
+                                    pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5])),
+                                    pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7])));
+    }
+    codes[rt] = r < M ? __ldg(c.ridx + r) : -1;
+    tc_fence_before();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (releaser) mbar_arrive_remote(tempty_bar, 0);   // the accumulator is free for the next tile
+    // pixels continuing into the previous / next tile (finished by the fix-up kernel)
+    const int r0 = mt * BM;
+    const int g_first = codes[0] >= 0 ? codes[0] >> 5 : -1;
+    const int head = (r0 > 0 && g_first >= 0 && (__ldg(c.ridx + r0 - 1) >> 5) == g_first) ? g_first : -2;
+    const int last = min(BM, M - r0) - 1;
+    const int g_last = last >= 0 ? codes[last] >> 5 : -1;
+    const int tail = (last == BM - 1 && r0 + BM < M && (__ldg(c.ridx + r0 + BM) >> 5) == g_last) ? g_last : -2;
+    const int my = codes[rt];
+    const int gq = my >= 0 ? my >> 5 : -1;
+    bf16 *out = static_cast<bf16 *>(c.out);
+    if (gq >= 0 && (gq == head || gq == tail)) {   // straddler: its delta row, as the conv kernel writes it
+        const uint4 *src = reinterpret_cast<const uint4 *>(stg + rt * SR);
+        for (int j = 0; j < C / 8; j++) reinterpret_cast<uint4 *>(out + (int64_t)(r + 1) * C)[j] = src[j];
+    }
+    const bool start = gq >= 0 && gq != head && gq != tail && (rt == 0 || (codes[rt - 1] >> 5) != gq);
+    uint32_t starts = __ballot_sync(0xffffffffu, start);
+    const float theta = __ldg(c.site.theta);
+    const int kind = c.site.act;
+    while (starts) {
+        const int s = quarter * 32 + __ffs(starts) - 1;
+        starts &= starts - 1;
+        const int g = codes[s] >> 5;
+        const uint32_t touched = c.rowmap ? __ldg(c.a.act + g) : 0xFFFFFFFFu;   // rowmap: gap slots are not touched
+        float xa[CPL], ya[CPL];
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = lane + 32 * i;
+            xa[i] = ch < C ? __ldg(c.site.x0 + (int64_t)g * C + ch) : 0.0f;
+            ya[i] = act_rt(kind, xa[i]);
+        }
+        uint32_t emit = 0;
+        for (int j = s; j < BM; j++) {
+            const int cj = codes[j];
+            if (cj < 0 || (cj >> 5) != g) break;
+            if (!((touched >> (cj & 31)) & 1u)) {   // gap slot: zero Delta, no site step
+                if (c.site.zero_gaps) {
+                    bf16 *o = out + (int64_t)(r0 + j + 1) * C;
+#pragma unroll
+                    for (int i = 0; i < CPL; i++)
+                        if (lane + 32 * i < C) o[lane + 32 * i] = __float2bfloat16_rn(0.0f);
+                }
+                continue;
+            }
+            float cand[CPL];
+            float mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + 32 * i;
+                const float v = ch < C ? __bfloat162float(stg[j * SR + ch]) : 0.0f;
+                xa[i] = __fadd_rn(xa[i], v);                            // reconstruct x (Eq.3)
+                cand[i] = __fsub_rn(act_rt(kind, xa[i]), ya[i]);        // restore the delta
+                mx = fmaxf(mx, fabsf(cand[i]));
+            }
+            mx = gmax<32>(mx, 0xffffffffu);
+            if (mx > theta) {                                           // truncation
+                bf16 *o = out + (int64_t)(r0 + j + 1) * C;
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    const int ch = lane + 32 * i;
+                    cand[i] = bf16_round(cand[i]);
+                    ya[i] = __fadd_rn(ya[i], cand[i]);
+                    if (ch < C) o[ch] = __float2bfloat16_rn(cand[i]);
+                }
+                emit |= 1u << (cj & 31);
+            } else if (c.site.zero_gaps) {
+                bf16 *o = out + (int64_t)(r0 + j + 1) * C;
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + 32 * i < C) o[lane + 32 * i] = __float2bfloat16_rn(0.0f);
+            }
+        }
+        if (lane == 0) c.site.words[g] = emit;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");   // shared rows read before the next tile overwrites them
+}
 
 // SMALL: convs on the network input with c_in <= 4 (stems).  The input delta
 // is the dense per-frame array padded to 4 channels (one aligned 8-byte bf16
@@ -217,12 +349,12 @@ struct Smem {
 // dense array holds zeros where the Subtraction truncated).  Dense mode
 // packs the fp32 reference frame's <= 4 channels into the same layout.
 // Weights are [Cout][ceil(taps/16)*64] with tap-major 4-channel pieces.
-template <int BN, bool DENSE, bool SMALL = false>
+template <int BN, bool DENSE, bool SMALL = false, bool SITE = false>
 __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const __grid_constant__ CUtensorMap tmap_b,
                                                              const __grid_constant__ CUtensorMap tmap_a) {
     st_pdl_enter();
     using namespace tc;
-    using S = Smem<BN>;
+    using S = Smem<BN, SITE>;
     constexpr int STAGES = S::STAGES;
     constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -481,11 +613,12 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     // one TMA 2D load into the same 128B-swizzled layout (rows /
                     // channels past the tensor zero-filled); thread 0 issues it
                     // with the weight tile below, the others only arrive
-                    if (m == 0) {
+                    if (m == 0) {   // thread 0's producer arrival carries the A bytes
                         mbar_arrive_tx(full + stage, S::A_BYTES);
                         tma_load_2d(sa, &tmap_a, ci0, mt * BM, full + stage);
+                    } else {
+                        mbar_arrive(full + stage);
                     }
-                    mbar_arrive(full + stage);
                 } else if (!async_a) {
                     // ---- fp32 activations -> bf16 (RNE): 2 rows x 16 float4 per instruction,
                     // two batches of 8 unconditional loads (an invalid source reads a safe
@@ -589,83 +722,68 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             mbar_wait(tfull + acc, acc_phase);
             tc_fence_after();
             const int r = mt * BM + row_in_tile;
+            if constexpr (SITE && !DENSE) {
+                site_epilogue<BN>(c, tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN,
+                                  smem + S::SITE_OFF, M, mt, quarter, lane, warp == 5 && lane == 0, tempty + acc);
+            } else {
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t v[32];
-                const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int n0 = nt * BN + c0;
-                if (r >= M || n0 >= g.Cout) continue;
-                const bool full_chunk = n0 + 32 <= g.Cout;
-                if (DENSE) {
-                    float *o = static_cast<float *>(c.out) + (int64_t)r * g.Cout + n0;
-                    if (full_chunk) {
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t v[32];
+                    const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    const int n0 = nt * BN + c0;
+                    if (r >= M || n0 >= g.Cout) continue;
+                    const bool full_chunk = n0 + 32 <= g.Cout;
+                    if (DENSE) {
+                        float *o = static_cast<float *>(c.out) + (int64_t)r * g.Cout + n0;
+                        if (full_chunk) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            float4 f;
-                            f.x = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
-                            f.y = __fadd_rn(__uint_as_float(v[j + 1]), __ldg(c.bias + n0 + j + 1));
-                            f.z = __fadd_rn(__uint_as_float(v[j + 2]), __ldg(c.bias + n0 + j + 2));
-                            f.w = __fadd_rn(__uint_as_float(v[j + 3]), __ldg(c.bias + n0 + j + 3));
-                            *reinterpret_cast<float4 *>(o + j) = f;
-                            if (c.act_out) {   // the consuming site's dense output f(x0) (+ bf16 shadow)
-                                float4 a;
-                                a.x = act_rt(c.act_kind, f.x);
-                                a.y = act_rt(c.act_kind, f.y);
-                                a.z = act_rt(c.act_kind, f.z);
-                                a.w = act_rt(c.act_kind, f.w);
-                                *reinterpret_cast<float4 *>(c.act_out + (int64_t)r * g.Cout + n0 + j) = a;
-                                if (c.act_bf)
-                                    *reinterpret_cast<uint2 *>(static_cast<bf16 *>(c.act_bf) + (int64_t)r * g.Cout + n0 + j) =
-                                        make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+                            for (int j = 0; j < 32; j += 4) {
+                                float4 f;
+                                f.x = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
+                                f.y = __fadd_rn(__uint_as_float(v[j + 1]), __ldg(c.bias + n0 + j + 1));
+                                f.z = __fadd_rn(__uint_as_float(v[j + 2]), __ldg(c.bias + n0 + j + 2));
+                                f.w = __fadd_rn(__uint_as_float(v[j + 3]), __ldg(c.bias + n0 + j + 3));
+                                *reinterpret_cast<float4 *>(o + j) = f;
                             }
-                        }
-                    } else if (c.act_out) {
-                        for (int j = 0; j < 32; j++)
-                            if (n0 + j < g.Cout) {
-                                const float x = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
-                                const float a = act_rt(c.act_kind, x);
-                                o[j] = x;
-                                c.act_out[(int64_t)r * g.Cout + n0 + j] = a;
-                                if (c.act_bf) static_cast<bf16 *>(c.act_bf)[(int64_t)r * g.Cout + n0 + j] = __float2bfloat16_rn(a);
-                            }
-                    } else {
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 32; j++)   // unrolled: v[] stays in registers
-                            if (n0 + j < g.Cout) o[j] = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
-                    }
-                } else {
-                    bf16 *o = static_cast<bf16 *>(c.out) + (int64_t)(r + 1) * g.Cout + n0;
-                    if (full_chunk) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            uint4 u;
-                            u.x = pack_bf16x2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
-                            u.y = pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                            u.z = pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
-                            u.w = pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
-                            *reinterpret_cast<uint4 *>(o + j) = u;
+                            for (int j = 0; j < 32; j++)   // unrolled: v[] stays in registers
+                                if (n0 + j < g.Cout) o[j] = __fadd_rn(__uint_as_float(v[j]), __ldg(c.bias + n0 + j));
                         }
                     } else {
+                        bf16 *o = static_cast<bf16 *>(c.out) + (int64_t)(r + 1) * g.Cout + n0;
+                        if (full_chunk) {
 #pragma unroll
-                        for (int j = 0; j < 32; j++)
-                            if (n0 + j < g.Cout) o[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                            for (int j = 0; j < 32; j += 8) {
+                                uint4 u;
+                                u.x = pack_bf16x2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+                                u.y = pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                                u.z = pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+                                u.w = pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
+                                *reinterpret_cast<uint4 *>(o + j) = u;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; j++)
+                                if (n0 + j < g.Cout) o[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                        }
                     }
                 }
+                tc_fence_before();
+                asm volatile("bar.sync 1, 128;" ::: "memory");   // all 4 epilogue warps done with acc
+                if (warp == 5 && lane == 0) mbar_arrive_remote(tempty + acc, 0);
             }
-            tc_fence_before();
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // all 4 epilogue warps done with acc
-            if (warp == 5 && lane == 0) mbar_arrive_remote(tempty + acc, 0);
         }
     }
     __syncwarp();     // reconverge role-divergent warps before the .aligned cluster barrier
@@ -677,13 +795,13 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     }
 }
 
-template <int BN, bool DENSE, bool SMALL = false>
+template <int BN, bool DENSE, bool SMALL = false, bool SITE = false>
 static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s, int num_sms,
                       const CUtensorMap *tmap_a = nullptr) {
-    using S = tc::Smem<BN>;
+    using S = tc::Smem<BN, SITE>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_conv_tc<BN, DENSE, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+        cudaFuncSetAttribute(k_conv_tc<BN, DENSE, SMALL, SITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
         attr = true;
     }
     const int ntn = (c.g.Cout + BN - 1) / BN;
@@ -703,7 +821,7 @@ static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE, SMALL>, c, *tmap, tmap_a ? *tmap_a : *tmap);
+    cudaLaunchKernelEx(&cfg, k_conv_tc<BN, DENSE, SMALL, SITE>, c, *tmap, tmap_a ? *tmap_a : *tmap);
 }
 
 // c_in % 8 == 0 (16-byte bf16 row pieces; each tap zero-padded to a multiple
@@ -752,7 +870,15 @@ int conv_tc_bn(int cout) { return cout >= 256 ? 256 : cout >= 128 ? 128 : cout >
 // TMA descriptor of the bf16 weights [Cout][K] (K contiguous): box 64 x BN,
 // 128-byte swizzle matching the UMMA SWIZZLE_128B K-major smem layout,
 // out-of-bounds rows (Cout not a multiple of BN) zero-filled.
+static bool make_weight_tmap_bn(void *tmap_out, const void *wbf, int K, int Cout, int BN);
 bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout) {
+    return make_weight_tmap_bn(tmap_out, wbf, K, Cout, conv_tc_bn(Cout));
+}
+static int conv_tc_site_bn(int cout);
+bool make_weight_tmap_site(void *tmap_out, const void *wbf, int K, int Cout) {
+    return make_weight_tmap_bn(tmap_out, wbf, K, Cout, conv_tc_site_bn(Cout));
+}
+static bool make_weight_tmap_bn(void *tmap_out, const void *wbf, int K, int Cout, int BN) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -762,7 +888,6 @@ bool make_weight_tmap(void *tmap_out, const void *wbf, int K, int Cout) {
             return false;
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    const int BN = conv_tc_bn(Cout);
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)Cout};
     cuuint64_t strides[1] = {(cuuint64_t)K * 2};
     cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)(BN / 2)};   // half tile per CTA of a pair
@@ -807,6 +932,15 @@ void launch_conv_tc(const ConvCall &c, const void *tmap_v, cudaStream_t s, const
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    if (!c.dense && c.site.on) {   // one N tile covering c_out, the site in the epilogue
+        switch (conv_tc_site_bn(c.g.Cout)) {
+        case 32: launch_tc<32, false, false, true>(c, tmap, s, num_sms, tmap_a); break;
+        case 64: launch_tc<64, false, false, true>(c, tmap, s, num_sms, tmap_a); break;
+        case 128: launch_tc<128, false, false, true>(c, tmap, s, num_sms, tmap_a); break;
+        default: launch_tc<256, false, false, true>(c, tmap, s, num_sms, tmap_a); break;
+        }
+        return;
+    }
 #define TC_BN(BN_) \
     (c.dense ? launch_tc<BN_, true>(c, tmap, s, num_sms, tmap_a) : launch_tc<BN_, false>(c, tmap, s, num_sms, tmap_a))
     switch (conv_tc_bn(c.g.Cout)) {
@@ -816,6 +950,85 @@ void launch_conv_tc(const ConvCall &c, const void *tmap_v, cudaStream_t s, const
     default: TC_BN(32); break;
     }
 #undef TC_BN
+}
+
+
+// ---- conv + site: pixels whose M rows continue across a 128-row tile
+// boundary (their delta rows were written by both tiles' epilogues): one warp
+// per boundary runs the site step of k_site_pw over the pixel's rows (the
+// conv's row layout: rows 1 + pbase .. + popc(act)), in place.
+template <int CPL>
+__global__ void __launch_bounds__(256) k_tc_site_fixup(ConvCall c, DView conv) {
+    st_pdl_enter();
+    const int M = *c.m_dev;
+    const int C = c.g.Cout;
+    const int lane = threadIdx.x & 31;
+    const int nb = (M + tc::BM - 1) / tc::BM;   // boundaries 1 .. nb-1
+    const int k = 1 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    if (k >= nb) return;
+    const int rb = k * tc::BM;
+    const int ga = __ldg(c.ridx + rb - 1) >> 5, gb = __ldg(c.ridx + rb) >> 5;
+    if (ga != gb) return;
+    const int g = ga;
+    uint32_t a = __ldg(conv.act + g);
+    const uint32_t sl = __ldg(conv.slot + g);
+    const int64_t base = 1 + __ldg(conv.pbase + g);
+    const float theta = __ldg(c.site.theta);
+    const int kind = c.site.act;
+    bf16 *out = static_cast<bf16 *>(c.out);
+    float xa[CPL], ya[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; i++) {
+        const int ch = lane + 32 * i;
+        xa[i] = ch < C ? __ldg(c.site.x0 + (int64_t)g * C + ch) : 0.0f;
+        ya[i] = act_rt(kind, xa[i]);
+    }
+    uint32_t emit = 0;
+    while (a) {
+        const int t1 = __ffs(a) - 1;
+        a &= a - 1;
+        const int64_t row = base + __popc(sl & lowmask(t1));
+        float cand[CPL];
+        float mx = 0.0f;
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = lane + 32 * i;
+            const float v = ch < C ? __bfloat162float(out[row * C + ch]) : 0.0f;
+            xa[i] = __fadd_rn(xa[i], v);
+            cand[i] = __fsub_rn(act_rt(kind, xa[i]), ya[i]);
+            mx = fmaxf(mx, fabsf(cand[i]));
+        }
+        mx = gmax<32>(mx, 0xffffffffu);
+        if (mx > theta) {
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const int ch = lane + 32 * i;
+                cand[i] = bf16_round(cand[i]);
+                ya[i] = __fadd_rn(ya[i], cand[i]);
+                if (ch < C) out[row * C + ch] = __float2bfloat16_rn(cand[i]);
+            }
+            emit |= 1u << t1;
+        } else if (c.site.zero_gaps) {
+#pragma unroll
+            for (int i = 0; i < CPL; i++)
+                if (lane + 32 * i < C) out[row * C + lane + 32 * i] = __float2bfloat16_rn(0.0f);
+        }
+    }
+    if (lane == 0) c.site.words[g] = emit;
+}
+
+bool conv_tc_site_eligible(const Geo &g) { return conv_tc_eligible(g) && g.Cout <= 256; }
+static int conv_tc_site_bn(int cout) { return cout <= 32 ? 32 : cout <= 64 ? 64 : cout <= 128 ? 128 : 256; }
+
+void launch_tc_site_fixup(const ConvCall &c, DView conv, cudaStream_t s) {
+    const int64_t nb = (c.m_cap + tc::BM - 1) / tc::BM;   // upper bound of the boundaries
+    const int grid = (int)std::max<int64_t>(1, (nb + 7) / 8);
+    switch (conv_tc_site_bn(c.g.Cout)) {
+    case 32: k_tc_site_fixup<1><<<grid, 256, 0, s>>>(c, conv); break;
+    case 64: k_tc_site_fixup<2><<<grid, 256, 0, s>>>(c, conv); break;
+    case 128: k_tc_site_fixup<4><<<grid, 256, 0, s>>>(c, conv); break;
+    default: k_tc_site_fixup<8><<<grid, 256, 0, s>>>(c, conv); break;
+    }
 }
 
 }  // namespace st

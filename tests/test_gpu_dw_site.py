@@ -151,3 +151,47 @@ def test_rowmap_vs_oracle_fp32():
     for b in range(fr.shape[0]):
         compare_chunk(enc, net, fr[b], th, b, exact=False)
     enc.close()
+
+
+# ---- tcgen05 conv + ReLU / SiLU site in the conv's epilogue (N2; BF16 mode)
+def _tc_site_net(cout, act, k, seed):
+    n = Net(3, 26, 34, f"tcsite{cout}{act}{k}")
+    x = n.relu(n.conv(-1, 32, 3, 1, 1))
+    y = n.conv(x, cout, k, 1, k // 2)                  # tcgen05 conv, c_out <= 256
+    y = n.relu(y) if act == "relu" else n.silu(y)      # its only consumer: site in the epilogue
+    y = n.conv(y, 32, 3, 1, 1)
+    x = n.relu(n.add(y, x))
+    z = n.conv(x, cout, 1, 1, 0)                       # 1x1 on an ADD layout (rowmap) + site
+    z = n.relu(z) if act == "relu" else n.silu(z)
+    n.output(n.conv(z, 16, 1, 1, 0))
+    init_weights(n, seed)
+    return n
+
+
+@pytest.mark.parametrize("cout,act,k", [(32, "relu", 3), (96, "silu", 3), (136, "relu", 1), (256, "silu", 3)])
+def test_tc_site_epilogue_matches_separate(cout, act, k, monkeypatch):
+    """Bit-identical to the separate conv + site kernels (ST_NO_FUSE_TC=1):
+    pixels continuing across 128-row tiles (the fix-up kernel) included --
+    2 chunks x 12 frames of 26x34 give hundreds of tiles per conv."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    net = _tc_site_net(cout, act, k, 40 + cout)
+    fr = torch.from_numpy(frames_for(26, 34, 500 + cout, L=12)).cuda()
+    outs = {}
+    for mode in ("fused", "separate"):
+        if mode == "separate":
+            monkeypatch.setenv("ST_NO_FUSE_TC", "1")
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision="bf16")
+        res = []
+        for th in (0.02, 0.0, 0.08):
+            for _ in range(2):
+                enc.encode_reference(fr[:, 0])
+                enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs[mode] = res
+        enc.close()
+    for (og, cg), (oe, ce) in zip(outs["fused"], outs["separate"]):
+        assert np.array_equal(cg, ce), "per-site per-frame counts"
+        for a, b in zip(og, oe):
+            assert np.array_equal(a, b), f"tap outputs differ (max {np.abs(a - b).max():.3e})"
