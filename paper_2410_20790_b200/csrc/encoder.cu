@@ -70,6 +70,7 @@ struct LayerRT {
     float *wk = nullptr, *bias = nullptr;
     uint16_t *wbf = nullptr;  // bf16 [Cout][K] (tc layers)
     alignas(64) unsigned char tmap[128] = {};   // CUtensorMap of wbf (tc layers)
+    alignas(64) unsigned char tmap_site[128] = {};   // the same weights with the one-tile N box (tc_site)
     // 1x1/s1 tc convs: A-operand TMA maps over contiguous rows (dense: the
     // input's bf16 shadow; sparse: the rowmap layout's rows), re-encoded per plan
     alignas(64) unsigned char tmap_ad[128] = {};
@@ -533,11 +534,14 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             r.act_of = r.src;
         }
     // tcgen05 conv -> ReLU / SiLU (its only consumer, c_out <= 256): the site
-    // runs in the conv's epilogue; the weight map is rebuilt
-    // for the one-tile N width
+    // runs in the conv's epilogue, with a weight map for the
+    // one-tile N width.  Opt-in (ST_FUSE_TC=1): measured slower on every
+    // workload -- the per-pixel site chain in the 4 epilogue warps of one CTA
+    // per SM cannot keep up with the MMA pipeline (cfg5 sparse convs 3.1 ->
+    // 19.7 ms for 3.2 ms of site kernels saved; cfg4 +3 ms; cfg2 +0.1 ms)
     {
-        const char *nf = getenv("ST_NO_FUSE_TC");   // A/B switch
-        if (e->bf && !(nf && nf[0] == '1') && !cfg->streaming && !cfg->debug_retain)
+        const char *ff = getenv("ST_FUSE_TC");
+        if (e->bf && (ff && ff[0] == '1') && !cfg->streaming && !cfg->debug_retain)
             for (int i = 0; i < n; i++) {
                 LayerRT &r = e->L[i];
                 if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0 || r.fused_dw >= 0 || r.fused_pool >= 0 ||
@@ -546,7 +550,7 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
                 LayerRT &cv = e->L[r.src];
                 if (cv.kind != ST_CONV || !cv.tc || cv.n_consumers != 1 || !conv_tc_site_eligible(cv.geo)) continue;
                 const int64_t K = (int64_t)cv.spec.k_h * cv.spec.k_w * conv_tc_cpad(cv.geo.Cin);
-                if (!make_weight_tmap_site(cv.tmap, cv.wbf, (int)K, cv.C))
+                if (!make_weight_tmap_site(cv.tmap_site, cv.wbf, (int)K, cv.C))
                     return fail(e.get(), ST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 cv.tc_site = i;
                 r.fused_tc = r.src;
@@ -1278,7 +1282,8 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                     tc_site_setup(e, l, c, s);
                 }
                 LAUNCH(e, l.tc ? KC_TC_SPARSE : KC_CONV_SPARSE, i, s,
-                       l.tc ? launch_conv_tc(c, l.tmap, s, l.tma_as ? l.tmap_as : nullptr) : launch_conv_f32(c, s));
+                       l.tc ? launch_conv_tc(c, l.tc_site >= 0 ? l.tmap_site : l.tmap, s, l.tma_as ? l.tmap_as : nullptr)
+                            : launch_conv_f32(c, s));
                 if (l.tc_site >= 0) LAUNCH(e, KC_TC_SITE_FIX, l.tc_site, s, launch_tc_site_fixup(c, in, s));
                 c.tma_a = false;
                 c.site.on = false;
@@ -1324,7 +1329,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             LAUNCH(e, l.depthwise ? KC_DW_SPARSE : l.tc ? KC_TC_SPARSE : l.tc_small ? KC_STEM_SPARSE : KC_CONV_SPARSE, i, s,
                    dw_pm        ? launch_dwconv_pm(c, act, pb, s)
                    : l.depthwise ? launch_dwconv_f32(c, s)
-                   : l.tc       ? launch_conv_tc(c, l.tmap, s)
+                   : l.tc       ? launch_conv_tc(c, l.tc_site >= 0 ? l.tmap_site : l.tmap, s)
                    : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
                                 : launch_conv_f32(c, s));
             if (l.tc_site >= 0) {

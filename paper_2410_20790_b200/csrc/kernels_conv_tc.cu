@@ -284,18 +284,37 @@ __device__ __forceinline__ void site_epilogue(const ConvCall &c, uint32_t taddr,
     uint32_t starts = __ballot_sync(0xffffffffu, start);
     const float theta = __ldg(c.site.theta);
     const int kind = c.site.act;
+    // x0 rows (and rowmap touched words) of the next two pixels in flight
+    // while the current one is stepped: the dense x0 of scattered pixels is
+    // an HBM round trip each
+    float p0[CPL], p1[CPL];
+    uint32_t tw0 = 0xFFFFFFFFu, tw1 = 0xFFFFFFFFu;
+    auto fetch = [&](uint32_t st, float (&dst)[CPL], uint32_t &tw) {
+        if (!st) return;
+        const int g = codes[quarter * 32 + __ffs(st) - 1] >> 5;
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            const int ch = lane + 32 * i;
+            dst[i] = ch < C ? __ldg(c.site.x0 + (int64_t)g * C + ch) : 0.0f;
+        }
+        tw = c.rowmap ? __ldg(c.a.act + g) : 0xFFFFFFFFu;   // rowmap: gap slots are not touched
+    };
+    fetch(starts, p0, tw0);
+    fetch(starts & (starts - 1), p1, tw1);
     while (starts) {
         const int s = quarter * 32 + __ffs(starts) - 1;
         starts &= starts - 1;
         const int g = codes[s] >> 5;
-        const uint32_t touched = c.rowmap ? __ldg(c.a.act + g) : 0xFFFFFFFFu;   // rowmap: gap slots are not touched
+        const uint32_t touched = tw0;
         float xa[CPL], ya[CPL];
 #pragma unroll
         for (int i = 0; i < CPL; i++) {
-            const int ch = lane + 32 * i;
-            xa[i] = ch < C ? __ldg(c.site.x0 + (int64_t)g * C + ch) : 0.0f;
+            xa[i] = p0[i];
             ya[i] = act_rt(kind, xa[i]);
+            p0[i] = p1[i];
         }
+        tw0 = tw1;
+        fetch(starts & (starts - 1), p1, tw1);   // the pixel after the next
         uint32_t emit = 0;
         for (int j = s; j < BM; j++) {
             const int cj = codes[j];

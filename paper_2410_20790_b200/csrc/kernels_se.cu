@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_se_delta_sums_v(DView in, int N, int C,
         m_sl[threadIdx.x] = sl;
         m_row[threadIdx.x] = r1;
         __syncthreads();
-        const int np = min(256, p1 - pb);
+        const int np = mine ? min(256, p1 - pb) : 0;   // threads without a (frame, channel group) only stage
         for (int k0 = 0; k0 < np; k0 += 8) {
             float v[8][8];
             uint32_t on = 0;

@@ -170,17 +170,20 @@ def _tc_site_net(cout, act, k, seed):
 
 @pytest.mark.parametrize("cout,act,k", [(32, "relu", 3), (96, "silu", 3), (136, "relu", 1), (256, "silu", 3)])
 def test_tc_site_epilogue_matches_separate(cout, act, k, monkeypatch):
-    """Bit-identical to the separate conv + site kernels (ST_NO_FUSE_TC=1):
-    pixels continuing across 128-row tiles (the fix-up kernel) included --
-    2 chunks x 12 frames of 26x34 give hundreds of tiles per conv."""
+    """The epilogue site (opt-in, ST_FUSE_TC=1) is bit-identical to the
+    separate conv + site kernels: pixels continuing across 128-row tiles (the
+    fix-up kernel) included -- 2 chunks x 12 frames of 26x34 give hundreds of
+    tiles per conv."""
     import torch
     from paper_2410_20790_b200 import Encoder
     net = _tc_site_net(cout, act, k, 40 + cout)
     fr = torch.from_numpy(frames_for(26, 34, 500 + cout, L=12)).cuda()
     outs = {}
     for mode in ("fused", "separate"):
-        if mode == "separate":
-            monkeypatch.setenv("ST_NO_FUSE_TC", "1")
+        if mode == "fused":
+            monkeypatch.setenv("ST_FUSE_TC", "1")
+        else:
+            monkeypatch.delenv("ST_FUSE_TC", raising=False)
         enc = Encoder(net, fr.shape[0], fr.shape[1], precision="bf16")
         res = []
         for th in (0.02, 0.0, 0.08):
