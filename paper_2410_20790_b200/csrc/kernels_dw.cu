@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(32 * DWW_WARPS) k_dwconv_site_w(ConvCall c, Dw
 // the same bits), rounds it, advances y_acc and writes the row.
 constexpr int DWS_WARPS = 8;
 template <int KMAX, class T, int ACT>
-__global__ void __launch_bounds__(32 * DWS_WARPS, 1) k_dwconv_site_wide(ConvCall c, DwSite d) {
+__global__ void __launch_bounds__(32 * DWS_WARPS, 2) k_dwconv_site_wide(ConvCall c, DwSite d) {
     st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 4 : 3;
     constexpr bool PAIR = sizeof(T) == 2;
@@ -1175,7 +1175,7 @@ static void launch_dws_wide_k(const ConvCall &c, const DwSite &d, int64_t BNo, c
         cudaFuncSetAttribute(k_dwconv_site_wide<KMAX, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = smem;
     }
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo + DWS_WARPS - 1) / DWS_WARPS, 148 * 4));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo + DWS_WARPS - 1) / DWS_WARPS, 148 * 8));
     k_dwconv_site_wide<KMAX, T, ACT><<<grid, 32 * DWS_WARPS, smem, s>>>(c, d);
 }
 

@@ -16,8 +16,14 @@ namespace st {
 // ------------------------------------------------------------ subtraction
 // Frame element -> fp32: float frames as they are; uint8 frames v / 255.0f
 // (reading R20; IEEE division, the same value the fp32 input path receives).
-__device__ __forceinline__ float frame_val(const float *p) { return __ldg(p); }
-__device__ __forceinline__ float frame_val(const uint8_t *p) { return __fdiv_rn((float)__ldg(p), 255.0f); }
+__device__ __forceinline__ float frame_val(const float *p, const float *) { return __ldg(p); }
+// uint8: the value v / 255.0f (IEEE division) from a per-CTA table of the
+// 256 quotients -- the same bits, without a division per element
+__device__ __forceinline__ float frame_val(const uint8_t *p, const float *tab) { return tab[__ldg(p)]; }
+__device__ __forceinline__ void fill_u8_table(float *tab) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = __fdiv_rn((float)i, 255.0f);
+    __syncthreads();
+}
 
 template <int C, class T, class FT>
 __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__ ref, int64_t ref_stride,
@@ -25,6 +31,8 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
                                                        int N, int n_diff, const float *__restrict__ theta_p,
                                                        uint32_t *__restrict__ act, T *__restrict__ ddelta) {
     st_pdl_enter();
+    __shared__ float u8tab[256];
+    if (sizeof(FT) == 1) fill_u8_table(u8tab);
     const float theta = __ldg(theta_p);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
@@ -48,7 +56,7 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
         float mx = 0.0f;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            raw[c] = __fsub_rn(frame_val(f + t1 * fs + c), S[c]);
+            raw[c] = __fsub_rn(frame_val(f + t1 * fs + c, u8tab), S[c]);
             mx = fmaxf(mx, fabsf(raw[c]));
         }
         const bool on = mx > theta;             // R1: strict comparison
@@ -74,6 +82,8 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
                                                        const int32_t *__restrict__ pbase, T *__restrict__ rows,
                                                        float *s_save) {
     st_pdl_enter();
+    __shared__ float u8tab[256];
+    if (sizeof(FT) == 1) fill_u8_table(u8tab);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)B * N) return;
     uint32_t w = act[i];
@@ -91,7 +101,7 @@ __global__ void __launch_bounds__(256) k_subtract_rows(const float *__restrict__
         w &= w - 1;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const float e = rnd<T>(__fsub_rn(frame_val(f + t1 * fs + c), S[c]));   // emitted delta
+            const float e = rnd<T>(__fsub_rn(frame_val(f + t1 * fs + c, u8tab), S[c]));   // emitted delta
             S[c] = __fadd_rn(S[c], e);
             str<T>(o + c, e);
         }
