@@ -134,6 +134,9 @@ struct DwSite {
 };
 bool dwconv_site_fusable(const Geo &g);
 void launch_dwconv_site(const ConvCall &c, const DwSite &d, cudaStream_t s);
+// team form (kernels_dw_team.cu): one CTA of ceil(C/256) warps per output pixel, C <= DWT_MAXC
+constexpr int DWT_MAXC = 16 * 256;
+void launch_dwconv_site_team(const ConvCall &c, const DwSite &d, cudaStream_t s);
 // BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu).  Weights bf16
 // [Cout][K] are read through a TMA descriptor (CUtensorMap, 128 bytes)
 // built once at create by make_weight_tmap.

@@ -987,8 +987,9 @@ static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
 // the fmaf chain runs over the taps in (dy, dx) order from +0, bias last
 // (R18; FP32 mode bit-identical to k_dw_tile and the oracle).  Epilogue: the
 // fp32 output, and for a fused site its dense output f(x0) (+ bf16 shadow).
-template <class TS, int KK>
-__global__ void __launch_bounds__(256) k_dw_dense(ConvCall c, int TOH, int TOW) {
+template <class TS, int KK, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int TOW) {
+    constexpr bool WREG = KK > 0 && MINB < 3;   // 3x3 weights in registers (72 floats) unless occupancy is asked for
     st_pdl_enter();
     extern __shared__ __align__(16) unsigned char dwd_smem[];
     const Geo g = c.g;
@@ -1032,8 +1033,8 @@ __global__ void __launch_bounds__(256) k_dw_dense(ConvCall c, int TOH, int TOW) 
     const int c0 = cs0 + cg * 8;
     float bb[8];
     RowIO<float, 8>::load(c.bias + c0, bb);
-    float wr[KK > 0 ? KK * 8 : 1];
-    if constexpr (KK > 0) {
+    float wr[WREG ? KK * 8 : 1];
+    if constexpr (WREG) {
 #pragma unroll
         for (int t = 0; t < KK; t++) RowIO<float, 8>::load(w_s + t * csw + cg * 8, *reinterpret_cast<float(*)[8]>(wr + 8 * t));
     }
@@ -1046,7 +1047,7 @@ __global__ void __launch_bounds__(256) k_dw_dense(ConvCall c, int TOH, int TOW) 
 #pragma unroll
         for (int i = 0; i < 8; i++) acc[i] = 0.0f;
         const TS *base = stg + (size_t)(loy * g.sh * FW + lox * g.sw) * csw + cg * 8;
-        if constexpr (KK > 0) {
+        if constexpr (WREG) {
 #pragma unroll
             for (int t = 0; t < KK; t++) {
                 const int dy = t / (KK == 9 ? 3 : 1), dx = t - dy * (KK == 9 ? 3 : 1);
@@ -1054,6 +1055,16 @@ __global__ void __launch_bounds__(256) k_dw_dense(ConvCall c, int TOH, int TOW) 
                 RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
 #pragma unroll
                 for (int i = 0; i < 8; i++) acc[i] = fmaf(wr[8 * t + i], v[i], acc[i]);
+            }
+        } else if constexpr (KK > 0) {
+#pragma unroll
+            for (int t = 0; t < KK; t++) {
+                const int dy = t / (KK == 9 ? 3 : 1), dx = t - dy * (KK == 9 ? 3 : 1);
+                float v[8], wv[8];
+                RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
+                RowIO<float, 8>::load(w_s + t * csw + cg * 8, wv);
+#pragma unroll
+                for (int i = 0; i < 8; i++) acc[i] = fmaf(wv[i], v[i], acc[i]);
             }
         } else {
             for (int dy = 0; dy < g.kh; dy++)
@@ -1095,12 +1106,22 @@ static bool launch_dw_dense_t(const ConvCall &c, cudaStream_t s) {
     const bool k3 = g.kh == 3 && g.kw == 3;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_dw_dense<TS, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
-        cudaFuncSetAttribute(k_dw_dense<TS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(k_dw_dense<TS, 9, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(k_dw_dense<TS, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(k_dw_dense<TS, 9, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(k_dw_dense<TS, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
         attr = true;
     }
-    if (k3) k_dw_dense<TS, 9><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
-    else k_dw_dense<TS, 0><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+    // default: weights from shared memory, <= 80 registers (3 CTAs / SM)
+    const char *mb = getenv("ST_DW_DENSE_MINB");   // 2: weights in registers (measured 6 % slower on cfg5)
+    const bool occ = !mb || atoi(mb) >= 3;
+    if (occ) {
+        if (k3) k_dw_dense<TS, 9, 3><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+        else k_dw_dense<TS, 0, 3><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+    } else {
+        if (k3) k_dw_dense<TS, 9, 2><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+        else k_dw_dense<TS, 0, 2><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+    }
     return true;
 }
 
@@ -1152,7 +1173,8 @@ void launch_dwconv_pm(const ConvCall &c, const uint32_t *out_act, const int32_t 
 }
 
 bool dwconv_site_fusable(const Geo &g) {
-    return g.Cin % 8 == 0 && g.kh * g.kw <= 25 && DWS_WARPS * (25 * 16 + 3 * g.Cin * 4) <= 200 * 1024;
+    return g.Cin % 8 == 0 && g.kh * g.kw <= 25 &&
+           (g.Cin <= DWT_MAXC || DWS_WARPS * (25 * 16 + 3 * g.Cin * 4) <= 200 * 1024);
 }
 
 template <int G, int KMAX, class T, int ACT>
@@ -1197,6 +1219,15 @@ static void launch_dws_t(const ConvCall &c, const DwSite &d, cudaStream_t s) {
     const int C = c.g.Cin;
     const bool k9 = c.g.kh * c.g.kw <= 9;
     static const bool grouped = [] { const char *v = getenv("ST_DW_GROUPED"); return v && v[0] == '1'; }();
+    // ST_DW_TEAM: 0 = never the team form, 1 (default) = C > 32, 2 = every C
+    // (cfg5: 17.9 -> 12.3 ms of depthwise sites per step with the default;
+    // at C <= 32 the team form idles 28 of 32 lanes: 4.0 -> 10.0 ms)
+    const char *tv = getenv("ST_DW_TEAM");   // read per launch (graph capture): tests switch it
+    const int team = tv ? atoi(tv) : 1;
+    if (team != 0 && C <= DWT_MAXC && ((team >= 1 && C > 32) || team == 2)) {
+        launch_dwconv_site_team(c, d, s);
+        return;
+    }
     if (!grouped && C > 32 && C <= 256) {   // warp per pixel (uniform control flow); C <= 32: 8+ pixels per warp
 #define L_DWW(CPL_)                                                             \
     {                                                                           \

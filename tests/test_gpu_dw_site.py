@@ -42,7 +42,8 @@ def dw_net(C, k, s, act, h, w, seed):
 
 
 CASES = [(8, 3, 1, "relu", 19, 23), (24, 3, 2, "silu", 21, 26), (64, 5, 1, "relu", 14, 17),
-         (136, 3, 1, "silu", 12, 13), (264, 5, 2, "relu", 11, 14), (520, 3, 1, "silu", 9, 10)]
+         (136, 3, 1, "silu", 12, 13), (264, 5, 2, "relu", 11, 14), (520, 3, 1, "silu", 9, 10),
+         (672, 5, 1, "silu", 9, 11), (1152, 5, 1, "relu", 6, 7)]
 
 
 def frames_for(h, w, seed, B=2, L=9):
@@ -74,6 +75,38 @@ def test_fused_dw_site_matches_separate(C, k, s, act, h, w, precision, monkeypat
         assert np.array_equal(cg, ce), "per-site per-frame counts"
         for a, b in zip(og, oe):
             assert np.array_equal(a, b), f"tap outputs differ (max {np.abs(a - b).max():.3e})"
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("C,k,s,act,h,w", CASES)
+def test_dw_site_forms_identical(C, k, s, act, h, w, precision, monkeypatch):
+    """The team forms (one CTA of ceil(C/256) warps per pixel; ST_DW_TEAM=2
+    for every C): the sequential-pipeline kernel (ST_DWT_TB=0) and the
+    frame-pair kernel (ST_DWT_TB=2/4), and the narrow / warp / wide forms
+    (ST_DW_TEAM=0) give the same bits: the per-channel operations are the
+    same, only the work split differs."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    net = dw_net(C, k, s, act, h, w, 7 + C)
+    fr = torch.from_numpy(frames_for(h, w, 300 + C)).cuda()
+    outs = []
+    for team, tb in (("2", "0"), ("2", "2"), ("2", "4"), ("0", "2")):
+        monkeypatch.setenv("ST_DW_TEAM", team)
+        monkeypatch.setenv("ST_DWT_TB", tb)
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.03, 0.0):
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs.append(res)
+        enc.close()
+    for other in outs[1:]:
+        for (og, cg), (oe, ce) in zip(outs[0], other):
+            assert np.array_equal(cg, ce), "per-site per-frame counts"
+            for a, b in zip(og, oe):
+                assert np.array_equal(a, b), f"tap outputs differ (max {np.abs(a - b).max():.3e})"
 
 
 @pytest.mark.parametrize("C,k,s,act,h,w", CASES)
