@@ -526,10 +526,14 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
             LayerRT &r = e->L[i];
             if ((r.kind != ST_RELU && r.kind != ST_SILU) || r.src < 0 || r.fused_dw >= 0 || r.fused_pool >= 0) continue;
             LayerRT &cv = e->L[r.src];
-            // tensor-core convs excluded: their epilogue (4 warps, a row per
-            // thread) is store-bound already; the extra f(x0) + shadow stores
-            // measured slower than the separate activation pass
-            if (cv.kind != ST_CONV || cv.depthwise || cv.n_consumers != 1 || cv.tc || cv.tc_small) continue;
+            // tensor-core convs: the dense epilogue stages 32 x 32 blocks through
+            // shared memory and writes f(x0) (+ bf16 shadow) with the same coalesced
+            // stores (ST_TC_ACT=0: the separate activation pass, as when the
+            // epilogue wrote a row per thread and measured slower)
+            const char *tca = getenv("ST_TC_ACT");   // read per create (tests switch it)
+            const bool tc_act = tca && tca[0] == '1';
+            if (cv.kind != ST_CONV || cv.depthwise || cv.n_consumers != 1) continue;
+            if ((cv.tc || cv.tc_small) && !tc_act) continue;
             cv.act_site = i;
             r.act_of = r.src;
         }

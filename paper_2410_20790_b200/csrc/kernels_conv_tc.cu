@@ -39,7 +39,11 @@ namespace st {
 
 namespace tc {
 
-constexpr int BM = 128, BK = 64, NPROD = 128, NTHREADS = 288;
+// warps 0-3 producers, 4 MMA issuer, 5 .. 5 + NEPI - 1 epilogue: two warps per
+// TMEM lane quarter (each half of the accumulator's 32-column chunks), since
+// the epilogue of one CTA per SM bounds the dense and 1x1 convs
+constexpr int NEPI = 8;
+constexpr int BM = 128, BK = 64, NPROD = 128, NTHREADS = 160 + 32 * NEPI;
 constexpr int SMEM_MAX = 232448;   // 227 KB opt-in dynamic shared memory per CTA
 constexpr int TAPS = 9;   // max k_h*k_w taken by the tensor-core path (1x1, 2x2, 3x3)
 
@@ -197,7 +201,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return r;
 }
 
-template <int BN, bool SITE = false>
+template <int BN, bool SITE = false, bool DSTG = false>
 struct Smem {
     static constexpr int A_BYTES = BM * BK * 2;          // 16 KB: this CTA's 128 rows of the M=256 tile
     static constexpr int B_BYTES = (BN / 2) * BK * 2;    // this CTA's half of the BN weight rows
@@ -206,10 +210,14 @@ struct Smem {
     // their row codes, read back by the site step of the epilogue
     static constexpr int SROW = BN + 8;
     static constexpr int SITE_BYTES = SITE ? BM * SROW * 2 + BM * 4 + 64 : 0;
-    static constexpr int STAGES_FIT = (SMEM_MAX - 256 - 1024 - SITE_BYTES) / STAGE;
+    // DSTG (dense mode): per epilogue warp a 32 x 32 fp32 transpose buffer (row
+    // stride 33), so each store instruction writes whole 128-byte row pieces
+    static constexpr int DSTG_BYTES = DSTG ? NEPI * 32 * 33 * 4 : 0;
+    static constexpr int STAGES_FIT = (SMEM_MAX - 256 - 1024 - SITE_BYTES - DSTG_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int SITE_OFF = STAGES * STAGE;
-    static constexpr int BAR_OFF = SITE_OFF + SITE_BYTES;
+    static constexpr int DSTG_OFF = SITE_OFF + SITE_BYTES;
+    static constexpr int BAR_OFF = DSTG_OFF + DSTG_BYTES;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers, + alignment slack
 };
 
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                                                              const __grid_constant__ CUtensorMap tmap_a) {
     st_pdl_enter();
     using namespace tc;
-    using S = Smem<BN, SITE>;
+    using S = Smem<BN, SITE, DENSE>;
     constexpr int STAGES = S::STAGES;
     constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -732,9 +740,11 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     } else {
         // ===================== epilogue =====================
         const int quarter = warp & 3;            // TMEM lane quarter accessible by this warp
+        const int half = (warp - 5) >> 2;        // which 32-column chunks of the accumulator
         const int row_in_tile = quarter * 32 + lane;
         int it = 0;
-        for (int w = cid; w < nwork; w += ncl, it++) {
+        // the site epilogue (SITE) runs in warps 5-8 only (its barriers count 128 threads)
+        for (int w = cid; w < nwork && !(SITE && !DENSE && half > 0); w += ncl, it++) {
             const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
@@ -746,7 +756,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                                   smem + S::SITE_OFF, M, mt, quarter, lane, warp == 5 && lane == 0, tempty + acc);
             } else {
 #pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
+                for (int c0 = 32 * half; c0 < BN; c0 += 32 * (NEPI / 4)) {
                     uint32_t v[32];
                     const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
                     asm volatile(
@@ -761,6 +771,51 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                         : "r"(taddr));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     const int n0 = nt * BN + c0;
+                    if (DENSE) {
+                        // bias, then a transpose through shared memory: lane l of the
+                        // copy-out covers row 4k + l/8, columns 4(l%8)..+3 -- four whole
+                        // 128-byte row pieces per store instruction (a row per thread
+                        // wrote 32 row pieces of 16 bytes per instruction); the
+                        // consuming site's dense output f(x0) (+ bf16 shadow) from the
+                        // same registers
+                        if (n0 >= g.Cout) continue;   // warp-uniform
+                        float *stg = reinterpret_cast<float *>(smem + S::DSTG_OFF) + (warp - 5) * (32 * 33);
+#pragma unroll
+                        for (int j = 0; j < 32; j++)
+                            stg[lane * 33 + j] =
+                                __fadd_rn(__uint_as_float(v[j]), n0 + j < g.Cout ? __ldg(c.bias + n0 + j) : 0.0f);
+                        __syncwarp();
+                        const int cc = (lane & 7) * 4;
+#pragma unroll
+                        for (int k = 0; k < 8; k++) {
+                            const int rl = 4 * k + (lane >> 3);
+                            const int rr = mt * BM + quarter * 32 + rl;
+                            if (rr < M && n0 + cc < g.Cout) {
+                                float4 f;
+                                f.x = stg[rl * 33 + cc];
+                                f.y = stg[rl * 33 + cc + 1];
+                                f.z = stg[rl * 33 + cc + 2];
+                                f.w = stg[rl * 33 + cc + 3];
+                                const int64_t oi = (int64_t)rr * g.Cout + n0 + cc;
+                                *reinterpret_cast<float4 *>(static_cast<float *>(c.out) + oi) = f;
+                                if (c.act_out) {
+                                    f.x = act_rt(c.act_kind, f.x);
+                                    f.y = act_rt(c.act_kind, f.y);
+                                    f.z = act_rt(c.act_kind, f.z);
+                                    f.w = act_rt(c.act_kind, f.w);
+                                    *reinterpret_cast<float4 *>(c.act_out + oi) = f;
+                                    if (c.act_bf) {
+                                        uint2 u;
+                                        u.x = pack_bf16x2(f.x, f.y);
+                                        u.y = pack_bf16x2(f.z, f.w);
+                                        *reinterpret_cast<uint2 *>(static_cast<bf16 *>(c.act_bf) + oi) = u;
+                                    }
+                                }
+                            }
+                        }
+                        __syncwarp();   // buffer reused by the next chunk
+                        continue;
+                    }
                     if (r >= M || n0 >= g.Cout) continue;
                     const bool full_chunk = n0 + 32 <= g.Cout;
                     if (DENSE) {
@@ -800,7 +855,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     }
                 }
                 tc_fence_before();
-                asm volatile("bar.sync 1, 128;" ::: "memory");   // all 4 epilogue warps done with acc
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");   // all epilogue warps done with acc
                 if (warp == 5 && lane == 0) mbar_arrive_remote(tempty + acc, 0);
             }
         }
@@ -817,7 +872,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
 template <int BN, bool DENSE, bool SMALL = false, bool SITE = false>
 static void launch_tc(const ConvCall &c, const CUtensorMap *tmap, cudaStream_t s, int num_sms,
                       const CUtensorMap *tmap_a = nullptr) {
-    using S = tc::Smem<BN, SITE>;
+    using S = tc::Smem<BN, SITE, DENSE>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_conv_tc<BN, DENSE, SMALL, SITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);

@@ -322,6 +322,140 @@ __global__ void __launch_bounds__(32 * DWT_MAXNW) k_dwconv_site_seq(ConvCall c, 
     }
 }
 
+// Channel-strided sequential form (C <= 64): ONE WARP per output pixel, lane
+// l owns channels l, l + 32 (CPL = ceil(C/32)), so a narrow row is one
+// coalesced 2-byte access per lane and every lane works -- the 8-channel
+// team form idles 28 of 32 lanes at C = 32.  Same pipeline (the next
+// frame's tap rows in flight during the site step) and the same per-channel
+// operations in the same order.
+constexpr int DWS_SEQS_WARPS = 8;
+template <int KMAX, int TB, int CPL, class T, int ACT>
+__global__ void __launch_bounds__(32 * DWS_SEQS_WARPS) k_dwconv_site_seqs(ConvCall c, DwSite d) {
+    st_pdl_enter();
+    const float theta = __ldg(d.theta);
+    const Geo g = c.g;
+    const int Nin = g.Hin * g.Win, Nout = g.Wout * g.Hout;
+    const int C = g.Cin, ntaps = g.kh * g.kw;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int BNo = c.B * Nout;
+    const T *A = static_cast<const T *>(c.a.rows) + lane;
+    T *SR = static_cast<T *>(d.site_rows) + lane;
+    T *CR = d.conv_rows ? static_cast<T *>(d.conv_rows) + lane : nullptr;
+    const float *W = c.wk + lane;
+    const int tdy = lane < ntaps ? lane / g.kw : 0, tdx = lane < ntaps ? lane - tdy * g.kw : 0;
+    const int nwarps = gridDim.x * DWS_SEQS_WARPS;
+    for (int bq = blockIdx.x * DWS_SEQS_WARPS + wid; bq < BNo; bq += nwarps) {
+        uint32_t w = __ldg(d.out_act + bq);
+        if (!w) {
+            if (lane == 0) d.site_act[bq] = 0u;
+            continue;
+        }
+        const int b = bq / Nout, q = bq - b * Nout;
+        const int oy = q / g.Wout, ox = q - oy * g.Wout;
+        uint32_t ma = 0, ms = 0;
+        int mz = 0;
+        if (lane < ntaps) {   // tap lanes: {act, slot, 1 + pbase} of the tap's input pixel
+            const int iy = oy * g.sh - g.ph + tdy, ix = ox * g.sw - g.pw + tdx;
+            if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+                const int bp = b * Nin + iy * g.Win + ix;
+                ma = __ldg(c.a.act + bp);
+                ms = __ldg(c.a.slot + bp);
+                mz = 1 + __ldg(c.a.pbase + bp);
+            }
+        }
+        float xa[CPL], ya[CPL];
+#pragma unroll
+        for (int i = 0; i < CPL; i++) {
+            xa[i] = lane + 32 * i < C ? __ldg(d.x0 + (int64_t)bq * C + lane + 32 * i) : 0.0f;
+            ya[i] = actf<ACT>(xa[i]);
+        }
+        int orow = 1 + __ldg(d.out_pbase + bq);
+        uint32_t emit = 0;
+        // the first TB taps active at frame tt: rows in flight; the rest stay in todo
+        uint32_t todo = 0;
+        int rcur = 0, tp[TB];
+        float v[TB][CPL];
+        auto issue = [&](int tt) {
+            rcur = mz + __popc(ms & lowmask(tt));
+            todo = __ballot_sync(0xffffffffu, (ma >> tt) & 1u);
+#pragma unroll
+            for (int j = 0; j < TB; j++) {
+                tp[j] = todo ? __ffs(todo) - 1 : -1;
+                if (todo) todo &= todo - 1;
+                const int r = __shfl_sync(0xffffffffu, rcur, tp[j] < 0 ? 0 : tp[j]);
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    v[j][i] = (tp[j] >= 0 && lane + 32 * i < C) ? ldr<T>(A + (int64_t)r * C + 32 * i) : 0.0f;
+            }
+        };
+        auto consume = [&](float (&acc)[CPL]) {
+#pragma unroll
+            for (int j = 0; j < TB; j++) {
+                if (tp[j] < 0) continue;
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + 32 * i < C) acc[i] = fmaf(__ldg(W + tp[j] * C + 32 * i), v[j][i], acc[i]);
+            }
+        };
+        int t = __ffs(w) - 1;
+        w &= w - 1;
+        issue(t);
+        while (true) {
+            float acc[CPL];
+#pragma unroll
+            for (int i = 0; i < CPL; i++) acc[i] = 0.0f;
+            consume(acc);
+            while (todo) {   // more than TB active taps (ascending order kept)
+#pragma unroll
+                for (int j = 0; j < TB; j++) {
+                    tp[j] = todo ? __ffs(todo) - 1 : -1;
+                    if (todo) todo &= todo - 1;
+                    const int r = __shfl_sync(0xffffffffu, rcur, tp[j] < 0 ? 0 : tp[j]);
+#pragma unroll
+                    for (int i = 0; i < CPL; i++)
+                        v[j][i] = (tp[j] >= 0 && lane + 32 * i < C) ? ldr<T>(A + (int64_t)r * C + 32 * i) : 0.0f;
+                }
+                consume(acc);
+            }
+            const int tn = w ? __ffs(w) - 1 : -1;
+            if (w) w &= w - 1;
+            if (tn >= 0) issue(tn);   // next frame's rows in flight during the site step
+            // site step (k_site_pw's operations, in its order)
+            float cand[CPL];
+            float mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL; i++) {
+                const float dv = rnd<T>(acc[i]);                   // the conv's stored delta
+                xa[i] = __fadd_rn(xa[i], dv);                      // reconstruct x (Eq.3)
+                cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);      // restore the delta
+                mx = fmaxf(mx, fabsf(cand[i]));
+            }
+            if (CR)
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + 32 * i < C) str<T>(CR + (int64_t)orow * C + 32 * i, acc[i]);
+            mx = gmax<32>(mx, 0xffffffffu);
+            if (mx > theta) {                                      // truncation
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    cand[i] = rnd<T>(cand[i]);
+                    ya[i] = __fadd_rn(ya[i], cand[i]);
+                    if (lane + 32 * i < C) str<T>(SR + (int64_t)orow * C + 32 * i, cand[i]);
+                }
+                emit |= 1u << t;
+            } else if (d.zero_gaps) {                              // a rowmap conv reads this slot as a row
+#pragma unroll
+                for (int i = 0; i < CPL; i++)
+                    if (lane + 32 * i < C) str<T>(SR + (int64_t)orow * C + 32 * i, 0.0f);
+            }
+            orow++;
+            if (tn < 0) break;
+            t = tn;
+        }
+        if (lane == 0) d.site_act[bq] = emit;
+    }
+}
+
 static int dw_sm_count() {
     static int n = 0;
     if (!n) {
@@ -348,6 +482,20 @@ static void launch_team_k(const ConvCall &c, const DwSite &d, cudaStream_t s) {
     k_dwconv_site_team<KMAX, TB, T, ACT><<<grid, 32 * NW, 0, s>>>(c, d);
 }
 
+template <int KMAX, int CPL, class T, int ACT>
+static void launch_seqs_k(const ConvCall &c, const DwSite &d, cudaStream_t s) {
+    const int64_t BNo = (int64_t)c.B * c.g.Hout * c.g.Wout;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dwconv_site_seqs<KMAX, 4, CPL, T, ACT>,
+                                                      32 * DWS_SEQS_WARPS, 0);
+        if (per_sm <= 0) per_sm = 1;
+    }
+    const int64_t want = (BNo + DWS_SEQS_WARPS - 1) / DWS_SEQS_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)dw_sm_count() * per_sm));
+    k_dwconv_site_seqs<KMAX, 4, CPL, T, ACT><<<grid, 32 * DWS_SEQS_WARPS, 0, s>>>(c, d);
+}
+
 template <int KMAX, class T, int ACT>
 static void launch_seq_k(const ConvCall &c, const DwSite &d, cudaStream_t s) {
     const int64_t BNo = (int64_t)c.B * c.g.Hout * c.g.Wout;
@@ -369,6 +517,20 @@ static void launch_team_t(const ConvCall &c, const DwSite &d, cudaStream_t s) {
     const int tbv = tb ? atoi(tb) : 0;
     const bool tb4 = tbv == 4;
     if (tbv != 2 && tbv != 4 && (int64_t)c.B * c.g.Hout * c.g.Wout < (1ll << 31)) {   // row indices are int32 (pbase)
+        // ST_DW_STRIDED=1: the channel-strided warp form for C <= 64 (opt-in: cfg5's
+        // 540x960x32 layer 4.0 -> 6.3 ms against the narrow form, cfg3's 0.70 -> 0.95)
+        const char *sv = getenv("ST_DW_STRIDED");
+        if (c.g.Cin <= 64 && sv && sv[0] == '1') {
+            const bool k9 = c.g.kh * c.g.kw <= 9;
+            if (c.g.Cin <= 32) {
+                if (k9) launch_seqs_k<9, 1, T, ACT>(c, d, s);
+                else launch_seqs_k<25, 1, T, ACT>(c, d, s);
+            } else {
+                if (k9) launch_seqs_k<9, 2, T, ACT>(c, d, s);
+                else launch_seqs_k<25, 2, T, ACT>(c, d, s);
+            }
+            return;
+        }
         if (c.g.kh * c.g.kw <= 9) launch_seq_k<9, T, ACT>(c, d, s);
         else launch_seq_k<25, T, ACT>(c, d, s);
         return;

@@ -248,6 +248,96 @@ __global__ void __launch_bounds__(256) k_se_delta_sums_c(DView in, int N, int C,
     }
 }
 
+// ---- (i-b4) the same sums from per-frame row lists: the CTA bins the
+// active (pixel, frame) rows of each 256-pixel batch by frame in shared
+// memory (ordered: per frame a ballot rank inside the warp plus the earlier
+// warps' counts, so a list is in pixel order and the sums are reproducible),
+// then thread (replica, t, 8-channel group) adds every R-th row of frame t's
+// list -- only rows that exist are loaded (the sweep forms above test every
+// pixel of the batch for every frame), four in flight per thread.
+template <class T>
+__global__ void __launch_bounds__(256) k_se_delta_sums_f(DView in, int N, int C, int F, int ppb, int CS, int R,
+                                                         double *__restrict__ dsum) {
+    st_pdl_enter();
+    extern __shared__ double part[];                    // [R][F][CS], then the lists [F][256] int32
+    int *lst = reinterpret_cast<int *>(part + (size_t)R * F * CS);
+    __shared__ int wcnt[8][32], foff[8][32], fcnt[32];
+    const T *rows = static_cast<const T *>(in.rows);
+    const int b = blockIdx.z, ncg = CS / 8;
+    const int per = F * ncg;
+    const int rep = threadIdx.x / per, rem = threadIdx.x - rep * per;
+    const int t = rem / ncg, cg = rem - t * ncg;
+    const int c0 = blockIdx.y * CS + cg * 8;
+    const bool mine = rep < R && c0 < C;   // C % 8 == 0
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc[i] = 0.0;
+    const int p0 = blockIdx.x * ppb, p1 = min(N, p0 + ppb);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int pb = p0; pb < p1; pb += 256) {
+        const int p = pb + threadIdx.x;
+        uint32_t a = 0, sl = 0;
+        int r1 = 0;
+        if (p < p1) {
+            const int64_t bp = (int64_t)b * N + p;
+            a = __ldg(in.act + bp);
+            if (a) {
+                sl = __ldg(in.slot + bp);
+                r1 = 1 + __ldg(in.pbase + bp);
+            }
+        }
+        for (int f = 0; f < F; f++) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (a >> f) & 1u);
+            if (lane == 0) wcnt[wid][f] = __popc(bal);
+        }
+        __syncthreads();
+        if (threadIdx.x < F) {
+            int o = 0;
+            for (int w = 0; w < 8; w++) {
+                foff[w][threadIdx.x] = o;
+                o += wcnt[w][threadIdx.x];
+            }
+            fcnt[threadIdx.x] = o;
+        }
+        __syncthreads();
+        for (int f = 0; f < F; f++) {   // uniform loop: the ballot again gives this lane's rank at f
+            const uint32_t bal = __ballot_sync(0xffffffffu, (a >> f) & 1u);
+            if ((a >> f) & 1u)
+                lst[f * 256 + foff[wid][f] + __popc(bal & lowmask(lane))] = r1 + __popc(sl & lowmask(f));
+        }
+        __syncthreads();
+        if (mine) {
+            const int n = fcnt[t];
+            const int *L = lst + t * 256;
+            for (int k0 = rep; k0 < n; k0 += 4 * R) {
+                float v[4][8];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int k = k0 + u * R;
+                    const int row = k < n ? L[k] : 0;   // row 0 = zeros
+                    RowIO<T, 8>::load(rows + (int64_t)row * C + c0, v[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+#pragma unroll
+                    for (int i = 0; i < 8; i++) acc[i] += (double)v[u][i];
+            }
+        }
+        __syncthreads();   // lists reused by the next batch
+    }
+    if (mine)
+#pragma unroll
+        for (int i = 0; i < 8; i++) part[((size_t)rep * F + t) * CS + cg * 8 + i] = acc[i];
+    __syncthreads();
+    for (int j = threadIdx.x; j < F * CS; j += blockDim.x) {
+        const int tt = j / CS, cc = blockIdx.y * CS + (j - tt * CS);
+        if (cc >= C) continue;
+        double sum = 0.0;
+        for (int r = 0; r < R; r++) sum += part[((size_t)r * F) * CS + j];
+        if (sum != 0.0) atomicAdd(dsum + ((int64_t)b * F + tt) * C + cc, sum);
+    }
+}
+
 // ---- (i-b3) the same sums with uniform control flow: the CTA compacts the
 // active pixels of each 256-pixel batch (frame word, slot, row base) into
 // shared memory; warp w owns frames t = w, w + 8, ... and walks the list --
@@ -786,9 +876,10 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
         dim3 grid(cdiv(N, ppb), cdiv(C, CS), B);
         const int R = std::max(1, 256 / (F * (CS / 8)));   // replicas of the (t, cg) threads
         const size_t sm = (size_t)R * F * CS * sizeof(double);
-        // default (mode 0): the thread-per-(frame, 8 channels) sweep below; the
-        // compacted-list forms measured slower on cfg5 (kept as A/B switches)
-        static const int mode = [] { const char *v = getenv("ST_SE_SUMS"); return v ? atoi(v) : 0; }();
+        // 3 (default): per-frame row lists (cfg5 delta sums 4.2 -> 2.0 ms per step);
+        // 0: the per-(frame, channel group) sweep; 1 / 2: compacted-pixel forms
+        const char *mv = getenv("ST_SE_SUMS");   // read per launch (graph capture): tests switch it
+        const int mode = mv ? atoi(mv) : 3;
         if (mode == 2) {   // warp per frame over the compacted active pixels
             const int cpl = std::min(8, (C + 31) / 32);
             dim3 gw(cdiv(N, ppb), cdiv(C, 32 * (cpl == 3 ? 4 : cpl > 4 ? 8 : cpl)), B);
@@ -805,6 +896,18 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
                 if (bf) k_se_delta_sums_w<8, bf16><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
                 else k_se_delta_sums_w<8, float><<<gw, 256, 0, s>>>(in, N, C, F, ppb, dsum);
             }
+            return;
+        }
+        const size_t smf = sm + (size_t)F * 256 * 4;
+        if (mode == 3 && smf <= 200 * 1024) {
+            static size_t attr = 0;
+            if (smf > 48 * 1024 && smf > attr) {
+                cudaFuncSetAttribute(k_se_delta_sums_f<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);
+                cudaFuncSetAttribute(k_se_delta_sums_f<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);
+                attr = smf;
+            }
+            if (bf) k_se_delta_sums_f<bf16><<<grid, 256, smf, s>>>(in, N, C, F, ppb, CS, R, dsum);
+            else k_se_delta_sums_f<float><<<grid, 256, smf, s>>>(in, N, C, F, ppb, CS, R, dsum);
             return;
         }
         if (mode == 1 && sm <= 48 * 1024) {

@@ -80,19 +80,23 @@ def test_fused_dw_site_matches_separate(C, k, s, act, h, w, precision, monkeypat
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("C,k,s,act,h,w", CASES)
 def test_dw_site_forms_identical(C, k, s, act, h, w, precision, monkeypatch):
-    """The team forms (one CTA of ceil(C/256) warps per pixel; ST_DW_TEAM=2
-    for every C): the sequential-pipeline kernel (ST_DWT_TB=0) and the
-    frame-pair kernel (ST_DWT_TB=2/4), and the narrow / warp / wide forms
-    (ST_DW_TEAM=0) give the same bits: the per-channel operations are the
-    same, only the work split differs."""
+    """The team forms (ST_DW_TEAM=2: every C): the channel-strided warp form
+    for C <= 64 (ST_DW_STRIDED=1), the 8-channel sequential-pipeline team
+    kernel (ST_DWT_TB=0), the frame-pair kernel (ST_DWT_TB=2/4), and the
+    narrow / warp / wide forms (ST_DW_TEAM=0) give the same bits: the
+    per-channel operations are the same, only the work split differs."""
     import torch
     from paper_2410_20790_b200 import Encoder
     net = dw_net(C, k, s, act, h, w, 7 + C)
     fr = torch.from_numpy(frames_for(h, w, 300 + C)).cuda()
     outs = []
-    for team, tb in (("2", "0"), ("2", "2"), ("2", "4"), ("0", "2")):
-        monkeypatch.setenv("ST_DW_TEAM", team)
-        monkeypatch.setenv("ST_DWT_TB", tb)
+    for env in ({"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "0"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "2", "ST_DW_STRIDED": "1"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "4", "ST_DW_STRIDED": "1"},
+                {"ST_DW_TEAM": "0", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
         res = []
         for th in (0.03, 0.0):

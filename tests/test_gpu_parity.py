@@ -137,6 +137,72 @@ def test_se_site(theta):
         compare_chunk(enc, n, fr[b], theta, b, exact=False)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_se_sums_forms_identical(precision, monkeypatch):
+    """The SE per-frame delta sums (R8) from per-frame row lists
+    (ST_SE_SUMS=3) and from the per-(frame, channel group) sweep (0) give the
+    same outputs and counts: the fp64 sums of the same rows in another order."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    net = W.models.efficientnet_b0(64, 96)
+    init_weights(net, 17)
+    u8 = W.gen_video(2, 9, 64, 96, 3, 77, n_objects=4, size=(8, 24), speed=(1, 3), noise_q=0.1, noise_amp=2)
+    fr = torch.from_numpy(W.to_float(u8)).cuda()
+    outs = []
+    for mode in ("0", "3"):
+        monkeypatch.setenv("ST_SE_SUMS", mode)
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.03, 0.0):
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs.append(res)
+        enc.close()
+    for (og, cg), (oe, ce) in zip(*outs):
+        assert np.array_equal(cg, ce)
+        for a, b in zip(og, oe):
+            assert np.array_equal(a, b), f"max {np.abs(a - b).max():.3e}"
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_tc_dense_act_epilogue_identical(precision, monkeypatch):
+    """A tensor-core conv whose only consumer is a ReLU / SiLU writes the
+    site's dense output f(x0) (+ bf16 shadow) from its staged epilogue
+    (opt-in, ST_TC_ACT=1); the results equal the separate dense activation
+    pass (ST_TC_ACT=0) bit for bit (MBConv expand convs, ResNet-style 3x3
+    convs, a stem)."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    n = Net(3, 24, 40, "tcact")
+    x = n.relu(n.conv(-1, 32, 3, 2, 1))                 # stem (tcgen05 small) + ReLU
+    y = n.silu(n.conv(x, 96, 1, 1, 0))                  # expand 1x1 + SiLU
+    y = n.silu(n.conv(y, 96, 3, 1, 1, groups=96))
+    y = n.conv(y, 40, 1, 1, 0)
+    z = n.relu(n.conv(y, 72, 3, 1, 1))                  # 3x3 tcgen05 + ReLU (c_out not a multiple of 32)
+    n.output(n.conv(z, 16, 1, 1, 0))
+    init_weights(n, 23)
+    u8 = W.gen_video(2, 7, 24, 40, 3, 55, n_objects=3, size=(4, 12), speed=(1, 2), noise_q=0.1, noise_amp=2)
+    fr = torch.from_numpy(W.to_float(u8)).cuda()
+    outs = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ST_TC_ACT", mode)
+        enc = Encoder(n, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.03, 0.0):
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs.append(res)
+        enc.close()
+    for (og, cg), (oe, ce) in zip(*outs):
+        assert np.array_equal(cg, ce)
+        for a, b in zip(og, oe):
+            assert np.array_equal(a, b), f"max {np.abs(a - b).max():.3e}"
+
+
 def test_efficientnet_small():
     net = W.models.efficientnet_b0(64, 64)
     init_weights(net, 13)
