@@ -182,9 +182,10 @@ def ncu_traffic(kernel_class, cid, precision):
     try:
         with open(p) as f:
             d = json.load(f)
-        if d.get("config") != cid or d.get("precision", "bf16") != precision:
+        k = d.get("kernels", {}).get(kernel_class, {})
+        if k.get("config") != cid or k.get("precision", "bf16") != precision:
             return None
-        return d.get("kernels", {}).get(kernel_class, {}).get("dram_bytes_per_launch")
+        return k.get("dram_bytes_per_launch")
     except Exception:
         return None
 

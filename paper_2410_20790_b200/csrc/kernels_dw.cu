@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(256, 3) k_dwconv_pm(ConvCall c, const uint32_t
 // the separate site kernel), so the conv's delta rows never reach HBM
 // (written only when d.conv_rows is set: debug_retain).  Narrow form: C <=
 // G*8, one 8-channel chunk per lane, state in registers.
-template <int G, int KMAX, class T, int ACT>
-__global__ void __launch_bounds__(256, 2) k_dwconv_site(ConvCall c, DwSite d) {
+template <int G, int KMAX, class T, int ACT, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_dwconv_site(ConvCall c, DwSite d) {
     st_pdl_enter();
     constexpr int TB = KMAX > 9 ? 4 : 3;
     constexpr bool PAIR = sizeof(T) == 2;
@@ -1180,13 +1180,21 @@ bool dwconv_site_fusable(const Geo &g) {
 template <int G, int KMAX, class T, int ACT>
 static void launch_dws_k(const ConvCall &c, const DwSite &d, int64_t BNo, cudaStream_t s) {
     constexpr int smem = (256 / G) * KMAX * 16;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_dwconv_site<G, KMAX, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((BNo * G + 255) / 256, 148 * 16));
-    k_dwconv_site<G, KMAX, T, ACT><<<grid, 256, smem, s>>>(c, d);
+    // ST_DWN_MINB: resident CTAs per SM the narrow form is compiled for (2: <= 128
+    // registers; 3: <= 80; 4: <= 64)
+    const char *mb = getenv("ST_DWN_MINB");
+    const int minb = mb ? atoi(mb) : 2;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_dwconv_site<G, KMAX, T, ACT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_dwconv_site<G, KMAX, T, ACT, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_dwconv_site<G, KMAX, T, ACT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
+    attr = true;
+    if (minb == 3) k_dwconv_site<G, KMAX, T, ACT, 3><<<grid, 256, smem, s>>>(c, d);
+    else if (minb == 4) k_dwconv_site<G, KMAX, T, ACT, 4><<<grid, 256, smem, s>>>(c, d);
+    else k_dwconv_site<G, KMAX, T, ACT, 2><<<grid, 256, smem, s>>>(c, d);
 }
 
 template <int KMAX, class T, int ACT>
