@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsparsetem.so")
+# ST_LIB: another in-tree build of the same library (the checked build,
+# libsparsetem_checked.so) -- never a fallback
+LIB_PATH = os.environ.get("ST_LIB") or os.path.join(HERE, "libsparsetem.so")
 
 KIND = dict(conv=0, relu=1, silu=2, maxpool=3, add=4, se=5, output=6)
 PRECISION = dict(fp32=0, bf16=1)

@@ -1,6 +1,6 @@
 """Build libsparsetem.so in-tree with nvcc for sm_100a (no JIT, no torch ext).
 
-    python -m paper_2410_20790_b200.build [--force]
+    python -m paper_2410_20790_b200.build [--force] [--checked]
 
 Every .cu/.cpp under csrc/ is compiled to an object (in parallel) and linked
 into paper_2410_20790_b200/libsparsetem.so.  Flags: -gencode
@@ -19,12 +19,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libsparsetem.so")
+# --checked: -DST_BOUNDS_CHECK (row-index asserts, csrc/common.cuh ST_CHECK) into
+# libsparsetem_checked.so (load it with ST_LIB=<path>); objects kept apart
+CHECKED = "--checked" in sys.argv or os.environ.get("ST_BUILD_CHECKED") == "1"
+OBJ = os.path.join(ROOT, "build", "obj_checked" if CHECKED else "obj")
+LIB = os.path.join(HERE, "libsparsetem_checked.so" if CHECKED else "libsparsetem.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O3",
-          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"]
+          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"] + \
+    (["-DST_BOUNDS_CHECK"] if CHECKED else [])
 
 
 def _sources():

@@ -7,6 +7,26 @@
 
 #include "kernels.h"
 
+// Checked build (python -m paper_2410_20790_b200.build --checked -> libsparsetem_checked.so,
+// -DST_BOUNDS_CHECK): row indices of gathers / scatters against the tensor's
+// row count, a trap with the failing condition on a violation.  The pool's
+// compute-sanitizer is closed, so this build is the memory-safety check.
+#ifdef ST_BOUNDS_CHECK
+#include <cstdio>
+#define ST_CHECK(cond)                                                                   \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("ST_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                   \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define ST_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 namespace st {
 
 // Programmatic dependent launch: inside the captured step graph the edges
@@ -42,6 +62,14 @@ template <> __device__ __forceinline__ void str<bf16>(bf16 *p, float v) { *p = _
 template <class T> __device__ __forceinline__ float rnd(float v);
 template <> __device__ __forceinline__ float rnd<float>(float v) { return v; }
 template <> __device__ __forceinline__ float rnd<bf16>(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+// a pair rounded to the stored type (bf16: one cvt.rn.bf16x2 -- RNE per lane)
+template <class T> __device__ __forceinline__ float2 rnd2(float2 v);
+template <> __device__ __forceinline__ float2 rnd2<float>(float2 v) { return v; }
+template <> __device__ __forceinline__ float2 rnd2<bf16>(float2 v) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(v.y), "f"(v.x));
+    return make_float2(__uint_as_float(r << 16), __uint_as_float(r & 0xFFFF0000u));
+}
 // RNE bf16 rounding of an fp32 value, kept as fp32 (BF16-mode conv operands)
 __device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 // 4 consecutive elements -> float4 (p 4-element aligned)
@@ -72,12 +100,48 @@ __device__ __forceinline__ float sigm_f(float x) { return __fdiv_rn(1.0f, __fadd
 // BF16 mode (tolerance parity, R22-BF16): single-precision MUFU exp and
 // approximate division -- within a few fp32 ulp of the exact form, far below
 // the bf16 rounding of every emitted delta.
-__device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+// x * 1 / (1 + 2^(-x log2 e)) with the flush-to-zero MUFU forms (ex2.approx.ftz,
+// rcp.approx.ftz): five instructions, no denormal range fix-ups (ncu: the
+// __fdividef(x, 1 + __expf(-x)) form cost ~12 per channel in the site kernels,
+// whose per-row instruction count bounds them)
+__device__ __forceinline__ float silu_fast(float x) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return x * r;
+}
+
+// ---- packed fp32x2 (FADD2 / FMUL2 / FFMA2, sm_100): each lane of a pair is
+// rounded exactly as the scalar operation, so results are bit-identical
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// a - b as fma(b, -1, a): one rounding of the exact difference, the same bits
+// as __fsub_rn(a, b) including the signs of zeros
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a); }
+__device__ __forceinline__ float2 silu2_fast(float2 x) {
+    const float2 t = mul2(x, make_float2(-1.4426950408889634f, -1.4426950408889634f));
+    float e0, e1, r0, r1;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t.y));
+    const float2 d = add2(make_float2(e0, e1), make_float2(1.0f, 1.0f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d.y));
+    return mul2(x, make_float2(r0, r1));
+}
 
 // pointwise non-linearity f of a site (kind fixed at compile time / at run time)
 template <int ACT>
 __device__ __forceinline__ float actf(float x) {
     return ACT == ACT_RELU ? relu_f(x) : ACT == ACT_SILU ? silu_f(x) : silu_fast(x);
+}
+// the same on a pair (silu2_fast is silu_fast lane by lane: x * -log2e, 1 + e
+// and x * r round like their scalar forms)
+template <int ACT>
+__device__ __forceinline__ float2 actf2(float2 x) {
+    if constexpr (ACT == ACT_SILU_FAST) return silu2_fast(x);
+    else return make_float2(actf<ACT>(x.x), actf<ACT>(x.y));
 }
 __device__ __forceinline__ float act_rt(int kind, float x) {
     return kind == ACT_RELU ? relu_f(x) : kind == ACT_SILU ? silu_f(x) : silu_fast(x);

@@ -949,7 +949,14 @@ extern "C" st_status st_encode_reference_u8(st_encoder *e, const uint8_t *ref_de
     return ST_OK;
 }
 
+static int64_t rows_cap_of(const st_encoder *e, int t);
+static DView view_of_(const st_encoder *e, int t);
 static DView view_of(const st_encoder *e, int t) {
+    DView v = view_of_(e, t);
+    v.nrows = rows_cap_of(e, t) + 1;
+    return v;
+}
+static DView view_of_(const st_encoder *e, int t) {
     DView v;
     if (t < 0) {
         v.act = e->p<uint32_t>(e->in_act);
@@ -1326,6 +1333,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 d.site_rows = const_cast<void *>(view_of(e, l.dw_site).rows);
                 d.conv_rows = r.b_rows >= 0 ? e->ptr(l.b_rows) : nullptr;   // own site rows: keep the conv's too
                 d.zero_gaps = r.zero_gaps;
+                d.site_nrows = std::min(view_of(e, l.dw_site).nrows, l.rows_cap + 1);
                 LAUNCH(e, KC_DW_SITE, i, s, launch_dwconv_site(c, d, s));
                 break;
             }

@@ -21,6 +21,7 @@ struct DView {
     const uint32_t *slot = nullptr;
     const int32_t *pbase = nullptr;
     const void *rows = nullptr;   // float or bf16 [1+cap][C]
+    int64_t nrows = INT64_MAX;    // 1 + cap (ST_CHECK bounds in the checked build)
 };
 
 struct Geo {   // conv / pool geometry
@@ -131,12 +132,16 @@ struct DwSite {
     void *site_rows = nullptr;           // site emitted rows, in the conv's row layout
     void *conv_rows = nullptr;           // optional (debug_retain): the conv's own delta rows
     bool zero_gaps = false;              // zero rows at touched, not emitted slots (rowmap consumer)
+    int64_t site_nrows = INT64_MAX;      // rows of site_rows / conv_rows (ST_CHECK)
 };
 bool dwconv_site_fusable(const Geo &g);
 void launch_dwconv_site(const ConvCall &c, const DwSite &d, cudaStream_t s);
 // team form (kernels_dw_team.cu): one CTA of ceil(C/256) warps per output pixel, C <= DWT_MAXC
 constexpr int DWT_MAXC = 16 * 256;
 void launch_dwconv_site_team(const ConvCall &c, const DwSite &d, cudaStream_t s);
+// tile form (kernels_dw_team.cu): C <= 32, k x k <= 9, stride <= 2
+bool dwconv_site_tile_ok(const Geo &g);
+void launch_dwconv_site_tile(const ConvCall &c, const DwSite &d, cudaStream_t s);
 // BF16 mode, tcgen05 tensor cores (kernels_conv_tc.cu).  Weights bf16
 // [Cout][K] are read through a TMA descriptor (CUtensorMap, 128 bytes)
 // built once at create by make_weight_tmap.

@@ -610,8 +610,10 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             } else {
                 // this tile's lookups (issued a tile ago) -> delta-row index per tap (-1 = zero)
 #pragma unroll
-                for (int t = 0; t < TAPS; t++)
+                for (int t = 0; t < TAPS; t++) {
                     tapidx[t] = ((n_a[t] >> n_t1) & 1u) ? 1 + n_pb[t] + __popc(n_sl[t] & lowmask(n_t1)) : -1;
+                    ST_CHECK(tapidx[t] < 0 || tapidx[t] < c.a.nrows);
+                }
                 fetch_taps(w + ncl, code_nx);    // next tile's lookups in flight
                 code_nx = code_of(w + 2 * ncl);  // and the row code after that
             }

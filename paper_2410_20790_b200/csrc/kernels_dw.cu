@@ -1232,6 +1232,13 @@ static void launch_dws_t(const ConvCall &c, const DwSite &d, cudaStream_t s) {
     // at C <= 32 the team form idles 28 of 32 lanes: 4.0 -> 10.0 ms)
     const char *tv = getenv("ST_DW_TEAM");   // read per launch (graph capture): tests switch it
     const int team = tv ? atoi(tv) : 1;
+    // ST_DW_TILE (default 1): the tile form for C <= 32, k x k <= 9 (shared-memory
+    // staged footprint rows; cfg5 540x960x32: 4.05 -> 3.47 ms, cfg3 0.70 -> 0.49)
+    const char *tl = getenv("ST_DW_TILE");
+    if (!(tl && tl[0] == '0') && team != 0 && dwconv_site_tile_ok(c.g)) {
+        launch_dwconv_site_tile(c, d, s);
+        return;
+    }
     if (team != 0 && C <= DWT_MAXC && ((team >= 1 && C > 32) || team == 2)) {
         launch_dwconv_site_team(c, d, s);
         return;

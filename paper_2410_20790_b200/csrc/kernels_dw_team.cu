@@ -32,12 +32,15 @@ struct DwVec {   // one lane's 8 channels of a row, raw
         for (int i = 0; i < NV; i++) u[i] = __ldg(reinterpret_cast<const uint4 *>(p) + i);
     }
     __device__ __forceinline__ void fma_into(const float (&w)[8], float (&acc)[8]) const {
-        if constexpr (sizeof(T) == 2) {
+        if constexpr (sizeof(T) == 2) {   // FFMA2: per lane the fmaf of the scalar chain
             const uint32_t v[4] = {u[0].x, u[0].y, u[0].z, u[0].w};
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                acc[2 * q] = fmaf(w[2 * q], __uint_as_float(v[q] << 16), acc[2 * q]);
-                acc[2 * q + 1] = fmaf(w[2 * q + 1], __uint_as_float(v[q] & 0xFFFF0000u), acc[2 * q + 1]);
+                const float2 r = fma2(f2(w[2 * q], w[2 * q + 1]),
+                                      f2(__uint_as_float(v[q] << 16), __uint_as_float(v[q] & 0xFFFF0000u)),
+                                      f2(acc[2 * q], acc[2 * q + 1]));
+                acc[2 * q] = r.x;
+                acc[2 * q + 1] = r.y;
             }
         } else {
             const uint32_t v[8] = {u[0].x, u[0].y, u[0].z, u[0].w, u[1].x, u[1].y, u[1].z, u[1].w};
@@ -190,8 +193,11 @@ __global__ void DWT_MAXREG k_dwconv_site_team(ConvCall c, DwSite d) {
 // the memory parallelism of a frame pair at the register cost of one frame,
 // and half the code (one site step per iteration).  32-bit pixel and row
 // indices (the launcher checks B*N and the row count fit).
+#ifndef DWS_SEQ_BOUNDS
+#define DWS_SEQ_BOUNDS __launch_bounds__(32 * DWT_MAXNW)
+#endif
 template <int KMAX, int TB, class T, int ACT>
-__global__ void __launch_bounds__(32 * DWT_MAXNW) k_dwconv_site_seq(ConvCall c, DwSite d) {
+__global__ void DWS_SEQ_BOUNDS k_dwconv_site_seq(ConvCall c, DwSite d) {
     st_pdl_enter();
     __shared__ float red[2][DWT_MAXNW];
     const int NW = blockDim.x >> 5;
@@ -251,7 +257,10 @@ __global__ void __launch_bounds__(32 * DWT_MAXNW) k_dwconv_site_seq(ConvCall c, 
                 tp[j] = todo ? __ffs(todo) - 1 : -1;
                 if (todo) todo &= todo - 1;
                 const int r = __shfl_sync(0xffffffffu, rcur, tp[j] < 0 ? 0 : tp[j]);
-                if (on && tp[j] >= 0) v[j].load(A + (int64_t)r * C);
+                if (on && tp[j] >= 0) {
+                    ST_CHECK(r > 0 && r < c.a.nrows);
+                    v[j].load(A + (int64_t)r * C);
+                }
             }
         };
         auto consume = [&](float (&acc)[8]) {
@@ -284,16 +293,21 @@ __global__ void __launch_bounds__(32 * DWT_MAXNW) k_dwconv_site_seq(ConvCall c, 
             const int tn = w ? __ffs(w) - 1 : -1;
             if (w) w &= w - 1;
             if (tn >= 0) issue(tn);   // next frame's rows in flight during the site step
-            // site step (k_site_pw's operations, in its order)
+            // site step (k_site_pw's operations, in its order; fp32x2 pairs)
             float cand[8];
             float mx = 0.0f;
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const float dv = rnd<T>(acc[i]);                   // the conv's stored delta
-                xa[i] = __fadd_rn(xa[i], dv);                      // reconstruct x (Eq.3)
-                cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);      // restore the delta
-                mx = fmaxf(mx, fabsf(cand[i]));
+            for (int i = 0; i < 8; i += 2) {
+                const float2 dv = rnd2<T>(f2(acc[i], acc[i + 1]));               // the conv's stored delta
+                const float2 x = add2(f2(xa[i], xa[i + 1]), dv);                 // reconstruct x (Eq.3)
+                const float2 cd = sub2(actf2<ACT>(x), f2(ya[i], ya[i + 1]));     // restore the delta
+                xa[i] = x.x;
+                xa[i + 1] = x.y;
+                cand[i] = cd.x;
+                cand[i + 1] = cd.y;
+                mx = fmaxf(mx, fmaxf(fabsf(cd.x), fabsf(cd.y)));
             }
+            ST_CHECK(orow > 0 && orow < d.site_nrows);
             if (CR && on) RowIO<T, 8>::store(CR + (int64_t)orow * C, acc);
             mx = gmax<32>(mx, 0xffffffffu);
             if (NW > 1) {
@@ -304,9 +318,13 @@ __global__ void __launch_bounds__(32 * DWT_MAXNW) k_dwconv_site_seq(ConvCall c, 
             }
             if (mx > theta) {                                      // truncation
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    cand[i] = rnd<T>(cand[i]);
-                    ya[i] = __fadd_rn(ya[i], cand[i]);
+                for (int i = 0; i < 8; i += 2) {
+                    const float2 r = rnd2<T>(f2(cand[i], cand[i + 1]));
+                    const float2 y = add2(f2(ya[i], ya[i + 1]), r);
+                    cand[i] = r.x;
+                    cand[i + 1] = r.y;
+                    ya[i] = y.x;
+                    ya[i + 1] = y.y;
                 }
                 if (on) RowIO<T, 8>::store(SR + (int64_t)orow * C, cand);
                 emit |= 1u << t;
@@ -456,6 +474,216 @@ __global__ void __launch_bounds__(32 * DWS_SEQS_WARPS) k_dwconv_site_seqs(ConvCa
     }
 }
 
+// Tile form for narrow layers (C <= 32, k x k <= 9; the default there): a CTA
+// owns an output tile of one chunk -- 256 / G pixels, G = ceil(C/8) lanes per
+// pixel, 8 channels per lane.  Rows are ordered (chunk, pixel, frame), so the
+// delta rows of one image row of the tile's input footprint are ONE contiguous
+// range: the CTA copies those ranges (every frame's rows, cp.async 16-byte
+// pieces) into shared memory once, then each pixel group walks its touched
+// frames with the tap rows read from shared memory -- no per-frame global
+// round trips, no per-group metadata walk (the 9 taps' frame / slot words and
+// staged row bases are registers).  A tile whose rows exceed the staging
+// capacity reads its taps from global memory instead (same operations).  Per
+// channel: the fmaf chain over active taps in ascending order from +0, then
+// the site step of k_site_pw -- bit-identical to the other forms.
+constexpr int DWT_TILE_STG = 32 * 1024;   // staged row bytes per CTA
+template <int G, class T, int ACT>
+__global__ void __launch_bounds__(256) k_dwconv_site_tile(ConvCall c, DwSite d, int TH, int TW) {
+    st_pdl_enter();
+    __shared__ float w_s[9 * 32];
+    __shared__ uint32_t f_act[17 * 33], f_sl[17 * 33];
+    __shared__ int32_t f_off[17 * 33];            // staged row of the pixel's first row (-1: outside)
+    __shared__ int32_t r_lo[17], r_len[17], r_so[18];
+    __shared__ int ovf;
+    extern __shared__ __align__(16) unsigned char dwt_stage[];
+    const T *stg = reinterpret_cast<const T *>(dwt_stage);
+    const float theta = __ldg(d.theta);
+    const Geo g = c.g;
+    const int C = g.Cin, kk = g.kh * g.kw;
+    const int Nin = g.Hin * g.Win, Nout = g.Hout * g.Wout;
+    const int ntx = (g.Wout + TW - 1) / TW, nty = (g.Hout + TH - 1) / TH;
+    const int tile = blockIdx.x % (ntx * nty), b = blockIdx.x / (ntx * nty);
+    const int ty = tile / ntx, tx = tile - ty * ntx;
+    const int FH = (TH - 1) * g.sh + g.kh, FW = (TW - 1) * g.sw + g.kw, FP = FH * FW;
+    const int fy0 = ty * TH * g.sh - g.ph, fx0 = tx * TW * g.sw - g.pw;
+    const int tid = threadIdx.x;
+    const T *A = static_cast<const T *>(c.a.rows);
+    for (int i = tid; i < kk * C; i += 256) w_s[(i / C) * 32 + i % C] = __ldg(c.wk + i);
+    // footprint metadata; per footprint image row the contiguous range of rows
+    for (int p = tid; p < FP; p += 256) {
+        const int iy = fy0 + p / FW, ix = fx0 + p % FW;
+        uint32_t a = 0, sl = 0;
+        int off = -1;
+        if (iy >= 0 && iy < g.Hin && ix >= 0 && ix < g.Win) {
+            const int gp = b * Nin + iy * g.Win + ix;
+            a = __ldg(c.a.act + gp);
+            sl = __ldg(c.a.slot + gp);
+            off = 1 + __ldg(c.a.pbase + gp);   // global row for now
+        }
+        f_act[p] = a;
+        f_sl[p] = sl;
+        f_off[p] = off;
+    }
+    __syncthreads();
+    if (tid < FH) {   // row range of footprint row tid (pixels inside the map)
+        int lo = -1, hi = -1;
+        for (int x = 0; x < FW; x++) {
+            const int p = tid * FW + x;
+            if (f_off[p] < 0) continue;
+            if (lo < 0) lo = f_off[p];
+            hi = f_off[p] + __popc(f_sl[p]);
+        }
+        r_lo[tid] = lo;
+        r_len[tid] = lo < 0 ? 0 : hi - lo;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int so = 0;
+        for (int y = 0; y < FH; y++) {
+            r_so[y] = so;
+            so += r_len[y];
+        }
+        r_so[FH] = so;
+        ovf = so * C * (int)sizeof(T) > DWT_TILE_STG;
+    }
+    __syncthreads();
+    const bool use_smem = !ovf;
+    if (use_smem) {
+        // copy the ranges: 16-byte pieces (C % 8 == 0 -> a row is whole pieces)
+        const int ppr = C * (int)sizeof(T) / 16;   // pieces per row
+        const int total = r_so[FH] * ppr;
+        for (int k = tid; k < total; k += 256) {
+            const int srow = k / ppr, pc = k - srow * ppr;
+            int y = 0;
+            while (r_so[y + 1] <= srow) y++;
+            const int64_t grow = r_lo[y] + (srow - r_so[y]);
+            ST_CHECK(grow > 0 && grow < c.a.nrows);
+            const unsigned char *src = reinterpret_cast<const unsigned char *>(A + grow * C) + pc * 16;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                             dwt_stage + (size_t)srow * C * sizeof(T) + pc * 16)),
+                         "l"(src));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // staged row of each footprint pixel's first row
+        for (int p = tid; p < FP; p += 256)
+            if (f_off[p] >= 0) {
+                const int y = p / FW;
+                f_off[p] = r_so[y] + (f_off[p] - r_lo[y]);
+            }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    // ---- the pixel groups
+    const int pix = tid / G, lane = tid % G;
+    const int ly = pix / TW, lx = pix - ly * TW;
+    const int oy = ty * TH + ly, ox = tx * TW + lx;
+    const unsigned gmask = group_mask<G == 3 ? 4 : G>();
+    if (oy >= g.Hout || ox >= g.Wout) return;   // whole groups (G | 32)
+    const int bq = b * Nout + oy * g.Wout + ox;
+    uint32_t w = __ldg(d.out_act + bq);
+    const int c0 = lane * 8;
+    const bool on = c0 < C;
+    if (!w) {
+        if (lane == 0) d.site_act[bq] = 0u;
+        return;
+    }
+    // the 9 taps: frame word, slot word, first row (staged or global)
+    uint32_t ta[9], ts[9];
+    int tr[9];
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+        ta[k] = 0u;
+        ts[k] = 0u;
+        tr[k] = 0;
+        if (k < kk) {
+            const int dy = k / g.kw, dx = k - dy * g.kw;
+            const int p = (ly * g.sh + dy) * FW + lx * g.sw + dx;
+            ta[k] = f_act[p];
+            ts[k] = f_sl[p];
+            tr[k] = f_off[p];
+        }
+    }
+    if (!use_smem)   // global rows: recompute the first rows from the map
+#pragma unroll
+        for (int k = 0; k < 9; k++)
+            if (k < kk && ta[k]) {
+                const int dy = k / g.kw, dx = k - dy * g.kw;
+                const int iy = oy * g.sh - g.ph + dy, ix = ox * g.sw - g.pw + dx;
+                tr[k] = 1 + __ldg(c.a.pbase + b * Nin + iy * g.Win + ix);
+            }
+    float xa[8], ya[8];
+    if (on) {
+        RowIO<float, 8>::load(d.x0 + (int64_t)bq * C + c0, xa);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; i++) xa[i] = 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) ya[i] = actf<ACT>(xa[i]);
+    T *SR = static_cast<T *>(d.site_rows);
+    T *CR = static_cast<T *>(d.conv_rows);
+    int orow = 1 + __ldg(d.out_pbase + bq);
+    uint32_t emit = 0;
+    while (w) {
+        const int t = __ffs(w) - 1;
+        w &= w - 1;
+        const uint32_t lm = lowmask(t);
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) acc[i] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 9; k++) {
+            if (k >= kk || !((ta[k] >> t) & 1u) || !on) continue;
+            const int r = tr[k] + __popc(ts[k] & lm);
+            ST_CHECK(use_smem ? (r >= 0 && r < r_so[FH]) : (r > 0 && r < c.a.nrows));
+            float v[8], wv[8];
+            if (use_smem) RowIO<T, 8>::load(stg + (size_t)r * C + c0, v);
+            else RowIO<T, 8>::load(A + (int64_t)r * C + c0, v);
+            RowIO<float, 8>::load(w_s + k * 32 + c0, wv);
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {   // FFMA2: per lane the fmaf of the scalar chain
+                const float2 r = fma2(f2(wv[i], wv[i + 1]), f2(v[i], v[i + 1]), f2(acc[i], acc[i + 1]));
+                acc[i] = r.x;
+                acc[i + 1] = r.y;
+            }
+        }
+        float cand[8];
+        float mx = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+            const float2 dv = rnd2<T>(f2(acc[i], acc[i + 1]));               // the conv's stored delta
+            const float2 x = add2(f2(xa[i], xa[i + 1]), dv);                 // reconstruct x (Eq.3)
+            const float2 cd = sub2(actf2<ACT>(x), f2(ya[i], ya[i + 1]));     // restore the delta
+            xa[i] = x.x;
+            xa[i + 1] = x.y;
+            cand[i] = cd.x;
+            cand[i + 1] = cd.y;
+            mx = fmaxf(mx, fmaxf(fabsf(cd.x), fabsf(cd.y)));
+        }
+        ST_CHECK(orow > 0 && orow < d.site_nrows);
+        if (CR && on) RowIO<T, 8>::store(CR + (int64_t)orow * C + c0, acc);
+        mx = gmax<G == 3 ? 4 : G>(mx, gmask);
+        if (mx > theta) {                                      // truncation
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+                const float2 r = rnd2<T>(f2(cand[i], cand[i + 1]));
+                const float2 y = add2(f2(ya[i], ya[i + 1]), r);
+                cand[i] = r.x;
+                cand[i + 1] = r.y;
+                ya[i] = y.x;
+                ya[i + 1] = y.y;
+            }
+            if (on) RowIO<T, 8>::store(SR + (int64_t)orow * C + c0, cand);
+            emit |= 1u << t;
+        } else if (d.zero_gaps && on) {                        // a rowmap conv reads this slot as a row
+            const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            RowIO<T, 8>::store(SR + (int64_t)orow * C + c0, z);
+        }
+        orow++;
+    }
+    if (lane == 0) d.site_act[bq] = emit;
+}
+
 static int dw_sm_count() {
     static int n = 0;
     if (!n) {
@@ -551,6 +779,45 @@ void launch_dwconv_site_team(const ConvCall &c, const DwSite &d, cudaStream_t s)
     } else {
         if (d.act == ACT_RELU) launch_team_t<float, ACT_RELU>(c, d, s);
         else launch_team_t<float, ACT_SILU>(c, d, s);
+    }
+}
+
+
+// tile form: C <= 32 (C % 8 == 0), k x k <= 9, stride <= 2 (footprint <= 17 x 33)
+template <int G, class T, int ACT>
+static void launch_tile_k(const ConvCall &c, const DwSite &d, cudaStream_t s) {
+    const int TW = G >= 4 ? 8 : 16, TH = (256 / G) / TW;
+    const int ntx = (c.g.Wout + TW - 1) / TW, nty = (c.g.Hout + TH - 1) / TH;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dwconv_site_tile<G, T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, DWT_TILE_STG);
+        attr = true;
+    }
+    k_dwconv_site_tile<G, T, ACT><<<c.B * ntx * nty, 256, DWT_TILE_STG, s>>>(c, d, TH, TW);
+}
+
+template <class T, int ACT>
+static void launch_tile_t(const ConvCall &c, const DwSite &d, cudaStream_t s) {
+    const int C = c.g.Cin;
+    if (C <= 8) launch_tile_k<1, T, ACT>(c, d, s);
+    else if (C <= 16) launch_tile_k<2, T, ACT>(c, d, s);
+    else launch_tile_k<4, T, ACT>(c, d, s);
+}
+
+bool dwconv_site_tile_ok(const Geo &g) {
+    if (g.Cin > 32 || g.Cin % 8 != 0 || g.kh * g.kw > 9 || g.sh > 2 || g.sw > 2) return false;
+    const int G = g.Cin <= 8 ? 1 : g.Cin <= 16 ? 2 : 4;
+    const int TW = G >= 4 ? 8 : 16, TH = (256 / G) / TW;
+    return (TH - 1) * g.sh + g.kh <= 17 && (TW - 1) * g.sw + g.kw <= 33;
+}
+
+void launch_dwconv_site_tile(const ConvCall &c, const DwSite &d, cudaStream_t s) {
+    if (c.bf) {
+        if (d.act == ACT_RELU) launch_tile_t<bf16, ACT_RELU>(c, d, s);
+        else launch_tile_t<bf16, ACT_SILU_FAST>(c, d, s);
+    } else {
+        if (d.act == ACT_RELU) launch_tile_t<float, ACT_RELU>(c, d, s);
+        else launch_tile_t<float, ACT_SILU>(c, d, s);
     }
 }
 

@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(256) k_se_delta_sums_f(DView in, int N, int C,
                 for (int u = 0; u < 4; u++) {
                     const int k = k0 + u * R;
                     const int row = k < n ? L[k] : 0;   // row 0 = zeros
+                    ST_CHECK(row >= 0 && row < in.nrows);
                     RowIO<T, 8>::load(rows + (int64_t)row * C + c0, v[u]);
                 }
 #pragma unroll

@@ -238,25 +238,52 @@ __global__ void __launch_bounds__(256) k_site_pw(DView in, const float *__restri
                 a &= a - 1;
             }
 #pragma unroll
-            for (int j = 0; j < P; j++)              // issue all P row loads before any use
+            for (int j = 0; j < P; j++) {            // issue all P row loads before any use
+                ST_CHECK(rws[j] >= 0 && rws[j] < in.nrows);
                 row_load<T, CPL>(rows + rws[j] * C, c0, C, full, v[j]);
+            }
 #pragma unroll
             for (int j = 0; j < P; j++) {            // then step the frames in order
                 if (t1s[j] < 0) continue;
                 float cand[CPL];
                 float mx = 0.0f;
+                if constexpr (CPL % 2 == 0) {        // fp32x2 pairs: the same bits as the scalar form
 #pragma unroll
-                for (int i = 0; i < CPL; i++) {
-                    xa[i] = __fadd_rn(xa[i], v[j][i]);                 // reconstruct x (Eq.3)
-                    cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);      // restore the delta
-                    mx = fmaxf(mx, fabsf(cand[i]));
+                    for (int i = 0; i < CPL; i += 2) {
+                        const float2 x = add2(f2(xa[i], xa[i + 1]), f2(v[j][i], v[j][i + 1]));   // Eq.3
+                        const float2 cd = sub2(actf2<ACT>(x), f2(ya[i], ya[i + 1]));
+                        xa[i] = x.x;
+                        xa[i + 1] = x.y;
+                        cand[i] = cd.x;
+                        cand[i + 1] = cd.y;
+                        mx = fmaxf(mx, fmaxf(fabsf(cd.x), fabsf(cd.y)));
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        xa[i] = __fadd_rn(xa[i], v[j][i]);                 // reconstruct x (Eq.3)
+                        cand[i] = __fsub_rn(actf<ACT>(xa[i]), ya[i]);      // restore the delta
+                        mx = fmaxf(mx, fabsf(cand[i]));
+                    }
                 }
                 mx = gmax<G>(mx, mask);
                 if (mx > theta) {                                      // truncation
+                    if constexpr (CPL % 2 == 0) {
 #pragma unroll
-                    for (int i = 0; i < CPL; i++) {
-                        cand[i] = rnd<T>(cand[i]);
-                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                        for (int i = 0; i < CPL; i += 2) {
+                            const float2 r = rnd2<T>(f2(cand[i], cand[i + 1]));
+                            const float2 y = add2(f2(ya[i], ya[i + 1]), r);
+                            cand[i] = r.x;
+                            cand[i + 1] = r.y;
+                            ya[i] = y.x;
+                            ya[i + 1] = y.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < CPL; i++) {
+                            cand[i] = rnd<T>(cand[i]);
+                            ya[i] = __fadd_rn(ya[i], cand[i]);
+                        }
                     }
                     row_store<T, CPL>(out_rows + rws[j] * C, c0, C, full, cand);
                     emit |= 1u << t1s[j];

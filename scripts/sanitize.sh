@@ -10,7 +10,7 @@ out=${1:-gpurun_out/sanitize}
 mkdir -p "$out"
 export ST_NO_GRAPHS=1 PYTHONUNBUFFERED=1
 SEL='tests/test_gpu_parity.py::test_cfg1_toy_exact tests/test_gpu_parity.py::test_random_nets[0] tests/test_gpu_parity.py::test_random_nets[3] tests/test_gpu_parity.py::test_se_site tests/test_gpu_parity.py::test_relu_maxpool_geometries_exact tests/test_gpu_dw_site.py::test_fused_dw_site_matches_separate tests/test_gpu_dw_site.py::test_rowmap_matches_gathered tests/test_gpu_bf16.py::test_tc_conv_kernel_unit tests/test_gpu_bf16.py::test_tc_stem_kernel_unit tests/test_gpu_memory.py::test_capacity_overflow_reissue tests/test_gpu_dw_site.py::test_dw_site_forms_identical tests/test_gpu_parity.py::test_se_sums_forms_identical tests/test_gpu_parity.py::test_tc_dense_act_epilogue_identical'
-for tool in memcheck racecheck synccheck initcheck; do
+for tool in ${SAN_TOOLS:-memcheck racecheck synccheck initcheck}; do
   extra=""
   [ "$tool" = "memcheck" ] && extra="--leak-check no"
   [ "$tool" = "initcheck" ] && extra="--track-unused-memory no"

@@ -43,7 +43,8 @@ def dw_net(C, k, s, act, h, w, seed):
 
 CASES = [(8, 3, 1, "relu", 19, 23), (24, 3, 2, "silu", 21, 26), (64, 5, 1, "relu", 14, 17),
          (136, 3, 1, "silu", 12, 13), (264, 5, 2, "relu", 11, 14), (520, 3, 1, "silu", 9, 10),
-         (672, 5, 1, "silu", 9, 11), (1152, 5, 1, "relu", 6, 7)]
+         (672, 5, 1, "silu", 9, 11), (1152, 5, 1, "relu", 6, 7), (32, 3, 1, "silu", 18, 21),
+         (16, 3, 2, "relu", 20, 37)]
 
 
 def frames_for(h, w, seed, B=2, L=9):
@@ -80,7 +81,8 @@ def test_fused_dw_site_matches_separate(C, k, s, act, h, w, precision, monkeypat
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("C,k,s,act,h,w", CASES)
 def test_dw_site_forms_identical(C, k, s, act, h, w, precision, monkeypatch):
-    """The team forms (ST_DW_TEAM=2: every C): the channel-strided warp form
+    """The tile form for C <= 32 (ST_DW_TILE=1: shared-memory staged
+    footprint rows), the team forms (ST_DW_TEAM=2: every C): the channel-strided warp form
     for C <= 64 (ST_DW_STRIDED=1), the 8-channel sequential-pipeline team
     kernel (ST_DWT_TB=0), the frame-pair kernel (ST_DWT_TB=2/4), and the
     narrow / warp / wide forms (ST_DW_TEAM=0) give the same bits: the
@@ -90,11 +92,12 @@ def test_dw_site_forms_identical(C, k, s, act, h, w, precision, monkeypatch):
     net = dw_net(C, k, s, act, h, w, 7 + C)
     fr = torch.from_numpy(frames_for(h, w, 300 + C)).cuda()
     outs = []
-    for env in ({"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1"},
-                {"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "0"},
-                {"ST_DW_TEAM": "2", "ST_DWT_TB": "2", "ST_DW_STRIDED": "1"},
-                {"ST_DW_TEAM": "2", "ST_DWT_TB": "4", "ST_DW_STRIDED": "1"},
-                {"ST_DW_TEAM": "0", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1"}):
+    for env in ({"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1", "ST_DW_TILE": "1"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1", "ST_DW_TILE": "0"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "0", "ST_DW_STRIDED": "0", "ST_DW_TILE": "0"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "2", "ST_DW_STRIDED": "1", "ST_DW_TILE": "0"},
+                {"ST_DW_TEAM": "2", "ST_DWT_TB": "4", "ST_DW_STRIDED": "1", "ST_DW_TILE": "0"},
+                {"ST_DW_TEAM": "0", "ST_DWT_TB": "0", "ST_DW_STRIDED": "1", "ST_DW_TILE": "0"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
