@@ -160,6 +160,12 @@ struct st_encoder {
     std::vector<GraphEnt> graphs;
     cudaStream_t gstream = nullptr;            // capture / replay stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // dense / diff overlap: the reference (dense) pass of every layer runs on
+    // dstream up to ov_k layers ahead of the diff pass (0 = one stream)
+    int ov_k = 0;
+    cudaStream_t dstream = nullptr;
+    std::vector<cudaEvent_t> ev_d, ev_s;
+    cudaEvent_t ev_dfork = nullptr, ev_djoin = nullptr;
     // state
     int staged_chunks = 0;       // >0 after encode_reference
     // streaming continuation (N1): cont = the chunks already ran a diff call
@@ -562,6 +568,11 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     }
     for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
     e->cap_fit.assign(n + 1, -1);
+    {   // ST_OVERLAP=0: one stream; ST_OVERLAP_K: lookahead in layers (default 3)
+        const char *ov = getenv("ST_OVERLAP"), *ok = getenv("ST_OVERLAP_K"), *np = getenv("ST_PDL");
+        const bool off = (ov && ov[0] == '0') || cfg->streaming || cfg->debug_retain || (np && np[0] == '1');
+        e->ov_k = off ? 0 : std::max(1, ok ? atoi(ok) : 3);
+    }
     st_status r = plan(e.get());
     if (r == ST_OK) r = alloc_fixed(e.get());
     if (r == ST_OK) encode_act_maps(e.get());
@@ -787,6 +798,15 @@ static st_status plan(st_encoder *e) {
             const LayerRT &cv = e->L[e->L[e->L[i].fused_relu].src];
             if (cv.b_y0 >= 0) e->bufs[cv.b_y0].last = std::max(e->bufs[cv.b_y0].last, t_of(i));
         }
+    // dense / diff overlap: a layer's dense op may run up to ov_k layers ahead of
+    // its step (it waits for the diff pass of layer i - ov_k), so every buffer a
+    // dense op writes -- y0, its bf16 shadow, the SE's sums / gate table -- is
+    // live from ov_k steps earlier; consumers still finish by their own step
+    // (a diff op waits for the dense op of its layer)
+    if (e->ov_k > 0)
+        for (auto &l : e->L)
+            for (int id : {l.b_y0, l.b_ybf, l.b_se})
+                if (id >= 0) e->bufs[id].first = std::max(0, e->bufs[id].first - e->ov_k);
     // ---- first-fit arena assignment, largest first
     std::vector<int> order(e->bufs.size());
     for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
@@ -879,6 +899,17 @@ static st_status alloc_fixed(st_encoder *e) {
     CUDA_OK(e, cudaStreamCreateWithFlags(&e->gstream, cudaStreamNonBlocking));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+    if (e->ov_k > 0) {
+        CUDA_OK(e, cudaStreamCreateWithFlags(&e->dstream, cudaStreamNonBlocking));
+        CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_dfork, cudaEventDisableTiming));
+        CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_djoin, cudaEventDisableTiming));
+        e->ev_d.resize(e->L.size());
+        e->ev_s.resize(e->L.size());
+        for (size_t i = 0; i < e->L.size(); i++) {
+            CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_d[i], cudaEventDisableTiming));
+            CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_s[i], cudaEventDisableTiming));
+        }
+    }
     (void)take(0);
     CUDA_OK(e, cudaMalloc(&e->ref, B * Nin * e->in_C * 4));
     // zero rows (row 0 of every rows buffer) are written per step (arena reuse)
@@ -901,6 +932,11 @@ extern "C" void st_encoder_destroy(st_encoder *e) {
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->gstream) cudaStreamDestroy(e->gstream);
+    if (e->dstream) cudaStreamDestroy(e->dstream);
+    if (e->ev_dfork) cudaEventDestroy(e->ev_dfork);
+    if (e->ev_djoin) cudaEventDestroy(e->ev_djoin);
+    for (auto ev : e->ev_d) cudaEventDestroy(ev);
+    for (auto ev : e->ev_s) cudaEventDestroy(ev);
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     delete e;
 }
@@ -1190,6 +1226,20 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
     };
     const float *S0 = cont ? e->p<float>(e->in_S) : e->ref;   // Subtraction buffer at call start
     if (strm && !cont) fcopy(e->in_S, e->ref, B * per);
+    // dense / diff overlap: dense ops on sD, diff ops on s; the diff
+    // ops of layer i wait for its dense op, the dense op of layer i for the
+    // diff ops of layer i - ov_k (the arena's lifetimes assume that bound)
+    const bool ov = e->ov_k > 0 && !strm && F > 0;
+    cudaStream_t sD = ov ? e->dstream : s;
+    if (ov) {
+        CUDA_OK(e, cudaEventRecord(e->ev_dfork, s));
+        CUDA_OK(e, cudaStreamWaitEvent(sD, e->ev_dfork, 0));
+    }
+    auto dense_done = [&](int i) {
+        if (!ov) return;
+        cudaEventRecord(e->ev_d[i], sD);
+        cudaStreamWaitEvent(s, e->ev_d[i], 0);
+    };
 
     // ---------------- input site: Subtraction + truncation + compaction (a2)
     if (F > 0) {
@@ -1222,7 +1272,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
     export_words(-1);
 
     if (e->in_refbf >= 0 && !cont)
-        LAUNCH(e, KC_DENSE_MISC, -1, s, launch_pad4_bf16(e->ref, (int64_t)B * Nin, e->in_C, e->ptr(e->in_refbf), s));
+        LAUNCH(e, KC_DENSE_MISC, -1, sD, launch_pad4_bf16(e->ref, (int64_t)B * Nin, e->in_C, e->ptr(e->in_refbf), sD));
     // ---------------- layers in topological order, dense then diff ("N")
     for (int i = 0; i < n; i++) {
         LayerRT &l = e->L[i];
@@ -1232,6 +1282,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
         const float *x_src = dense_of(e, l.src);
         long long *st = e->stats + 3 * i;
         DView in = F > 0 ? view_of(e, l.src) : DView{};
+        if (ov && i >= e->ov_k) cudaStreamWaitEvent(sD, e->ev_s[i - e->ov_k], 0);
         // rows_in / touched of this layer: roofline accounting only, collected
         // when profiling is on (st_set_profiling) so the timed step skips them
         if (F > 0 && l.kind != ST_OUTPUT && e->prof && l.fused_relu < 0)
@@ -1258,14 +1309,15 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
                 c.act_kind = r.kind == ST_RELU ? ACT_RELU : bf ? ACT_SILU_FAST : ACT_SILU;
             }
             if (!cont)
-                LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, s,
-                       l.depthwise  ? launch_dwconv_f32(c, s)
-                       : l.tc       ? (c.tma_a = l.tma_ad, launch_conv_tc(c, l.tmap, s, l.tma_ad ? l.tmap_ad : nullptr))
-                       : l.tc_small ? launch_conv_tc_small(c, l.tmap, s)
-                                    : launch_conv_f32(c, s));
+                LAUNCH(e, l.depthwise ? KC_DW_DENSE : l.tc ? KC_TC_DENSE : l.tc_small ? KC_STEM_DENSE : KC_CONV_DENSE, i, sD,
+                       l.depthwise  ? launch_dwconv_f32(c, sD)
+                       : l.tc       ? (c.tma_a = l.tma_ad, launch_conv_tc(c, l.tmap, sD, l.tma_ad ? l.tmap_ad : nullptr))
+                       : l.tc_small ? launch_conv_tc_small(c, l.tmap, sD)
+                                    : launch_conv_f32(c, sD));
             c.tma_a = false;
             if (l.b_ybf >= 0 && !cont)
-                LAUNCH(e, KC_DENSE_MISC, i, s, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, s));
+                LAUNCH(e, KC_DENSE_MISC, i, sD, launch_to_bf16(e->p<float>(l.b_y0), ybf_of(e, i), (int64_t)B * N * l.C, sD));
+            dense_done(i);
             if (F == 0) break;
             if (l.rowmap) {   // 1x1/s1: a plain GEMM over the rows of the input's layout
                 zero_row(l.b_rows, l.C);
@@ -1363,8 +1415,9 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             const bool skip_dense = (l.fused_pool >= 0 && !strm && !e->cfg.debug_retain) || l.fused_dw >= 0 ||
                                     l.act_of >= 0;
             if (!cont && !skip_dense)
-                LAUNCH(e, KC_DENSE_MISC, i, s,
-                       launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), s));
+                LAUNCH(e, KC_DENSE_MISC, i, sD,
+                       launch_dense_act(x_src, e->p<float>(l.b_y0), (int64_t)B * N * l.C, dense_kind, ybf_of(e, i), sD));
+            dense_done(i);
             SiteState sst;
             const float *x_init = x_src;
             if (strm && l.sx[0] >= 0) {   // in-place state; first call: from the dense reference pass
@@ -1393,10 +1446,11 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
         case ST_MAXPOOL: {
             if (!cont) {
                 const bool relu_in = l.fused_relu >= 0 && !strm && !e->cfg.debug_retain;
-                LAUNCH(e, KC_DENSE_MISC, i, s,
+                LAUNCH(e, KC_DENSE_MISC, i, sD,
                        launch_dense_maxpool(relu_in ? dense_of(e, e->L[l.fused_relu].src) : x_src,
-                                            e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), s, relu_in));
+                                            e->p<float>(l.b_y0), B, l.geo, ybf_of(e, i), sD, relu_in));
             }
+            dense_done(i);
             // streaming state: x_acc of the input pixels ping-pongs (windows of
             // neighbouring tiles share pixels), y_acc of the outputs in place
             SiteState sst;
@@ -1462,8 +1516,9 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
         case ST_ADD: {
             const float *x2 = dense_of(e, l.src2);
             if (!cont)
-                LAUNCH(e, KC_DENSE_MISC, i, s,
-                       launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, ybf_of(e, i), s));
+                LAUNCH(e, KC_DENSE_MISC, i, sD,
+                       launch_dense_add(x_src, x2, e->p<float>(l.b_y0), (int64_t)B * N * l.C, ybf_of(e, i), sD));
+            dense_done(i);
             if (F == 0) break;
             DView in2 = view_of(e, l.src2);
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
@@ -1485,14 +1540,21 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             uint32_t *refresh = reinterpret_cast<uint32_t *>(s_tab + (int64_t)B * (F + 1) * l.C);
             float *gate_tab = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(refresh + B) + 63) & ~uintptr_t(63));
             const int H = l.spec.se_hidden;
-            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_colsum(x_src, B, (int)N, l.C, sum0, s));
-            if (F > 0) LAUNCH(e, KC_SE_SUMS, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
-            LAUNCH(e, KC_SE_SUMS, i, s,
-                   launch_se_schedule(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2,
-                                      thresholds + l.site, gate_tab, s_tab, refresh, s));
-            LAUNCH(e, KC_SE_SUMS, i, s,
-                   launch_se_dense_apply(x_src, s_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), ybf_of(e, i), s));
+            // dense part: the reference gates (frame 0) depend on sum0 alone; the
+            // dense apply reads gate_tab row 0 (= s_tab row 0, same layout)
+            LAUNCH(e, KC_SE_SUMS, i, sD, launch_se_colsum(x_src, B, (int)N, l.C, sum0, sD));
+            LAUNCH(e, KC_SE_SUMS, i, sD,
+                   launch_se_gates(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2, 0, 1,
+                                   gate_tab, sD));
+            LAUNCH(e, KC_SE_SUMS, i, sD,
+                   launch_se_dense_apply(x_src, gate_tab, B, (int)N, l.C, F, e->p<float>(l.b_y0), ybf_of(e, i), sD));
+            dense_done(i);
             if (F == 0) break;
+            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_delta_sums(in, B, (int)N, l.C, F, bf, dsum, s));
+            LAUNCH(e, KC_SE_SUMS, i, s,
+                   launch_se_gates(sum0, dsum, B, (int)N, l.C, H, F, l.se_w1, l.se_b1, l.se_w2, l.se_b2, 1, F,
+                                   gate_tab, s));
+            LAUNCH(e, KC_SE_SUMS, i, s, launch_se_sched(gate_tab, B, l.C, F, thresholds + l.site, s_tab, refresh, s));
             uint32_t *slot = e->p<uint32_t>(l.b_slot);
             int32_t *pb = e->p<int32_t>(l.b_pbase);
             LAUNCH(e, KC_SE_SUMS, i, s, launch_se_slots(in.act, refresh, B, (int)N, slot, s));
@@ -1507,6 +1569,7 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
             break;
         }
         case ST_OUTPUT: {
+            dense_done(i);
             DView v = F > 0 ? in : DView{};
             float *o_state = strm ? e->p<float>(l.sx[0]) : nullptr;   // last output = next call's frame 0
             LAUNCH(e, KC_ACCUM, i, s,
@@ -1520,7 +1583,12 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
         // a fused ReLU's words are written by its pool's pass
         if (l.kind != ST_OUTPUT && l.fused_pool < 0) export_words(i);
         if (l.fused_relu >= 0) export_words(l.fused_relu);
+        if (ov) cudaEventRecord(e->ev_s[i], s);
         (void)Cs;
+    }
+    if (ov) {   // join the dense stream back
+        CUDA_OK(e, cudaEventRecord(e->ev_djoin, sD));
+        CUDA_OK(e, cudaStreamWaitEvent(s, e->ev_djoin, 0));
     }
     CUDA_OK(e, cudaGetLastError());
     return ST_OK;

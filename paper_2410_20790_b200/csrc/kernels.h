@@ -223,6 +223,13 @@ void launch_se_delta_sums(DView in, int B, int N, int C, int F, bool bf, double 
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                         const float *b1, const float *w2, const float *b2, const float *theta, float *gate_tab,
                         float *s_tab, uint32_t *refresh, cudaStream_t s);
+// split form of launch_se_schedule: gates of frames t0 .. t0 + nt - 1 (frame 0 =
+// the reference, from sum0 alone: the dense pass computes it, the diff pass
+// frames 1 .. F), then the sequential refresh schedule over frames 1 .. F
+void launch_se_gates(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
+                     const float *b1, const float *w2, const float *b2, int t0, int nt, float *gate_tab, cudaStream_t s);
+void launch_se_sched(const float *gate_tab, int B, int C, int F, const float *theta, float *s_tab, uint32_t *refresh,
+                     cudaStream_t s);
 // y (fp32) and ybf (bf16 shadow) each nullable
 void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, void *ybf,
                            cudaStream_t s);

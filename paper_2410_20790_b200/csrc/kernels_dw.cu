@@ -1064,7 +1064,11 @@ __global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int
                 RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
                 RowIO<float, 8>::load(w_s + t * csw + cg * 8, wv);
 #pragma unroll
-                for (int i = 0; i < 8; i++) acc[i] = fmaf(wv[i], v[i], acc[i]);
+                for (int i = 0; i < 8; i += 2) {   // FFMA2: per lane the scalar fmaf
+                    const float2 r = fma2(f2(wv[i], wv[i + 1]), f2(v[i], v[i + 1]), f2(acc[i], acc[i + 1]));
+                    acc[i] = r.x;
+                    acc[i + 1] = r.y;
+                }
             }
         } else {
             for (int dy = 0; dy < g.kh; dy++)

@@ -433,12 +433,12 @@ __device__ void se_gate_block(const float *m, int C, int H, const float *w1, con
 // is accumulated in frame order (as the sequential schedule would).
 __global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum0, const double *__restrict__ dsum,
                                                   int N, int C, int H, int F, const float *w1, const float *b1,
-                                                  const float *w2, const float *b2, float *__restrict__ gate_tab) {
+                                                  const float *w2, const float *b2, int t0, float *__restrict__ gate_tab) {
     st_pdl_enter();
     extern __shared__ float sm[];
     float *mean = sm;          // [C]
     float *hid = mean + C;     // [H]
-    const int t = blockIdx.x, b = blockIdx.y;
+    const int t = t0 + blockIdx.x, b = blockIdx.y;
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
         double run = sum0[(int64_t)b * C + c];
         for (int t1 = 0; t1 < t; t1++) run += dsum[((int64_t)b * F + t1) * C + c];
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(256) k_se_site(DView in, const float *__restri
             if (lane == 0) out_act[bp] = 0;
             continue;
         }
-        const int b = (int)(bp / N);
+        const int b = BN < (1ll << 31) ? (int)bp / N : (int)(bp / N);   // 32-bit division when it fits
         const float *st = s_tab + (int64_t)b * (F + 1) * C;
         const uint32_t a = __ldg(in.act + bp);
         float xa[CPL], ya[CPL];
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(256) k_se_site_v(DView in, const float *__rest
             if (lane == 0) out_act[bp] = 0;
             continue;
         }
-        const int b = (int)(bp / N);
+        const int b = BN < (1ll << 31) ? (int)bp / N : (int)(bp / N);   // 32-bit division when it fits
         const float *st = s_tab + (int64_t)b * (F + 1) * C;
         {
             float s0[CPL];
@@ -700,18 +700,44 @@ __global__ void __launch_bounds__(256) k_se_site_v(DView in, const float *__rest
                 const bool act = (a >> t1) & 1u;
                 float cand[CPL];
                 float mx = 0.0f;
+                if constexpr (CPL % 2 == 0) {   // fp32x2 pairs: the scalar form's bits per lane
 #pragma unroll
-                for (int i = 0; i < CPL; i++) {
-                    if (act) xa[i] = __fadd_rn(xa[i], v[j][i]);
-                    cand[i] = __fsub_rn(__fmul_rn(xa[i], sn[j][i]), ya[i]);
-                    mx = fmaxf(mx, fabsf(cand[i]));
+                    for (int i = 0; i < CPL; i += 2) {
+                        float2 x = f2(xa[i], xa[i + 1]);
+                        if (act) x = add2(x, f2(v[j][i], v[j][i + 1]));
+                        const float2 cd = sub2(mul2(x, f2(sn[j][i], sn[j][i + 1])), f2(ya[i], ya[i + 1]));
+                        xa[i] = x.x;
+                        xa[i + 1] = x.y;
+                        cand[i] = cd.x;
+                        cand[i + 1] = cd.y;
+                        mx = fmaxf(mx, fmaxf(fabsf(cd.x), fabsf(cd.y)));
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        if (act) xa[i] = __fadd_rn(xa[i], v[j][i]);
+                        cand[i] = __fsub_rn(__fmul_rn(xa[i], sn[j][i]), ya[i]);
+                        mx = fmaxf(mx, fabsf(cand[i]));
+                    }
                 }
                 mx = gmax<G>(mx, mask);
                 if (mx > theta) {
+                    if constexpr (CPL % 2 == 0) {
 #pragma unroll
-                    for (int i = 0; i < CPL; i++) {
-                        cand[i] = rnd<T>(cand[i]);
-                        ya[i] = __fadd_rn(ya[i], cand[i]);
+                        for (int i = 0; i < CPL; i += 2) {
+                            const float2 r = rnd2<T>(f2(cand[i], cand[i + 1]));
+                            const float2 y = add2(f2(ya[i], ya[i + 1]), r);
+                            cand[i] = r.x;
+                            cand[i + 1] = r.y;
+                            ya[i] = y.x;
+                            ya[i + 1] = y.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < CPL; i++) {
+                            cand[i] = rnd<T>(cand[i]);
+                            ya[i] = __fadd_rn(ya[i], cand[i]);
+                        }
                     }
                     if (c0 < C) row_store<T, CPL>(out_rows + (obase + __popc(Tw & lowmask(t1))) * (int64_t)C, c0, C,
                                                   full, cand);
@@ -755,7 +781,7 @@ __global__ void __launch_bounds__(32 * SE_WIDE_WARPS) k_se_site_wide(DView in, c
             if (lane == 0) out_act[bp] = 0;
             continue;
         }
-        const int b = (int)(bp / N);
+        const int b = BN < (1ll << 31) ? (int)bp / N : (int)(bp / N);   // 32-bit division when it fits
         const float *st = s_tab + (int64_t)b * (F + 1) * C;
         const uint32_t a = __ldg(in.act + bp);
         const int ibase = a ? 1 + __ldg(in.pbase + bp) : 0;
@@ -835,7 +861,30 @@ void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, in
         cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    k_se_gates<<<dim3(F + 1, B), 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, gate_tab);
+    k_se_gates<<<dim3(F + 1, B), 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, 0, gate_tab);
+    static size_t attr2 = 0;
+    const size_t smem2 = (size_t)C * 4;
+    if (smem2 > 48 * 1024 && smem2 > attr2) {
+        cudaFuncSetAttribute(k_se_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        attr2 = smem2;
+    }
+    k_se_schedule<<<B, 256, smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
+}
+
+void launch_se_gates(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
+                     const float *b1, const float *w2, const float *b2, int t0, int nt, float *gate_tab, cudaStream_t s) {
+    if (nt <= 0) return;
+    const size_t smem = (size_t)(C + H) * 4;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    k_se_gates<<<dim3(nt, B), 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, t0, gate_tab);
+}
+
+void launch_se_sched(const float *gate_tab, int B, int C, int F, const float *theta, float *s_tab, uint32_t *refresh,
+                     cudaStream_t s) {
     static size_t attr2 = 0;
     const size_t smem2 = (size_t)C * 4;
     if (smem2 > 48 * 1024 && smem2 > attr2) {

@@ -203,6 +203,42 @@ def test_tc_dense_act_epilogue_identical(precision, monkeypatch):
             assert np.array_equal(a, b), f"max {np.abs(a - b).max():.3e}"
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("model", ["effnet", "resnet"])
+def test_dense_diff_overlap_identical(precision, model, monkeypatch):
+    """The reference (dense) pass on its own stream, up to ST_OVERLAP_K layers
+    ahead of the diff pass (arena lifetimes extended to match), gives the same
+    outputs and counts as one stream (ST_OVERLAP=0), eager and replayed from
+    the captured graph, with lookahead 1 and 3."""
+    import torch
+    from paper_2410_20790_b200 import Encoder
+    if model == "effnet":
+        net = W.models.efficientnet_b0(64, 96)
+    else:
+        net = W.models.resnet18(64, 96)
+    init_weights(net, 29)
+    u8 = W.gen_video(2, 9, 64, 96, 3, 81, n_objects=4, size=(8, 24), speed=(1, 3), noise_q=0.1, noise_amp=2)
+    fr = torch.from_numpy(W.to_float(u8)).cuda()
+    outs = []
+    for ov, k in (("0", "3"), ("1", "1"), ("1", "3")):
+        monkeypatch.setenv("ST_OVERLAP", ov)
+        monkeypatch.setenv("ST_OVERLAP_K", k)
+        enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
+        res = []
+        for th in (0.03, 0.03, 0.0):   # first sight eager, then graph capture + replay
+            enc.encode_reference(fr[:, 0])
+            enc.encode_diff(fr[:, 1:], th)
+            torch.cuda.synchronize()
+            res.append(([enc.outputs(t).cpu().numpy().copy() for t in enc.taps], enc.get_sparsity()[0].copy()))
+        outs.append(res)
+        enc.close()
+    for other in outs[1:]:
+        for (og, cg), (oe, ce) in zip(outs[0], other):
+            assert np.array_equal(cg, ce)
+            for a, b in zip(og, oe):
+                assert np.array_equal(a, b), f"max {np.abs(a - b).max():.3e}"
+
+
 def test_efficientnet_small():
     net = W.models.efficientnet_b0(64, 64)
     init_weights(net, 13)
