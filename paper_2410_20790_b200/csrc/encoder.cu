@@ -1229,7 +1229,9 @@ static st_status issue_step(st_encoder *e, const void *frames_dev, bool u8, int 
     // dense / diff overlap: dense ops on sD, diff ops on s; the diff
     // ops of layer i wait for its dense op, the dense op of layer i for the
     // diff ops of layer i - ov_k (the arena's lifetimes assume that bound)
-    const bool ov = e->ov_k > 0 && !strm && F > 0;
+    // (profiled passes run on one stream: their per-launch event times are the
+    // kernels' own, not the overlap's; the arena's lifetimes hold either way)
+    const bool ov = e->ov_k > 0 && !strm && F > 0 && !e->prof;
     cudaStream_t sD = ov ? e->dstream : s;
     if (ov) {
         CUDA_OK(e, cudaEventRecord(e->ev_dfork, s));

@@ -39,8 +39,8 @@ namespace st {
 
 namespace tc {
 
-// warps 0-3 producers, 4 MMA issuer, 5 .. 5 + NEPI - 1 epilogue: two groups of
-// four warps (one per TMEM lane quarter each) draining alternate tiles, since
+// warps 0-3 producers, 4 MMA issuer, 5 .. 5 + NEPI - 1 epilogue: two warps per
+// TMEM lane quarter (each half of the accumulator's 32-column chunks), since
 // the epilogue of one CTA per SM bounds the dense and 1x1 convs
 constexpr int NEPI = 8;
 constexpr int BM = 128, BK = 64, NPROD = 128, NTHREADS = 160 + 32 * NEPI;
@@ -213,12 +213,12 @@ struct Smem {
     // DSTG (dense mode): per epilogue warp a 32 x 32 fp32 transpose buffer (row
     // stride 33), so each store instruction writes whole 128-byte row pieces
     static constexpr int DSTG_BYTES = DSTG ? NEPI * 32 * 33 * 4 : 0;
-    static constexpr int STAGES_FIT = (SMEM_MAX - 512 - 1024 - SITE_BYTES - DSTG_BYTES) / STAGE;
+    static constexpr int STAGES_FIT = (SMEM_MAX - 256 - 1024 - SITE_BYTES - DSTG_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int SITE_OFF = STAGES * STAGE;
     static constexpr int DSTG_OFF = SITE_OFF + SITE_BYTES;
     static constexpr int BAR_OFF = DSTG_OFF + DSTG_BYTES;
-    static constexpr int TOTAL = BAR_OFF + 512 + 1024;   // + barriers, + alignment slack
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers, + alignment slack
 };
 
 }  // namespace tc
@@ -383,20 +383,15 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     using namespace tc;
     using S = Smem<BN, SITE, DENSE>;
     constexpr int STAGES = S::STAGES;
-    // accumulators in TMEM (512 columns): 4 while they fit, so the MMAs run up
-    // to 3 tiles ahead of the epilogue; two epilogue groups (warps 5-8, 9-12)
-    // drain alternate tiles concurrently (the site epilogue: one group, 2 accs)
-    constexpr int NACC = (SITE && !DENSE) ? 2 : (BN <= 128 ? 4 : 2);
-    constexpr int NGRP = (SITE && !DENSE) ? 1 : 2;
-    constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
+    constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);   // this CTA's stage landed
     uint64_t *pfull = full + STAGES;     // leader only: the peer's stage landed (relayed)
     uint64_t *empty = pfull + STAGES;
     uint64_t *tfull = empty + STAGES;
-    uint64_t *tempty = tfull + NACC;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NACC);
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const Geo g = c.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -423,7 +418,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             mbar_init(pfull + s, 1);          // the peer's relay
             mbar_init(empty + s, 1);          // the leader's multicast MMA commit
         }
-        for (int a = 0; a < NACC; a++) {
+        for (int a = 0; a < 2; a++) {
             mbar_init(tfull + a, 1);          // the leader's multicast MMA commit
             mbar_init(tempty + a, 2);         // both CTAs' epilogues drained the accumulator
         }
@@ -710,8 +705,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
             uint32_t phase = 0;
             int it = 0;
             for (int w = cid; w < nwork; w += ncl, it++) {
-                const int acc = it % NACC;
-                const uint32_t acc_phase = (it / NACC) & 1;
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(tempty + acc, acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + acc * BN;
@@ -747,15 +742,14 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
     } else {
         // ===================== epilogue =====================
         const int quarter = warp & 3;            // TMEM lane quarter accessible by this warp
-        const int grp = (warp - 5) >> 2;         // epilogue group: tiles it with it % NGRP == grp
+        const int half = (warp - 5) >> 2;        // which 32-column chunks of the accumulator
         const int row_in_tile = quarter * 32 + lane;
         int it = 0;
         // the site epilogue (SITE) runs in warps 5-8 only (its barriers count 128 threads)
-        for (int w = cid; w < nwork && grp < NGRP; w += ncl, it++) {
-            if (NGRP > 1 && it % NGRP != grp) continue;   // the other group's tile
+        for (int w = cid; w < nwork && !(SITE && !DENSE && half > 0); w += ncl, it++) {
             const int mt = 2 * (w / ntn) + (int)rank, nt = w % ntn;
-            const int acc = it % NACC;                    // NGRP | NACC: an accumulator has one group
-            const uint32_t acc_phase = (it / NACC) & 1;
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(tfull + acc, acc_phase);
             tc_fence_after();
             const int r = mt * BM + row_in_tile;
@@ -764,7 +758,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                                   smem + S::SITE_OFF, M, mt, quarter, lane, warp == 5 && lane == 0, tempty + acc);
             } else {
 #pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
+                for (int c0 = 32 * half; c0 < BN; c0 += 32 * (NEPI / 4)) {
                     uint32_t v[32];
                     const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
                     asm volatile(
@@ -863,8 +857,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1) k_conv_tc(ConvCall c, const _
                     }
                 }
                 tc_fence_before();
-                asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group's 4 warps done with acc
-                if (warp == 5 + 4 * grp && lane == 0) mbar_arrive_remote(tempty + acc, 0);
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");   // all epilogue warps done with acc
+                if (warp == 5 && lane == 0) mbar_arrive_remote(tempty + acc, 0);
             }
         }
     }

@@ -977,8 +977,9 @@ static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
 }
 
 // Dense (reference-frame) depthwise, register form.  A CTA owns an output
-// tile of one chunk and a channel slice of <= 64 channels (8-channel groups,
-// ncg | 256 so every thread keeps ONE group for the whole tile).  The tile's
+// tile of one chunk and a channel slice of <= 64 channels (8-channel groups;
+// every thread keeps ONE group for the whole tile, the threads past the last
+// whole pixel group idle when the group count does not divide 256).  The tile's
 // input footprint is staged once into shared memory, zero-padded, already in
 // the contract's operand precision (BF16 mode: bf16-rounded values stored as
 // bf16, R22-BF16; FP32 mode: fp32), so the inner loop is per tap one
@@ -989,7 +990,7 @@ static void launch_dw_t(const ConvCall &c, cudaStream_t s) {
 // fp32 output, and for a fused site its dense output f(x0) (+ bf16 shadow).
 template <class TS, int KK, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int TOW) {
-    constexpr bool WREG = KK > 0 && MINB < 3;   // 3x3 weights in registers (72 floats) unless occupancy is asked for
+    constexpr bool WREG = KK == 9 && MINB < 3;   // 3x3 weights in registers (72 floats) unless occupancy is asked for
     st_pdl_enter();
     extern __shared__ __align__(16) unsigned char dwd_smem[];
     const Geo g = c.g;
@@ -1029,7 +1030,7 @@ __global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int
         RowIO<TS, 8>::store(stg + (size_t)p * csw + cg * 8, v);   // bf16 staging rounds (RNE)
     }
     __syncthreads();
-    const int cg = tid % ncg;               // fixed per thread (ncg | 256)
+    const int cg = tid % ncg;               // fixed per thread
     const int c0 = cs0 + cg * 8;
     float bb[8];
     RowIO<float, 8>::load(c.bias + c0, bb);
@@ -1039,7 +1040,9 @@ __global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int
         for (int t = 0; t < KK; t++) RowIO<float, 8>::load(w_s + t * csw + cg * 8, *reinterpret_cast<float(*)[8]>(wr + 8 * t));
     }
     const int TOc = TOH * TOW;
-    for (int o = tid / ncg; o < TOc; o += 256 / ncg) {
+    // ncg need not divide 256: the threads past the last whole pixel group idle
+    const int o0 = tid < (256 / ncg) * ncg ? tid / ncg : TOc;
+    for (int o = o0; o < TOc; o += 256 / ncg) {
         const int loy = o / TOW, lox = o - loy * TOW;
         const int oy = ty * TOH + loy, ox = tx * TOW + lox;
         if (oy >= g.Hout || ox >= g.Wout) continue;
@@ -1050,7 +1053,7 @@ __global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int
         if constexpr (WREG) {
 #pragma unroll
             for (int t = 0; t < KK; t++) {
-                const int dy = t / (KK == 9 ? 3 : 1), dx = t - dy * (KK == 9 ? 3 : 1);
+                const int dy = t / (KK == 25 ? 5 : 3), dx = t - dy * (KK == 25 ? 5 : 3);
                 float v[8];
                 RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
 #pragma unroll
@@ -1059,7 +1062,7 @@ __global__ void __launch_bounds__(256, MINB) k_dw_dense(ConvCall c, int TOH, int
         } else if constexpr (KK > 0) {
 #pragma unroll
             for (int t = 0; t < KK; t++) {
-                const int dy = t / (KK == 9 ? 3 : 1), dx = t - dy * (KK == 9 ? 3 : 1);
+                const int dy = t / (KK == 25 ? 5 : 3), dx = t - dy * (KK == 25 ? 5 : 3);
                 float v[8], wv[8];
                 RowIO<TS, 8>::load(base + (size_t)(dy * FW + dx) * csw, v);
                 RowIO<float, 8>::load(w_s + t * csw + cg * 8, wv);
@@ -1097,8 +1100,6 @@ template <class TS>
 static bool launch_dw_dense_t(const ConvCall &c, cudaStream_t s) {
     const Geo &g = c.g;
     if (g.Cin % 8 != 0) return false;
-    for (int cs0 = 0; cs0 < g.Cin; cs0 += 64)   // every slice's group count divides 256
-        if (256 % (std::min(64, g.Cin - cs0) / 8) != 0) return false;
     const int csw = std::min(64, g.Cin);
     const int stg_budget = 64 * 1024;
     const int fp_max = std::min<int>(1024, stg_budget / (csw * (int)sizeof(TS)));
@@ -1107,20 +1108,22 @@ static bool launch_dw_dense_t(const ConvCall &c, cudaStream_t s) {
     const int FP = ((TOH - 1) * g.sh + g.kh) * ((TOW - 1) * g.sw + g.kw);
     const size_t sm = (size_t)g.kh * g.kw * 64 * 4 + (size_t)FP * csw * sizeof(TS) + 64;
     const int64_t grid = (int64_t)c.B * ((g.Hout + TOH - 1) / TOH) * ((g.Wout + TOW - 1) / TOW) * ((g.Cin + 63) / 64);
-    const bool k3 = g.kh == 3 && g.kw == 3;
+    const bool k3 = g.kh == 3 && g.kw == 3, k5 = g.kh == 5 && g.kw == 5;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_dw_dense<TS, 9, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
         cudaFuncSetAttribute(k_dw_dense<TS, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
         cudaFuncSetAttribute(k_dw_dense<TS, 9, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(k_dw_dense<TS, 25, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
         cudaFuncSetAttribute(k_dw_dense<TS, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
         attr = true;
     }
     // default: weights from shared memory, <= 80 registers (3 CTAs / SM)
     const char *mb = getenv("ST_DW_DENSE_MINB");   // 2: weights in registers (measured 6 % slower on cfg5)
     const bool occ = !mb || atoi(mb) >= 3;
-    if (occ) {
+    if (occ) {   // 3x3 / 5x5 unrolled (weights from shared memory), other shapes looped
         if (k3) k_dw_dense<TS, 9, 3><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
+        else if (k5) k_dw_dense<TS, 25, 3><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
         else k_dw_dense<TS, 0, 3><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);
     } else {
         if (k3) k_dw_dense<TS, 9, 2><<<(unsigned)grid, 256, sm, s>>>(c, TOH, TOW);

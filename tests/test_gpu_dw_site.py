@@ -44,7 +44,7 @@ def dw_net(C, k, s, act, h, w, seed):
 CASES = [(8, 3, 1, "relu", 19, 23), (24, 3, 2, "silu", 21, 26), (64, 5, 1, "relu", 14, 17),
          (136, 3, 1, "silu", 12, 13), (264, 5, 2, "relu", 11, 14), (520, 3, 1, "silu", 9, 10),
          (672, 5, 1, "silu", 9, 11), (1152, 5, 1, "relu", 6, 7), (32, 3, 1, "silu", 18, 21),
-         (16, 3, 2, "relu", 20, 37)]
+         (16, 3, 2, "relu", 20, 37), (240, 5, 1, "silu", 10, 12)]
 
 
 def frames_for(h, w, seed, B=2, L=9):
