@@ -411,12 +411,34 @@ __global__ void __launch_bounds__(256) k_se_delta_sums_w(DView in, int N, int C,
 }
 
 // gate of one chunk from fp32 means m[C] (block-wide; hid/gate in smem)
+// SE_WCH: channels of W1 staged per round (row stride SE_WCH + 1: conflict-free)
+constexpr int SE_WCH = 128;
 __device__ void se_gate_block(const float *m, int C, int H, const float *w1, const float *b1, const float *w2,
-                              const float *b2, float *hid, float *gate) {
-    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+                              const float *b2, float *hid, float *gate, float *wbuf) {
+    if (H <= (int)blockDim.x) {
+        // W1 staged through shared memory in SE_WCH-channel rounds (coalesced,
+        // all threads loading): the per-output fmaf chain over c ascending is
+        // unchanged, but its operands no longer wait on one global load each
+        const int j = threadIdx.x;
         float acc = 0.0f;
-        for (int c = 0; c < C; c++) acc = fmaf(__ldg(w1 + (int64_t)j * C + c), m[c], acc);
-        hid[j] = silu_f(__fadd_rn(acc, __ldg(b1 + j)));
+        for (int c0 = 0; c0 < C; c0 += SE_WCH) {
+            const int cw = min(SE_WCH, C - c0);
+            for (int i = threadIdx.x; i < H * cw; i += blockDim.x) {
+                const int jj = i / cw, k = i - jj * cw;
+                wbuf[jj * (SE_WCH + 1) + k] = __ldg(w1 + (int64_t)jj * C + c0 + k);
+            }
+            __syncthreads();
+            if (j < H)
+                for (int k = 0; k < cw; k++) acc = fmaf(wbuf[j * (SE_WCH + 1) + k], m[c0 + k], acc);
+            __syncthreads();
+        }
+        if (j < H) hid[j] = silu_f(__fadd_rn(acc, __ldg(b1 + j)));
+    } else {
+        for (int j = threadIdx.x; j < H; j += blockDim.x) {
+            float acc = 0.0f;
+            for (int c = 0; c < C; c++) acc = fmaf(__ldg(w1 + (int64_t)j * C + c), m[c], acc);
+            hid[j] = silu_f(__fadd_rn(acc, __ldg(b1 + j)));
+        }
     }
     __syncthreads();
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -438,6 +460,7 @@ __global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum
     extern __shared__ float sm[];
     float *mean = sm;          // [C]
     float *hid = mean + C;     // [H]
+    float *wbuf = hid + H;     // [H][SE_WCH + 1] (H <= blockDim.x)
     const int t = t0 + blockIdx.x, b = blockIdx.y;
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
         double run = sum0[(int64_t)b * C + c];
@@ -445,7 +468,7 @@ __global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum
         mean[c] = (float)(run / (double)N);
     }
     __syncthreads();
-    se_gate_block(mean, C, H, w1, b1, w2, b2, hid, gate_tab + ((int64_t)b * (F + 1) + t) * C);
+    se_gate_block(mean, C, H, w1, b1, w2, b2, hid, gate_tab + ((int64_t)b * (F + 1) + t) * C, wbuf);
 }
 
 // ---- (ii-b) refresh schedule, one CTA per chunk (frames sequential):
@@ -855,7 +878,7 @@ void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStr
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                         const float *b1, const float *w2, const float *b2, const float *theta, float *gate_tab,
                         float *s_tab, uint32_t *refresh, cudaStream_t s) {
-    const size_t smem = (size_t)(C + H) * 4;
+    const size_t smem = (size_t)(C + H + (H <= 256 ? H * (SE_WCH + 1) : 0)) * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -874,7 +897,7 @@ void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, in
 void launch_se_gates(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                      const float *b1, const float *w2, const float *b2, int t0, int nt, float *gate_tab, cudaStream_t s) {
     if (nt <= 0) return;
-    const size_t smem = (size_t)(C + H) * 4;
+    const size_t smem = (size_t)(C + H + (H <= 256 ? H * (SE_WCH + 1) : 0)) * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
