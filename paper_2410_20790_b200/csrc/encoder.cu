@@ -900,7 +900,19 @@ static st_status alloc_fixed(st_encoder *e) {
     CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
     CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     if (e->ov_k > 0) {
-        CUDA_OK(e, cudaStreamCreateWithFlags(&e->dstream, cudaStreamNonBlocking));
+        // ST_OVERLAP_PRIO: the dense stream's priority relative to the diff pass
+        // (-1 lower -- the default: the diff pass is the critical path --, 0 equal,
+        // 1 higher); the capture / replay stream carries the diff pass
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        const char *pp = getenv("ST_OVERLAP_PRIO");
+        const int pr = pp ? atoi(pp) : -1;
+        if (pr != 0) {
+            cudaStreamDestroy(e->gstream);
+            CUDA_OK(e, cudaStreamCreateWithPriority(&e->gstream, cudaStreamNonBlocking, pr < 0 ? greatest : least));
+        }
+        CUDA_OK(e, cudaStreamCreateWithPriority(&e->dstream, cudaStreamNonBlocking,
+                                                pr < 0 ? least : pr > 0 ? greatest : least));
         CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_dfork, cudaEventDisableTiming));
         CUDA_OK(e, cudaEventCreateWithFlags(&e->ev_djoin, cudaEventDisableTiming));
         e->ev_d.resize(e->L.size());
@@ -1147,7 +1159,8 @@ static st_status encode_diff(st_encoder *e, const void *frames_dev, bool u8, int
                 if (r) return r;
                 if (ce != cudaSuccess) return fail(e, ST_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
                 if (e->use_pdl) make_edges_programmatic(g);
-                CUDA_OK(e, cudaGraphInstantiate(&ent->exec, g, 0));
+                // node priorities from the capturing streams (dense / diff overlap)
+                CUDA_OK(e, cudaGraphInstantiate(&ent->exec, g, e->ov_k > 0 ? cudaGraphInstantiateFlagUseNodePriority : 0));
                 cudaGraphDestroy(g);
                 ent->launches = e->launches;
             }

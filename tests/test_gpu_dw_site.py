@@ -238,3 +238,18 @@ def test_tc_site_epilogue_matches_separate(cout, act, k, monkeypatch):
         assert np.array_equal(cg, ce), "per-site per-frame counts"
         for a, b in zip(og, oe):
             assert np.array_equal(a, b), f"tap outputs differ (max {np.abs(a - b).max():.3e})"
+
+
+def test_depthwise_over_25_taps_rejected():
+    """Depthwise kernels take at most 5x5 taps; a 7x7 depthwise conv is
+    rejected at create (ST_ERR_UNSUPPORTED) instead of silently dropping
+    taps 25-48."""
+    from paper_2410_20790_b200 import Encoder
+    from paper_2410_20790_b200.binding import StError
+    n = Net(3, 16, 16, "dw7")
+    x = n.relu(n.conv(-1, 16, 3, 1, 1))
+    x = n.relu(n.conv(x, 16, 7, 1, 3, groups=16))
+    n.output(n.conv(x, 8, 1, 1, 0))
+    init_weights(n, 3)
+    with pytest.raises(StError, match="unsupported|UNSUPPORTED"):
+        Encoder(n, 1, 4, precision="bf16")
