@@ -733,7 +733,12 @@ static void launch_seq_k(const ConvCall &c, const DwSite &d, cudaStream_t s) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[NW], k_dwconv_site_seq<KMAX, 4, T, ACT>, 32 * NW, 0);
         if (per_sm[NW] <= 0) per_sm[NW] = 1;
     }
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(BNo, (int64_t)dw_sm_count() * per_sm[NW]));
+    // ST_DWT_OCC: fraction of the resident capacity the persistent grid takes
+    // (below 1 leaves room for the overlapped dense pass)
+    const char *oc = getenv("ST_DWT_OCC");
+    const double occ = oc ? atof(oc) : 1.0;
+    const int64_t cap = std::max<int64_t>(1, (int64_t)(dw_sm_count() * per_sm[NW] * occ));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(BNo, cap));
     k_dwconv_site_seq<KMAX, 4, T, ACT><<<grid, 32 * NW, 0, s>>>(c, d);
 }
 
