@@ -190,6 +190,20 @@ def ncu_traffic(kernel_class, cid, precision):
         return None
 
 
+def ncu_issue(kernel_class, cid):
+    """Duration-weighted warp-instructions issued per scheduler cycle (of 1.0)
+    of the class in the same committed capture, or None: an HBM fraction far
+    below 1 with traffic == algorithmic bytes and issue near 1 says the
+    kernel is instruction-issue bound, not memory bound."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            k = json.load(f).get("kernels", {}).get(kernel_class, {})
+        return k.get("issued_warp_per_scheduler_mean") if k.get("config") == cid else None
+    except Exception:
+        return None
+
+
 def gen_chunks(cfg, ids, L):
     """uint8 [len(ids)][L][H][W][C] of the config's chunks (seed per chunk),
     generated in worker processes (the generator is numpy, ~0.1 s per 1080p
@@ -531,7 +545,8 @@ def main():
         ach = (d["bytes"] / nl) / (d["ms"] / nl / 1e3) / 1e9 if d["bytes"] else None
         roof = {"bound": "hbm", "achieved": ach, "peak": p_hbm, "unit": "GB/s", "frac": (ach / p_hbm) if ach else None,
                 "peak_source": f"{peak_src} hbm_gbs"}
-    roof.update({"traffic": ncu_traffic(dom, cfg.cid, args.precision), "kernel": dom,
+    roof.update({"traffic": ncu_traffic(dom, cfg.cid, args.precision), "issue_per_scheduler": ncu_issue(dom, cfg.cid),
+                 "kernel": dom,
                  "alg_bytes_per_launch": d["bytes"] / nl, "alg_flops_per_launch": d["flops"] / nl,
                  "launches_per_step": d["launches"] / args.steps, "share_of_step": share})
 
