@@ -1,6 +1,9 @@
 // common.cuh -- device helpers shared by the sm_100a kernels (internal).
 #pragma once
 #include <algorithm>
+#include <cstdlib>
+#include <unordered_map>
+#include <algorithm>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -166,6 +169,35 @@ __device__ __forceinline__ float gmax(float v, unsigned mask) {
 }
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// grid of a grid-stride kernel: at most one wave of resident CTAs (the
+// occupancy calculator's count x SMs), so no partial last wave idles SMs;
+// ST_SITE_GRID=old keeps the caller's cap instead
+// (the occupancy query runs once per kernel, on the eager first step: no CUDA
+// calls of that kind inside a graph capture)
+template <class K>
+inline int resident_grid(K kernel, int threads, size_t smem, int64_t want, int old_cap) {
+    const char *v = getenv("ST_SITE_GRID");
+    if (v && v[0] == 'o') return (int)std::max<int64_t>(1, std::min<int64_t>(want, old_cap));
+    static int sms = 0;
+    static std::unordered_map<const void *, int> per_sm;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    auto it = per_sm.find(reinterpret_cast<const void *>(kernel));
+    int per = 0;
+    if (it == per_sm.end()) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess) per = 0;
+        per_sm[reinterpret_cast<const void *>(kernel)] = per;
+    } else {
+        per = it->second;
+    }
+    if (per <= 0) return (int)std::max<int64_t>(1, std::min<int64_t>(want, old_cap));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per * sms));
+}
 
 // host-side dispatch on the row type
 #define ST_ROW_DISPATCH(bf, ...)            \

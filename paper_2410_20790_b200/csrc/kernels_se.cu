@@ -1023,8 +1023,8 @@ void launch_se_site(DView in, const float *x0, const float *s_tab, int B, int N,
     }
     if (C % 8 == 0 && C <= 1280) {   // vectorised blocked form
 #define L_SEV(G_, CPL_)                                                                                          \
-    k_se_site_v<G_, CPL_, T><<<grid_for(G_), 256, 0, s>>>(in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, \
-                                                          static_cast<T *>(out_rows), zero_gaps)
+    k_se_site_v<G_, CPL_, T><<<resident_grid(k_se_site_v<G_, CPL_, T>, 256, 0, cdiv(BN * G_, 256), 148 * 8), 256, 0, s>>>( \
+        in, x0, s_tab, N, C, F, BN, theta, slot, pbase, out_act, static_cast<T *>(out_rows), zero_gaps)
 #define SEV_CH                            \
     if (C <= 8) L_SEV(1, 8);              \
     else if (C <= 16) L_SEV(2, 8);        \

@@ -465,14 +465,17 @@ void launch_site_pointwise(DView in, const float *x0, int B, int N, int C, int a
 
 #define L_PW(G_, CPL_)                                                                                 \
     {                                                                                                  \
-        const int grid = groups_grid(BN, G_);                                                          \
-        if (act == ACT_RELU)                                                                           \
-            k_site_pw<G_, CPL_, ACT_RELU, T><<<grid, 256, 0, s>>>(in, x0, BN, C, theta, out_act,       \
+        const int64_t want = cdiv(BN * G_, 256);                                                       \
+        if (act == ACT_RELU) {                                                                         \
+            auto kf = k_site_pw<G_, CPL_, ACT_RELU, T>;                                                \
+            kf<<<resident_grid(kf, 256, 0, want, 148 * 8), 256, 0, s>>>(in, x0, BN, C, theta, out_act,  \
                                                                   static_cast<T *>(out_rows), st,      \
                                                                   zero_gaps);                          \
-        else /* SiLU: exact (double exp) in FP32 mode, fast in BF16 mode */                            \
-            k_site_pw<G_, CPL_, (sizeof(T) == 4 ? ACT_SILU : ACT_SILU_FAST), T><<<grid, 256, 0, s>>>(  \
+        } else { /* SiLU: exact (double exp) in FP32 mode, fast in BF16 mode */                        \
+            auto kf = k_site_pw<G_, CPL_, (sizeof(T) == 4 ? ACT_SILU : ACT_SILU_FAST), T>;             \
+            kf<<<resident_grid(kf, 256, 0, want, 148 * 8), 256, 0, s>>>(                               \
                 in, x0, BN, C, theta, out_act, static_cast<T *>(out_rows), st, zero_gaps);             \
+        }                                                                                              \
     }
     ST_ROW_DISPATCH(bf, SITE_DISPATCH(C, L_PW));
 #undef L_PW
