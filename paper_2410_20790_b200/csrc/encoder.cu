@@ -568,10 +568,10 @@ extern "C" st_status st_encoder_create(const st_encoder_config *cfg, const st_la
     }
     for (auto &l : e->L) { l.spec.w = l.spec.b = l.spec.w2 = l.spec.b2 = nullptr; }
     e->cap_fit.assign(n + 1, -1);
-    {   // ST_OVERLAP=0: one stream; ST_OVERLAP_K: lookahead in layers (default 3)
+    {   // ST_OVERLAP=0: one stream; ST_OVERLAP_K: lookahead in layers (default 6)
         const char *ov = getenv("ST_OVERLAP"), *ok = getenv("ST_OVERLAP_K"), *np = getenv("ST_PDL");
         const bool off = (ov && ov[0] == '0') || cfg->streaming || cfg->debug_retain || (np && np[0] == '1');
-        e->ov_k = off ? 0 : std::max(1, ok ? atoi(ok) : 3);
+        e->ov_k = off ? 0 : std::max(1, ok ? atoi(ok) : 6);
     }
     st_status r = plan(e.get());
     if (r == ST_OK) r = alloc_fixed(e.get());

@@ -209,7 +209,7 @@ def test_dense_diff_overlap_identical(precision, model, monkeypatch):
     """The reference (dense) pass on its own stream, up to ST_OVERLAP_K layers
     ahead of the diff pass (arena lifetimes extended to match), gives the same
     outputs and counts as one stream (ST_OVERLAP=0), eager and replayed from
-    the captured graph, with lookahead 1 and 3."""
+    the captured graph, with lookahead 1, 3 and 12."""
     import torch
     from paper_2410_20790_b200 import Encoder
     if model == "effnet":
@@ -220,7 +220,7 @@ def test_dense_diff_overlap_identical(precision, model, monkeypatch):
     u8 = W.gen_video(2, 9, 64, 96, 3, 81, n_objects=4, size=(8, 24), speed=(1, 3), noise_q=0.1, noise_amp=2)
     fr = torch.from_numpy(W.to_float(u8)).cuda()
     outs = []
-    for ov, k in (("0", "3"), ("1", "1"), ("1", "3")):
+    for ov, k in (("0", "3"), ("1", "1"), ("1", "3"), ("1", "12")):
         monkeypatch.setenv("ST_OVERLAP", ov)
         monkeypatch.setenv("ST_OVERLAP_K", k)
         enc = Encoder(net, fr.shape[0], fr.shape[1], precision=precision)
