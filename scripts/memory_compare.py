@@ -36,6 +36,7 @@ a = ap.parse_args()
 
 import torch  # noqa: E402
 from paper_2410_20790_b200 import Encoder  # noqa: E402
+from paper_2410_20790_b200.binding import StError  # noqa: E402
 import oracle  # noqa: E402  (test infrastructure: the accountant's element counts only)
 
 dev = torch.device("cuda:0")
@@ -76,7 +77,11 @@ for cid in [int(c) for c in a.configs.split(",")]:
         # every site's x_acc / y_acc from frame to frame;
         # dense: the own dense path, one frame of each chunk per call
         Lm = {"vanilla": 2, "dense": 1}.get(mode, L)
-        enc = Encoder(net, B, Lm, precision=a.precision, streaming=mode in ("streaming", "vanilla"))
+        try:
+            enc = Encoder(net, B, Lm, precision=a.precision, streaming=mode in ("streaming", "vanilla"))
+        except StError as err:   # SE nets: the gate schedule spans a call (R8), no streaming caches
+            res[mode] = {"unsupported": str(err)}
+            continue
         mem = dict(enc.memory_report(), device_bytes=enc.device_bytes())
         if mode == "sparsebatch":
             def step():
