@@ -426,7 +426,8 @@ __global__ void __launch_bounds__(256, MINB) k_dwconv_site(ConvCall c, DwSite d)
     }
 }
 
-// Warp form (C <= 256, the default): ONE WARP PER OUTPUT PIXEL, lane l owns
+// Warp form (C <= 256; ST_DW_TEAM=0 -- the team form in kernels_dw_team.cu is the
+// default): ONE WARP PER OUTPUT PIXEL, lane l owns
 // channels l, l+32, ... (CPL = ceil(C/32)), so every warp's control flow --
 // the frame loop, the live-tap walk, the emit decision -- is uniform (ncu on
 // the 8-pixels-per-warp form: 2.3 G instructions for one 540x960x32 layer,
