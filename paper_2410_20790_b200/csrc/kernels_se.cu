@@ -453,7 +453,7 @@ __device__ void se_gate_block(const float *m, int C, int H, const float *w1, con
 // mean_t = (sum0 + dsum_1 + ... + dsum_t) / N do not depend on the refresh
 // decisions, so the F+1 gate evaluations run in parallel.  The running sum
 // is accumulated in frame order (as the sequential schedule would).
-__global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum0, const double *__restrict__ dsum,
+__global__ void __launch_bounds__(1024) k_se_gates(const double *__restrict__ sum0, const double *__restrict__ dsum,
                                                   int N, int C, int H, int F, const float *w1, const float *b1,
                                                   const float *w2, const float *b2, int t0, float *__restrict__ gate_tab) {
     st_pdl_enter();
@@ -474,13 +474,13 @@ __global__ void __launch_bounds__(256) k_se_gates(const double *__restrict__ sum
 // ---- (ii-b) refresh schedule, one CTA per chunk (frames sequential):
 // s_tab[b][t][c] = s_emit in force at frame t (t = 0: reference gate);
 // refresh[b] bit t-1 = refresh at t.
-__global__ void __launch_bounds__(256) k_se_schedule(const float *__restrict__ gate_tab, int C, int F,
+__global__ void __launch_bounds__(1024) k_se_schedule(const float *__restrict__ gate_tab, int C, int F,
                                                      const float *__restrict__ theta_p, float *__restrict__ s_tab,
                                                      uint32_t *__restrict__ refresh) {
     st_pdl_enter();
     const float theta = __ldg(theta_p);
     extern __shared__ float semit[];   // [C]
-    __shared__ float red[8];
+    __shared__ float red[32];
     __shared__ int do_refresh;
     const int b = blockIdx.x;
     const float *gt = gate_tab + (int64_t)b * (F + 1) * C;
@@ -875,35 +875,41 @@ void launch_se_colsum(const float *x, int B, int N, int C, double *sum0, cudaStr
     k_se_colsum<<<grid, 256, 0, s>>>(x, N, C, ppb, sum0);
 }
 
+// threads per block of the per-chunk gate kernels: one CTA per (frame, chunk)
+// or per chunk, latency-bound chains -- wide layers spread over 1024 threads
+static int se_threads(int C) { return C > 256 ? 1024 : 256; }
+
 void launch_se_schedule(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                         const float *b1, const float *w2, const float *b2, const float *theta, float *gate_tab,
                         float *s_tab, uint32_t *refresh, cudaStream_t s) {
-    const size_t smem = (size_t)(C + H + (H <= 256 ? H * (SE_WCH + 1) : 0)) * 4;
+    const int nth = se_threads(C);
+    const size_t smem = (size_t)(C + H + (H <= nth ? H * (SE_WCH + 1) : 0)) * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    k_se_gates<<<dim3(F + 1, B), 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, 0, gate_tab);
+    k_se_gates<<<dim3(F + 1, B), nth, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, 0, gate_tab);
     static size_t attr2 = 0;
     const size_t smem2 = (size_t)C * 4;
     if (smem2 > 48 * 1024 && smem2 > attr2) {
         cudaFuncSetAttribute(k_se_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         attr2 = smem2;
     }
-    k_se_schedule<<<B, 256, smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
+    k_se_schedule<<<B, se_threads(C), smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
 }
 
 void launch_se_gates(const double *sum0, const double *dsum, int B, int N, int C, int H, int F, const float *w1,
                      const float *b1, const float *w2, const float *b2, int t0, int nt, float *gate_tab, cudaStream_t s) {
     if (nt <= 0) return;
-    const size_t smem = (size_t)(C + H + (H <= 256 ? H * (SE_WCH + 1) : 0)) * 4;
+    const int nth = se_threads(C);
+    const size_t smem = (size_t)(C + H + (H <= nth ? H * (SE_WCH + 1) : 0)) * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(k_se_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    k_se_gates<<<dim3(nt, B), 256, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, t0, gate_tab);
+    k_se_gates<<<dim3(nt, B), nth, smem, s>>>(sum0, dsum, N, C, H, F, w1, b1, w2, b2, t0, gate_tab);
 }
 
 void launch_se_sched(const float *gate_tab, int B, int C, int F, const float *theta, float *s_tab, uint32_t *refresh,
@@ -914,7 +920,7 @@ void launch_se_sched(const float *gate_tab, int B, int C, int F, const float *th
         cudaFuncSetAttribute(k_se_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         attr2 = smem2;
     }
-    k_se_schedule<<<B, 256, smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
+    k_se_schedule<<<B, se_threads(C), smem2, s>>>(gate_tab, C, F, theta, s_tab, refresh);
 }
 
 void launch_se_dense_apply(const float *x, const float *s_tab, int B, int N, int C, int F, float *y, void *ybf,
