@@ -9,7 +9,7 @@
 // consecutive pixels' words with one coalesced 128-byte load and a pixel's
 // frames are one register.  Compaction is an ordered exclusive scan of
 // popc(word) -- deterministic, no atomics on the data path.
-#include "common.cuh"
+#include "rowio.cuh"
 
 namespace st {
 
@@ -67,9 +67,7 @@ __global__ void __launch_bounds__(256) k_subtract_mask(const float *__restrict__
             if (on) S[c] = __fadd_rn(S[c], e);  // R3: S += emitted
             e4[c] = e;
         }
-        if (dd)
-#pragma unroll
-            for (int c = 0; c < 4; c++) str<T>(dd + t1 * dfs + c, e4[c]);
+        if (dd) RowIO<T, 4>::store(dd + t1 * dfs, e4);   // one 8-byte (bf16) / 16-byte (fp32) store
         if (on) w |= 1u << t1;
     }
     act[i] = w;
